@@ -1,0 +1,184 @@
+/*
+ * convq.h -- C ABI of libconvq.so: B200 (sm_100a) quantized INT8/INT4
+ * implicit-GEMM 2-D convolution with s32 accumulation, input quantize/pack,
+ * and a fused requantize + repack epilogue that writes the next layer's
+ * packed NHWC layout.
+ *
+ * The operation (section 2.1): a convolution over feature map
+ * width W, height H, input channels I (= C here), output channels O (= K),
+ * kernel R x S, batch N "can be translated into matrix multiplication of
+ * (N*H*W, I*R*S) x (I*R*S, O)".  Output spatial size uses floor:
+ *   P = (H + 2*pad - R)/stride + 1,   Q = (W + 2*pad - S)/stride + 1.
+ * For every output pixel (n,p,q) and output channel k:
+ *   acc[n,p,q,k] = sum_{r,s,c} x[n, p*stride-pad+r, q*stride-pad+s, c] * w[k,r,s,c]
+ * (out-of-range x reads as 0), then (section 3.2.2: "relu, batch
+ * normalization, and bias addition ... finally clipped to lower bits and
+ * packed"):
+ *   y[n,p,q,k] = clamp(rne(fmaf((float)acc, scale[k], shift[k])), lo, hi)
+ *   lo = relu ? 0 : -2^(bits-1),  hi = 2^(bits-1) - 1
+ * packed into `bits`-bit two's-complement codes (section 1:
+ * "8 consecutive values (in 32-bit) into a packed vector of 4-bit elements").
+ *
+ * Conventions for every entry point:
+ *   - Tensor pointers are DEVICE pointers unless stated, 16-byte aligned.
+ *     The caller owns every tensor; the library never frees them.
+ *   - Calls are asynchronous on the plan's (or the given) CUDA stream; kernel
+ *     faults surface at the next synchronisation, as usual in CUDA.
+ *   - Functions returning int return CONV_Q_OK (0) or a negative CONV_Q_E*
+ *     code; conv_q_plan returns NULL on error.  conv_q_last_error() then holds
+ *     a thread-local message.
+ *   - Packed layouts (bits = 8 or 4), channel-innermost:
+ *       s8: byte c of a pixel row = (uint8) q[c]
+ *       s4: 32-bit word c/8 holds q[c] & 0xF at bits 4*(c mod 8)
+ *           (little-nibble-first), i.e. byte c/2, low nibble = even c.
+ *     One pixel row is C*bits/8 bytes and must be a multiple of 16 bytes.
+ *   - x : packed NHWC  [N][H][W][C*bits/8]
+ *     w : packed KRSC  [K][R][S][C*bits/8]   (C innermost)
+ *     scale: 2*K floats [scale_0..scale_{K-1}, shift_0..shift_{K-1}]
+ *     y : packed NHWC  [N][P][Q][K*bits/8]   (== next layer's x), or
+ *         int32 NHWC   [N][P][Q][K] in CONV_Q_OUT_S32 mode (raw accumulators).
+ */
+#ifndef CONVQ_H
+#define CONVQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define CONVQ_API __attribute__((visibility("default")))
+#else
+#define CONVQ_API
+#endif
+
+/* status codes */
+#define CONV_Q_OK            0
+#define CONV_Q_EINVAL       (-1)  /* bad argument: dims < 1, stride/pad/bits out of range, NULL or misaligned pointer */
+#define CONV_Q_EUNSUPPORTED (-2)  /* valid conv the kernels do not cover, e.g. C*bits or K*bits not a multiple of 128 */
+#define CONV_Q_EOVERFLOW    (-3)  /* R*S*C*2^(2*bits-2) may exceed int32 (accumulator guard, PAPER.md:166 s3.2.1) */
+#define CONV_Q_ECUDA        (-4)  /* a CUDA runtime/driver call failed (no device, launch failure, ...) */
+#define CONV_Q_ENOMEM       (-5)  /* host or device allocation failed */
+
+/* output modes (conv_q_plan_set_epilogue) */
+#define CONV_Q_OUT_PACKED    0    /* requantize + repack to bits-bit NHWC (default) */
+#define CONV_Q_OUT_S32       1    /* raw int32 accumulators (debug / parity) */
+
+typedef struct conv_q_plan_s conv_q_plan_t;   /* opaque; owned by the library */
+
+typedef struct conv_q_info_s {
+    int N, H, W, C, K, R, S, stride, pad, bits;
+    int P, Q;                 /* output spatial size (floor) */
+    int64_t M;                /* GEMM rows  = N*P*Q */
+    int64_t Kg;               /* GEMM depth = R*S*C */
+    int64_t x_bytes, w_bytes, y_bytes, y_s32_bytes;
+    int relu, out_mode;
+    int num_candidates;       /* TileConfig candidates valid for this shape */
+    int config_index;         /* currently selected candidate */
+    char config[64];          /* its name, e.g. "bm128_bn128_kc128_st4_c1" */
+    float tuned_us;           /* median time of the selected config if tuned, else -1 */
+    int64_t macs;             /* M * K * Kg: multiply-accumulates of one run */
+} conv_q_info_t;
+
+/*
+ * Create a plan for one convolution shape (the paper's problem statement,
+ * N, H, W, I(=C), O(=K), R, S, plus stride and pad).
+ * bits in {4, 8} applies to x, w and y.  Host-only: validates the shape,
+ * derives P, Q, M, Kg, enumerates the valid TileConfig candidates and picks a
+ * default (conv_q_plan_tune re-picks by timing).  Needs a CUDA device only to
+ * read its SM count; on a machine without one the plan is still created and
+ * conv_q_run returns CONV_Q_ECUDA.
+ * Errors (NULL + last_error):
+ *   EINVAL       any dim < 1, stride not in [1,8], pad not in [0,127],
+ *                R-1 or S-1 > 255, P or Q < 1, bits not in {4,8}
+ *   EUNSUPPORTED C*bits or K*bits not a multiple of 128, C not a multiple of 32
+ *                (pad C with conv_q_quantize), or C*bits/8 > 65535
+ *   EOVERFLOW    R*S*C * 2^(2*bits-2) > 2^31-1
+ */
+CONVQ_API conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, int S,
+                           int stride, int pad, int bits);
+
+/*
+ * Run the plan: y = requant(conv(x, w), scale) (or raw s32 accumulators).
+ * x, w, scale, y: device pointers in the layouts above, 16-byte aligned.
+ * Never allocates; one launch of the implicit-GEMM kernel on the plan's stream.
+ * Errors: EINVAL (NULL / misaligned pointer), ECUDA (no device, launch failure).
+ * One run in flight per plan is allowed (the plan caches tensor maps).
+ */
+CONVQ_API int conv_q_run(conv_q_plan_t *plan, const void *x, const void *w, const float *scale, void *y);
+
+/* Stream for subsequent runs (a cudaStream_t; NULL = legacy default stream). */
+CONVQ_API int conv_q_plan_set_stream(conv_q_plan_t *plan, void *stream);
+
+/* relu in {0,1}; out_mode CONV_Q_OUT_PACKED or CONV_Q_OUT_S32. */
+CONVQ_API int conv_q_plan_set_epilogue(conv_q_plan_t *plan, int relu, int out_mode);
+
+/* TileConfig candidates: count, names, manual selection. */
+CONVQ_API int conv_q_plan_num_candidates(const conv_q_plan_t *plan);
+CONVQ_API int conv_q_plan_candidate_name(const conv_q_plan_t *plan, int index, char *buf, int buflen);
+CONVQ_API int conv_q_plan_set_config(conv_q_plan_t *plan, int index);
+
+/*
+ * Per-shape tile configuration picked by timing ("the best
+ * scheduling of MMA instructions varies for different convolution sizes";
+ * the B200 analog of the paper's exhaustive search, Table 1).
+ * Times every candidate on the given (caller-owned, valid) buffers with CUDA
+ * events -- `warmup` untimed runs then the median of `reps` -- selects the
+ * fastest and records it in the in-process cache (and in the JSON file named
+ * by $CONV_Q_CACHE, if set).  y is overwritten.  Synchronises the stream.
+ * Returns the selected index (>= 0) or an error code.
+ */
+CONVQ_API int conv_q_plan_tune(conv_q_plan_t *plan, const void *x, const void *w, const float *scale,
+                     void *y, int warmup, int reps);
+
+/* Fill *info (host memory). */
+CONVQ_API int conv_q_plan_info(const conv_q_plan_t *plan, conv_q_info_t *info);
+
+CONVQ_API void conv_q_plan_destroy(conv_q_plan_t *plan);
+
+/*
+ * Quantize + pack (section 1).  x_fp16: device fp16 NHWC
+ * [N][H][W][C]; xq: device packed NHWC with C' = conv_q_padded_channels(C,bits)
+ * channels ([N][H][W][C'*bits/8] bytes); channels [C, C') are written as 0.
+ *   q = clamp(rne(fp32(x) * inv_scale), -2^(bits-1), 2^(bits-1)-1); NaN -> lo.
+ * stream: cudaStream_t or NULL.  Errors: EINVAL, ECUDA.
+ */
+CONVQ_API int conv_q_quantize(const void *x_fp16, int N, int H, int W, int C, float inv_scale,
+                    int bits, void *xq, void *stream);
+
+/* C' = C rounded up to a multiple of 32 channels: one 32-byte tcgen05 K step
+ * for s8 and a whole 16-byte pixel row for s4 (reading 14). */
+CONVQ_API int conv_q_padded_channels(int C, int bits);
+
+/*
+ * Pack weights once per model (off the per-run path): w_krsc is a device int8
+ * [K][R][S][C] array of codes already in [-2^(bits-1), 2^(bits-1)-1] (values
+ * outside are truncated to their low `bits` bits); w_packed receives
+ * [K][R][S][C*bits/8] bytes.  C*bits must be a multiple of 128.
+ */
+CONVQ_API int conv_q_pack_weights(const int8_t *w_krsc, int K, int R, int S, int C, int bits,
+                        void *w_packed, void *stream);
+
+/* Thread-local status code of the last failed call on this thread (0 if none). */
+CONVQ_API int conv_q_last_status(void);
+
+/* Thread-local message for the last error on this thread ("" if none). */
+CONVQ_API const char *conv_q_last_error(void);
+
+/* ABI version (major*100 + minor). */
+CONVQ_API int conv_q_version(void);
+
+/*
+ * Measurement only (roofline denominator): run a tcgen05.mma
+ * kind::i8 loop (M=128, N=256, K=32, operands resident in shared memory, no
+ * HBM traffic) on every SM for `iters` MMAs per CTA and report the achieved
+ * dense INT8 rate in ops/s (2 ops per MAC) in *ops_per_s.  Synchronises.
+ */
+CONVQ_API int conv_q_int8_peak(int iters, double *ops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONVQ_H */

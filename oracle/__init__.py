@@ -110,7 +110,7 @@ def out_dim(H: int, R: int, stride: int, pad: int) -> int:
 
 
 def padded_channels(C: int, bits: int) -> int:
-    """C' = ceil(C*b/128)*128/b: channels rounded up to whole 16-byte rows."""
+    """C' = ceil(C/32)*32: whole 32-channel granules (DESIGN reading 14)."""
     return int(_load().oracle_padded_channels(C, bits))
 
 

@@ -120,13 +120,14 @@ ORACLE_API void oracle_unpack(const uint8_t *p, int64_t count, int bits, int8_t 
 
 /* ------------------------------------------------------------------------
  * Quantize + pack an fp16 NHWC tensor into packed NHWC with C' channels,
- * C' = ceil(C*b/128)*128/b (16-byte pixel rows); channels [C, C') are 0.
+ * C' = ceil(C/32)*32 (reading 14: whole 32-channel granules, i.e. >= 16-byte
+ * pixel rows for both widths); channels [C, C') are 0.
  * (section 1; reading 1, reading 7 for the zero padding value.)
  * ---------------------------------------------------------------------- */
 ORACLE_API int64_t oracle_padded_channels(int64_t C, int bits)
 {
-    int64_t per16 = 128 / bits;                 /* channels per 16 bytes */
-    return (C + per16 - 1) / per16 * per16;
+    (void)bits;
+    return (C + 31) / 32 * 32;
 }
 
 ORACLE_API void oracle_quantize(const uint16_t *x, int64_t N, int64_t H, int64_t W,

@@ -1,0 +1,252 @@
+"""B200-native quantized INT8/INT4 implicit-GEMM convolution (arXiv 2202.06819).
+
+Thin Python binding over the C ABI of ``libconvq.so`` (``include/convq.h``):
+argument marshalling only.  Every step of the path -- quantize/pack, the
+implicit-GEMM convolution on tcgen05 tensor cores, the fused requantize +
+repack epilogue -- runs in the CUDA kernels of ``csrc/``.  PyTorch is used only
+for device memory and streams (``Tensor.data_ptr()``,
+``torch.cuda.current_stream()``).  There is no CPU fallback: if the extension
+is missing or no B200 is present, calls raise ``ConvQError``.
+
+Names follow the paper's problem statement (section 2.1): N, H, W,
+C (= I, input channels), K (= O, output channels), R, S, stride, pad, bits.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+__all__ = [
+    "ConvQError", "ConvPlan", "PlanInfo", "load", "quantize", "pack_weights", "padded_channels",
+    "int8_peak", "out_dim", "OUT_PACKED", "OUT_S32",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libconvq.so")
+
+OK, EINVAL, EUNSUPPORTED, EOVERFLOW, ECUDA, ENOMEM = 0, -1, -2, -3, -4, -5
+OUT_PACKED, OUT_S32 = 0, 1
+_CODE_NAMES = {EINVAL: "EINVAL", EUNSUPPORTED: "EUNSUPPORTED", EOVERFLOW: "EOVERFLOW",
+               ECUDA: "ECUDA", ENOMEM: "ENOMEM"}
+
+
+class ConvQError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_CODE_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("N", "H", "W", "C", "K", "R", "S", "stride", "pad", "bits", "P", "Q")] + [
+        ("M", ctypes.c_int64), ("Kg", ctypes.c_int64), ("x_bytes", ctypes.c_int64), ("w_bytes", ctypes.c_int64),
+        ("y_bytes", ctypes.c_int64), ("y_s32_bytes", ctypes.c_int64), ("relu", ctypes.c_int),
+        ("out_mode", ctypes.c_int), ("num_candidates", ctypes.c_int), ("config_index", ctypes.c_int),
+        ("config", ctypes.c_char * 64), ("tuned_us", ctypes.c_float), ("macs", ctypes.c_int64)]
+
+
+@dataclass
+class PlanInfo:
+    N: int; H: int; W: int; C: int; K: int; R: int; S: int; stride: int; pad: int; bits: int
+    P: int; Q: int; M: int; Kg: int
+    x_bytes: int; w_bytes: int; y_bytes: int; y_s32_bytes: int
+    relu: int; out_mode: int; num_candidates: int; config_index: int; config: str; tuned_us: float; macs: int
+
+
+_lib = None
+
+
+def load(build_if_missing: bool = False) -> ctypes.CDLL:
+    """Load libconvq.so (in-tree).  Raises if it is absent: no fallback path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        if build_if_missing:
+            from . import _build
+            _build.build()
+        else:
+            raise ConvQError(ECUDA, f"{LIB_PATH} not built; run `python __graft_entry__.py build` "
+                                    "(or paper_2202_06819_b200/_build.py)")
+    lib = ctypes.CDLL(LIB_PATH)
+    i, vp, f = ctypes.c_int, ctypes.c_void_p, ctypes.c_float
+    lib.conv_q_plan.restype = vp
+    lib.conv_q_plan.argtypes = [i] * 10
+    lib.conv_q_run.restype = i
+    lib.conv_q_run.argtypes = [vp, vp, vp, vp, vp]
+    lib.conv_q_plan_set_stream.restype = i
+    lib.conv_q_plan_set_stream.argtypes = [vp, vp]
+    lib.conv_q_plan_set_epilogue.restype = i
+    lib.conv_q_plan_set_epilogue.argtypes = [vp, i, i]
+    lib.conv_q_plan_num_candidates.restype = i
+    lib.conv_q_plan_num_candidates.argtypes = [vp]
+    lib.conv_q_plan_candidate_name.restype = i
+    lib.conv_q_plan_candidate_name.argtypes = [vp, i, ctypes.c_char_p, i]
+    lib.conv_q_plan_set_config.restype = i
+    lib.conv_q_plan_set_config.argtypes = [vp, i]
+    lib.conv_q_plan_tune.restype = i
+    lib.conv_q_plan_tune.argtypes = [vp, vp, vp, vp, vp, i, i]
+    lib.conv_q_plan_info.restype = i
+    lib.conv_q_plan_info.argtypes = [vp, ctypes.POINTER(_Info)]
+    lib.conv_q_plan_destroy.restype = None
+    lib.conv_q_plan_destroy.argtypes = [vp]
+    lib.conv_q_quantize.restype = i
+    lib.conv_q_quantize.argtypes = [vp, i, i, i, i, f, i, vp, vp]
+    lib.conv_q_padded_channels.restype = i
+    lib.conv_q_padded_channels.argtypes = [i, i]
+    lib.conv_q_pack_weights.restype = i
+    lib.conv_q_pack_weights.argtypes = [vp, i, i, i, i, i, vp, vp]
+    lib.conv_q_last_status.restype = i
+    lib.conv_q_last_status.argtypes = []
+    lib.conv_q_last_error.restype = ctypes.c_char_p
+    lib.conv_q_last_error.argtypes = []
+    lib.conv_q_version.restype = i
+    lib.conv_q_version.argtypes = []
+    lib.conv_q_int8_peak.restype = i
+    lib.conv_q_int8_peak.argtypes = [i, ctypes.POINTER(ctypes.c_double)]
+    _lib = lib
+    return lib
+
+
+def _check(rc: int) -> int:
+    if rc < 0:
+        raise ConvQError(rc, load().conv_q_last_error().decode())
+    return rc
+
+
+def _ptr(t) -> int:
+    """Device address of a torch tensor (or a raw int address)."""
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def out_dim(H: int, R: int, stride: int, pad: int) -> int:
+    return (H + 2 * pad - R) // stride + 1
+
+
+def padded_channels(C: int, bits: int) -> int:
+    return _check(load().conv_q_padded_channels(C, bits))
+
+
+class ConvPlan:
+    """conv_q_plan(N,H,W,C,K,R,S,stride,pad,bits) + conv_q_run(plan,x,w,scale,y)."""
+
+    def __init__(self, N, H, W, C, K, R, S, stride, pad, bits, relu=False, out_mode=OUT_PACKED):
+        lib = load()
+        h = lib.conv_q_plan(N, H, W, C, K, R, S, stride, pad, bits)
+        if not h:
+            raise ConvQError(lib.conv_q_last_status(), lib.conv_q_last_error().decode())
+        self._h = ctypes.c_void_p(h)
+        self.N, self.H, self.W, self.C, self.K = N, H, W, C, K
+        self.R, self.S, self.stride, self.pad, self.bits = R, S, stride, pad, bits
+        self.P, self.Q = out_dim(H, R, stride, pad), out_dim(W, S, stride, pad)
+        self.set_epilogue(relu, out_mode)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.conv_q_plan_destroy(h)
+            self._h = None
+
+    # -- configuration
+    def set_epilogue(self, relu: bool, out_mode: int = OUT_PACKED):
+        _check(load().conv_q_plan_set_epilogue(self._h, int(bool(relu)), out_mode))
+        self.relu, self.out_mode = bool(relu), out_mode
+
+    def set_stream(self, stream):
+        _check(load().conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
+
+    def candidates(self) -> list[str]:
+        lib = load()
+        n = _check(lib.conv_q_plan_num_candidates(self._h))
+        out = []
+        for i in range(n):
+            buf = ctypes.create_string_buffer(64)
+            _check(lib.conv_q_plan_candidate_name(self._h, i, buf, 64))
+            out.append(buf.value.decode())
+        return out
+
+    def set_config(self, index: int):
+        _check(load().conv_q_plan_set_config(self._h, index))
+
+    def info(self) -> PlanInfo:
+        inf = _Info()
+        _check(load().conv_q_plan_info(self._h, ctypes.byref(inf)))
+        d = {n: getattr(inf, n) for n, _ in _Info._fields_}
+        d["config"] = inf.config.decode()
+        return PlanInfo(**d)
+
+    # -- sizes (bytes)
+    @property
+    def x_bytes(self):
+        return self.N * self.H * self.W * self.C * self.bits // 8
+
+    @property
+    def w_bytes(self):
+        return self.K * self.R * self.S * self.C * self.bits // 8
+
+    @property
+    def y_bytes(self):
+        return self.N * self.P * self.Q * self.K * self.bits // 8
+
+    @property
+    def macs(self):
+        return self.N * self.P * self.Q * self.K * self.R * self.S * self.C
+
+    # -- execution
+    def run(self, x, w, scale, y, stream=None):
+        """y <- requant(conv(x, w)) on `stream` (default: torch's current stream)."""
+        lib = load()
+        _check(lib.conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
+        _check(lib.conv_q_run(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)),
+                              ctypes.c_void_p(_ptr(scale)), ctypes.c_void_p(_ptr(y))))
+        return y
+
+    def tune(self, x, w, scale, y, warmup=3, reps=10, stream=None) -> int:
+        lib = load()
+        _check(lib.conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
+        return _check(lib.conv_q_plan_tune(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)),
+                                           ctypes.c_void_p(_ptr(scale)), ctypes.c_void_p(_ptr(y)),
+                                           warmup, reps))
+
+
+def quantize(x_fp16, inv_scale: float, bits: int, out=None, stream=None):
+    """fp16 NHWC torch tensor -> packed NHWC uint8 tensor with C' channels."""
+    import torch
+    N, H, W, C = x_fp16.shape
+    assert x_fp16.dtype == torch.float16 and x_fp16.is_contiguous()
+    Cp = padded_channels(C, bits)
+    if out is None:
+        out = torch.empty((N, H, W, Cp * bits // 8), dtype=torch.uint8, device=x_fp16.device)
+    _check(load().conv_q_quantize(ctypes.c_void_p(x_fp16.data_ptr()), N, H, W, C, float(inv_scale), bits,
+                                  ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def pack_weights(w_codes, bits: int, out=None, stream=None):
+    """int8 KRSC codes (torch, device) -> packed KRSC uint8 [K,R,S,C*bits/8]."""
+    import torch
+    K, R, S, C = w_codes.shape
+    assert w_codes.dtype == torch.int8 and w_codes.is_contiguous()
+    if out is None:
+        out = torch.empty((K, R, S, C * bits // 8), dtype=torch.uint8, device=w_codes.device)
+    _check(load().conv_q_pack_weights(ctypes.c_void_p(w_codes.data_ptr()), K, R, S, C, bits,
+                                      ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def int8_peak(iters: int = 200000) -> float:
+    """Measured dense tcgen05 kind::i8 rate (ops/s) with operands in smem."""
+    v = ctypes.c_double(0.0)
+    _check(load().conv_q_int8_peak(iters, ctypes.byref(v)))
+    return v.value

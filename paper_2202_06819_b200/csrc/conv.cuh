@@ -1,0 +1,384 @@
+// conv.cuh -- the implicit-GEMM quantized convolution kernel for sm_100a.
+//
+// GEMM view (section 2.1): rows m = (n,p,q) output pixels
+// (M = N*P*Q), columns = K output channels, depth = R*S*C.  The im2col matrix
+// (Fig. 1) is never materialized: each k-block's A tile (BM
+// consecutive output pixels x KCH channels of one filter tap (r,s)) is fetched
+// by one TMA im2col-mode load from the packed NHWC input; out-of-bounds taps
+// (zero padding) are zero-filled by the TMA unit and never read from HBM.
+// The T4 design's block/warp/WMMA-atom tiling (Fig. 1) becomes
+// one CTA tile = one tcgen05.mma M=128 x N=BN instruction stream, accumulating
+// s32 in TMEM; the register-level packing of section 3.2
+// becomes a per-thread epilogue: tcgen05.ld gives a thread one output pixel's
+// BN channels, so requantize + pack happen in registers with no shuffles, and
+// the packed tile (BITS/32 of the s32 size, Fig. 7) is staged in
+// shared memory and written by one TMA store straight into the next layer's
+// packed NHWC layout (section 3.3's layout consistency).
+//
+// INT4: sm_100a has no 4-bit integer MMA kind (tcgen05 kinds: f16, tf32,
+// f8f6f4, i8).  Packed s4 tiles are TMA-loaded at half the bytes, then a
+// transform warpgroup expands every nibble v to the byte 16*v (exact s8) in the
+// UMMA swizzled layout; both operands are scaled by 16, so the accumulator
+// holds 256*acc and the epilogue shifts it back (exact).
+//
+// Warp roles (persistent CTA, one per SM):
+//   warp 0      TMA producer (one lane)
+//   warp 1      TMEM allocator + MMA issuer (one lane)
+//   warps 2..5  epilogue (128 threads = 128 TMEM lanes = BM rows)
+//   warps 6..9  INT4 only: s4 -> s8 transform
+// Pipelines: smem ring full/empty(/ready) mbarriers; TMEM double-buffered
+// accumulator acc_full/acc_empty so the epilogue of tile i overlaps the
+// mainloop of tile i+1.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include "ptx.cuh"
+
+namespace convq {
+
+constexpr int BM = 128;
+constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
+
+struct ConvParams {
+    int N, H, W, C, K, R, S, stride, pad;
+    int P, Q;
+    int M;          // N*P*Q
+    int row_bytes;  // packed bytes per input pixel row = C*BITS/8
+    int num_cblk;   // channel chunks per tap = C / KCH
+    int num_kb;     // k-blocks per tile = R*S*num_cblk
+    int n_tiles;    // ceil(K / BN)
+    int num_tiles;  // m_tiles * n_tiles
+    int relu;
+    const float *scale;  // [2K] scale then shift
+    int32_t *y32;        // s32 output (OUT_S32)
+};
+
+template <int BITS, int BN, int KCH, int OUT_S32>
+struct ConvCfg {
+    static constexpr int LOAD_ROW = KCH * BITS / 8;        // packed bytes per row per k-block
+    static constexpr int A_S8 = BM * KCH;                   // s8 A tile bytes
+    static constexpr int B_S8 = BN * KCH;
+    static constexpr int A_PK = BITS == 4 ? BM * LOAD_ROW : 0;
+    static constexpr int B_PK = BITS == 4 ? BN * LOAD_ROW : 0;
+    static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
+    static constexpr int STAGE_TX = (BM + BN) * LOAD_ROW;    // TMA bytes per stage
+    static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
+    static constexpr int OUT_SUBW = OUT_ROW < 128 ? OUT_ROW : 128;  // TMA store box width
+    static constexpr int OUT_NSUB = OUT_ROW / OUT_SUBW;
+    static constexpr int OUT_BYTES = OUT_S32 ? 0 : BM * OUT_ROW;
+    static constexpr int BAR_BYTES = 1024;
+    static constexpr int STAGES_FIT = (SMEM_LIMIT - 1024 - BAR_BYTES - OUT_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + OUT_BYTES + BAR_BYTES;
+    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int NUM_THREADS = BITS == 4 ? 320 : 192;
+    static constexpr uint32_t IDESC = idesc_i8(BM, BN);
+    static_assert(STAGES >= 2, "tile does not fit shared memory");
+    static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
+    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+    static_assert(TMEM_COLS <= 512, "TMEM");
+};
+
+// Swizzle<B,4,3> on a byte offset inside a tile whose rows are `span` bytes
+// (span = 128/64/32 -> SW128/SW64/SW32, 16 -> none): XOR the 16-byte chunk
+// index with the 128-byte-line index bits, as TMA and UMMA both apply it.
+template <int SPAN>
+__device__ __forceinline__ uint32_t swz(uint32_t off) {
+    constexpr uint32_t MASK = SPAN / 16 - 1;
+    return off ^ (((off >> 7) & MASK) << 4);
+}
+
+// s4 nibbles -> s8 bytes holding 16*v (nibble moved to the high half).
+// w: 8 nibbles, channel i at bits [4i,4i+4).  lo/hi: channels 0-3 / 4-7.
+__device__ __forceinline__ void expand_s4(uint32_t w, uint32_t &lo, uint32_t &hi) {
+    uint32_t even = (w << 4) & 0xF0F0F0F0u;  // byte i = nibble 2i << 4
+    uint32_t odd = w & 0xF0F0F0F0u;          // byte i = nibble 2i+1 << 4
+    lo = __byte_perm(even, odd, 0x5140);
+    hi = __byte_perm(even, odd, 0x7362);
+}
+
+// Expand a packed s4 tile [rows][KCH/2 bytes] (TMA-swizzled for its span) into
+// an s8 tile [rows][KCH bytes] in the UMMA K-major swizzled layout.
+template <int KCH>
+__device__ __forceinline__ void expand_tile(const uint8_t *src, uint8_t *dst, int rows, int tid, int nthr) {
+    constexpr int PW = KCH / 2;      // packed row bytes
+    constexpr int PPR = PW / 16;     // 16-byte pieces per packed row
+    for (int i = tid; i < rows * PPR; i += nthr) {
+        int row = i / PPR, j = i - row * PPR;
+        uint4 v = *reinterpret_cast<const uint4 *>(src + swz<PW>(row * PW + j * 16));
+        uint32_t o[8];
+        expand_s4(v.x, o[0], o[1]);
+        expand_s4(v.y, o[2], o[3]);
+        expand_s4(v.z, o[4], o[5]);
+        expand_s4(v.w, o[6], o[7]);
+        *reinterpret_cast<uint4 *>(dst + swz<KCH>(row * KCH + (2 * j) * 16)) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4 *>(dst + swz<KCH>(row * KCH + (2 * j + 1) * 16)) = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+}
+
+// Requantize (section 3.2.2; DESIGN readings 4-5):
+// y = clamp(rne(fmaf((float)acc, scale, shift)), lo, hi).
+__device__ __forceinline__ int requant1(int acc, float sc, float sh, float lo, float hi) {
+    float f = __int2float_rn(acc);
+    float v = __fmaf_rn(f, sc, sh);
+    float r = rintf(v);
+    return __float2int_rz(fminf(fmaxf(r, lo), hi));
+}
+
+template <int BITS, int BN, int KCH, int OUT_S32>
+__global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 1)
+    conv_igemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                      const __grid_constant__ CUtensorMap tm_y, const ConvParams p) {
+    using Cfg = ConvCfg<BITS, BN, KCH, OUT_S32>;
+    constexpr int STAGES = Cfg::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+    // ---- carve shared memory (every tile 1024-byte aligned)
+    uint8_t *a_s8 = smem;                               // [STAGES][BM*KCH]
+    uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][BN*KCH]
+    uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][BM*KCH/2]
+    uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][BN*KCH/2]
+    uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [OUT_NSUB][BM][OUT_SUBW]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(out_stage + Cfg::OUT_BYTES);
+    uint64_t *full = bars;                  // TMA -> (transform | MMA)
+    uint64_t *empty = bars + STAGES;        // MMA -> TMA
+    uint64_t *ready = bars + 2 * STAGES;    // transform -> MMA (INT4)
+    uint64_t *acc_full = bars + 3 * STAGES; // MMA -> epilogue [2]
+    uint64_t *acc_empty = acc_full + 2;     // epilogue -> MMA [2]
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tm_a);
+        tma_prefetch_desc(&tm_b);
+        if (!OUT_S32) tma_prefetch_desc(&tm_y);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+            mbar_init(&ready[s], 4);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    const int PQ = p.P * p.Q;
+
+    if (warp == 0) {
+        // =========================== TMA producer ===========================
+        if (lane == 0) {
+            const uint64_t pol_a = policy_evict_normal();  // activations: re-read by R*S taps and n-tiles
+            const uint64_t pol_b = policy_evict_last();    // weights: re-read by every m-tile
+            uint8_t *a_dst = BITS == 4 ? a_pk : a_s8;
+            uint8_t *b_dst = BITS == 4 ? b_pk : b_s8;
+            constexpr int A_LD = BITS == 4 ? Cfg::A_PK : Cfg::A_S8;
+            constexpr int B_LD = BITS == 4 ? Cfg::B_PK : Cfg::B_S8;
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
+                const int m0 = m_blk * BM;
+                const int n0 = m0 / PQ, rem = m0 - n0 * PQ;
+                const int p0 = rem / p.Q, q0 = rem - p0 * p.Q;
+                const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad;
+                int tap = 0, cblk = 0;
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    const int r = tap / p.S, s = tap - r * p.S;
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_TX);
+                    tma_load_im2col_4d(a_dst + stage * A_LD, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0,
+                                       (uint16_t)s, (uint16_t)r, pol_a);
+                    tma_load_2d(b_dst + stage * B_LD, &tm_b, &full[stage], tap * p.row_bytes + cblk * Cfg::LOAD_ROW,
+                                n_blk * BN, pol_b);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    if (++cblk == p.num_cblk) { cblk = 0; ++tap; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // =========================== MMA issuer =============================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+                const int buf = local & 1;
+                const uint32_t aphase = (local >> 1) & 1;
+                mbar_wait(&acc_empty[buf], aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + buf * BN;
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    mbar_wait(BITS == 4 ? &ready[stage] : &full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(a_s8 + stage * Cfg::A_S8);
+                    const uint32_t b_addr = smem_u32(b_s8 + stage * Cfg::B_S8);
+#pragma unroll
+                    for (int k = 0; k < KCH / 32; ++k) {
+                        mma_i8(d_tmem, umma_desc_kmajor(a_addr + 32 * k, KCH), umma_desc_kmajor(b_addr + 32 * k, KCH),
+                               Cfg::IDESC, (kb | k) != 0);
+                    }
+                    mma_commit(&empty[stage]);  // frees the smem stage when these MMAs complete
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&acc_full[buf]);  // accumulator ready for the epilogue
+            }
+        }
+    } else if (warp < 6) {
+        // =========================== epilogue ===============================
+        const int quad = warp & 3;              // TMEM lane quadrant this warp may access
+        const int row = quad * 32 + lane;       // tile row = output pixel
+        const bool leader = (warp == 2 && lane == 0);
+        const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
+        const float hi = (float)((1 << (BITS - 1)) - 1);
+        int local = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+            const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
+            const int buf = local & 1;
+            const uint32_t aphase = (local >> 1) & 1;
+            const int m = m_blk * BM + row;
+            if (!OUT_S32) {
+                // staging buffer must have been read out by the previous TMA store
+                if (leader) tma_store_wait_read0();
+                named_bar_sync(1, 128);
+            }
+            mbar_wait(&acc_full[buf], aphase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(taddr + c * 32, v);  // includes tcgen05.wait::ld
+                if (c == BN / 32 - 1) {  // whole accumulator is in registers: hand TMEM back
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&acc_empty[buf]);
+                }
+                const int col0 = n_blk * BN + c * 32;
+                if (OUT_S32) {
+                    if (m < p.M) {
+                        int32_t *dst = p.y32 + (int64_t)m * p.K + col0;
+                        if (col0 + 32 <= p.K) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                int4 t;
+                                t.x = BITS == 4 ? ((int)v[j] >> 8) : (int)v[j];
+                                t.y = BITS == 4 ? ((int)v[j + 1] >> 8) : (int)v[j + 1];
+                                t.z = BITS == 4 ? ((int)v[j + 2] >> 8) : (int)v[j + 2];
+                                t.w = BITS == 4 ? ((int)v[j + 3] >> 8) : (int)v[j + 3];
+                                *reinterpret_cast<int4 *>(dst + j) = t;
+                            }
+                        } else {
+                            for (int j = 0; j < 32 && col0 + j < p.K; ++j)
+                                dst[j] = BITS == 4 ? ((int)v[j] >> 8) : (int)v[j];
+                        }
+                    }
+                } else {
+                    float sc[32], sh[32];
+                    if (col0 + 32 <= p.K) {
+                        const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
+                        const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            float4 a = __ldg(s4 + j), b = __ldg(h4 + j);
+                            sc[4 * j] = a.x; sc[4 * j + 1] = a.y; sc[4 * j + 2] = a.z; sc[4 * j + 3] = a.w;
+                            sh[4 * j] = b.x; sh[4 * j + 1] = b.y; sh[4 * j + 2] = b.z; sh[4 * j + 3] = b.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            bool ok = col0 + j < p.K;
+                            sc[j] = ok ? __ldg(p.scale + col0 + j) : 0.f;
+                            sh[j] = ok ? __ldg(p.scale + p.K + col0 + j) : 0.f;
+                        }
+                    }
+                    int q[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        int a = BITS == 4 ? ((int)v[j] >> 8) : (int)v[j];
+                        q[j] = requant1(a, sc[j], sh[j], lo, hi);
+                    }
+                    // packed bytes of this 32-column chunk: 32 (s8) or 16 (s4)
+                    constexpr int CHUNK_BYTES = 32 * BITS / 8;
+                    const int byte0 = c * CHUNK_BYTES;
+                    uint8_t *sub = out_stage + (byte0 / Cfg::OUT_SUBW) * (BM * Cfg::OUT_SUBW);
+                    const int inrow = byte0 % Cfg::OUT_SUBW;
+                    if constexpr (BITS == 8) {
+#pragma unroll
+                        for (int piece = 0; piece < 2; ++piece) {
+                            uint32_t w4[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const int b = piece * 16 + 4 * k;
+                                uint32_t ab = __byte_perm((uint32_t)q[b], (uint32_t)q[b + 1], 0x0040);
+                                uint32_t cd = __byte_perm((uint32_t)q[b + 2], (uint32_t)q[b + 3], 0x0040);
+                                w4[k] = __byte_perm(ab, cd, 0x5410);
+                            }
+                            *reinterpret_cast<uint4 *>(sub + swz<Cfg::OUT_SUBW>(row * Cfg::OUT_SUBW + inrow + piece * 16)) =
+                                make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                        }
+                    } else {
+                        uint32_t w4[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            uint32_t w = 0;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) w |= ((uint32_t)q[8 * k + i] & 0xFu) << (4 * i);
+                            w4[k] = w;
+                        }
+                        *reinterpret_cast<uint4 *>(sub + swz<Cfg::OUT_SUBW>(row * Cfg::OUT_SUBW + inrow)) =
+                            make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    }
+                }
+            }
+            if (!OUT_S32) {
+                fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
+                named_bar_sync(1, 128);
+                if (leader) {
+#pragma unroll
+                    for (int s = 0; s < Cfg::OUT_NSUB; ++s)
+                        tma_store_2d(&tm_y, out_stage + s * (BM * Cfg::OUT_SUBW), n_blk * Cfg::OUT_ROW + s * Cfg::OUT_SUBW,
+                                     m_blk * BM);
+                    tma_store_commit();
+                }
+            }
+        }
+        if (!OUT_S32 && leader) tma_store_wait0();
+    } else {
+        // =========================== INT4 transform =========================
+        if constexpr (BITS == 4) {
+            const int tid = threadIdx.x - 192;  // 0..127
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    expand_tile<KCH>(a_pk + stage * Cfg::A_PK, a_s8 + stage * Cfg::A_S8, BM, tid, 128);
+                    expand_tile<KCH>(b_pk + stage * Cfg::B_PK, b_s8 + stage * Cfg::B_S8, BN, tid, 128);
+                    fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.mma
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&ready[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    }
+}
+
+}  // namespace convq

@@ -1,0 +1,618 @@
+// convq.cu -- libconvq.so: host side of the C ABI declared in include/convq.h.
+//
+// Responsibilities: validate shapes (incl. the
+// accumulator overflow guard of PAPER.md:166 s3.2.1), derive the GEMM view
+// (PAPER.md:56 s2.1), enumerate TileConfig candidates, pick one by timing on
+// the device ("the best scheduling of MMA instructions varies for
+// different convolution sizes"), encode the TMA tensor maps (im2col for the
+// activations, tiled for weights and output) and launch the kernels.
+// No CPU fallback: without a CUDA device every compute call returns
+// CONV_Q_ECUDA.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/convq.h"
+#include "conv.cuh"
+#include "pack.cuh"
+#include "peak.cuh"
+
+using namespace convq;
+
+// ============================================================== errors
+static thread_local std::string g_err;
+static thread_local int g_status = CONV_Q_OK;
+
+static int set_err(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    g_status = code;
+    return code;
+}
+#define CUDA_TRY(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (expr);                                                                    \
+        if (e_ != cudaSuccess) return set_err(CONV_Q_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+extern "C" const char *conv_q_last_error(void) { return g_err.c_str(); }
+extern "C" int conv_q_last_status(void) { return g_status; }
+extern "C" int conv_q_version(void) { return 100; }
+
+// ============================================================== driver entry points
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                      const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                      CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+typedef CUresult (*PFN_encodeIm2col_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                       const cuuint64_t *, const int *, const int *, cuuint32_t, cuuint32_t,
+                                       const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                       CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_t g_encode_tiled = nullptr;
+static PFN_encodeIm2col_t g_encode_im2col = nullptr;
+static int g_num_sms = 0;
+static std::once_flag g_init_once;
+static int g_init_status = CONV_Q_OK;
+static std::string g_init_msg;
+
+static void init_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) {
+        g_init_status = CONV_Q_ECUDA;
+        g_init_msg = std::string("no usable CUDA device: ") + cudaGetErrorString(e);
+        cudaGetLastError();
+        return;
+    }
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0) {
+        g_init_status = CONV_Q_ECUDA;
+        g_init_msg = "libconvq.so is built for sm_100a (B200); device is sm_" + std::to_string(major * 10 + minor);
+        return;
+    }
+    cudaDriverEntryPointQueryResult q1, q2;
+    void *f1 = nullptr, *f2 = nullptr;
+    e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f1, cudaEnableDefault, &q1);
+    if (e == cudaSuccess) e = cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f2, cudaEnableDefault, &q2);
+    if (e != cudaSuccess || !f1 || !f2) {
+        g_init_status = CONV_Q_ECUDA;
+        g_init_msg = "cuTensorMapEncode* driver entry points unavailable";
+        return;
+    }
+    g_encode_tiled = reinterpret_cast<PFN_encodeTiled_t>(f1);
+    g_encode_im2col = reinterpret_cast<PFN_encodeIm2col_t>(f2);
+}
+static int ensure_device() {
+    std::call_once(g_init_once, init_device);
+    if (g_init_status != CONV_Q_OK) return set_err(g_init_status, "%s", g_init_msg.c_str());
+    return CONV_Q_OK;
+}
+
+static CUtensorMapSwizzle swizzle_for(int span) {
+    return span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+         : span == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+         : span == 32  ? CU_TENSOR_MAP_SWIZZLE_32B
+                       : CU_TENSOR_MAP_SWIZZLE_NONE;
+}
+
+// ============================================================== plan
+struct Cand {
+    int bn, kch;
+};
+
+struct conv_q_plan_s {
+    int N, H, W, C, K, R, S, stride, pad, bits;
+    int P, Q;
+    int64_t M, Kg;
+    int row_bytes;     // C*bits/8
+    int out_row;       // K*bits/8
+    int relu = 0, out_mode = CONV_Q_OUT_PACKED;
+    cudaStream_t stream = nullptr;
+    std::vector<Cand> cands;
+    int sel = 0;
+    float tuned_us = -1.f;
+    // tensor-map cache (re-encoded when a pointer or the config changes)
+    CUtensorMap tm_a, tm_b, tm_y;
+    const void *c_x = nullptr, *c_w = nullptr, *c_y = nullptr;
+    int c_sel = -1, c_mode = -1;
+};
+
+static std::string cand_name(const conv_q_plan_s *p, int i) {
+    char b[64];
+    snprintf(b, sizeof b, "bm128_bn%d_kc%d_c1", p->cands[i].bn, p->cands[i].kch);
+    return b;
+}
+
+static std::string shape_key(const conv_q_plan_s *p) {
+    char b[160];
+    snprintf(b, sizeof b, "N%d_H%d_W%d_C%d_K%d_R%d_S%d_st%d_p%d_b%d_sm%d_m%d_r%d", p->N, p->H, p->W, p->C, p->K, p->R,
+             p->S, p->stride, p->pad, p->bits, g_num_sms, p->out_mode, p->relu);
+    return b;
+}
+
+// in-process tuning cache, optionally mirrored to $CONV_Q_CACHE (one JSON object)
+static std::mutex g_cache_mu;
+static std::map<std::string, std::pair<std::string, float>> g_cache;
+static bool g_cache_loaded = false;
+
+static void cache_load_locked() {
+    if (g_cache_loaded) return;
+    g_cache_loaded = true;
+    const char *path = getenv("CONV_Q_CACHE");
+    if (!path) return;
+    FILE *f = fopen(path, "r");
+    if (!f) return;
+    char line[512];
+    while (fgets(line, sizeof line, f)) {
+        char key[200], cfg[64];
+        float us;
+        if (sscanf(line, " \"%199[^\"]\": {\"config\": \"%63[^\"]\", \"us\": %f", key, cfg, &us) == 3)
+            g_cache[key] = {cfg, us};
+    }
+    fclose(f);
+}
+static void cache_store_locked() {
+    const char *path = getenv("CONV_Q_CACHE");
+    if (!path) return;
+    std::string tmp = std::string(path) + ".tmp";
+    FILE *f = fopen(tmp.c_str(), "w");
+    if (!f) return;
+    fprintf(f, "{\n");
+    size_t i = 0;
+    for (auto &kv : g_cache)
+        fprintf(f, "  \"%s\": {\"config\": \"%s\", \"us\": %.3f}%s\n", kv.first.c_str(), kv.second.first.c_str(),
+                kv.second.second, ++i < g_cache.size() ? "," : "");
+    fprintf(f, "}\n");
+    fclose(f);
+    rename(tmp.c_str(), path);
+}
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+static void enumerate_candidates(conv_q_plan_s *p) {
+    p->cands.clear();
+    for (int kch : {128, 64, 32}) {
+        if (p->C % kch) continue;
+        for (int bn : {64, 128, 256}) {
+            if (bn > 64 && bn / 2 >= p->K) continue;  // a narrower tile already covers K
+            p->cands.push_back({bn, kch});
+        }
+    }
+}
+
+// Default pick before tuning: deepest K chunk, then the widest N tile whose
+// tile count still fills one wave of SMs (else the narrowest tile).
+static int default_candidate(const conv_q_plan_s *p) {
+    const int64_t m_tiles = ceil_div(p->M, BM);
+    const int sms = g_num_sms > 0 ? g_num_sms : 148;
+    int pick = -1, narrow = -1;
+    for (size_t i = 0; i < p->cands.size(); ++i) {
+        const Cand &c = p->cands[i];
+        if (c.kch != p->cands[0].kch) continue;
+        if (narrow < 0 || c.bn < p->cands[narrow].bn) narrow = (int)i;
+        if (m_tiles * ceil_div(p->K, c.bn) >= sms && (pick < 0 || c.bn > p->cands[pick].bn)) pick = (int)i;
+    }
+    return pick >= 0 ? pick : std::max(narrow, 0);
+}
+
+extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, int S, int stride, int pad,
+                                      int bits) {
+    g_err.clear();
+    g_status = CONV_Q_OK;
+    if (N < 1 || H < 1 || W < 1 || C < 1 || K < 1 || R < 1 || S < 1) {
+        set_err(CONV_Q_EINVAL, "every dimension must be >= 1 (N=%d H=%d W=%d C=%d K=%d R=%d S=%d)", N, H, W, C, K, R,
+                S);
+        return nullptr;
+    }
+    if (stride < 1 || stride > 8) {
+        set_err(CONV_Q_EINVAL, "stride %d outside [1,8] (TMA traversal stride limit)", stride);
+        return nullptr;
+    }
+    if (pad < 0 || pad > 127) {
+        set_err(CONV_Q_EINVAL, "pad %d outside [0,127] (im2col bounding-box corner range)", pad);
+        return nullptr;
+    }
+    if (R - 1 > 255 || S - 1 > 255) {
+        set_err(CONV_Q_EINVAL, "filter %dx%d too large (im2col offsets are 8-bit)", R, S);
+        return nullptr;
+    }
+    if (bits != 4 && bits != 8) {
+        set_err(CONV_Q_EINVAL, "bits must be 4 or 8, got %d", bits);
+        return nullptr;
+    }
+    if (pad - (R - 1) < -128 || pad - (S - 1) < -128) {
+        set_err(CONV_Q_EINVAL, "pad - (R-1) below -128 (im2col bounding-box corner range)");
+        return nullptr;
+    }
+    int64_t P = (int64_t)H + 2 * pad - R, Q = (int64_t)W + 2 * pad - S;
+    if (P < 0 || Q < 0) {
+        set_err(CONV_Q_EINVAL, "output is empty: H+2pad-R=%lld, W+2pad-S=%lld", (long long)P, (long long)Q);
+        return nullptr;
+    }
+    P = P / stride + 1;
+    Q = Q / stride + 1;
+    if (((int64_t)C * bits) % 128 || ((int64_t)K * bits) % 128) {
+        set_err(CONV_Q_EUNSUPPORTED,
+                "C*bits (%lld) and K*bits (%lld) must be multiples of 128 (16-byte pixel rows); pad C with "
+                "conv_q_quantize",
+                (long long)C * bits, (long long)K * bits);
+        return nullptr;
+    }
+    if (C % 32) {
+        set_err(CONV_Q_EUNSUPPORTED, "C=%d: the implicit-GEMM kernel needs C %% 32 == 0 (one MMA K step)", C);
+        return nullptr;
+    }
+    if ((int64_t)C * bits / 8 > 65535) {
+        set_err(CONV_Q_EUNSUPPORTED, "C*bits/8 = %lld bytes per pixel exceeds 65535", (long long)C * bits / 8);
+        return nullptr;
+    }
+    // Accumulator guard (PAPER.md:166 s3.2.1): |acc| <= R*S*C*2^(b-1)*2^(b-1)
+    // must fit int32.  INT4 runs on the MMA as 16x-scaled s8 operands, so its
+    // MMA accumulator holds 256*acc: bound R*S*C*2^14 there (same as s8).
+    const int64_t Kg = (int64_t)R * S * C;
+    const int64_t bound = Kg * (int64_t)(1 << 14);
+    if (bound > 2147483647LL) {
+        set_err(CONV_Q_EOVERFLOW, "R*S*C = %lld: accumulator bound %lld exceeds int32", (long long)Kg,
+                (long long)bound);
+        return nullptr;
+    }
+    const int64_t M = (int64_t)N * P * Q;
+    if (M > 2147483647LL - 256) {
+        set_err(CONV_Q_EUNSUPPORTED, "N*P*Q = %lld exceeds the 32-bit GEMM row index", (long long)M);
+        return nullptr;
+    }
+    auto *p = new (std::nothrow) conv_q_plan_s();
+    if (!p) {
+        set_err(CONV_Q_ENOMEM, "plan allocation failed");
+        return nullptr;
+    }
+    p->N = N; p->H = H; p->W = W; p->C = C; p->K = K; p->R = R; p->S = S;
+    p->stride = stride; p->pad = pad; p->bits = bits;
+    p->P = (int)P; p->Q = (int)Q; p->M = M; p->Kg = Kg;
+    p->row_bytes = C * bits / 8;
+    p->out_row = K * bits / 8;
+    std::call_once(g_init_once, init_device);  // SM count for the default pick; errors surface at run
+    enumerate_candidates(p);
+    p->sel = default_candidate(p);
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        cache_load_locked();
+        auto it = g_cache.find(shape_key(p));
+        if (it != g_cache.end())
+            for (size_t i = 0; i < p->cands.size(); ++i)
+                if (cand_name(p, (int)i) == it->second.first) {
+                    p->sel = (int)i;
+                    p->tuned_us = it->second.second;
+                }
+    }
+    return p;
+}
+
+extern "C" void conv_q_plan_destroy(conv_q_plan_t *p) { delete p; }
+
+extern "C" int conv_q_plan_set_stream(conv_q_plan_t *p, void *stream) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    p->stream = static_cast<cudaStream_t>(stream);
+    return CONV_Q_OK;
+}
+
+extern "C" int conv_q_plan_set_epilogue(conv_q_plan_t *p, int relu, int out_mode) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    if ((relu != 0 && relu != 1) || (out_mode != CONV_Q_OUT_PACKED && out_mode != CONV_Q_OUT_S32))
+        return set_err(CONV_Q_EINVAL, "relu must be 0/1 and out_mode PACKED(0)/S32(1)");
+    p->relu = relu;
+    p->out_mode = out_mode;
+    return CONV_Q_OK;
+}
+
+extern "C" int conv_q_plan_num_candidates(const conv_q_plan_t *p) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    return (int)p->cands.size();
+}
+
+extern "C" int conv_q_plan_candidate_name(const conv_q_plan_t *p, int i, char *buf, int len) {
+    if (!p || !buf || len < 1) return set_err(CONV_Q_EINVAL, "NULL argument");
+    if (i < 0 || i >= (int)p->cands.size()) return set_err(CONV_Q_EINVAL, "candidate %d out of range", i);
+    snprintf(buf, len, "%s", cand_name(p, i).c_str());
+    return CONV_Q_OK;
+}
+
+extern "C" int conv_q_plan_set_config(conv_q_plan_t *p, int i) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    if (i < 0 || i >= (int)p->cands.size()) return set_err(CONV_Q_EINVAL, "candidate %d out of range", i);
+    p->sel = i;
+    p->tuned_us = -1.f;
+    return CONV_Q_OK;
+}
+
+extern "C" int conv_q_plan_info(const conv_q_plan_t *p, conv_q_info_t *info) {
+    if (!p || !info) return set_err(CONV_Q_EINVAL, "NULL argument");
+    memset(info, 0, sizeof *info);
+    info->N = p->N; info->H = p->H; info->W = p->W; info->C = p->C; info->K = p->K;
+    info->R = p->R; info->S = p->S; info->stride = p->stride; info->pad = p->pad; info->bits = p->bits;
+    info->P = p->P; info->Q = p->Q; info->M = p->M; info->Kg = p->Kg;
+    info->x_bytes = (int64_t)p->N * p->H * p->W * p->row_bytes;
+    info->w_bytes = (int64_t)p->K * p->R * p->S * p->row_bytes;
+    info->y_bytes = p->M * p->out_row;
+    info->y_s32_bytes = p->M * p->K * 4;
+    info->relu = p->relu;
+    info->out_mode = p->out_mode;
+    info->num_candidates = (int)p->cands.size();
+    info->config_index = p->sel;
+    snprintf(info->config, sizeof info->config, "%s", p->cands.empty() ? "" : cand_name(p, p->sel).c_str());
+    info->tuned_us = p->tuned_us;
+    info->macs = p->M * p->K * p->Kg;
+    return CONV_Q_OK;
+}
+
+// ============================================================== launch
+template <int BITS, int BN, int KCH, int OUT>
+static int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
+    using Cfg = ConvCfg<BITS, BN, KCH, OUT>;
+    auto kern = conv_igemm_kernel<BITS, BN, KCH, OUT>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+        attr_set = true;
+    }
+    ConvParams prm;
+    prm.N = p->N; prm.H = p->H; prm.W = p->W; prm.C = p->C; prm.K = p->K; prm.R = p->R; prm.S = p->S;
+    prm.stride = p->stride; prm.pad = p->pad; prm.P = p->P; prm.Q = p->Q; prm.M = (int)p->M;
+    prm.row_bytes = p->row_bytes;
+    prm.num_cblk = p->C / KCH;
+    prm.num_kb = p->R * p->S * prm.num_cblk;
+    prm.n_tiles = (int)ceil_div(p->K, BN);
+    prm.num_tiles = (int)(ceil_div(p->M, BM) * prm.n_tiles);
+    prm.relu = p->relu;
+    prm.scale = scale;
+    prm.y32 = static_cast<int32_t *>(y);
+    const int grid = std::min(prm.num_tiles, g_num_sms);
+    kern<<<grid, Cfg::NUM_THREADS, Cfg::SMEM, p->stream>>>(p->tm_a, p->tm_b, p->tm_y, prm);
+    CUDA_TRY(cudaGetLastError());
+    return CONV_Q_OK;
+}
+
+template <int BITS, int OUT>
+static int dispatch_bn_kch(conv_q_plan_s *p, const float *scale, void *y) {
+    const Cand c = p->cands[p->sel];
+#define CONVQ_CASE(BN_, KC_) \
+    if (c.bn == BN_ && c.kch == KC_) return launch_conv<BITS, BN_, KC_, OUT>(p, scale, y);
+    CONVQ_CASE(64, 128) CONVQ_CASE(128, 128) CONVQ_CASE(256, 128)
+    CONVQ_CASE(64, 64) CONVQ_CASE(128, 64) CONVQ_CASE(256, 64)
+    CONVQ_CASE(64, 32) CONVQ_CASE(128, 32) CONVQ_CASE(256, 32)
+#undef CONVQ_CASE
+    return set_err(CONV_Q_EUNSUPPORTED, "no kernel instantiation for bn=%d kch=%d", c.bn, c.kch);
+}
+
+static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) {
+    const Cand c = p->cands[p->sel];
+    const int load_row = c.kch * p->bits / 8;
+    const CUtensorMapSwizzle sw_ld = swizzle_for(load_row);
+    // A: packed NHWC activations, im2col mode ("im2col layout"),
+    // {C bytes, W, H, N}; the bounding box walks output pixels with the conv
+    // stride; the corners make out-of-image taps read as zero (padding).
+    {
+        cuuint64_t dims[4] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->W, (cuuint64_t)p->H, (cuuint64_t)p->N};
+        cuuint64_t strides[3] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->row_bytes * p->W,
+                                 (cuuint64_t)p->row_bytes * p->W * p->H};
+        int lower[2] = {-p->pad, -p->pad};                          // {W, H}
+        int upper[2] = {p->pad - (p->S - 1), p->pad - (p->R - 1)};  // {W, H}
+        cuuint32_t estr[4] = {1, (cuuint32_t)p->stride, (cuuint32_t)p->stride, 1};
+        CUresult r = g_encode_im2col(&p->tm_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(x), dims, strides,
+                                     lower, upper, (cuuint32_t)load_row, (cuuint32_t)BM, estr,
+                                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw_ld, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeIm2col(x) failed: %d", (int)r);
+    }
+    // B: packed KRSC weights as a 2-D [K][R*S*C bytes] matrix, tiled.
+    {
+        cuuint64_t dims[2] = {(cuuint64_t)p->R * p->S * p->row_bytes, (cuuint64_t)p->K};
+        cuuint64_t strides[1] = {(cuuint64_t)p->R * p->S * p->row_bytes};
+        cuuint32_t box[2] = {(cuuint32_t)load_row, (cuuint32_t)c.bn};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = g_encode_tiled(&p->tm_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(w), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw_ld,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(w) failed: %d", (int)r);
+    }
+    // Y: packed NHWC output as a 2-D [M][K*bits/8 bytes] matrix (== the next
+    // layer's x; PAPER.md:261 layout consistency).  Unused in S32 mode.
+    if (p->out_mode == CONV_Q_OUT_PACKED) {
+        const int out_row_tile = c.bn * p->bits / 8;
+        const int subw = out_row_tile < 128 ? out_row_tile : 128;
+        cuuint64_t dims[2] = {(cuuint64_t)p->out_row, (cuuint64_t)p->M};
+        cuuint64_t strides[1] = {(cuuint64_t)p->out_row};
+        cuuint32_t box[2] = {(cuuint32_t)subw, (cuuint32_t)BM};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = g_encode_tiled(&p->tm_y, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, y, dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(subw), CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(y) failed: %d", (int)r);
+    } else {
+        memset(&p->tm_y, 0, sizeof p->tm_y);
+    }
+    p->c_x = x; p->c_w = w; p->c_y = y; p->c_sel = p->sel; p->c_mode = p->out_mode;
+    return CONV_Q_OK;
+}
+
+static bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
+
+extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    if (!x || !w || !scale || !y) return set_err(CONV_Q_EINVAL, "NULL tensor pointer");
+    if (!aligned16(x) || !aligned16(w) || !aligned16(scale) || !aligned16(y))
+        return set_err(CONV_Q_EINVAL, "tensor pointers must be 16-byte aligned");
+    int rc = ensure_device();
+    if (rc) return rc;
+    if (p->c_x != x || p->c_w != w || p->c_y != y || p->c_sel != p->sel || p->c_mode != p->out_mode) {
+        rc = encode_maps(p, x, w, y);
+        if (rc) return rc;
+    }
+    const bool s32 = p->out_mode == CONV_Q_OUT_S32;
+    if (p->bits == 8) return s32 ? dispatch_bn_kch<8, 1>(p, scale, y) : dispatch_bn_kch<8, 0>(p, scale, y);
+    return s32 ? dispatch_bn_kch<4, 1>(p, scale, y) : dispatch_bn_kch<4, 0>(p, scale, y);
+}
+
+extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y,
+                                int warmup, int reps) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    if (warmup < 0 || reps < 1) return set_err(CONV_Q_EINVAL, "warmup >= 0 and reps >= 1 required");
+    int rc = ensure_device();
+    if (rc) return rc;
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    int best = -1;
+    float best_us = 0.f;
+    std::vector<float> ts(reps);
+    const int saved = p->sel;
+    for (int i = 0; i < (int)p->cands.size(); ++i) {
+        p->sel = i;
+        for (int k = 0; k < warmup; ++k)
+            if ((rc = conv_q_run(p, x, w, scale, y))) break;
+        if (rc) break;
+        for (int k = 0; k < reps; ++k) {
+            cudaEventRecord(e0, p->stream);
+            rc = conv_q_run(p, x, w, scale, y);
+            cudaEventRecord(e1, p->stream);
+            if (rc) break;
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            ts[k] = ms * 1000.f;
+        }
+        if (rc) break;
+        std::sort(ts.begin(), ts.end());
+        float med = ts[reps / 2];
+        if (best < 0 || med < best_us) {
+            best = i;
+            best_us = med;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc) {
+        p->sel = saved;
+        return rc;
+    }
+    cudaError_t e = cudaStreamSynchronize(p->stream);
+    if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "tuning run failed: %s", cudaGetErrorString(e));
+    p->sel = best;
+    p->tuned_us = best_us;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        cache_load_locked();
+        g_cache[shape_key(p)] = {cand_name(p, best), best_us};
+        cache_store_locked();
+    }
+    return best;
+}
+
+// ============================================================== quantize / pack
+extern "C" int conv_q_padded_channels(int C, int bits) {
+    if (C < 1 || (bits != 4 && bits != 8)) return set_err(CONV_Q_EINVAL, "C >= 1 and bits in {4,8} required");
+    return (C + 31) / 32 * 32;  // 32-channel granule (reading 14): >= 16-byte rows for s4 and s8
+}
+
+static int grid_for(int64_t items, int threads) {
+    const int sms = g_num_sms > 0 ? g_num_sms : 148;
+    int64_t blocks = ceil_div(items, threads);
+    int64_t cap = (int64_t)sms * 8;  // 8 resident 256-thread blocks per SM
+    return (int)std::max<int64_t>(1, std::min(blocks, cap));
+}
+
+extern "C" int conv_q_quantize(const void *x_fp16, int N, int H, int W, int C, float inv_scale, int bits, void *xq,
+                               void *stream) {
+    if (!x_fp16 || !xq) return set_err(CONV_Q_EINVAL, "NULL tensor pointer");
+    if (N < 1 || H < 1 || W < 1 || C < 1) return set_err(CONV_Q_EINVAL, "dimensions must be >= 1");
+    if (bits != 4 && bits != 8) return set_err(CONV_Q_EINVAL, "bits must be 4 or 8");
+    if (!aligned16(xq)) return set_err(CONV_Q_EINVAL, "xq must be 16-byte aligned");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int Cp = conv_q_padded_channels(C, bits);
+    const int64_t npix = (int64_t)N * H * W;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (Cp == C && aligned16(x_fp16)) {
+        const int64_t n_out_vec = npix * C * bits / 128;
+        const int grid = grid_for(ceil_div(n_out_vec, 4), 256);
+        if (bits == 8)
+            quantize_flat_kernel<8, 4><<<grid, 256, 0, st>>>(static_cast<const uint4 *>(x_fp16),
+                                                            static_cast<uint4 *>(xq), n_out_vec, inv_scale);
+        else
+            quantize_flat_kernel<4, 4><<<grid, 256, 0, st>>>(static_cast<const uint4 *>(x_fp16),
+                                                            static_cast<uint4 *>(xq), n_out_vec, inv_scale);
+    } else {
+        const int vec_per_pix = Cp * bits / 128;
+        const int grid = grid_for(npix * vec_per_pix, 256);
+        if (bits == 8)
+            quantize_padded_kernel<8><<<grid, 256, 0, st>>>(static_cast<const __half *>(x_fp16),
+                                                           static_cast<uint4 *>(xq), npix, C, vec_per_pix, inv_scale);
+        else
+            quantize_padded_kernel<4><<<grid, 256, 0, st>>>(static_cast<const __half *>(x_fp16),
+                                                           static_cast<uint4 *>(xq), npix, C, vec_per_pix, inv_scale);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return CONV_Q_OK;
+}
+
+extern "C" int conv_q_pack_weights(const int8_t *w, int K, int R, int S, int C, int bits, void *wp, void *stream) {
+    if (!w || !wp) return set_err(CONV_Q_EINVAL, "NULL tensor pointer");
+    if (K < 1 || R < 1 || S < 1 || C < 1) return set_err(CONV_Q_EINVAL, "dimensions must be >= 1");
+    if (bits != 4 && bits != 8) return set_err(CONV_Q_EINVAL, "bits must be 4 or 8");
+    if (((int64_t)C * bits) % 128) return set_err(CONV_Q_EUNSUPPORTED, "C*bits must be a multiple of 128");
+    if (!aligned16(w) || !aligned16(wp)) return set_err(CONV_Q_EINVAL, "pointers must be 16-byte aligned");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int64_t n_out_vec = (int64_t)K * R * S * C * bits / 128;
+    const int grid = grid_for(n_out_vec, 256);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (bits == 8)
+        pack_weights_kernel<8><<<grid, 256, 0, st>>>(w, static_cast<uint4 *>(wp), n_out_vec);
+    else
+        pack_weights_kernel<4><<<grid, 256, 0, st>>>(w, static_cast<uint4 *>(wp), n_out_vec);
+    CUDA_TRY(cudaGetLastError());
+    return CONV_Q_OK;
+}
+
+// ============================================================== peak
+extern "C" int conv_q_int8_peak(int iters, double *ops_per_s) {
+    if (iters < 1 || !ops_per_s) return set_err(CONV_Q_EINVAL, "iters >= 1 and non-NULL output required");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int smem = 1024 + (128 + 256) * 128 + 64;
+    CUDA_TRY(cudaFuncSetAttribute(int8_peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int *sink = nullptr;
+    CUDA_TRY(cudaMalloc(&sink, sizeof(int)));
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    int8_peak_kernel<<<g_num_sms, 128, smem>>>(std::min(iters, 1024), sink);  // warm-up
+    cudaEventRecord(e0);
+    int8_peak_kernel<<<g_num_sms, 128, smem>>>(iters, sink);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "peak kernel failed: %s", cudaGetErrorString(e));
+    *ops_per_s = 2.0 * 128 * 256 * 32 * (double)iters * g_num_sms / (ms * 1e-3);
+    return CONV_Q_OK;
+}

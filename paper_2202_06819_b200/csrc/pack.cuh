@@ -1,0 +1,156 @@
+// pack.cuh -- a1 activation quantize + pack (fp16 NHWC -> packed s8/s4 NHWC)
+// and a2 weight pack (int8 KRSC codes -> packed KRSC).
+//
+// PAPER.md:42 (section 1): "In the case of INT4 MMA, the packing includes
+// quantization of 8 consecutive values (in 32-bit) into a packed vector of
+// 4-bit elements. This low-level data alignment incurs noticeable overhead with
+// additional memory accesses."  The kernel is HBM-bound (2 + b/8 bytes per
+// element): every thread moves whole 16-byte vectors, loads first, grid sized
+// to a multiple of the SM count.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+
+namespace convq {
+
+// q = clamp(rne(fp32(x) * inv_scale), lo, hi); NaN -> lo (max.f32 returns the
+// non-NaN operand), +-inf saturate.  One binary32 multiply (no FMA), RNE.
+__device__ __forceinline__ int quant1(__half h, float inv_scale, float lo, float hi) {
+    float f = __half2float(h);
+    float v = __fmul_rn(f, inv_scale);
+    float r = rintf(v);
+    float c = fminf(fmaxf(r, lo), hi);
+    return __float2int_rz(c);
+}
+
+// 4 codes (int32 each, already in range) -> 4 bytes, code i in byte i.
+__device__ __forceinline__ uint32_t pack4_s8(int a, int b, int c, int d) {
+    uint32_t ab = __byte_perm((uint32_t)a, (uint32_t)b, 0x0040);
+    uint32_t cd = __byte_perm((uint32_t)c, (uint32_t)d, 0x0040);
+    return __byte_perm(ab, cd, 0x5410);
+}
+// 8 codes -> one 32-bit word, code i in bits [4i, 4i+4) (little-nibble-first).
+__device__ __forceinline__ uint32_t pack8_s4(const int (&q)[8]) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w |= ((uint32_t)q[i] & 0xFu) << (4 * i);
+    return w;
+}
+
+// Fast path: C == C' (no channel padding), so the packed tensor is the flat
+// element stream.  Each work item produces one 16-byte output vector:
+// 16 codes (s8, reads 32 B) or 32 codes (s4, reads 64 B).
+template <int BITS, int UNROLL>
+__global__ void __launch_bounds__(256) quantize_flat_kernel(const uint4 *__restrict__ x, uint4 *__restrict__ y,
+                                                           int64_t n_out_vec, float inv_scale) {
+    constexpr int IN_VEC = BITS == 8 ? 2 : 4;  // 16-byte fp16 vectors per output vector
+    const float lo = -(float)(1 << (BITS - 1)), hi = (float)((1 << (BITS - 1)) - 1);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < n_out_vec;
+         base += stride * UNROLL) {
+        uint4 in[UNROLL][IN_VEC];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            int64_t o = base + u * stride;
+            if (o < n_out_vec) {
+#pragma unroll
+                for (int v = 0; v < IN_VEC; ++v) in[u][v] = __ldcs(x + o * IN_VEC + v);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            int64_t o = base + u * stride;
+            if (o >= n_out_vec) break;
+            uint32_t out[4];
+            if constexpr (BITS == 8) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {  // 4 codes per output word
+                    const __half *h = reinterpret_cast<const __half *>(&in[u][k / 2]) + (k % 2) * 4;
+                    out[k] = pack4_s8(quant1(h[0], inv_scale, lo, hi), quant1(h[1], inv_scale, lo, hi),
+                                      quant1(h[2], inv_scale, lo, hi), quant1(h[3], inv_scale, lo, hi));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {  // 8 codes per output word = one input vector
+                    const __half *h = reinterpret_cast<const __half *>(&in[u][k]);
+                    int q[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) q[i] = quant1(h[i], inv_scale, lo, hi);
+                    out[k] = pack8_s4(q);
+                }
+            }
+            __stcs(y + o, make_uint4(out[0], out[1], out[2], out[3]));
+        }
+    }
+}
+
+// General path (C' > C, e.g. conv1's C=3 -> 16/32): one 16-byte output vector
+// per work item, scalar fp16 loads, padded channels written as code 0.
+template <int BITS>
+__global__ void __launch_bounds__(256) quantize_padded_kernel(const __half *__restrict__ x, uint4 *__restrict__ y,
+                                                             int64_t npix, int C, int vec_per_pix,
+                                                             float inv_scale) {
+    constexpr int CH = BITS == 8 ? 16 : 32;  // channels per output vector
+    const float lo = -(float)(1 << (BITS - 1)), hi = (float)((1 << (BITS - 1)) - 1);
+    const int64_t total = npix * vec_per_pix;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        int64_t pix = o / vec_per_pix;
+        int c0 = (int)(o - pix * vec_per_pix) * CH;
+        int q[CH];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            int c = c0 + i;
+            q[i] = c < C ? quant1(x[pix * C + c], inv_scale, lo, hi) : 0;
+        }
+        uint32_t out[4];
+        if constexpr (BITS == 8) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) out[k] = pack4_s8(q[4 * k], q[4 * k + 1], q[4 * k + 2], q[4 * k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int t[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) t[i] = q[8 * k + i];
+                out[k] = pack8_s4(t);
+            }
+        }
+        y[o] = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+}
+
+// a2: int8 codes [rows][C] -> packed [rows][C*BITS/8]; one 16-byte output
+// vector per work item (C*BITS % 128 == 0 is required by the caller).
+template <int BITS>
+__global__ void __launch_bounds__(256) pack_weights_kernel(const int8_t *__restrict__ w, uint4 *__restrict__ y,
+                                                          int64_t n_out_vec) {
+    constexpr int CH = BITS == 8 ? 16 : 32;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n_out_vec;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        const int8_t *src = w + o * CH;
+        uint32_t out[4];
+        if constexpr (BITS == 8) {
+            uint4 v = *reinterpret_cast<const uint4 *>(src);
+            out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+        } else {
+            uint4 v0 = *reinterpret_cast<const uint4 *>(src);
+            uint4 v1 = *reinterpret_cast<const uint4 *>(src + 16);
+            const int8_t *b0 = reinterpret_cast<const int8_t *>(&v0);
+            const int8_t *b1 = reinterpret_cast<const int8_t *>(&v1);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int t[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    int c = 8 * k + i;
+                    t[i] = c < 16 ? b0[c] : b1[c - 16];
+                }
+                out[k] = pack8_s4(t);
+            }
+        }
+        y[o] = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+}
+
+}  // namespace convq

@@ -60,11 +60,11 @@ def test_quantize_specials():
 
 
 def test_quantize_tensor_padding_and_layout():
-    """C=3 pads to C'=16 (s8) / 32 (s4) with zero codes; real channels equal
+    """C=3 pads to C'=32 (reading 14) with zero codes; real channels equal
     the scalar quantizer; pixel order is NHWC."""
     g = np.random.default_rng(1)
     x = g.standard_normal((2, 3, 5, 3)).astype(np.float16)
-    for bits, cp in ((8, 16), (4, 32)):
+    for bits, cp in ((8, 32), (4, 32)):
         assert oracle.padded_channels(3, bits) == cp
         xq = oracle.quantize(x, 7.0, bits)
         assert xq.shape == (2, 3, 5, cp * bits // 8)
