@@ -24,11 +24,12 @@
 // Warp roles (persistent CTA, one per SM):
 //   warp 0      TMA producer (one lane)
 //   warp 1      TMEM allocator + MMA issuer (one lane)
-//   warps 2..5  epilogue (128 threads = 128 TMEM lanes = BM rows)
-//   warps 6..9  INT4 only: s4 -> s8 transform
+//   warps 2..5  epilogue warpgroup 0 (128 threads = 128 TMEM lanes = BM rows)
+//   warps 6..9  epilogue warpgroup 1
+//   warps 10-13 INT4 only: s4 -> s8 transform
 // Pipelines: smem ring full/empty(/ready) mbarriers; TMEM double-buffered
-// accumulator acc_full/acc_empty so the epilogue of tile i overlaps the
-// mainloop of tile i+1.
+// accumulator acc_full/acc_empty; warpgroup e drains buffer e, so the
+// requantization of two tiles and the mainloop of a third overlap.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -65,13 +66,16 @@ struct ConvCfg {
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUT_SUBW = OUT_ROW < 128 ? OUT_ROW : 128;  // TMA store box width
     static constexpr int OUT_NSUB = OUT_ROW / OUT_SUBW;
-    static constexpr int OUT_BYTES = OUT_S32 ? 0 : BM * OUT_ROW;
+    static constexpr int OUT_BYTES = OUT_S32 ? 0 : BM * OUT_ROW;   // staging per epilogue warpgroup
+    static constexpr int NUM_EPI = 2;                               // epilogue warpgroups (one per TMEM buffer)
     static constexpr int BAR_BYTES = 1024;
-    static constexpr int STAGES_FIT = (SMEM_LIMIT - 1024 - BAR_BYTES - OUT_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES_FIT = (SMEM_LIMIT - 1024 - BAR_BYTES - NUM_EPI * OUT_BYTES) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + OUT_BYTES + BAR_BYTES;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NUM_EPI * OUT_BYTES + BAR_BYTES;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr int NUM_THREADS = BITS == 4 ? 320 : 192;
+    static constexpr int EPI_WARP0 = 2;                             // warps 2..9: epilogue WG0, WG1
+    static constexpr int XF_WARP0 = EPI_WARP0 + 4 * NUM_EPI;        // INT4 transform warps
+    static constexpr int NUM_THREADS = 32 * (XF_WARP0 + (BITS == 4 ? 4 : 0));
     static constexpr uint32_t IDESC = idesc_i8(BM, BN);
     static_assert(STAGES >= 2, "tile does not fit shared memory");
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
@@ -117,12 +121,31 @@ __device__ __forceinline__ void expand_tile(const uint8_t *src, uint8_t *dst, in
 }
 
 // Requantize (section 3.2.2; DESIGN readings 4-5):
-// y = clamp(rne(fmaf((float)acc, scale, shift)), lo, hi).
-__device__ __forceinline__ int requant1(int acc, float sc, float sh, float lo, float hi) {
+//   y = clamp(rne(fmaf((float)acc, scale, shift)), lo, hi)
+// computed without the quarter-rate FRND/F2I conversions: clamp first (the
+// bounds are integers, so clamp-then-round == round-then-clamp, and NaN -> lo
+// through max.f32 either way), then add 1.5*2^23: for |u| <= 2^22 the IEEE
+// add rounds u to the nearest integer (ties to even) and leaves it, two's
+// complement, in the low mantissa bits.  Returns those bits; the caller
+// takes the low byte / nibble as the packed code.
+constexpr float RNE_MAGIC = 12582912.0f;  // 1.5 * 2^23
+__device__ __forceinline__ uint32_t requant_bits(int acc, float sc, float sh, float lo, float hi) {
     float f = __int2float_rn(acc);
-    float v = __fmaf_rn(f, sc, sh);
-    float r = rintf(v);
-    return __float2int_rz(fminf(fmaxf(r, lo), hi));
+    float u = __fmaf_rn(f, sc, sh);
+    u = fminf(fmaxf(u, lo), hi);
+    return __float_as_uint(__fadd_rn(u, RNE_MAGIC));
+}
+// low bytes of four requant_bits results -> one packed s8 word
+__device__ __forceinline__ uint32_t pack4_low_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+// low nibbles of eight requant_bits results -> one packed s4 word
+__device__ __forceinline__ uint32_t pack8_low_nibbles(const uint32_t *r) {
+    uint32_t b01 = (r[0] & 0xFu) | ((r[1] << 4) & 0xF0u);
+    uint32_t b23 = (r[2] & 0xFu) | ((r[3] << 4) & 0xF0u);
+    uint32_t b45 = (r[4] & 0xFu) | ((r[5] << 4) & 0xF0u);
+    uint32_t b67 = (r[6] & 0xFu) | ((r[7] << 4) & 0xF0u);
+    return __byte_perm(__byte_perm(b01, b23, 0x0040), __byte_perm(b45, b67, 0x0040), 0x5410);
 }
 
 template <int BITS, int BN, int KCH, int OUT_S32>
@@ -139,8 +162,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
     uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][BN*KCH]
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][BM*KCH/2]
     uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][BN*KCH/2]
-    uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [OUT_NSUB][BM][OUT_SUBW]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(out_stage + Cfg::OUT_BYTES);
+    uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [NUM_EPI][OUT_NSUB][BM][OUT_SUBW]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(out_stage + Cfg::NUM_EPI * Cfg::OUT_BYTES);
     uint64_t *full = bars;                  // TMA -> (transform | MMA)
     uint64_t *empty = bars + STAGES;        // MMA -> TMA
     uint64_t *ready = bars + 2 * STAGES;    // transform -> MMA (INT4)
@@ -233,27 +256,30 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
                 mma_commit(&acc_full[buf]);  // accumulator ready for the epilogue
             }
         }
-    } else if (warp < 6) {
+    } else if (warp < Cfg::XF_WARP0) {
         // =========================== epilogue ===============================
+        // Warpgroup e owns TMEM accumulator buffer e and so every other tile;
+        // each has its own staging buffer, so one group's TMA store overlaps
+        // the other group's requantization.
+        const int e = (warp - Cfg::EPI_WARP0) >> 2;
         const int quad = warp & 3;              // TMEM lane quadrant this warp may access
         const int row = quad * 32 + lane;       // tile row = output pixel
-        const bool leader = (warp == 2 && lane == 0);
+        const bool leader = ((warp & 3) == (Cfg::EPI_WARP0 & 3)) && lane == 0;
+        uint8_t *stage_e = out_stage + e * Cfg::OUT_BYTES;
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
         const float hi = (float)((1 << (BITS - 1)) - 1);
-        int local = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+        int j = 0;
+        for (int tile = blockIdx.x + e * gridDim.x; tile < p.num_tiles; tile += 2 * gridDim.x, ++j) {
             const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
-            const int buf = local & 1;
-            const uint32_t aphase = (local >> 1) & 1;
             const int m = m_blk * BM + row;
             if (!OUT_S32) {
-                // staging buffer must have been read out by the previous TMA store
+                // this group's staging buffer must have been read out by its previous TMA store
                 if (leader) tma_store_wait_read0();
-                named_bar_sync(1, 128);
+                named_bar_sync(1 + e, 128);
             }
-            mbar_wait(&acc_full[buf], aphase);
+            mbar_wait(&acc_full[e], j & 1);
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + e * BN;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t v[32];
@@ -261,7 +287,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
                 if (c == BN / 32 - 1) {  // whole accumulator is in registers: hand TMEM back
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&acc_empty[buf]);
+                    if (lane == 0) mbar_arrive(&acc_empty[e]);
                 }
                 const int col0 = n_blk * BN + c * 32;
                 if (OUT_S32) {
@@ -269,84 +295,74 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
                         int32_t *dst = p.y32 + (int64_t)m * p.K + col0;
                         if (col0 + 32 <= p.K) {
 #pragma unroll
-                            for (int j = 0; j < 32; j += 4) {
+                            for (int q = 0; q < 32; q += 4) {
                                 int4 t;
-                                t.x = BITS == 4 ? ((int)v[j] >> 8) : (int)v[j];
-                                t.y = BITS == 4 ? ((int)v[j + 1] >> 8) : (int)v[j + 1];
-                                t.z = BITS == 4 ? ((int)v[j + 2] >> 8) : (int)v[j + 2];
-                                t.w = BITS == 4 ? ((int)v[j + 3] >> 8) : (int)v[j + 3];
-                                *reinterpret_cast<int4 *>(dst + j) = t;
+                                t.x = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
+                                t.y = BITS == 4 ? ((int)v[q + 1] >> 8) : (int)v[q + 1];
+                                t.z = BITS == 4 ? ((int)v[q + 2] >> 8) : (int)v[q + 2];
+                                t.w = BITS == 4 ? ((int)v[q + 3] >> 8) : (int)v[q + 3];
+                                *reinterpret_cast<int4 *>(dst + q) = t;
                             }
                         } else {
-                            for (int j = 0; j < 32 && col0 + j < p.K; ++j)
-                                dst[j] = BITS == 4 ? ((int)v[j] >> 8) : (int)v[j];
+                            for (int q = 0; q < 32 && col0 + q < p.K; ++q)
+                                dst[q] = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
                         }
                     }
                 } else {
-                    float sc[32], sh[32];
+                    uint32_t r[32];
                     if (col0 + 32 <= p.K) {
                         const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
                         const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            float4 a = __ldg(s4 + j), b = __ldg(h4 + j);
-                            sc[4 * j] = a.x; sc[4 * j + 1] = a.y; sc[4 * j + 2] = a.z; sc[4 * j + 3] = a.w;
-                            sh[4 * j] = b.x; sh[4 * j + 1] = b.y; sh[4 * j + 2] = b.z; sh[4 * j + 3] = b.w;
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 a = __ldg(s4 + q), b = __ldg(h4 + q);
+                            const int x0 = BITS == 4 ? ((int)v[4 * q] >> 8) : (int)v[4 * q];
+                            const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
+                            const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
+                            const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
+                            r[4 * q] = requant_bits(x0, a.x, b.x, lo, hi);
+                            r[4 * q + 1] = requant_bits(x1, a.y, b.y, lo, hi);
+                            r[4 * q + 2] = requant_bits(x2, a.z, b.z, lo, hi);
+                            r[4 * q + 3] = requant_bits(x3, a.w, b.w, lo, hi);
                         }
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            bool ok = col0 + j < p.K;
-                            sc[j] = ok ? __ldg(p.scale + col0 + j) : 0.f;
-                            sh[j] = ok ? __ldg(p.scale + p.K + col0 + j) : 0.f;
+                        for (int q = 0; q < 32; ++q) {
+                            const bool ok = col0 + q < p.K;  // columns past K are clipped by the TMA store
+                            const float sc = ok ? __ldg(p.scale + col0 + q) : 0.f;
+                            const float sh = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
+                            r[q] = requant_bits(BITS == 4 ? ((int)v[q] >> 8) : (int)v[q], sc, sh, lo, hi);
                         }
-                    }
-                    int q[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        int a = BITS == 4 ? ((int)v[j] >> 8) : (int)v[j];
-                        q[j] = requant1(a, sc[j], sh[j], lo, hi);
                     }
                     // packed bytes of this 32-column chunk: 32 (s8) or 16 (s4)
                     constexpr int CHUNK_BYTES = 32 * BITS / 8;
                     const int byte0 = c * CHUNK_BYTES;
-                    uint8_t *sub = out_stage + (byte0 / Cfg::OUT_SUBW) * (BM * Cfg::OUT_SUBW);
+                    uint8_t *sub = stage_e + (byte0 / Cfg::OUT_SUBW) * (BM * Cfg::OUT_SUBW);
                     const int inrow = byte0 % Cfg::OUT_SUBW;
                     if constexpr (BITS == 8) {
 #pragma unroll
                         for (int piece = 0; piece < 2; ++piece) {
-                            uint32_t w4[4];
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const int b = piece * 16 + 4 * k;
-                                uint32_t ab = __byte_perm((uint32_t)q[b], (uint32_t)q[b + 1], 0x0040);
-                                uint32_t cd = __byte_perm((uint32_t)q[b + 2], (uint32_t)q[b + 3], 0x0040);
-                                w4[k] = __byte_perm(ab, cd, 0x5410);
-                            }
+                            const uint32_t *rr = r + 16 * piece;
                             *reinterpret_cast<uint4 *>(sub + swz<Cfg::OUT_SUBW>(row * Cfg::OUT_SUBW + inrow + piece * 16)) =
-                                make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                                make_uint4(pack4_low_bytes(rr[0], rr[1], rr[2], rr[3]),
+                                           pack4_low_bytes(rr[4], rr[5], rr[6], rr[7]),
+                                           pack4_low_bytes(rr[8], rr[9], rr[10], rr[11]),
+                                           pack4_low_bytes(rr[12], rr[13], rr[14], rr[15]));
                         }
                     } else {
-                        uint32_t w4[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            uint32_t w = 0;
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) w |= ((uint32_t)q[8 * k + i] & 0xFu) << (4 * i);
-                            w4[k] = w;
-                        }
                         *reinterpret_cast<uint4 *>(sub + swz<Cfg::OUT_SUBW>(row * Cfg::OUT_SUBW + inrow)) =
-                            make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                            make_uint4(pack8_low_nibbles(r), pack8_low_nibbles(r + 8), pack8_low_nibbles(r + 16),
+                                       pack8_low_nibbles(r + 24));
                     }
                 }
             }
             if (!OUT_S32) {
                 fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
-                named_bar_sync(1, 128);
+                named_bar_sync(1 + e, 128);
                 if (leader) {
 #pragma unroll
                     for (int s = 0; s < Cfg::OUT_NSUB; ++s)
-                        tma_store_2d(&tm_y, out_stage + s * (BM * Cfg::OUT_SUBW), n_blk * Cfg::OUT_ROW + s * Cfg::OUT_SUBW,
+                        tma_store_2d(&tm_y, stage_e + s * (BM * Cfg::OUT_SUBW), n_blk * Cfg::OUT_ROW + s * Cfg::OUT_SUBW,
                                      m_blk * BM);
                     tma_store_commit();
                 }
@@ -356,7 +372,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
     } else {
         // =========================== INT4 transform =========================
         if constexpr (BITS == 4) {
-            const int tid = threadIdx.x - 192;  // 0..127
+            const int tid = threadIdx.x - 32 * Cfg::XF_WARP0;  // 0..127
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {

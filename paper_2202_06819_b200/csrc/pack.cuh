@@ -14,22 +14,25 @@
 namespace convq {
 
 // q = clamp(rne(fp32(x) * inv_scale), lo, hi); NaN -> lo (max.f32 returns the
-// non-NaN operand), +-inf saturate.  One binary32 multiply (no FMA), RNE.
+// non-NaN operand), +-inf saturate.  One binary32 multiply (no FMA).  The
+// rounding uses the 1.5*2^23 add after the clamp (integer bounds, so
+// clamp-then-round == round-then-clamp): the code is left in the low bits of
+// the returned word, which the packers below read as a byte / nibble.
 __device__ __forceinline__ int quant1(__half h, float inv_scale, float lo, float hi) {
     float f = __half2float(h);
     float v = __fmul_rn(f, inv_scale);
-    float r = rintf(v);
-    float c = fminf(fmaxf(r, lo), hi);
-    return __float2int_rz(c);
+    float c = fminf(fmaxf(v, lo), hi);
+    return __float_as_int(__fadd_rn(c, 12582912.0f));
 }
 
-// 4 codes (int32 each, already in range) -> 4 bytes, code i in byte i.
+// 4 codes (low byte of each word) -> 4 bytes, code i in byte i.
 __device__ __forceinline__ uint32_t pack4_s8(int a, int b, int c, int d) {
     uint32_t ab = __byte_perm((uint32_t)a, (uint32_t)b, 0x0040);
     uint32_t cd = __byte_perm((uint32_t)c, (uint32_t)d, 0x0040);
     return __byte_perm(ab, cd, 0x5410);
 }
-// 8 codes -> one 32-bit word, code i in bits [4i, 4i+4) (little-nibble-first).
+// 8 codes (low nibble of each word) -> one 32-bit word, code i in bits [4i, 4i+4)
+// (little-nibble-first).
 __device__ __forceinline__ uint32_t pack8_s4(const int (&q)[8]) {
     uint32_t w = 0;
 #pragma unroll

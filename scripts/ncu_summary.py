@@ -1,0 +1,43 @@
+"""Summarise an ncu --set full report: python scripts/ncu_summary.py gpurun_out/x.ncu-rep"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "sm__cycles_elapsed.avg", "launch__grid_size", "launch__block_size",
+    "launch__registers_per_thread", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_tensor_subpipe_imma.sum",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "lts__t_bytes.sum", "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum",
+    "smsp__inst_executed.sum",
+]
+
+
+def main(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, u = rows[0], rows[1]
+    for v in rows[2:]:
+        d = dict(zip(h, v))
+        un = dict(zip(h, u))
+        print("kernel:", d.get("Kernel Name", "")[:100])
+        for k in KEYS:
+            if k in d:
+                print(f"  {k:90s} {d[k]:>16s} {un.get(k, '')}")
+        stalls = [(k, float(d[k])) for k in d if k.startswith("smsp__average_warps_issue_stalled_") and
+                  k.endswith("_per_issue_active.ratio") and d[k] not in ("", "n/a")]
+        stalls.sort(key=lambda t: -t[1])
+        print("  top stalls (warps per issue-active):")
+        for k, val in stalls[:8]:
+            print(f"    {k.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):40s} {val:.3f}")
+
+
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        main(p)
