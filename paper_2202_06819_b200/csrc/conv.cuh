@@ -24,12 +24,12 @@
 // Warp roles (persistent CTA, one per SM):
 //   warp 0      TMA producer (one lane)
 //   warp 1      TMEM allocator + MMA issuer (one lane)
-//   warps 2..5  epilogue warpgroup 0 (128 threads = 128 TMEM lanes = BM rows)
-//   warps 6..9  epilogue warpgroup 1
-//   warps 10-13 INT4 only: s4 -> s8 transform
+//   warps 2..    epilogue: 4 warpgroups (INT8) / 2 (INT4), each warp owning the
+//                32 TMEM lanes (= tile rows = output pixels) of its quadrant
+//   last 4 warps INT4 only: s4 -> s8 transform
 // Pipelines: smem ring full/empty(/ready) mbarriers; TMEM double-buffered
-// accumulator acc_full/acc_empty; warpgroup e drains buffer e, so the
-// requantization of two tiles and the mainloop of a third overlap.
+// accumulator acc_full/acc_empty; buffer b is drained by its own warpgroups,
+// so the requantization of two tiles and the mainloop of a third overlap.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -66,14 +66,18 @@ struct ConvCfg {
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUT_SUBW = OUT_ROW < 128 ? OUT_ROW : 128;  // TMA store box width
     static constexpr int OUT_NSUB = OUT_ROW / OUT_SUBW;
-    static constexpr int OUT_BYTES = OUT_S32 ? 0 : BM * OUT_ROW;   // staging per epilogue warpgroup
-    static constexpr int NUM_EPI = 2;                               // epilogue warpgroups (one per TMEM buffer)
+    static constexpr int OUT_BYTES = OUT_S32 ? 0 : BM * OUT_ROW;   // staging per TMEM buffer
+    static constexpr int NUM_EPI = BITS == 8 ? 4 : 2;               // epilogue warpgroups
+    static constexpr int EPI_PER_BUF = NUM_EPI / 2;                 // warpgroups per TMEM buffer
+    static constexpr int EPI_COLS = BN / EPI_PER_BUF;               // columns one warpgroup drains
+    static constexpr int CW = BITS == 8 ? 16 : 32;                  // columns per tcgen05.ld (16 B packed)
+    static constexpr int SS_BYTES = OUT_S32 ? 0 : 2 * BN * 4;       // scale+shift of one n-block
     static constexpr int BAR_BYTES = 1024;
-    static constexpr int STAGES_FIT = (SMEM_LIMIT - 1024 - BAR_BYTES - NUM_EPI * OUT_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES_FIT = (SMEM_LIMIT - 1024 - BAR_BYTES - 2 * (OUT_BYTES + SS_BYTES)) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NUM_EPI * OUT_BYTES + BAR_BYTES;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 2 * (OUT_BYTES + SS_BYTES) + BAR_BYTES;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr int EPI_WARP0 = 2;                             // warps 2..9: epilogue WG0, WG1
+    static constexpr int EPI_WARP0 = 2;                             // warps 2..: epilogue warpgroups
     static constexpr int XF_WARP0 = EPI_WARP0 + 4 * NUM_EPI;        // INT4 transform warps
     static constexpr int NUM_THREADS = 32 * (XF_WARP0 + (BITS == 4 ? 4 : 0));
     static constexpr uint32_t IDESC = idesc_i8(BM, BN);
@@ -162,8 +166,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
     uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][BN*KCH]
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][BM*KCH/2]
     uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][BN*KCH/2]
-    uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [NUM_EPI][OUT_NSUB][BM][OUT_SUBW]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(out_stage + Cfg::NUM_EPI * Cfg::OUT_BYTES);
+    uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [2][OUT_NSUB][BM][OUT_SUBW]
+    float *ss_smem = reinterpret_cast<float *>(out_stage + 2 * Cfg::OUT_BYTES);  // [2][2*BN]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(out_stage + 2 * (Cfg::OUT_BYTES + Cfg::SS_BYTES));
     uint64_t *full = bars;                  // TMA -> (transform | MMA)
     uint64_t *empty = bars + STAGES;        // MMA -> TMA
     uint64_t *ready = bars + 2 * STAGES;    // transform -> MMA (INT4)
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 4);
+            mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF);
         }
         fence_mbar_init();
     }
@@ -258,44 +263,56 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
         }
     } else if (warp < Cfg::XF_WARP0) {
         // =========================== epilogue ===============================
-        // Warpgroup e owns TMEM accumulator buffer e and so every other tile;
-        // each has its own staging buffer, so one group's TMA store overlaps
-        // the other group's requantization.
+        // TMEM buffer b (every other tile) is drained by EPI_PER_BUF warpgroups,
+        // each owning EPI_COLS of its BN columns; each buffer has its own
+        // staging tile and scale/shift copy, so one buffer's TMA store and the
+        // other buffer's requantization overlap.
+        constexpr int EPB = Cfg::EPI_PER_BUF;
         const int e = (warp - Cfg::EPI_WARP0) >> 2;
-        const int quad = warp & 3;              // TMEM lane quadrant this warp may access
-        const int row = quad * 32 + lane;       // tile row = output pixel
-        const bool leader = ((warp & 3) == (Cfg::EPI_WARP0 & 3)) && lane == 0;
-        uint8_t *stage_e = out_stage + e * Cfg::OUT_BYTES;
+        const int b = e / EPB;                     // TMEM buffer
+        const int half = e % EPB;                  // column part
+        const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
+        const int row = quad * 32 + lane;          // tile row = output pixel
+        const int ptid = (e % EPB) * 128 + (threadIdx.x & 127);  // thread index within the buffer's group
+        const bool leader = ptid == 0;
+        const uint32_t bar_id = 1 + b, bar_n = 128 * EPB;
+        uint8_t *stage_b = out_stage + b * Cfg::OUT_BYTES;
+        float *ss_b = ss_smem + b * 2 * BN;
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
         const float hi = (float)((1 << (BITS - 1)) - 1);
         int j = 0;
-        for (int tile = blockIdx.x + e * gridDim.x; tile < p.num_tiles; tile += 2 * gridDim.x, ++j) {
+        for (int tile = blockIdx.x + b * gridDim.x; tile < p.num_tiles; tile += 2 * gridDim.x, ++j) {
             const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
             const int m = m_blk * BM + row;
             if (!OUT_S32) {
-                // this group's staging buffer must have been read out by its previous TMA store
-                if (leader) tma_store_wait_read0();
-                named_bar_sync(1 + e, 128);
+                if (leader) tma_store_wait_read0();   // staging of this buffer's previous tile read out
+                for (int i = ptid; i < 2 * BN; i += bar_n) {   // this n-block's scale and shift
+                    const int col = n_blk * BN + (i % BN);
+                    ss_b[i] = col < p.K ? __ldg(p.scale + (i < BN ? 0 : p.K) + col) : 0.f;
+                }
+                named_bar_sync(bar_id, bar_n);
             }
-            mbar_wait(&acc_full[e], j & 1);
+            mbar_wait(&acc_full[b], j & 1);
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + e * BN;
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + b * BN + half * Cfg::EPI_COLS;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(taddr + c * 32, v);  // includes tcgen05.wait::ld
-                if (c == BN / 32 - 1) {  // whole accumulator is in registers: hand TMEM back
+            for (int c = 0; c < Cfg::EPI_COLS / Cfg::CW; ++c) {
+                uint32_t v[Cfg::CW];
+                if constexpr (Cfg::CW == 16) tmem_ld_32x32b_x16(taddr + c * Cfg::CW, v);
+                else tmem_ld_32x32b_x32(taddr + c * Cfg::CW, v);
+                if (c == Cfg::EPI_COLS / Cfg::CW - 1) {  // this group's columns are in registers
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&acc_empty[e]);
+                    if (lane == 0) mbar_arrive(&acc_empty[b]);
                 }
-                const int col0 = n_blk * BN + c * 32;
+                const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
+                const int col0 = n_blk * BN + ccol;
                 if (OUT_S32) {
                     if (m < p.M) {
                         int32_t *dst = p.y32 + (int64_t)m * p.K + col0;
-                        if (col0 + 32 <= p.K) {
+                        if (col0 + Cfg::CW <= p.K) {
 #pragma unroll
-                            for (int q = 0; q < 32; q += 4) {
+                            for (int q = 0; q < Cfg::CW; q += 4) {
                                 int4 t;
                                 t.x = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
                                 t.y = BITS == 4 ? ((int)v[q + 1] >> 8) : (int)v[q + 1];
@@ -304,65 +321,49 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
                                 *reinterpret_cast<int4 *>(dst + q) = t;
                             }
                         } else {
-                            for (int q = 0; q < 32 && col0 + q < p.K; ++q)
+                            for (int q = 0; q < Cfg::CW && col0 + q < p.K; ++q)
                                 dst[q] = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
                         }
                     }
                 } else {
-                    uint32_t r[32];
-                    if (col0 + 32 <= p.K) {
-                        const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
-                        const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
+                    uint32_t r[Cfg::CW];
+                    const float4 *s4 = reinterpret_cast<const float4 *>(ss_b + ccol);
+                    const float4 *h4 = reinterpret_cast<const float4 *>(ss_b + BN + ccol);
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float4 a = __ldg(s4 + q), b = __ldg(h4 + q);
-                            const int x0 = BITS == 4 ? ((int)v[4 * q] >> 8) : (int)v[4 * q];
-                            const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
-                            const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
-                            const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
-                            r[4 * q] = requant_bits(x0, a.x, b.x, lo, hi);
-                            r[4 * q + 1] = requant_bits(x1, a.y, b.y, lo, hi);
-                            r[4 * q + 2] = requant_bits(x2, a.z, b.z, lo, hi);
-                            r[4 * q + 3] = requant_bits(x3, a.w, b.w, lo, hi);
-                        }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 32; ++q) {
-                            const bool ok = col0 + q < p.K;  // columns past K are clipped by the TMA store
-                            const float sc = ok ? __ldg(p.scale + col0 + q) : 0.f;
-                            const float sh = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
-                            r[q] = requant_bits(BITS == 4 ? ((int)v[q] >> 8) : (int)v[q], sc, sh, lo, hi);
-                        }
+                    for (int q = 0; q < Cfg::CW / 4; ++q) {
+                        const float4 sa = s4[q], sb = h4[q];
+                        const int x0 = BITS == 4 ? ((int)v[4 * q] >> 8) : (int)v[4 * q];
+                        const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
+                        const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
+                        const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
+                        r[4 * q] = requant_bits(x0, sa.x, sb.x, lo, hi);
+                        r[4 * q + 1] = requant_bits(x1, sa.y, sb.y, lo, hi);
+                        r[4 * q + 2] = requant_bits(x2, sa.z, sb.z, lo, hi);
+                        r[4 * q + 3] = requant_bits(x3, sa.w, sb.w, lo, hi);
                     }
-                    // packed bytes of this 32-column chunk: 32 (s8) or 16 (s4)
-                    constexpr int CHUNK_BYTES = 32 * BITS / 8;
-                    const int byte0 = c * CHUNK_BYTES;
-                    uint8_t *sub = stage_e + (byte0 / Cfg::OUT_SUBW) * (BM * Cfg::OUT_SUBW);
+                    // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
+                    const int byte0 = ccol * BITS / 8;
+                    uint8_t *sub = stage_b + (byte0 / Cfg::OUT_SUBW) * (BM * Cfg::OUT_SUBW);
                     const int inrow = byte0 % Cfg::OUT_SUBW;
+                    uint4 pk;
                     if constexpr (BITS == 8) {
-#pragma unroll
-                        for (int piece = 0; piece < 2; ++piece) {
-                            const uint32_t *rr = r + 16 * piece;
-                            *reinterpret_cast<uint4 *>(sub + swz<Cfg::OUT_SUBW>(row * Cfg::OUT_SUBW + inrow + piece * 16)) =
-                                make_uint4(pack4_low_bytes(rr[0], rr[1], rr[2], rr[3]),
-                                           pack4_low_bytes(rr[4], rr[5], rr[6], rr[7]),
-                                           pack4_low_bytes(rr[8], rr[9], rr[10], rr[11]),
-                                           pack4_low_bytes(rr[12], rr[13], rr[14], rr[15]));
-                        }
+                        pk = make_uint4(pack4_low_bytes(r[0], r[1], r[2], r[3]), pack4_low_bytes(r[4], r[5], r[6], r[7]),
+                                        pack4_low_bytes(r[8], r[9], r[10], r[11]),
+                                        pack4_low_bytes(r[12], r[13], r[14], r[15]));
                     } else {
-                        *reinterpret_cast<uint4 *>(sub + swz<Cfg::OUT_SUBW>(row * Cfg::OUT_SUBW + inrow)) =
-                            make_uint4(pack8_low_nibbles(r), pack8_low_nibbles(r + 8), pack8_low_nibbles(r + 16),
-                                       pack8_low_nibbles(r + 24));
+                        pk = make_uint4(pack8_low_nibbles(r), pack8_low_nibbles(r + 8), pack8_low_nibbles(r + 16),
+                                        pack8_low_nibbles(r + 24));
                     }
+                    *reinterpret_cast<uint4 *>(sub + swz<Cfg::OUT_SUBW>(row * Cfg::OUT_SUBW + inrow)) = pk;
                 }
             }
             if (!OUT_S32) {
                 fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
-                named_bar_sync(1 + e, 128);
+                named_bar_sync(bar_id, bar_n);
                 if (leader) {
 #pragma unroll
                     for (int s = 0; s < Cfg::OUT_NSUB; ++s)
-                        tma_store_2d(&tm_y, stage_e + s * (BM * Cfg::OUT_SUBW), n_blk * Cfg::OUT_ROW + s * Cfg::OUT_SUBW,
+                        tma_store_2d(&tm_y, stage_b + s * (BM * Cfg::OUT_SUBW), n_blk * Cfg::OUT_ROW + s * Cfg::OUT_SUBW,
                                      m_blk * BM);
                     tma_store_commit();
                 }
