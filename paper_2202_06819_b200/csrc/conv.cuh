@@ -32,6 +32,7 @@
 // so the requantization of two tiles and the mainloop of a third overlap.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda.h>
 #include "ptx.cuh"
 
@@ -50,19 +51,24 @@ struct ConvParams {
     int n_tiles;    // ceil(K / BN)
     int num_tiles;  // m_tiles * n_tiles
     int relu;
+    int cvt_magic;       // |acc| <= 2^22 guaranteed: int->float via the 1.5*2^23 add (FMA pipe)
+    int one;             // = 1, opaque to the compiler (keeps an integer add on the FMA pipe)
     const float *scale;  // [2K] scale then shift
     int32_t *y32;        // s32 output (OUT_S32)
 };
 
-template <int BITS, int BN, int KCH, int OUT_S32>
+template <int BITS, int BN, int KCH, int OUT_S32, int CG>
 struct ConvCfg {
+    // CG = CTAs per tile (1, or 2 = a CTA pair running tcgen05.mma.cta_group::2
+    // with M = 256: each CTA stages its own 128 A rows and BN/2 B rows).
+    static constexpr int BNL = BN / CG;                     // B rows staged per CTA
     static constexpr int LOAD_ROW = KCH * BITS / 8;        // packed bytes per row per k-block
     static constexpr int A_S8 = BM * KCH;                   // s8 A tile bytes
-    static constexpr int B_S8 = BN * KCH;
+    static constexpr int B_S8 = BNL * KCH;
     static constexpr int A_PK = BITS == 4 ? BM * LOAD_ROW : 0;
-    static constexpr int B_PK = BITS == 4 ? BN * LOAD_ROW : 0;
+    static constexpr int B_PK = BITS == 4 ? BNL * LOAD_ROW : 0;
     static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
-    static constexpr int STAGE_TX = (BM + BN) * LOAD_ROW;    // TMA bytes per stage
+    static constexpr int STAGE_TX = (BM + BNL) * LOAD_ROW;   // TMA bytes per stage per CTA
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUT_SUBW = OUT_ROW < 128 ? OUT_ROW : 128;  // TMA store box width
     static constexpr int OUT_NSUB = OUT_ROW / OUT_SUBW;
@@ -74,16 +80,17 @@ struct ConvCfg {
     static constexpr int SS_BYTES = OUT_S32 ? 0 : 2 * BN * 4;       // scale+shift of one n-block
     static constexpr int BAR_BYTES = 1024;
     static constexpr int STAGES_FIT = (SMEM_LIMIT - 1024 - BAR_BYTES - 2 * (OUT_BYTES + SS_BYTES)) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 2 * (OUT_BYTES + SS_BYTES) + BAR_BYTES;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr int EPI_WARP0 = 2;                             // warps 2..: epilogue warpgroups
     static constexpr int XF_WARP0 = EPI_WARP0 + 4 * NUM_EPI;        // INT4 transform warps
     static constexpr int NUM_THREADS = 32 * (XF_WARP0 + (BITS == 4 ? 4 : 0));
-    static constexpr uint32_t IDESC = idesc_i8(BM, BN);
+    static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
     static_assert(STAGES >= 2, "tile does not fit shared memory");
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
-    static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+    static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
+    static_assert(CG == 1 || CG == 2, "CG");
     static_assert(TMEM_COLS <= 512, "TMEM");
 };
 
@@ -133,8 +140,19 @@ __device__ __forceinline__ void expand_tile(const uint8_t *src, uint8_t *dst, in
 // complement, in the low mantissa bits.  Returns those bits; the caller
 // takes the low byte / nibble as the packed code.
 constexpr float RNE_MAGIC = 12582912.0f;  // 1.5 * 2^23
-__device__ __forceinline__ uint32_t requant_bits(int acc, float sc, float sh, float lo, float hi) {
-    float f = __int2float_rn(acc);
+// (float)acc, exact, for |acc| <= 2^22: the word 0x4B400000 + acc is the
+// float 1.5*2^23 + acc; subtracting 1.5*2^23 is exact.  Both steps run on the
+// FMA pipe (integer multiply-add by a runtime 1 that the compiler cannot fold
+// into an ALU add, then a float add) instead of one ALU-pipe I2FP: the
+// epilogue is ALU-bound (FMNMX clamps, PRMT packing).
+__device__ __forceinline__ float small_int_to_float(int acc, int one) {
+    int w;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(w) : "r"(acc), "r"(one), "r"(0x4B400000));
+    return __fsub_rn(__int_as_float(w), RNE_MAGIC);
+}
+template <bool MAGIC>
+__device__ __forceinline__ uint32_t requant_bits(int acc, float sc, float sh, float lo, float hi, int one) {
+    float f = MAGIC ? small_int_to_float(acc, one) : __int2float_rn(acc);
     float u = __fmaf_rn(f, sc, sh);
     u = fminf(fmaxf(u, lo), hi);
     return __float_as_uint(__fadd_rn(u, RNE_MAGIC));
@@ -152,20 +170,23 @@ __device__ __forceinline__ uint32_t pack8_low_nibbles(const uint32_t *r) {
     return __byte_perm(__byte_perm(b01, b23, 0x0040), __byte_perm(b45, b67, 0x0040), 0x5410);
 }
 
-template <int BITS, int BN, int KCH, int OUT_S32>
-__global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 1)
+template <int BITS, int BN, int KCH, int OUT_S32, int CG>
+__global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREADS, 1)
     conv_igemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_y, const ConvParams p) {
-    using Cfg = ConvCfg<BITS, BN, KCH, OUT_S32>;
+    using Cfg = ConvCfg<BITS, BN, KCH, OUT_S32, CG>;
     constexpr int STAGES = Cfg::STAGES;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment by offset (pointer arithmetic on the shared array keeps
+    // the compiler's shared-space inference: LDS/STS instead of generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
 
-    // ---- carve shared memory (every tile 1024-byte aligned)
+    // ---- carve shared memory (every tile 1024-byte aligned; identical offsets
+    // in both CTAs of a pair, as cta_group::2 descriptors require)
     uint8_t *a_s8 = smem;                               // [STAGES][BM*KCH]
-    uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][BN*KCH]
+    uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][BNL*KCH]
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][BM*KCH/2]
-    uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][BN*KCH/2]
+    uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][BNL*KCH/2]
     uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [2][OUT_NSUB][BM][OUT_SUBW]
     float *ss_smem = reinterpret_cast<float *>(out_stage + 2 * Cfg::OUT_BYTES);  // [2][2*BN]
     uint64_t *bars = reinterpret_cast<uint64_t *>(out_stage + 2 * (Cfg::OUT_BYTES + Cfg::SS_BYTES));
@@ -178,6 +199,13 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;     // position in the CTA pair
+    const int tile0 = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
+    const int tstep = CG == 2 ? (int)num_clusters_x() : (int)gridDim.x;
+    // INT8 pairs count both CTAs' TMA bytes on the leader's full barrier; INT4
+    // pairs expand locally, then both CTAs' transform warps arrive on the
+    // leader's ready barrier.
+    constexpr bool PAIR_TX = CG == 2 && BITS == 8;
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tm_a);
@@ -186,17 +214,21 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
-            mbar_init(&ready[s], 4);
+            mbar_init(&ready[s], 4 * CG);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF);
+            mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF * CG);
         }
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
+    if (warp == 1) {
+        if constexpr (CG == 2) tmem_alloc_cg2<Cfg::TMEM_COLS>(tmem_holder);
+        else tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
+    }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync();   // barriers of both CTAs initialised before any remote use
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
@@ -213,33 +245,45 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
             constexpr int B_LD = BITS == 4 ? Cfg::B_PK : Cfg::B_S8;
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
                 const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
-                const int m0 = m_blk * BM;
+                const int m0 = m_blk * (BM * CG) + (int)rank * BM;   // this CTA's first output pixel
                 const int n0 = m0 / PQ, rem = m0 - n0 * PQ;
                 const int p0 = rem / p.Q, q0 = rem - p0 * p.Q;
                 const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad;
-                int tap = 0, cblk = 0;
+                const int brow = n_blk * BN + (int)rank * Cfg::BNL;  // this CTA's B rows
+                int r = 0, s = 0, cblk = 0, kcol = 0;
                 for (int kb = 0; kb < p.num_kb; ++kb) {
-                    const int r = tap / p.S, s = tap - r * p.S;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_TX);
-                    tma_load_im2col_4d(a_dst + stage * A_LD, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0,
-                                       (uint16_t)s, (uint16_t)r, pol_a);
-                    tma_load_2d(b_dst + stage * B_LD, &tm_b, &full[stage], tap * p.row_bytes + cblk * Cfg::LOAD_ROW,
-                                n_blk * BN, pol_b);
+                    if constexpr (PAIR_TX) {
+                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_TX);
+                        tma_load_im2col_4d_cg2(a_dst + stage * A_LD, &tm_a, fb, cblk * Cfg::LOAD_ROW, w0, h0, n0,
+                                               (uint16_t)s, (uint16_t)r, pol_a);
+                        tma_load_2d_cg2(b_dst + stage * B_LD, &tm_b, fb, kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_TX);
+                        tma_load_im2col_4d(a_dst + stage * A_LD, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0,
+                                           (uint16_t)s, (uint16_t)r, pol_a);
+                        tma_load_2d(b_dst + stage * B_LD, &tm_b, &full[stage], kcol + cblk * Cfg::LOAD_ROW, brow,
+                                    pol_b);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                    if (++cblk == p.num_cblk) { cblk = 0; ++tap; }
+                    if (++cblk == p.num_cblk) {            // next filter tap (r, s)
+                        cblk = 0;
+                        kcol += p.row_bytes;
+                        if (++s == p.S) { s = 0; ++r; }
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         // =========================== MMA issuer =============================
-        if (lane == 0) {
+        if (lane == 0 && rank == 0) {
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++local) {
+            for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++local) {
                 const int buf = local & 1;
                 const uint32_t aphase = (local >> 1) & 1;
                 mbar_wait(&acc_empty[buf], aphase ^ 1);
@@ -252,13 +296,19 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
                     const uint32_t b_addr = smem_u32(b_s8 + stage * Cfg::B_S8);
 #pragma unroll
                     for (int k = 0; k < KCH / 32; ++k) {
-                        mma_i8(d_tmem, umma_desc_kmajor(a_addr + 32 * k, KCH), umma_desc_kmajor(b_addr + 32 * k, KCH),
-                               Cfg::IDESC, (kb | k) != 0);
+                        const uint64_t ad = umma_desc_kmajor(a_addr + 32 * k, KCH);
+                        const uint64_t bd = umma_desc_kmajor(b_addr + 32 * k, KCH);
+                        if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad, bd, Cfg::IDESC, (kb | k) != 0);
+                        else mma_i8(d_tmem, ad, bd, Cfg::IDESC, (kb | k) != 0);
                     }
-                    mma_commit(&empty[stage]);  // frees the smem stage when these MMAs complete
+                    // frees the smem stage (in both CTAs) when these MMAs complete
+                    if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
+                    else mma_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(&acc_full[buf]);  // accumulator ready for the epilogue
+                // accumulator ready for the epilogue (of both CTAs)
+                if constexpr (CG == 2) mma_commit_cg2_mc(&acc_full[buf], 0x3);
+                else mma_commit(&acc_full[buf]);
             }
         }
     } else if (warp < Cfg::XF_WARP0) {
@@ -266,7 +316,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
         // TMEM buffer b (every other tile) is drained by EPI_PER_BUF warpgroups,
         // each owning EPI_COLS of its BN columns; each buffer has its own
         // staging tile and scale/shift copy, so one buffer's TMA store and the
-        // other buffer's requantization overlap.
+        // other buffer's requantization overlap.  In a CTA pair each CTA drains
+        // its own 128 rows (its TMEM half) and releases the leader's buffer.
         constexpr int EPB = Cfg::EPI_PER_BUF;
         const int e = (warp - Cfg::EPI_WARP0) >> 2;
         const int b = e / EPB;                     // TMEM buffer
@@ -278,12 +329,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
         const uint32_t bar_id = 1 + b, bar_n = 128 * EPB;
         uint8_t *stage_b = out_stage + b * Cfg::OUT_BYTES;
         float *ss_b = ss_smem + b * 2 * BN;
+        const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(&acc_empty[b]), 0) : 0;
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
         const float hi = (float)((1 << (BITS - 1)) - 1);
+        const int one = p.one;
         int j = 0;
-        for (int tile = blockIdx.x + b * gridDim.x; tile < p.num_tiles; tile += 2 * gridDim.x, ++j) {
+        for (int tile = tile0 + b * tstep; tile < p.num_tiles; tile += 2 * tstep, ++j) {
             const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
-            const int m = m_blk * BM + row;
+            const int mrow0 = m_blk * (BM * CG) + (int)rank * BM;
+            const int m = mrow0 + row;
             if (!OUT_S32) {
                 if (leader) tma_store_wait_read0();   // staging of this buffer's previous tile read out
                 for (int i = ptid; i < 2 * BN; i += bar_n) {   // this n-block's scale and shift
@@ -303,7 +357,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
                 if (c == Cfg::EPI_COLS / Cfg::CW - 1) {  // this group's columns are in registers
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&acc_empty[b]);
+                    if (lane == 0) {
+                        if constexpr (CG == 2) mbar_arrive_cluster(acc_empty_leader);
+                        else mbar_arrive(&acc_empty[b]);
+                    }
                 }
                 const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
                 const int col0 = n_blk * BN + ccol;
@@ -329,18 +386,22 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
                     uint32_t r[Cfg::CW];
                     const float4 *s4 = reinterpret_cast<const float4 *>(ss_b + ccol);
                     const float4 *h4 = reinterpret_cast<const float4 *>(ss_b + BN + ccol);
+                    auto requant_chunk = [&](auto magic) {
 #pragma unroll
-                    for (int q = 0; q < Cfg::CW / 4; ++q) {
-                        const float4 sa = s4[q], sb = h4[q];
-                        const int x0 = BITS == 4 ? ((int)v[4 * q] >> 8) : (int)v[4 * q];
-                        const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
-                        const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
-                        const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
-                        r[4 * q] = requant_bits(x0, sa.x, sb.x, lo, hi);
-                        r[4 * q + 1] = requant_bits(x1, sa.y, sb.y, lo, hi);
-                        r[4 * q + 2] = requant_bits(x2, sa.z, sb.z, lo, hi);
-                        r[4 * q + 3] = requant_bits(x3, sa.w, sb.w, lo, hi);
-                    }
+                        for (int q = 0; q < Cfg::CW / 4; ++q) {
+                            const float4 sa = s4[q], sb = h4[q];
+                            const int x0 = BITS == 4 ? ((int)v[4 * q] >> 8) : (int)v[4 * q];
+                            const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
+                            const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
+                            const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
+                            r[4 * q] = requant_bits<decltype(magic)::value>(x0, sa.x, sb.x, lo, hi, one);
+                            r[4 * q + 1] = requant_bits<decltype(magic)::value>(x1, sa.y, sb.y, lo, hi, one);
+                            r[4 * q + 2] = requant_bits<decltype(magic)::value>(x2, sa.z, sb.z, lo, hi, one);
+                            r[4 * q + 3] = requant_bits<decltype(magic)::value>(x3, sa.w, sb.w, lo, hi, one);
+                        }
+                    };
+                    if (p.cvt_magic) requant_chunk(std::true_type{});
+                    else requant_chunk(std::false_type{});
                     // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
                     const int byte0 = ccol * BITS / 8;
                     uint8_t *sub = stage_b + (byte0 / Cfg::OUT_SUBW) * (BM * Cfg::OUT_SUBW);
@@ -364,7 +425,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
 #pragma unroll
                     for (int s = 0; s < Cfg::OUT_NSUB; ++s)
                         tma_store_2d(&tm_y, stage_b + s * (BM * Cfg::OUT_SUBW), n_blk * Cfg::OUT_ROW + s * Cfg::OUT_SUBW,
-                                     m_blk * BM);
+                                     mrow0);
                     tma_store_commit();
                 }
             }
@@ -374,16 +435,20 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
         // =========================== INT4 transform =========================
         if constexpr (BITS == 4) {
             const int tid = threadIdx.x - 32 * Cfg::XF_WARP0;  // 0..127
+            const uint32_t ready0 = CG == 2 ? mapa_shared(smem_u32(&ready[0]), 0) : 0;
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     expand_tile<KCH>(a_pk + stage * Cfg::A_PK, a_s8 + stage * Cfg::A_S8, BM, tid, 128);
-                    expand_tile<KCH>(b_pk + stage * Cfg::B_PK, b_s8 + stage * Cfg::B_S8, BN, tid, 128);
+                    expand_tile<KCH>(b_pk + stage * Cfg::B_PK, b_s8 + stage * Cfg::B_S8, Cfg::BNL, tid, 128);
                     fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.mma
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&ready[stage]);
+                    if (lane == 0) {
+                        if constexpr (CG == 2) mbar_arrive_cluster(ready0 + 8u * stage);
+                        else mbar_arrive(&ready[stage]);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -391,10 +456,12 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32>::NUM_THREADS, 
     }
 
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync();   // the pair's MMAs and remote arrivals are complete
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+        if constexpr (CG == 2) tmem_dealloc_cg2<Cfg::TMEM_COLS>(tmem_base);
+        else tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
     }
 }
 

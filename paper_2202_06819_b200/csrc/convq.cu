@@ -113,7 +113,7 @@ static CUtensorMapSwizzle swizzle_for(int span) {
 
 // ============================================================== plan
 struct Cand {
-    int bn, kch;
+    int bn, kch, cg;  // N tile, K chunk (channels per k-block), CTAs per tile
 };
 
 struct conv_q_plan_s {
@@ -135,7 +135,8 @@ struct conv_q_plan_s {
 
 static std::string cand_name(const conv_q_plan_s *p, int i) {
     char b[64];
-    snprintf(b, sizeof b, "bm128_bn%d_kc%d_c1", p->cands[i].bn, p->cands[i].kch);
+    snprintf(b, sizeof b, "bm%d_bn%d_kc%d_c%d", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
+             p->cands[i].cg);
     return b;
 }
 
@@ -187,13 +188,14 @@ static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 static void enumerate_candidates(conv_q_plan_s *p) {
     p->cands.clear();
-    for (int kch : {128, 64, 32}) {
-        if (p->C % kch) continue;
-        for (int bn : {64, 128, 256}) {
-            if (bn > 64 && bn / 2 >= p->K) continue;  // a narrower tile already covers K
-            p->cands.push_back({bn, kch});
+    for (int cg : {1, 2})
+        for (int kch : {128, 64, 32}) {
+            if (p->C % kch) continue;
+            for (int bn : {64, 128, 256}) {
+                if (bn > 64 && bn / 2 >= p->K) continue;  // a narrower tile already covers K
+                p->cands.push_back({bn, kch, cg});
+            }
         }
-    }
 }
 
 // Default pick before tuning: deepest K chunk, then the widest N tile whose
@@ -204,7 +206,7 @@ static int default_candidate(const conv_q_plan_s *p) {
     int pick = -1, narrow = -1;
     for (size_t i = 0; i < p->cands.size(); ++i) {
         const Cand &c = p->cands[i];
-        if (c.kch != p->cands[0].kch) continue;
+        if (c.kch != p->cands[0].kch || c.cg != 1) continue;
         if (narrow < 0 || c.bn < p->cands[narrow].bn) narrow = (int)i;
         if (m_tiles * ceil_div(p->K, c.bn) >= sms && (pick < 0 || c.bn > p->cands[pick].bn)) pick = (int)i;
     }
@@ -362,10 +364,10 @@ extern "C" int conv_q_plan_info(const conv_q_plan_t *p, conv_q_info_t *info) {
 }
 
 // ============================================================== launch
-template <int BITS, int BN, int KCH, int OUT>
+template <int BITS, int BN, int KCH, int OUT, int CG>
 static int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
-    using Cfg = ConvCfg<BITS, BN, KCH, OUT>;
-    auto kern = conv_igemm_kernel<BITS, BN, KCH, OUT>;
+    using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG>;
+    auto kern = conv_igemm_kernel<BITS, BN, KCH, OUT, CG>;
     static bool attr_set = false;
     if (!attr_set) {
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
@@ -378,26 +380,44 @@ static int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.num_cblk = p->C / KCH;
     prm.num_kb = p->R * p->S * prm.num_cblk;
     prm.n_tiles = (int)ceil_div(p->K, BN);
-    prm.num_tiles = (int)(ceil_div(p->M, BM) * prm.n_tiles);
+    prm.num_tiles = (int)(ceil_div(p->M, BM * CG) * prm.n_tiles);
     prm.relu = p->relu;
+    // |acc| <= R*S*C*2^14 (s8 codes; INT4 after the >>8) -- the plan's guard
+    // arithmetic; the magic int->float is exact up to 2^22.
+    prm.cvt_magic = (BITS == 4 || p->Kg * 16384 <= (int64_t)(1 << 22)) ? 1 : 0;
+    prm.one = 1;
     prm.scale = scale;
     prm.y32 = static_cast<int32_t *>(y);
-    const int grid = std::min(prm.num_tiles, g_num_sms);
-    kern<<<grid, Cfg::NUM_THREADS, Cfg::SMEM, p->stream>>>(p->tm_a, p->tm_b, p->tm_y, prm);
-    CUDA_TRY(cudaGetLastError());
+    const int clusters = std::min(prm.num_tiles, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * CG);
+    cfg.blockDim = dim3(Cfg::NUM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = p->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p->tm_a, p->tm_b, p->tm_y, prm));
     return CONV_Q_OK;
 }
 
 template <int BITS, int OUT>
 static int dispatch_bn_kch(conv_q_plan_s *p, const float *scale, void *y) {
     const Cand c = p->cands[p->sel];
-#define CONVQ_CASE(BN_, KC_) \
-    if (c.bn == BN_ && c.kch == KC_) return launch_conv<BITS, BN_, KC_, OUT>(p, scale, y);
-    CONVQ_CASE(64, 128) CONVQ_CASE(128, 128) CONVQ_CASE(256, 128)
-    CONVQ_CASE(64, 64) CONVQ_CASE(128, 64) CONVQ_CASE(256, 64)
-    CONVQ_CASE(64, 32) CONVQ_CASE(128, 32) CONVQ_CASE(256, 32)
+#define CONVQ_CASE(BN_, KC_, CG_) \
+    if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_) return launch_conv<BITS, BN_, KC_, OUT, CG_>(p, scale, y);
+    CONVQ_CASE(64, 128, 1) CONVQ_CASE(128, 128, 1) CONVQ_CASE(256, 128, 1)
+    CONVQ_CASE(64, 64, 1) CONVQ_CASE(128, 64, 1) CONVQ_CASE(256, 64, 1)
+    CONVQ_CASE(64, 32, 1) CONVQ_CASE(128, 32, 1) CONVQ_CASE(256, 32, 1)
+    CONVQ_CASE(64, 128, 2) CONVQ_CASE(128, 128, 2) CONVQ_CASE(256, 128, 2)
+    CONVQ_CASE(64, 64, 2) CONVQ_CASE(128, 64, 2) CONVQ_CASE(256, 64, 2)
+    CONVQ_CASE(64, 32, 2) CONVQ_CASE(128, 32, 2) CONVQ_CASE(256, 32, 2)
 #undef CONVQ_CASE
-    return set_err(CONV_Q_EUNSUPPORTED, "no kernel instantiation for bn=%d kch=%d", c.bn, c.kch);
+    return set_err(CONV_Q_EUNSUPPORTED, "no kernel instantiation for bn=%d kch=%d cg=%d", c.bn, c.kch, c.cg);
 }
 
 static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) {
@@ -424,7 +444,7 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
     {
         cuuint64_t dims[2] = {(cuuint64_t)p->R * p->S * p->row_bytes, (cuuint64_t)p->K};
         cuuint64_t strides[1] = {(cuuint64_t)p->R * p->S * p->row_bytes};
-        cuuint32_t box[2] = {(cuuint32_t)load_row, (cuuint32_t)c.bn};
+        cuuint32_t box[2] = {(cuuint32_t)load_row, (cuuint32_t)(c.bn / c.cg)};  // this CTA's share of the N tile
         cuuint32_t estr[2] = {1, 1};
         CUresult r = g_encode_tiled(&p->tm_b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(w), dims, strides,
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw_ld,

@@ -64,22 +64,29 @@ __global__ void __launch_bounds__(256) quantize_flat_kernel(const uint4 *__restr
         for (int u = 0; u < UNROLL; ++u) {
             int64_t o = base + u * stride;
             if (o >= n_out_vec) break;
+            // the 8 (s8) or 16 (s4) input words hold 2 fp16 values each, low half first
+            uint32_t w[IN_VEC * 4];
+#pragma unroll
+            for (int v = 0; v < IN_VEC; ++v) {
+                w[4 * v] = in[u][v].x; w[4 * v + 1] = in[u][v].y; w[4 * v + 2] = in[u][v].z; w[4 * v + 3] = in[u][v].w;
+            }
+            int q[IN_VEC * 8];
+#pragma unroll
+            for (int i = 0; i < IN_VEC * 4; ++i) {
+                q[2 * i] = quant1(__ushort_as_half((unsigned short)(w[i] & 0xFFFFu)), inv_scale, lo, hi);
+                q[2 * i + 1] = quant1(__ushort_as_half((unsigned short)(w[i] >> 16)), inv_scale, lo, hi);
+            }
             uint32_t out[4];
             if constexpr (BITS == 8) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {  // 4 codes per output word
-                    const __half *h = reinterpret_cast<const __half *>(&in[u][k / 2]) + (k % 2) * 4;
-                    out[k] = pack4_s8(quant1(h[0], inv_scale, lo, hi), quant1(h[1], inv_scale, lo, hi),
-                                      quant1(h[2], inv_scale, lo, hi), quant1(h[3], inv_scale, lo, hi));
-                }
+                for (int k = 0; k < 4; ++k) out[k] = pack4_s8(q[4 * k], q[4 * k + 1], q[4 * k + 2], q[4 * k + 3]);
             } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {  // 8 codes per output word = one input vector
-                    const __half *h = reinterpret_cast<const __half *>(&in[u][k]);
-                    int q[8];
+                for (int k = 0; k < 4; ++k) {
+                    int t[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) q[i] = quant1(h[i], inv_scale, lo, hi);
-                    out[k] = pack8_s4(q);
+                    for (int i = 0; i < 8; ++i) t[i] = q[8 * k + i];
+                    out[k] = pack8_s4(t);
                 }
             }
             __stcs(y + o, make_uint4(out[0], out[1], out[2], out[3]));

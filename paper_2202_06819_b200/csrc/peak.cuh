@@ -10,8 +10,8 @@ namespace convq {
 
 __global__ void __launch_bounds__(128, 1) int8_peak_kernel(int iters, int *sink) {
     constexpr int PM = 128, PN = 256, KB = 128;  // A 128x128 B, B 256x128 B, SW128 K-major
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *a = smem;
     uint8_t *b = smem + PM * KB;
     uint64_t *done = reinterpret_cast<uint64_t *>(b + PN * KB);
