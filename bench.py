@@ -164,7 +164,8 @@ def run_ours(args):
         plans.append(cq.ConvPlan(B, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True))
         outs.append(torch.empty((B, L.P, L.Q, L.K * bits // 8), dtype=torch.uint8, device=dev))
     xq = torch.empty((B, 56, 56, 64 * bits // 8), dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)          # all work (and graph capture) on one side stream
+    torch.cuda.set_stream(stream)
     for p in plans:
         p.set_stream(stream)
 
@@ -200,9 +201,41 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region: exactly K steps, barrier + sync on both sides
+    # ---- CUDA graphs: one step = one graph launch (no per-kernel host launch
+    # cost); a second set of graphs carries per-launch timing events (external
+    # event-record nodes) for the per-layer / roofline numbers.
     n_ev_steps = min(args.steps, 20)                   # per-launch events on the last steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 2)] for _ in range(n_ev_steps)]
+    evs = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(layers) + 2)]
+           for _ in range(n_ev_steps)]
+    use_graph = not args.no_graph
+    graph, graphs_ev = None, None
+    if use_graph:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step()
+            graphs_ev = []
+            for e in evs:
+                ge = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(ge, stream=stream):
+                    step(e)
+                graphs_ev.append(ge)
+            for _ in range(args.warmup):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as ex:  # fall back to eager launches
+            print(f"[bench] CUDA graph capture failed ({ex}); eager launches", file=sys.stderr)
+            use_graph, graph, graphs_ev = False, None, None
+            evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(layers) + 2)] for _ in range(n_ev_steps)]
+
+    def run_step(j):
+        """Timed step number j of the window (j >= 0: with per-launch events)."""
+        if use_graph:
+            (graphs_ev[j] if j >= 0 else graph).replay()
+        else:
+            step(evs[j] if j >= 0 else None)
+
+    # ---- timed region: exactly K steps, barrier + sync on both sides
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -211,8 +244,7 @@ def run_ours(args):
     time.sleep(0.2)
     t0.record(stream)
     for s in range(args.steps):
-        j = s - (args.steps - n_ev_steps)
-        step(evs[j] if j >= 0 else None)
+        run_step(s - (args.steps - n_ev_steps))
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -236,7 +268,7 @@ def run_ours(args):
         h_out = torch.empty(outs[-1].shape, dtype=torch.uint8).pin_memory()
         for _ in range(2):
             x_in_f16.copy_(h_in, non_blocking=True)
-            step()
+            run_step(-1)
             h_out.copy_(outs[-1], non_blocking=True)
         torch.cuda.synchronize()
         k_e2e = max(3, min(args.steps, 50))
@@ -247,7 +279,7 @@ def run_ours(args):
         e0.record(stream)
         for _ in range(k_e2e):
             x_in_f16.copy_(h_in, non_blocking=True)
-            step()
+            run_step(-1)
             h_out.copy_(outs[-1], non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -333,7 +365,8 @@ def run_ours(args):
                        "kernels_per_step": len(layers) + 1, "parallelism": f"batch-shard dp{world}",
                        "l2": "inputs larger than L2: per-step working set %.2f GB >> 126 MB L2" % (
                            (bytes_step + B * 56 * 56 * 64 * 2) / 1e9),
-                       "stem_conv1": "timed separately (see stem)"},
+                       "stem_conv1": "timed separately (see stem)",
+                       "launch": "CUDA graph per step" if use_graph else "eager launches"},
             "conv_tops": round(achieved_tops, 1),
             "conv_frac_int8_peak": round(achieved_tops / int8_peak_tops, 3),
             "int8_peak_k7_tops": k7,
@@ -467,6 +500,7 @@ def main():
                     choices=["resnet50_int8_b256", "resnet18_int8_b1", "resnet18_int4_b16", "cfg1"])
     ap.add_argument("--batch", type=int, default=0, help="override per-GPU batch")
     ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-stem", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

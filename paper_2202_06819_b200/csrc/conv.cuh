@@ -21,12 +21,18 @@
 // UMMA swizzled layout; both operands are scaled by 16, so the accumulator
 // holds 256*acc and the epilogue shifts it back (exact).
 //
-// Warp roles (persistent CTA, one per SM):
-//   warp 0      TMA producer (one lane)
-//   warp 1      TMEM allocator + MMA issuer (one lane)
-//   warps 2..    epilogue: 4 warpgroups (INT8) / 2 (INT4), each warp owning the
+// Stages: one pipeline stage holds NSUB k-blocks (each a (tap, channel-block)
+// pair: KCH channels of one filter tap), filled by NSUB im2col + NSUB weight
+// loads, consumed by NSUB*KCH/32 MMAs and released by ONE tcgen05.commit: the
+// issuing thread's per-stage handshake (barrier wait + commit, several hundred
+// cycles) is amortised over >= ~1000 cycles of tensor work.
+//
+// Warp roles (persistent CTA, one per SM; CG = 2: a CTA pair per tile):
+//   warps 0..    epilogue: 4 warpgroups (INT8) / 2 (INT4), each warp owning the
 //                32 TMEM lanes (= tile rows = output pixels) of its quadrant
-//   last 4 warps INT4 only: s4 -> s8 transform
+//   next 4 warps INT4 only: s4 -> s8 transform
+//   next warp    TMA producer (converged warp, one elected lane issues)
+//   last warp    TMEM allocator + MMA issuer (converged warp, one elected lane)
 // Pipelines: smem ring full/empty(/ready) mbarriers; TMEM double-buffered
 // accumulator acc_full/acc_empty; buffer b is drained by its own warpgroups,
 // so the requantization of two tiles and the mainloop of a third overlap.
@@ -39,6 +45,14 @@
 namespace convq {
 
 constexpr int BM = 128;
+// per-CTA trace counters (cycles): where the control loops wait
+enum { TR_PROD_EMPTY = 0, TR_MMA_FULL, TR_MMA_ACC, TR_EPI_ACC, TR_MMA_ISSUE, TR_TOTAL, TR_TILES, TR_T0, TR_T1,
+       TR_TPDL, TR_SLOTS = 10 };
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
 
 struct ConvParams {
@@ -51,44 +65,68 @@ struct ConvParams {
     int n_tiles;    // ceil(K / BN)
     int num_tiles;  // m_tiles * n_tiles
     int relu;
-    int cvt_magic;       // |acc| <= 2^22 guaranteed: int->float via the 1.5*2^23 add (FMA pipe)
-    int one;             // = 1, opaque to the compiler (keeps an integer add on the FMA pipe)
+    int probe;           // measurement only: 0 normal, 1 = loads without MMAs, 2 = MMAs without loads
+    unsigned long long *trace;  // measurement only: per-CTA wait-cycle counters (TRACE_SLOTS each), or null
     const float *scale;  // [2K] scale then shift
-    int32_t *y32;        // s32 output (OUT_S32)
+    int32_t *y32;        // s32 output (OUT = OUT_S32)
+    uint8_t *y8;         // packed output for direct stores (OUT = OUT_DIRECT)
+    int out_row;         // packed output bytes per pixel row = K*BITS/8
 };
 
-template <int BITS, int BN, int KCH, int OUT_S32, int CG>
+// Output path of the epilogue.
+constexpr int OUT_TMA = 0;     // packed codes staged in smem, written by TMA stores
+constexpr int OUT_S32 = 1;     // raw int32 accumulators, direct global stores (debug / parity)
+constexpr int OUT_DIRECT = 2;  // packed codes, 16-byte direct global stores (no staging smem ->
+                               // deeper operand pipeline; L2 merges the row pieces)
+
+template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB>
 struct ConvCfg {
     // CG = CTAs per tile (1, or 2 = a CTA pair running tcgen05.mma.cta_group::2
     // with M = 256: each CTA stages its own 128 A rows and BN/2 B rows).
     static constexpr int BNL = BN / CG;                     // B rows staged per CTA
     static constexpr int LOAD_ROW = KCH * BITS / 8;        // packed bytes per row per k-block
-    static constexpr int A_S8 = BM * KCH;                   // s8 A tile bytes
-    static constexpr int B_S8 = BNL * KCH;
-    static constexpr int A_PK = BITS == 4 ? BM * LOAD_ROW : 0;
-    static constexpr int B_PK = BITS == 4 ? BNL * LOAD_ROW : 0;
+    static constexpr int A_SUB = BM * KCH;                  // s8 A sub-tile bytes (one k-block)
+    static constexpr int B_SUB = BNL * KCH;
+    static constexpr int A_S8 = NSUB * A_SUB;               // per stage
+    static constexpr int B_S8 = NSUB * B_SUB;
+    static constexpr int A_PK_SUB = BITS == 4 ? BM * LOAD_ROW : 0;
+    static constexpr int B_PK_SUB = BITS == 4 ? BNL * LOAD_ROW : 0;
+    static constexpr int A_PK = NSUB * A_PK_SUB;
+    static constexpr int B_PK = NSUB * B_PK_SUB;
     static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
-    static constexpr int STAGE_TX = (BM + BNL) * LOAD_ROW;   // TMA bytes per stage per CTA
+    static constexpr int SUB_TX = (BM + BNL) * LOAD_ROW;     // TMA bytes per k-block per CTA
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
-    static constexpr int OUT_SUBW = OUT_ROW < 128 ? OUT_ROW : 128;  // TMA store box width
-    static constexpr int OUT_NSUB = OUT_ROW / OUT_SUBW;
-    static constexpr int OUT_BYTES = OUT_S32 ? 0 : BM * OUT_ROW;   // staging per TMEM buffer
+    static constexpr int OUT_BYTES = OUT == OUT_TMA ? BM * OUT_ROW : 0;   // staging per TMEM buffer
     static constexpr int NUM_EPI = BITS == 8 ? 4 : 2;               // epilogue warpgroups
-    static constexpr int EPI_PER_BUF = NUM_EPI / 2;                 // warpgroups per TMEM buffer
-    static constexpr int EPI_COLS = BN / EPI_PER_BUF;               // columns one warpgroup drains
+    // TMEM accumulator buffers: as many as the 512 columns allow (max 4), so
+    // up to NBUF tiles are in the epilogue while the MMA fills the next one
+    static constexpr int NBUF = (512 / BN) < NUM_EPI ? (512 / BN) : NUM_EPI;
+    static constexpr int EPI_PER_BUF = NUM_EPI / NBUF;              // warpgroups per TMEM buffer
+    static constexpr int EPI_COLS = BN / EPI_PER_BUF;               // columns one warp drains (of its 32 rows)
+    static constexpr int EPI_ROW = EPI_COLS * BITS / 8;             // packed bytes of one row of a warp's slab
+    static constexpr int EPI_SUBW = EPI_ROW < 128 ? EPI_ROW : 128;  // TMA store box width (= swizzle span)
+    static constexpr int EPI_NSUB = EPI_ROW / EPI_SUBW;
+    static constexpr int SLAB = 32 * EPI_ROW;                       // one warp's staging slab
     static constexpr int CW = BITS == 8 ? 16 : 32;                  // columns per tcgen05.ld (16 B packed)
-    static constexpr int SS_BYTES = OUT_S32 ? 0 : 2 * BN * 4;       // scale+shift of one n-block
+    static constexpr int SS_BYTES = 0;
     static constexpr int BAR_BYTES = 1024;
-    static constexpr int STAGES_FIT = (SMEM_LIMIT - 1024 - BAR_BYTES - 2 * (OUT_BYTES + SS_BYTES)) / STAGE_BYTES;
+    static constexpr int STAGES_FIT = (SMEM_LIMIT - 1024 - BAR_BYTES - NBUF * (OUT_BYTES + SS_BYTES)) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 2 * (OUT_BYTES + SS_BYTES) + BAR_BYTES;
-    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr int EPI_WARP0 = 2;                             // warps 2..: epilogue warpgroups
-    static constexpr int XF_WARP0 = EPI_WARP0 + 4 * NUM_EPI;        // INT4 transform warps
-    static constexpr int NUM_THREADS = 32 * (XF_WARP0 + (BITS == 4 ? 4 : 0));
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) + BAR_BYTES;
+    static constexpr int TMEM_COLS = NBUF * BN < 32 ? 32 : NBUF * BN;
+    // Warp layout: epilogue warpgroups first, then (INT4) the transform
+    // warpgroup, then the TMA producer and the MMA issuer as the two highest
+    // warp ids -- the SMSP arbiter favours higher warp ids, so the two
+    // single-thread control loops are never starved by epilogue math.
+    static constexpr int EPI_WARP0 = 0;
+    static constexpr int XF_WARP0 = 4 * NUM_EPI;                    // INT4 transform warps
+    static constexpr int PROD_WARP = XF_WARP0 + (BITS == 4 ? 4 : 0);
+    static constexpr int MMA_WARP = PROD_WARP + 1;
+    static constexpr int NUM_THREADS = 32 * (MMA_WARP + 1);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
-    static_assert(STAGES >= 2, "tile does not fit shared memory");
+    static constexpr bool FITS = STAGES >= 2;                     // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
+    static_assert(NSUB == 1 || NSUB == 2 || NSUB == 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
     static_assert(CG == 1 || CG == 2, "CG");
     static_assert(TMEM_COLS <= 512, "TMEM");
@@ -140,19 +178,8 @@ __device__ __forceinline__ void expand_tile(const uint8_t *src, uint8_t *dst, in
 // complement, in the low mantissa bits.  Returns those bits; the caller
 // takes the low byte / nibble as the packed code.
 constexpr float RNE_MAGIC = 12582912.0f;  // 1.5 * 2^23
-// (float)acc, exact, for |acc| <= 2^22: the word 0x4B400000 + acc is the
-// float 1.5*2^23 + acc; subtracting 1.5*2^23 is exact.  Both steps run on the
-// FMA pipe (integer multiply-add by a runtime 1 that the compiler cannot fold
-// into an ALU add, then a float add) instead of one ALU-pipe I2FP: the
-// epilogue is ALU-bound (FMNMX clamps, PRMT packing).
-__device__ __forceinline__ float small_int_to_float(int acc, int one) {
-    int w;
-    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(w) : "r"(acc), "r"(one), "r"(0x4B400000));
-    return __fsub_rn(__int_as_float(w), RNE_MAGIC);
-}
-template <bool MAGIC>
-__device__ __forceinline__ uint32_t requant_bits(int acc, float sc, float sh, float lo, float hi, int one) {
-    float f = MAGIC ? small_int_to_float(acc, one) : __int2float_rn(acc);
+__device__ __forceinline__ uint32_t requant_bits(int acc, float sc, float sh, float lo, float hi) {
+    float f = __int2float_rn(acc);
     float u = __fmaf_rn(f, sc, sh);
     u = fminf(fmaxf(u, lo), hi);
     return __float_as_uint(__fadd_rn(u, RNE_MAGIC));
@@ -170,11 +197,12 @@ __device__ __forceinline__ uint32_t pack8_low_nibbles(const uint32_t *r) {
     return __byte_perm(__byte_perm(b01, b23, 0x0040), __byte_perm(b45, b67, 0x0040), 0x5410);
 }
 
-template <int BITS, int BN, int KCH, int OUT_S32, int CG>
-__global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREADS, 1)
+template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB>
+__global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>::NUM_THREADS, 1)
     conv_igemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_y, const ConvParams p) {
-    using Cfg = ConvCfg<BITS, BN, KCH, OUT_S32, CG>;
+    using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>;
+    static_assert(Cfg::FITS, "tile does not fit shared memory");
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment by offset (pointer arithmetic on the shared array keeps
@@ -183,22 +211,23 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREA
 
     // ---- carve shared memory (every tile 1024-byte aligned; identical offsets
     // in both CTAs of a pair, as cta_group::2 descriptors require)
-    uint8_t *a_s8 = smem;                               // [STAGES][BM*KCH]
-    uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][BNL*KCH]
-    uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][BM*KCH/2]
-    uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][BNL*KCH/2]
-    uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [2][OUT_NSUB][BM][OUT_SUBW]
-    float *ss_smem = reinterpret_cast<float *>(out_stage + 2 * Cfg::OUT_BYTES);  // [2][2*BN]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(out_stage + 2 * (Cfg::OUT_BYTES + Cfg::SS_BYTES));
+    uint8_t *a_s8 = smem;                               // [STAGES][NSUB][BM*KCH]
+    uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][NSUB][BNL*KCH]
+    uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][NSUB][BM*KCH/2]
+    uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][NSUB][BNL*KCH/2]
+    uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [NBUF][EPB][4 quads] slabs [EPI_NSUB][32][EPI_SUBW]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(out_stage + Cfg::NBUF * (Cfg::OUT_BYTES + Cfg::SS_BYTES));
     uint64_t *full = bars;                  // TMA -> (transform | MMA)
     uint64_t *empty = bars + STAGES;        // MMA -> TMA
     uint64_t *ready = bars + 2 * STAGES;    // transform -> MMA (INT4)
-    uint64_t *acc_full = bars + 3 * STAGES; // MMA -> epilogue [2]
-    uint64_t *acc_empty = acc_full + 2;     // epilogue -> MMA [2]
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(acc_empty + 2);
+    uint64_t *acc_full = bars + 3 * STAGES; // MMA -> epilogue [NBUF]
+    uint64_t *acc_empty = acc_full + 4;     // epilogue -> MMA [NBUF]
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(acc_empty + 4);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const long long t_start = p.trace ? clock64() : 0;
+    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * TR_SLOTS + TR_T0] = globaltimer_ns();
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;     // position in the CTA pair
     const int tile0 = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
     const int tstep = CG == 2 ? (int)num_clusters_x() : (int)gridDim.x;
@@ -210,19 +239,19 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREA
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tm_a);
         tma_prefetch_desc(&tm_b);
-        if (!OUT_S32) tma_prefetch_desc(&tm_y);
+        if (OUT == OUT_TMA) tma_prefetch_desc(&tm_y);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
             mbar_init(&ready[s], 4 * CG);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < Cfg::NBUF; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF * CG);
         }
         fence_mbar_init();
     }
-    if (warp == 1) {
+    if (warp == Cfg::MMA_WARP) {
         if constexpr (CG == 2) tmem_alloc_cg2<Cfg::TMEM_COLS>(tmem_holder);
         else tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
     }
@@ -231,122 +260,190 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREA
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    // PDL: everything above (barrier init, TMEM alloc, descriptor prefetch)
+    // overlapped the previous kernel's tail; global memory is touched only
+    // after pdl_wait() in the producer and epilogue roles.
+    if (threadIdx.x == 0) pdl_launch_dependents();
 
     const int PQ = p.P * p.Q;
 
-    if (warp == 0) {
+    if (warp == Cfg::PROD_WARP) {
         // =========================== TMA producer ===========================
-        if (lane == 0) {
-            const uint64_t pol_a = policy_evict_normal();  // activations: re-read by R*S taps and n-tiles
-            const uint64_t pol_b = policy_evict_last();    // weights: re-read by every m-tile
-            uint8_t *a_dst = BITS == 4 ? a_pk : a_s8;
-            uint8_t *b_dst = BITS == 4 ? b_pk : b_s8;
-            constexpr int A_LD = BITS == 4 ? Cfg::A_PK : Cfg::A_S8;
-            constexpr int B_LD = BITS == 4 ? Cfg::B_PK : Cfg::B_S8;
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
-                const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
-                const int m0 = m_blk * (BM * CG) + (int)rank * BM;   // this CTA's first output pixel
-                const int n0 = m0 / PQ, rem = m0 - n0 * PQ;
-                const int p0 = rem / p.Q, q0 = rem - p0 * p.Q;
-                const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad;
-                const int brow = n_blk * BN + (int)rank * Cfg::BNL;  // this CTA's B rows
-                int r = 0, s = 0, cblk = 0, kcol = 0;
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+        // The whole warp runs the loop (converged, uniform operands); one
+        // elected lane issues the expect-tx and the TMA loads.
+        const uint64_t pol_a = policy_evict_normal();  // activations: re-read by R*S taps and n-tiles
+        const uint64_t pol_b = policy_evict_last();    // weights: re-read by every m-tile
+        uint8_t *a_dst = BITS == 4 ? a_pk : a_s8;
+        uint8_t *b_dst = BITS == 4 ? b_pk : b_s8;
+        constexpr int A_LD = BITS == 4 ? Cfg::A_PK : Cfg::A_S8;
+        constexpr int B_LD = BITS == 4 ? Cfg::B_PK : Cfg::B_S8;
+        constexpr int A_LD_SUB = BITS == 4 ? Cfg::A_PK_SUB : Cfg::A_SUB;
+        constexpr int B_LD_SUB = BITS == 4 ? Cfg::B_PK_SUB : Cfg::B_SUB;
+        const uint32_t full0_leader = PAIR_TX ? mapa_shared(smem_u32(&full[0]), 0) : 0;
+        pdl_wait();
+        if (p.trace && lane == 0) p.trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+            const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
+            const int m0 = m_blk * (BM * CG) + (int)rank * BM;   // this CTA's first output pixel
+            const int n0 = m0 / PQ, rem = m0 - n0 * PQ;
+            const int p0 = rem / p.Q, q0 = rem - p0 * p.Q;
+            const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad;
+            const int brow = n_blk * BN + (int)rank * Cfg::BNL;  // this CTA's B rows
+            int r = 0, s = 0, cblk = 0, kcol = 0;
+            for (int kb = 0; kb < p.num_kb; kb += NSUB) {
+                const int nsub = min(NSUB, p.num_kb - kb);   // ragged last stage of a tile
+                {
+                    const long long t0 = p.trace ? clock64() : 0;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if constexpr (PAIR_TX) {
-                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_TX);
-                        tma_load_im2col_4d_cg2(a_dst + stage * A_LD, &tm_a, fb, cblk * Cfg::LOAD_ROW, w0, h0, n0,
-                                               (uint16_t)s, (uint16_t)r, pol_a);
-                        tma_load_2d_cg2(b_dst + stage * B_LD, &tm_b, fb, kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
+                    if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
+                }
+                const bool issuer = elect_one();
+                if (issuer) {
+                    if (p.probe == 2) {                       // measurement: no loads
+                        if (!PAIR_TX || rank == 0) mbar_arrive(&full[stage]);
+                    } else if (PAIR_TX) {
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * nsub * Cfg::SUB_TX);
                     } else {
-                        mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_TX);
-                        tma_load_im2col_4d(a_dst + stage * A_LD, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0,
-                                           (uint16_t)s, (uint16_t)r, pol_a);
-                        tma_load_2d(b_dst + stage * B_LD, &tm_b, &full[stage], kcol + cblk * Cfg::LOAD_ROW, brow,
-                                    pol_b);
+                        mbar_arrive_expect_tx(&full[stage], nsub * Cfg::SUB_TX);
                     }
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                for (int j = 0; j < nsub; ++j) {
+                    if (issuer && p.probe != 2) {
+                        uint8_t *ad = a_dst + stage * A_LD + j * A_LD_SUB;
+                        uint8_t *bd = b_dst + stage * B_LD + j * B_LD_SUB;
+                        if constexpr (PAIR_TX) {
+                            const uint32_t fb = full0_leader + 8u * stage;
+                            tma_load_im2col_4d_cg2(ad, &tm_a, fb, cblk * Cfg::LOAD_ROW, w0, h0, n0, (uint16_t)s,
+                                                   (uint16_t)r, pol_a);
+                            tma_load_2d_cg2(bd, &tm_b, fb, kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
+                        } else {
+                            tma_load_im2col_4d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0, (uint16_t)s,
+                                               (uint16_t)r, pol_a);
+                            tma_load_2d(bd, &tm_b, &full[stage], kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
+                        }
+                    }
                     if (++cblk == p.num_cblk) {            // next filter tap (r, s)
                         cblk = 0;
                         kcol += p.row_bytes;
                         if (++s == p.S) { s = 0; ++r; }
                     }
                 }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == Cfg::MMA_WARP) {
         // =========================== MMA issuer =============================
-        if (lane == 0 && rank == 0) {
+        // Whole warp (converged) waits; one elected lane issues the MMAs and
+        // commits.  Descriptors: base + byte offset >> 4 in the start-address
+        // field (addresses < 2^18, so the 14-bit field never carries).
+        if (rank == 0) {
+            const uint64_t a_desc0 = umma_desc_kmajor(smem_u32(a_s8), KCH);
+            const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(b_s8), KCH);
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
             for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++local) {
-                const int buf = local & 1;
-                const uint32_t aphase = (local >> 1) & 1;
-                mbar_wait(&acc_empty[buf], aphase ^ 1);
+                const int buf = local % Cfg::NBUF;
+                const uint32_t aphase = (local / Cfg::NBUF) & 1;
+                {
+                    const long long t0 = p.trace ? clock64() : 0;
+                    mbar_wait(&acc_empty[buf], aphase ^ 1);
+                    if (p.trace && lane == 0) {
+                        atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_ACC, clock64() - t0);
+                        atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_TILES, 1ull);
+                    }
+                }
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + buf * BN;
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = 0; kb < p.num_kb; kb += NSUB) {
+                    const int nsub = min(NSUB, p.num_kb - kb);
+                    long long t0 = p.trace ? clock64() : 0;
                     mbar_wait(BITS == 4 ? &ready[stage] : &full[stage], phase);
-                    tc_fence_after();
-                    const uint32_t a_addr = smem_u32(a_s8 + stage * Cfg::A_S8);
-                    const uint32_t b_addr = smem_u32(b_s8 + stage * Cfg::B_S8);
-#pragma unroll
-                    for (int k = 0; k < KCH / 32; ++k) {
-                        const uint64_t ad = umma_desc_kmajor(a_addr + 32 * k, KCH);
-                        const uint64_t bd = umma_desc_kmajor(b_addr + 32 * k, KCH);
-                        if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad, bd, Cfg::IDESC, (kb | k) != 0);
-                        else mma_i8(d_tmem, ad, bd, Cfg::IDESC, (kb | k) != 0);
+                    if (p.trace && lane == 0) {
+                        const long long t1 = clock64();
+                        atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
+                        t0 = t1;
                     }
-                    // frees the smem stage (in both CTAs) when these MMAs complete
-                    if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
-                    else mma_commit(&empty[stage]);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        if (p.probe == 1) {                // measurement: no MMAs
+                            if constexpr (CG == 2) {
+                                mbar_arrive(&empty[stage]);
+                                mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
+                            } else {
+                                mbar_arrive(&empty[stage]);
+                            }
+                        } else {
+                            const uint64_t ad0 = a_desc0 + (uint64_t)((stage * Cfg::A_S8) >> 4);
+                            const uint64_t bd0 = b_desc0 + (uint64_t)((stage * Cfg::B_S8) >> 4);
+#pragma unroll
+                            for (int j = 0; j < NSUB; ++j) {
+                                if (j < nsub) {
+                                    const uint64_t ad = ad0 + (uint64_t)((j * Cfg::A_SUB) >> 4);
+                                    const uint64_t bd = bd0 + (uint64_t)((j * Cfg::B_SUB) >> 4);
+#pragma unroll
+                                    for (int k = 0; k < KCH / 32; ++k) {
+                                        const uint32_t acc = (kb + j + k) != 0;
+                                        if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
+                                        else mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
+                                    }
+                                }
+                            }
+                            // frees the smem stage (in both CTAs) when these MMAs complete
+                            if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
+                            else mma_commit(&empty[stage]);
+                        }
+                    }
+                    __syncwarp();
+                    if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 // accumulator ready for the epilogue (of both CTAs)
-                if constexpr (CG == 2) mma_commit_cg2_mc(&acc_full[buf], 0x3);
-                else mma_commit(&acc_full[buf]);
+                if (elect_one()) {
+                    if constexpr (CG == 2) mma_commit_cg2_mc(&acc_full[buf], 0x3);
+                    else mma_commit(&acc_full[buf]);
+                }
+                __syncwarp();
             }
         }
     } else if (warp < Cfg::XF_WARP0) {
         // =========================== epilogue ===============================
-        // TMEM buffer b (every other tile) is drained by EPI_PER_BUF warpgroups,
-        // each owning EPI_COLS of its BN columns; each buffer has its own
-        // staging tile and scale/shift copy, so one buffer's TMA store and the
-        // other buffer's requantization overlap.  In a CTA pair each CTA drains
-        // its own 128 rows (its TMEM half) and releases the leader's buffer.
+        // Every warp works on its own: TMEM buffer b (every other tile) is
+        // drained by EPI_PER_BUF warpgroups; a warp owns the 32 rows of its
+        // TMEM lane quadrant and EPI_COLS columns.  Scale/shift come straight
+        // from L1 (warp-uniform loads), and with TMA output each warp stages
+        // its 32-row slab and issues its own bulk store: no CTA-level barrier
+        // anywhere in the epilogue.  In a CTA pair each CTA drains its own 128
+        // rows (its TMEM half) and releases the leader's buffer.
         constexpr int EPB = Cfg::EPI_PER_BUF;
         const int e = (warp - Cfg::EPI_WARP0) >> 2;
         const int b = e / EPB;                     // TMEM buffer
         const int half = e % EPB;                  // column part
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
         const int row = quad * 32 + lane;          // tile row = output pixel
-        const int ptid = (e % EPB) * 128 + (threadIdx.x & 127);  // thread index within the buffer's group
-        const bool leader = ptid == 0;
-        const uint32_t bar_id = 1 + b, bar_n = 128 * EPB;
-        uint8_t *stage_b = out_stage + b * Cfg::OUT_BYTES;
-        float *ss_b = ss_smem + b * 2 * BN;
+        uint8_t *slab = out_stage + b * Cfg::OUT_BYTES + (half * 4 + quad) * Cfg::SLAB;
         const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(&acc_empty[b]), 0) : 0;
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
         const float hi = (float)((1 << (BITS - 1)) - 1);
-        const int one = p.one;
+        pdl_wait();
         int j = 0;
-        for (int tile = tile0 + b * tstep; tile < p.num_tiles; tile += 2 * tstep, ++j) {
+        for (int tile = tile0 + b * tstep; tile < p.num_tiles; tile += Cfg::NBUF * tstep, ++j) {
             const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
             const int mrow0 = m_blk * (BM * CG) + (int)rank * BM;
             const int m = mrow0 + row;
-            if (!OUT_S32) {
-                if (leader) tma_store_wait_read0();   // staging of this buffer's previous tile read out
-                for (int i = ptid; i < 2 * BN; i += bar_n) {   // this n-block's scale and shift
-                    const int col = n_blk * BN + (i % BN);
-                    ss_b[i] = col < p.K ? __ldg(p.scale + (i < BN ? 0 : p.K) + col) : 0.f;
-                }
-                named_bar_sync(bar_id, bar_n);
+            if (OUT == OUT_TMA) {   // this warp's slab must have been read out by its previous store
+                if (lane == 0) tma_store_wait_read0();
+                __syncwarp();
             }
-            mbar_wait(&acc_full[b], j & 1);
+            {
+                const long long t0 = p.trace ? clock64() : 0;
+                mbar_wait(&acc_full[b], j & 1);
+                if (p.trace && lane == 0 && warp == Cfg::EPI_WARP0)
+                    atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_EPI_ACC, clock64() - t0);
+            }
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + b * BN + half * Cfg::EPI_COLS;
 #pragma unroll 1
@@ -354,7 +451,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREA
                 uint32_t v[Cfg::CW];
                 if constexpr (Cfg::CW == 16) tmem_ld_32x32b_x16(taddr + c * Cfg::CW, v);
                 else tmem_ld_32x32b_x32(taddr + c * Cfg::CW, v);
-                if (c == Cfg::EPI_COLS / Cfg::CW - 1) {  // this group's columns are in registers
+                if (c == Cfg::EPI_COLS / Cfg::CW - 1) {  // this warp's columns are in registers
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) {
@@ -364,7 +461,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREA
                 }
                 const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
                 const int col0 = n_blk * BN + ccol;
-                if (OUT_S32) {
+                if (OUT == OUT_S32) {
                     if (m < p.M) {
                         int32_t *dst = p.y32 + (int64_t)m * p.K + col0;
                         if (col0 + Cfg::CW <= p.K) {
@@ -384,29 +481,31 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREA
                     }
                 } else {
                     uint32_t r[Cfg::CW];
-                    const float4 *s4 = reinterpret_cast<const float4 *>(ss_b + ccol);
-                    const float4 *h4 = reinterpret_cast<const float4 *>(ss_b + BN + ccol);
-                    auto requant_chunk = [&](auto magic) {
+                    if (col0 + Cfg::CW <= p.K) {
+                        const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
+                        const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
 #pragma unroll
                         for (int q = 0; q < Cfg::CW / 4; ++q) {
-                            const float4 sa = s4[q], sb = h4[q];
+                            const float4 sa = __ldg(s4 + q), sb = __ldg(h4 + q);
                             const int x0 = BITS == 4 ? ((int)v[4 * q] >> 8) : (int)v[4 * q];
                             const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
                             const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
                             const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
-                            r[4 * q] = requant_bits<decltype(magic)::value>(x0, sa.x, sb.x, lo, hi, one);
-                            r[4 * q + 1] = requant_bits<decltype(magic)::value>(x1, sa.y, sb.y, lo, hi, one);
-                            r[4 * q + 2] = requant_bits<decltype(magic)::value>(x2, sa.z, sb.z, lo, hi, one);
-                            r[4 * q + 3] = requant_bits<decltype(magic)::value>(x3, sa.w, sb.w, lo, hi, one);
+                            r[4 * q] = requant_bits(x0, sa.x, sb.x, lo, hi);
+                            r[4 * q + 1] = requant_bits(x1, sa.y, sb.y, lo, hi);
+                            r[4 * q + 2] = requant_bits(x2, sa.z, sb.z, lo, hi);
+                            r[4 * q + 3] = requant_bits(x3, sa.w, sb.w, lo, hi);
                         }
-                    };
-                    if (p.cvt_magic) requant_chunk(std::true_type{});
-                    else requant_chunk(std::false_type{});
-                    // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
-                    const int byte0 = ccol * BITS / 8;
-                    uint8_t *sub = stage_b + (byte0 / Cfg::OUT_SUBW) * (BM * Cfg::OUT_SUBW);
-                    const int inrow = byte0 % Cfg::OUT_SUBW;
-                    uint4 pk;
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < Cfg::CW; ++q) {
+                            const bool ok = col0 + q < p.K;  // columns past K are never stored
+                            const float sc = ok ? __ldg(p.scale + col0 + q) : 0.f;
+                            const float sh = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
+                            r[q] = requant_bits(BITS == 4 ? ((int)v[q] >> 8) : (int)v[q], sc, sh, lo, hi);
+                        }
+                    }
+                    uint4 pk;   // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
                     if constexpr (BITS == 8) {
                         pk = make_uint4(pack4_low_bytes(r[0], r[1], r[2], r[3]), pack4_low_bytes(r[4], r[5], r[6], r[7]),
                                         pack4_low_bytes(r[8], r[9], r[10], r[11]),
@@ -415,23 +514,31 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREA
                         pk = make_uint4(pack8_low_nibbles(r), pack8_low_nibbles(r + 8), pack8_low_nibbles(r + 16),
                                         pack8_low_nibbles(r + 24));
                     }
-                    *reinterpret_cast<uint4 *>(sub + swz<Cfg::OUT_SUBW>(row * Cfg::OUT_SUBW + inrow)) = pk;
+                    const int sbyte = c * 16;                 // byte within this warp's slab row
+                    if constexpr (OUT == OUT_TMA) {
+                        uint8_t *sub = slab + (sbyte / Cfg::EPI_SUBW) * (32 * Cfg::EPI_SUBW);
+                        *reinterpret_cast<uint4 *>(sub + swz<Cfg::EPI_SUBW>(lane * Cfg::EPI_SUBW + sbyte % Cfg::EPI_SUBW)) = pk;
+                    } else {
+                        const int gbyte = n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + sbyte;
+                        if (m < p.M && gbyte < p.out_row)
+                            *reinterpret_cast<uint4 *>(p.y8 + (int64_t)m * p.out_row + gbyte) = pk;
+                    }
                 }
             }
-            if (!OUT_S32) {
+            if (OUT == OUT_TMA) {
                 fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
-                named_bar_sync(bar_id, bar_n);
-                if (leader) {
+                __syncwarp();
+                if (lane == 0) {
 #pragma unroll
-                    for (int s = 0; s < Cfg::OUT_NSUB; ++s)
-                        tma_store_2d(&tm_y, stage_b + s * (BM * Cfg::OUT_SUBW), n_blk * Cfg::OUT_ROW + s * Cfg::OUT_SUBW,
-                                     mrow0);
+                    for (int s = 0; s < Cfg::EPI_NSUB; ++s)
+                        tma_store_2d(&tm_y, slab + s * (32 * Cfg::EPI_SUBW),
+                                     n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + s * Cfg::EPI_SUBW, mrow0 + quad * 32);
                     tma_store_commit();
                 }
             }
         }
-        if (!OUT_S32 && leader) tma_store_wait0();
-    } else {
+        if (OUT == OUT_TMA && lane == 0) tma_store_wait0();
+    } else if (warp < Cfg::PROD_WARP) {
         // =========================== INT4 transform =========================
         if constexpr (BITS == 4) {
             const int tid = threadIdx.x - 32 * Cfg::XF_WARP0;  // 0..127
@@ -439,10 +546,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREA
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
-                for (int kb = 0; kb < p.num_kb; ++kb) {
+                for (int kb = 0; kb < p.num_kb; kb += NSUB) {
+                    const int nsub = min(NSUB, p.num_kb - kb);
                     mbar_wait(&full[stage], phase);
-                    expand_tile<KCH>(a_pk + stage * Cfg::A_PK, a_s8 + stage * Cfg::A_S8, BM, tid, 128);
-                    expand_tile<KCH>(b_pk + stage * Cfg::B_PK, b_s8 + stage * Cfg::B_S8, Cfg::BNL, tid, 128);
+                    for (int j = 0; j < nsub; ++j) {
+                        expand_tile<KCH>(a_pk + stage * Cfg::A_PK + j * Cfg::A_PK_SUB,
+                                         a_s8 + stage * Cfg::A_S8 + j * Cfg::A_SUB, BM, tid, 128);
+                        expand_tile<KCH>(b_pk + stage * Cfg::B_PK + j * Cfg::B_PK_SUB,
+                                         b_s8 + stage * Cfg::B_S8 + j * Cfg::B_SUB, Cfg::BNL, tid, 128);
+                    }
                     fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.mma
                     __syncwarp();
                     if (lane == 0) {
@@ -458,7 +570,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT_S32, CG>::NUM_THREA
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync();   // the pair's MMAs and remote arrivals are complete
     else __syncthreads();
-    if (warp == 1) {
+    if (p.trace && threadIdx.x == 0) {
+        atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_TOTAL, clock64() - t_start);
+        p.trace[blockIdx.x * TR_SLOTS + TR_T1] = globaltimer_ns();
+    }
+    if (warp == Cfg::MMA_WARP) {
         tc_fence_after();
         if constexpr (CG == 2) tmem_dealloc_cg2<Cfg::TMEM_COLS>(tmem_base);
         else tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);

@@ -113,7 +113,8 @@ static CUtensorMapSwizzle swizzle_for(int span) {
 
 // ============================================================== plan
 struct Cand {
-    int bn, kch, cg;  // N tile, K chunk (channels per k-block), CTAs per tile
+    int bn, kch, cg, nsub;  // N tile, channels per k-block, CTAs per tile, k-blocks per stage
+    int direct;             // packed output by direct stores (1) or smem staging + TMA store (0)
 };
 
 struct conv_q_plan_s {
@@ -127,6 +128,8 @@ struct conv_q_plan_s {
     std::vector<Cand> cands;
     int sel = 0;
     float tuned_us = -1.f;
+    int probe = 0;     // CONV_Q_PROBE (measurement only; results are garbage when != 0)
+    unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
     CUtensorMap tm_a, tm_b, tm_y;
     const void *c_x = nullptr, *c_w = nullptr, *c_y = nullptr;
@@ -135,8 +138,8 @@ struct conv_q_plan_s {
 
 static std::string cand_name(const conv_q_plan_s *p, int i) {
     char b[64];
-    snprintf(b, sizeof b, "bm%d_bn%d_kc%d_c%d", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
-             p->cands[i].cg);
+    snprintf(b, sizeof b, "bm%d_bn%d_kc%dx%d_c%d%s", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
+             p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "");
     return b;
 }
 
@@ -186,16 +189,42 @@ static void cache_store_locked() {
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Whether a TileConfig fits shared memory (>= 2 stages) for both output modes.
+template <int BITS>
+static bool cand_fits(const Cand &c) {
+#define CONVQ_FIT(BN_, KC_, NS_, CG_)                                                        \
+    if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.cg == CG_)                         \
+        return (c.direct ? ConvCfg<BITS, BN_, KC_, OUT_DIRECT, CG_, NS_>::FITS                \
+                         : ConvCfg<BITS, BN_, KC_, OUT_TMA, CG_, NS_>::FITS) &&               \
+               ConvCfg<BITS, BN_, KC_, OUT_S32, CG_, NS_>::FITS;
+#define CONVQ_FITS_BN(KC_, NS_, CG_) CONVQ_FIT(64, KC_, NS_, CG_) CONVQ_FIT(128, KC_, NS_, CG_) CONVQ_FIT(256, KC_, NS_, CG_)
+    CONVQ_FITS_BN(128, 2, 1) CONVQ_FITS_BN(128, 1, 1) CONVQ_FITS_BN(64, 4, 1) CONVQ_FITS_BN(64, 1, 1)
+    CONVQ_FITS_BN(32, 4, 1) CONVQ_FITS_BN(32, 1, 1)
+    CONVQ_FITS_BN(128, 2, 2) CONVQ_FITS_BN(128, 1, 2) CONVQ_FITS_BN(64, 4, 2) CONVQ_FITS_BN(64, 1, 2)
+    CONVQ_FITS_BN(32, 4, 2) CONVQ_FITS_BN(32, 1, 2)
+#undef CONVQ_FITS_BN
+#undef CONVQ_FIT
+    return false;
+}
+
 static void enumerate_candidates(conv_q_plan_s *p) {
     p->cands.clear();
-    for (int cg : {1, 2})
-        for (int kch : {128, 64, 32}) {
-            if (p->C % kch) continue;
-            for (int bn : {64, 128, 256}) {
-                if (bn > 64 && bn / 2 >= p->K) continue;  // a narrower tile already covers K
-                p->cands.push_back({bn, kch, cg});
+    // (channels per k-block, k-blocks per stage): >= 256 channel-bytes of K per
+    // stage where possible (8 MMAs per commit), plus the single-block variant
+    static const int kn[][2] = {{128, 2}, {128, 1}, {64, 4}, {64, 1}, {32, 4}, {32, 1}};
+    for (int direct : {0, 1})
+        for (int cg : {1, 2})
+            for (auto &q : kn) {
+                const int kch = q[0], nsub = q[1];
+                if (p->C % kch) continue;
+                if (kch < 128 && p->C % (2 * kch) == 0) continue;   // a wider k-block exists
+                for (int bn : {64, 128, 256}) {
+                    if (bn > 64 && bn / 2 >= p->K) continue;  // a narrower tile already covers K
+                    const Cand cand{bn, kch, cg, nsub, direct};
+                    if (!(p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand))) continue;
+                    p->cands.push_back(cand);
+                }
             }
-        }
 }
 
 // Default pick before tuning: deepest K chunk, then the widest N tile whose
@@ -206,7 +235,7 @@ static int default_candidate(const conv_q_plan_s *p) {
     int pick = -1, narrow = -1;
     for (size_t i = 0; i < p->cands.size(); ++i) {
         const Cand &c = p->cands[i];
-        if (c.kch != p->cands[0].kch || c.cg != 1) continue;
+        if (c.kch != p->cands[0].kch || c.nsub != p->cands[0].nsub || c.cg != 1 || c.direct) continue;
         if (narrow < 0 || c.bn < p->cands[narrow].bn) narrow = (int)i;
         if (m_tiles * ceil_div(p->K, c.bn) >= sms && (pick < 0 || c.bn > p->cands[pick].bn)) pick = (int)i;
     }
@@ -292,6 +321,7 @@ extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, 
     std::call_once(g_init_once, init_device);  // SM count for the default pick; errors surface at run
     enumerate_candidates(p);
     p->sel = default_candidate(p);
+    if (const char *pr = getenv("CONV_Q_PROBE")) p->probe = atoi(pr);
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
         cache_load_locked();
@@ -364,10 +394,10 @@ extern "C" int conv_q_plan_info(const conv_q_plan_t *p, conv_q_info_t *info) {
 }
 
 // ============================================================== launch
-template <int BITS, int BN, int KCH, int OUT, int CG>
+template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB>
 static int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
-    using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG>;
-    auto kern = conv_igemm_kernel<BITS, BN, KCH, OUT, CG>;
+    using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>;
+    auto kern = conv_igemm_kernel<BITS, BN, KCH, OUT, CG, NSUB>;
     static bool attr_set = false;
     if (!attr_set) {
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
@@ -382,25 +412,27 @@ static int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.n_tiles = (int)ceil_div(p->K, BN);
     prm.num_tiles = (int)(ceil_div(p->M, BM * CG) * prm.n_tiles);
     prm.relu = p->relu;
-    // |acc| <= R*S*C*2^14 (s8 codes; INT4 after the >>8) -- the plan's guard
-    // arithmetic; the magic int->float is exact up to 2^22.
-    prm.cvt_magic = (BITS == 4 || p->Kg * 16384 <= (int64_t)(1 << 22)) ? 1 : 0;
-    prm.one = 1;
+    prm.probe = p->probe;
+    prm.trace = p->trace;
     prm.scale = scale;
     prm.y32 = static_cast<int32_t *>(y);
+    prm.y8 = static_cast<uint8_t *>(y);
+    prm.out_row = p->out_row;
     const int clusters = std::min(prm.num_tiles, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * CG);
     cfg.blockDim = dim3(Cfg::NUM_THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = p->stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (griddepcontrol in the kernel)
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p->tm_a, p->tm_b, p->tm_y, prm));
     return CONV_Q_OK;
 }
@@ -408,16 +440,23 @@ static int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
 template <int BITS, int OUT>
 static int dispatch_bn_kch(conv_q_plan_s *p, const float *scale, void *y) {
     const Cand c = p->cands[p->sel];
-#define CONVQ_CASE(BN_, KC_, CG_) \
-    if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_) return launch_conv<BITS, BN_, KC_, OUT, CG_>(p, scale, y);
-    CONVQ_CASE(64, 128, 1) CONVQ_CASE(128, 128, 1) CONVQ_CASE(256, 128, 1)
-    CONVQ_CASE(64, 64, 1) CONVQ_CASE(128, 64, 1) CONVQ_CASE(256, 64, 1)
-    CONVQ_CASE(64, 32, 1) CONVQ_CASE(128, 32, 1) CONVQ_CASE(256, 32, 1)
-    CONVQ_CASE(64, 128, 2) CONVQ_CASE(128, 128, 2) CONVQ_CASE(256, 128, 2)
-    CONVQ_CASE(64, 64, 2) CONVQ_CASE(128, 64, 2) CONVQ_CASE(256, 64, 2)
-    CONVQ_CASE(64, 32, 2) CONVQ_CASE(128, 32, 2) CONVQ_CASE(256, 32, 2)
+#define CONVQ_CASE(BN_, KC_, NS_, CG_)                                            \
+    if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.cg == CG_) {          \
+        if constexpr (ConvCfg<BITS, BN_, KC_, OUT, CG_, NS_>::FITS)             \
+            return launch_conv<BITS, BN_, KC_, OUT, CG_, NS_>(p, scale, y);     \
+        else                                                                    \
+            return set_err(CONV_Q_EUNSUPPORTED, "tile config exceeds shared memory"); \
+    }
+#define CONVQ_CASES_BN(KC_, NS_, CG_) \
+    CONVQ_CASE(64, KC_, NS_, CG_) CONVQ_CASE(128, KC_, NS_, CG_) CONVQ_CASE(256, KC_, NS_, CG_)
+    CONVQ_CASES_BN(128, 2, 1) CONVQ_CASES_BN(128, 1, 1) CONVQ_CASES_BN(64, 4, 1) CONVQ_CASES_BN(64, 1, 1)
+    CONVQ_CASES_BN(32, 4, 1) CONVQ_CASES_BN(32, 1, 1)
+    CONVQ_CASES_BN(128, 2, 2) CONVQ_CASES_BN(128, 1, 2) CONVQ_CASES_BN(64, 4, 2) CONVQ_CASES_BN(64, 1, 2)
+    CONVQ_CASES_BN(32, 4, 2) CONVQ_CASES_BN(32, 1, 2)
+#undef CONVQ_CASES_BN
 #undef CONVQ_CASE
-    return set_err(CONV_Q_EUNSUPPORTED, "no kernel instantiation for bn=%d kch=%d cg=%d", c.bn, c.kch, c.cg);
+    return set_err(CONV_Q_EUNSUPPORTED, "no kernel instantiation for bn=%d kch=%d nsub=%d cg=%d", c.bn, c.kch,
+                   c.nsub, c.cg);
 }
 
 static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) {
@@ -453,12 +492,16 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
     }
     // Y: packed NHWC output as a 2-D [M][K*bits/8 bytes] matrix (== the next
     // layer's x; PAPER.md:261 layout consistency).  Unused in S32 mode.
-    if (p->out_mode == CONV_Q_OUT_PACKED) {
-        const int out_row_tile = c.bn * p->bits / 8;
-        const int subw = out_row_tile < 128 ? out_row_tile : 128;
+    if (p->out_mode == CONV_Q_OUT_PACKED && !c.direct) {
+        // one box = one epilogue warp's 32-row slab (or a 128-byte column block of it)
+        const int num_epi = p->bits == 8 ? 4 : 2;
+        const int nbuf = std::min(512 / c.bn, num_epi);
+        const int epb = num_epi / nbuf;
+        const int epi_row = c.bn / epb * p->bits / 8;
+        const int subw = epi_row < 128 ? epi_row : 128;
         cuuint64_t dims[2] = {(cuuint64_t)p->out_row, (cuuint64_t)p->M};
         cuuint64_t strides[1] = {(cuuint64_t)p->out_row};
-        cuuint32_t box[2] = {(cuuint32_t)subw, (cuuint32_t)BM};
+        cuuint32_t box[2] = {(cuuint32_t)subw, 32u};
         cuuint32_t estr[2] = {1, 1};
         CUresult r = g_encode_tiled(&p->tm_y, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, y, dims, strides, box, estr,
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(subw), CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -485,8 +528,12 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
         if (rc) return rc;
     }
     const bool s32 = p->out_mode == CONV_Q_OUT_S32;
-    if (p->bits == 8) return s32 ? dispatch_bn_kch<8, 1>(p, scale, y) : dispatch_bn_kch<8, 0>(p, scale, y);
-    return s32 ? dispatch_bn_kch<4, 1>(p, scale, y) : dispatch_bn_kch<4, 0>(p, scale, y);
+    const bool direct = p->cands[p->sel].direct != 0;
+    if (p->bits == 8)
+        return s32 ? dispatch_bn_kch<8, OUT_S32>(p, scale, y)
+                   : direct ? dispatch_bn_kch<8, OUT_DIRECT>(p, scale, y) : dispatch_bn_kch<8, OUT_TMA>(p, scale, y);
+    return s32 ? dispatch_bn_kch<4, OUT_S32>(p, scale, y)
+               : direct ? dispatch_bn_kch<4, OUT_DIRECT>(p, scale, y) : dispatch_bn_kch<4, OUT_TMA>(p, scale, y);
 }
 
 extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y,
@@ -571,12 +618,21 @@ extern "C" int conv_q_quantize(const void *x_fp16, int N, int H, int W, int C, f
     if (Cp == C && aligned16(x_fp16)) {
         const int64_t n_out_vec = npix * C * bits / 128;
         const int grid = grid_for(ceil_div(n_out_vec, 4), 256);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const uint4 *xs = static_cast<const uint4 *>(x_fp16);
+        uint4 *ys = static_cast<uint4 *>(xq);
         if (bits == 8)
-            quantize_flat_kernel<8, 4><<<grid, 256, 0, st>>>(static_cast<const uint4 *>(x_fp16),
-                                                            static_cast<uint4 *>(xq), n_out_vec, inv_scale);
+            CUDA_TRY(cudaLaunchKernelEx(&cfg, quantize_flat_kernel<8, 4>, xs, ys, n_out_vec, inv_scale));
         else
-            quantize_flat_kernel<4, 4><<<grid, 256, 0, st>>>(static_cast<const uint4 *>(x_fp16),
-                                                            static_cast<uint4 *>(xq), n_out_vec, inv_scale);
+            CUDA_TRY(cudaLaunchKernelEx(&cfg, quantize_flat_kernel<4, 4>, xs, ys, n_out_vec, inv_scale));
     } else {
         const int vec_per_pix = Cp * bits / 128;
         const int grid = grid_for(npix * vec_per_pix, 256);
@@ -634,5 +690,83 @@ extern "C" int conv_q_int8_peak(int iters, double *ops_per_s) {
     cudaFree(sink);
     if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "peak kernel failed: %s", cudaGetErrorString(e));
     *ops_per_s = 2.0 * 128 * 256 * 32 * (double)iters * g_num_sms / (ms * 1e-3);
+    return CONV_Q_OK;
+}
+
+// Measurement only: MMA pipeline handshake probe (see peak.cuh).  Returns the
+// achieved INT8 ops/s for `groups` groups of G MMAs (M=128, N=n) with at most
+// S-1 groups in flight (S=1: no waits).
+extern "C" CONVQ_API int conv_q_mma_pipe_probe(int groups, int G, int S, int n, double *ops_per_s) {
+    if (groups < 1 || G < 1 || S < 1 || S > 16 || n < 16 || n > 256 || (n % 16) || !ops_per_s)
+        return set_err(CONV_Q_EINVAL, "bad probe arguments");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int smem = 1024 + (128 + 256) * 128 + 256;
+    CUDA_TRY(cudaFuncSetAttribute(mma_pipe_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int *sink = nullptr;
+    CUDA_TRY(cudaMalloc(&sink, sizeof(int)));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    mma_pipe_probe_kernel<<<g_num_sms, 128, smem>>>(std::min(groups, 64), G, S, n, sink);
+    cudaEventRecord(e0);
+    mma_pipe_probe_kernel<<<g_num_sms, 128, smem>>>(groups, G, S, n, sink);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "probe kernel failed: %s", cudaGetErrorString(e));
+    *ops_per_s = 2.0 * 128 * n * 32 * (double)groups * G * g_num_sms / (ms * 1e-3);
+    return CONV_Q_OK;
+}
+
+// Measurement only: CTA-pair (cta_group::2, M=256) variant of the probe above.
+extern "C" CONVQ_API int conv_q_mma_pipe_probe2(int groups, int G, int S, int n, double *ops_per_s) {
+    if (groups < 1 || G < 1 || S < 1 || S > 16 || n < 32 || n > 256 || (n % 32) || !ops_per_s)
+        return set_err(CONV_Q_EINVAL, "bad probe arguments");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int smem = 1024 + (128 + 256) * 128 + 256;
+    CUDA_TRY(cudaFuncSetAttribute(mma_pipe_probe2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int *sink = nullptr;
+    CUDA_TRY(cudaMalloc(&sink, sizeof(int)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g_num_sms / 2 * 2);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int gw = std::min(groups, 64);
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, mma_pipe_probe2_kernel, gw, G, S, n, sink));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, mma_pipe_probe2_kernel, groups, G, S, n, sink));
+    cudaEventRecord(e1);
+    cudaError_t e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "probe2 kernel failed: %s", cudaGetErrorString(e));
+    *ops_per_s = 2.0 * 256 * n * 32 * (double)groups * G * (g_num_sms / 2) / (ms * 1e-3);
+    return CONV_Q_OK;
+}
+
+// Measurement only: per-CTA wait-cycle counters (see conv.cuh TR_*): the
+// caller passes a device buffer of >= 8 * grid u64 (zeroed), or NULL to stop.
+extern "C" CONVQ_API int conv_q_plan_set_trace(conv_q_plan_t *p, void *counters) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    p->trace = static_cast<unsigned long long *>(counters);
     return CONV_Q_OK;
 }

@@ -47,6 +47,8 @@ template <int BITS, int UNROLL>
 __global__ void __launch_bounds__(256) quantize_flat_kernel(const uint4 *__restrict__ x, uint4 *__restrict__ y,
                                                            int64_t n_out_vec, float inv_scale) {
     constexpr int IN_VEC = BITS == 8 ? 2 : 4;  // 16-byte fp16 vectors per output vector
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const float lo = -(float)(1 << (BITS - 1)), hi = (float)((1 << (BITS - 1)) - 1);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < n_out_vec;

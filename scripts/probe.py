@@ -1,0 +1,44 @@
+"""Time layers in normal / loads-only / MMA-only probe modes for every candidate.
+python scripts/probe.py l3.b1.c2 l1.b0.c2 ..."""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CODE = r'''
+import os, sys, json
+sys.path.insert(0, %r)
+import torch, numpy as np
+import paper_2202_06819_b200 as cq, workloads as wl
+name, N, bits = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+L = {l.name: l for l, _ in wl.resnet50_layers()}[name]
+g = wl.rng(9, 0)
+x, w, ss = wl.layer_inputs(g, L, N, bits)
+p = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
+xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
+y = torch.empty((N, L.P, L.Q, L.K * bits // 8), dtype=torch.uint8, device="cuda")
+res = {}
+for i, cname in enumerate(p.candidates()):
+    p.set_config(i)
+    for _ in range(3): p.run(xd, wd, sd, y)
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(20): p.run(xd, wd, sd, y)
+    e1.record(); torch.cuda.synchronize()
+    res[cname] = round(e0.elapsed_time(e1) / 20 * 1000, 1)
+print(json.dumps(res))
+''' % ROOT
+for name in sys.argv[1:]:
+    out = {}
+    for mode in (0, 1, 2):
+        env = dict(os.environ, CONV_Q_PROBE=str(mode))
+        r = subprocess.run([sys.executable, "-c", CODE, name, "256", "8"], env=env, capture_output=True, text=True)
+        out[mode] = r.stdout.strip() or r.stderr[-400:]
+    print(name)
+    import json
+    d = {m: json.loads(v) if v.startswith("{") else v for m, v in out.items()}
+    if all(isinstance(v, dict) for v in d.values()):
+        for c in d[0]:
+            print(f"  {c:24s} normal {d[0][c]:8.1f}us  loads-only {d[1][c]:8.1f}us  mma-only {d[2][c]:8.1f}us")
+    else:
+        print(d)

@@ -1,0 +1,44 @@
+"""Per-CTA wait attribution for a layer/config: python scripts/trace.py l3.b1.c2 [config...]"""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2202_06819_b200 as cq, workloads as wl
+lib = cq.load()
+lib.conv_q_plan_set_trace.restype = ctypes.c_int
+lib.conv_q_plan_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+name = sys.argv[1]
+L = {l.name: l for l, _ in wl.resnet50_layers()}[name]
+N, bits = 256, 8
+g = wl.rng(9, 0)
+x, w, ss = wl.layer_inputs(g, L, N, bits)
+p = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
+xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
+y = torch.empty((N, L.P, L.Q, L.K * bits // 8), dtype=torch.uint8, device="cuda")
+cfgs = sys.argv[2:] or p.candidates()
+names = ["prod_wait_empty", "mma_wait_full", "mma_wait_acc", "epi_wait_acc", "mma_issue", "total", "tiles"]
+for cname in cfgs:
+    p.set_config(p.candidates().index(cname))
+    for _ in range(3): p.run(xd, wd, sd, y)
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(10): p.run(xd, wd, sd, y)
+    e1.record(); torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / 10 * 1000
+    tr = torch.zeros(148 * 10, dtype=torch.int64, device="cuda")
+    h0, h1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    lib.conv_q_plan_set_trace(p._h, ctypes.c_void_p(tr.data_ptr()))
+    torch.cuda.synchronize()
+    h0.record()
+    p.run(xd, wd, sd, y)
+    h1.record()
+    torch.cuda.synchronize()
+    lib.conv_q_plan_set_trace(p._h, None)
+    t = tr.view(148, 10).double().cpu()
+    act = t[:, 5] > 0
+    m = t[act].mean(0)
+    s = "  ".join(f"{n}={m[i]/1965:6.1f}" for i, n in enumerate(names[:6]))
+    t0 = t[act, 7]; t1 = t[act, 8]; tp = t[act, 9]
+    base = t0.min()
+    print(f"{cname:26s} {us:6.1f}us (traced run {h0.elapsed_time(h1)*1000:6.1f}) ctas={int(act.sum())} "
+          f"tiles/cta={m[6]:.1f} {s} | start spread {(t0.max()-base)/1e3:.1f}us pdl_pass {(tp.min()-base)/1e3:.1f}.."
+          f"{(tp.max()-base)/1e3:.1f} end {(t1.min()-base)/1e3:.1f}..{(t1.max()-base)/1e3:.1f}us", flush=True)
