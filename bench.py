@@ -144,6 +144,10 @@ def run_ours(args):
     layers, B, bits, conv1, desc = workload_spec(args.workload)
     if args.batch:
         B = args.batch
+    B_global = B * world
+    if args.scaling == "strong":      # the global batch is split across ranks
+        B_global = B
+        _, B = wl.shard_batch(B_global, world, rank)
     g = wl.rng(4, 1000 + rank)
 
     # ---- setup (off the timed path): weights, scales, plans, buffers
@@ -286,7 +290,7 @@ def run_ours(args):
         te = torch.tensor([e0.elapsed_time(e1) / k_e2e], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(B * world / (float(te.item()) * 1e-3), 2), "unit": UNIT,
+        e2e = {"value": round(B_global / (float(te.item()) * 1e-3), 2), "unit": UNIT,
                "h2d_bytes_per_step": int(h_in.numel() * h_in.element_size()),
                "d2h_bytes_per_step": int(h_out.numel()), "ms_per_step": round(float(te.item()), 4)}
 
@@ -356,12 +360,12 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(B * world / (ms_per_step * 1e-3), 2), "unit": UNIT,
+            "metric": METRIC, "value": round(B_global / (ms_per_step * 1e-3), 2), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8" if bits == 8 else "int4",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int8" if bits == 8 else "int4",
             "data": "synthetic (seeded N(0,1) fp16 input, uniform weight codes, random-init ResNet shapes)",
             "config": {"workload": args.workload, "description": desc, "per_gpu_batch": B,
-                       "global_batch": B * world, "bits": bits, "conv_layers_per_step": len(layers),
+                       "global_batch": B_global, "bits": bits, "conv_layers_per_step": len(layers),
                        "kernels_per_step": len(layers) + 1, "parallelism": f"batch-shard dp{world}",
                        "l2": "inputs larger than L2: per-step working set %.2f GB >> 126 MB L2" % (
                            (bytes_step + B * 56 * 56 * 64 * 2) / 1e9),
@@ -499,6 +503,8 @@ def main():
     ap.add_argument("--workload", default="resnet50_int8_b256",
                     choices=["resnet50_int8_b256", "resnet18_int8_b1", "resnet18_int4_b16", "cfg1"])
     ap.add_argument("--batch", type=int, default=0, help="override per-GPU batch")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU runs its own batch; strong: the batch is split across GPUs")
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     ap.add_argument("--no-e2e", action="store_true")

@@ -175,3 +175,12 @@ def layer_inputs(g: np.random.Generator, layer: Layer, N: int, bits: int):
     sd = uniform_code_std(bits)
     ss = scale_shift(g, layer.K, layer.R * layer.S * layer.C, sd, sd, bits)
     return x, w, ss
+
+
+def shard_batch(global_batch: int, world: int, rank: int):
+    """Contiguous batch shard of `rank`: n_i = floor(N/g) + [i < N mod g].
+    Returns (first image, image count)."""
+    base, extra = divmod(global_batch, world)
+    count = base + (1 if rank < extra else 0)
+    start = rank * base + min(rank, extra)
+    return start, count
