@@ -1,6 +1,12 @@
-"""Build libconvq.so in-tree with nvcc for sm_100a (no torch extension, no JIT)."""
+"""Build libconvq.so in-tree with nvcc for sm_100a (no torch extension, no JIT).
+
+The kernel instantiations live in six translation units (kern_b{8,4}_o{0,1,2}.cu)
+compiled in parallel, plus the host library convq.cu; objects are linked into
+one shared library with the CUDA runtime linked statically."""
 from __future__ import annotations
 
+import concurrent.futures as cf
+import glob
 import os
 import subprocess
 import sys
@@ -8,34 +14,52 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libconvq.so")
-SOURCES = ["convq.cu"]
-HEADERS = ["conv.cuh", "pack.cuh", "peak.cuh", "ptx.cuh"]
+SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2)]
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-    "-shared", "--cudart", "static",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _deps():
+    return [os.path.join(CSRC, s) for s in SOURCES] + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        [os.path.join(ROOT, "include", "convq.h"), __file__]
+
+
+def _stale(target, deps) -> bool:
+    if not os.path.exists(target):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "convq.h")]
+    t = os.path.getmtime(target)
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def _compile(src, verbose):
+    nvcc = os.environ.get("NVCC", "nvcc")
+    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+    cmd = [nvcc, *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-I", os.path.join(ROOT, "include"),
+           "-c", src, "-o", obj]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-4000:]}")
+    return obj, r.stderr
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+    deps = _deps()
+    if not force and not _stale(LIB, deps):
         return LIB
+    os.makedirs(OBJ, exist_ok=True)
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    jobs = max(1, min(len(srcs), os.cpu_count() or 1))
+    with cf.ThreadPoolExecutor(jobs) as ex:
+        results = list(ex.map(lambda s: _compile(s, verbose), srcs))
+    if verbose:
+        for _, log in results:
+            sys.stderr.write(log)
     nvcc = os.environ.get("NVCC", "nvcc")
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc, *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []),
-           "-I", os.path.join(ROOT, "include"), *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
-    subprocess.check_call(cmd)
+    subprocess.check_call([nvcc, *ARCH, "-shared", "--cudart", "static", *[o for o, _ in results], "-o", tmp])
     os.replace(tmp, LIB)
     return LIB
 

@@ -67,6 +67,13 @@ struct ConvParams {
     int relu;
     int probe;           // measurement only: 0 normal, 1 = loads without MMAs, 2 = MMAs without loads
     unsigned long long *trace;  // measurement only: per-CTA wait-cycle counters (TRACE_SLOTS each), or null
+    // duplicate-aware (halo) mode, stride 1 only:
+    int Wp;              // padded input width W + 2 pad = MMA-row pitch of an output row
+    int rpt;             // output rows per 128-row tile
+    int tiles_per_img;   // ceil(P / rpt)
+    int m_tiles;         // N * tiles_per_img
+    int halo_tx;         // bytes of one halo TMA box
+    int desc_bo;         // 1: set the UMMA descriptor base offset for row-shifted windows
     const float *scale;  // [2K] scale then shift
     int32_t *y32;        // s32 output (OUT = OUT_S32)
     uint8_t *y8;         // packed output for direct stores (OUT = OUT_DIRECT)
@@ -79,13 +86,16 @@ constexpr int OUT_S32 = 1;     // raw int32 accumulators, direct global stores (
 constexpr int OUT_DIRECT = 2;  // packed codes, 16-byte direct global stores (no staging smem ->
                                // deeper operand pipeline; L2 merges the row pieces)
 
-template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB>
+template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO = 0>
 struct ConvCfg {
     // CG = CTAs per tile (1, or 2 = a CTA pair running tcgen05.mma.cta_group::2
     // with M = 256: each CTA stages its own 128 A rows and BN/2 B rows).
+    // HALO = 1: duplicate-aware A operand (section 3.1, Alg. 1):
+    // per (tile, channel block) ONE halo box of the padded input is loaded and
+    // every filter tap reads its A rows as a shifted window of it.
     static constexpr int BNL = BN / CG;                     // B rows staged per CTA
     static constexpr int LOAD_ROW = KCH * BITS / 8;        // packed bytes per row per k-block
-    static constexpr int A_SUB = BM * KCH;                  // s8 A sub-tile bytes (one k-block)
+    static constexpr int A_SUB = HALO ? 0 : BM * KCH;       // s8 A sub-tile bytes (one k-block)
     static constexpr int B_SUB = BNL * KCH;
     static constexpr int A_S8 = NSUB * A_SUB;               // per stage
     static constexpr int B_S8 = NSUB * B_SUB;
@@ -94,7 +104,9 @@ struct ConvCfg {
     static constexpr int A_PK = NSUB * A_PK_SUB;
     static constexpr int B_PK = NSUB * B_PK_SUB;
     static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
-    static constexpr int SUB_TX = (BM + BNL) * LOAD_ROW;     // TMA bytes per k-block per CTA
+    static constexpr int SUB_TX = ((HALO ? 0 : BM) + BNL) * LOAD_ROW;  // TMA bytes per k-block per CTA
+    static constexpr int HALO_BYTES = HALO ? 32768 : 0;      // one halo buffer (budget; checked at plan time)
+    static constexpr int NHALO = HALO ? 2 : 0;
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUT_BYTES = OUT == OUT_TMA ? BM * OUT_ROW : 0;   // staging per TMEM buffer
     static constexpr int NUM_EPI = BITS == 8 ? 4 : 2;               // epilogue warpgroups
@@ -110,9 +122,10 @@ struct ConvCfg {
     static constexpr int CW = BITS == 8 ? 16 : 32;                  // columns per tcgen05.ld (16 B packed)
     static constexpr int SS_BYTES = 0;
     static constexpr int BAR_BYTES = 1024;
-    static constexpr int STAGES_FIT = (SMEM_LIMIT - 1024 - BAR_BYTES - NBUF * (OUT_BYTES + SS_BYTES)) / STAGE_BYTES;
+    static constexpr int STAGES_FIT =
+        (SMEM_LIMIT - 1024 - BAR_BYTES - NBUF * (OUT_BYTES + SS_BYTES) - NHALO * HALO_BYTES) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) + BAR_BYTES;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * HALO_BYTES + BAR_BYTES;
     static constexpr int TMEM_COLS = NBUF * BN < 32 ? 32 : NBUF * BN;
     // Warp layout: epilogue warpgroups first, then (INT4) the transform
     // warpgroup, then the TMA producer and the MMA issuer as the two highest
@@ -124,9 +137,9 @@ struct ConvCfg {
     static constexpr int MMA_WARP = PROD_WARP + 1;
     static constexpr int NUM_THREADS = 32 * (MMA_WARP + 1);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
-    static constexpr bool FITS = STAGES >= 2;                     // else never instantiated
+    static constexpr bool FITS = STAGES >= 2 && (!HALO || (BITS == 8 && OUT != OUT_TMA));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
-    static_assert(NSUB == 1 || NSUB == 2 || NSUB == 4, "NSUB");
+    static_assert(NSUB >= 1 && NSUB <= 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
     static_assert(CG == 1 || CG == 2, "CG");
     static_assert(TMEM_COLS <= 512, "TMEM");
@@ -197,11 +210,11 @@ __device__ __forceinline__ uint32_t pack8_low_nibbles(const uint32_t *r) {
     return __byte_perm(__byte_perm(b01, b23, 0x0040), __byte_perm(b45, b67, 0x0040), 0x5410);
 }
 
-template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB>
-__global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>::NUM_THREADS, 1)
+template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO>
+__global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::NUM_THREADS, 1)
     conv_igemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_y, const ConvParams p) {
-    using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>;
+    using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>;
     static_assert(Cfg::FITS, "tile does not fit shared memory");
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -216,13 +229,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>::NUM_THR
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][NSUB][BM*KCH/2]
     uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][NSUB][BNL*KCH/2]
     uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [NBUF][EPB][4 quads] slabs [EPI_NSUB][32][EPI_SUBW]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(out_stage + Cfg::NBUF * (Cfg::OUT_BYTES + Cfg::SS_BYTES));
+    uint8_t *halo_buf = out_stage + Cfg::NBUF * (Cfg::OUT_BYTES + Cfg::SS_BYTES);   // HALO: [2][HALO_BYTES]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(halo_buf + Cfg::NHALO * Cfg::HALO_BYTES);
     uint64_t *full = bars;                  // TMA -> (transform | MMA)
     uint64_t *empty = bars + STAGES;        // MMA -> TMA
     uint64_t *ready = bars + 2 * STAGES;    // transform -> MMA (INT4)
     uint64_t *acc_full = bars + 3 * STAGES; // MMA -> epilogue [NBUF]
     uint64_t *acc_empty = acc_full + 4;     // epilogue -> MMA [NBUF]
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(acc_empty + 4);
+    uint64_t *hempty = acc_empty + 4;       // HALO: MMA -> TMA, halo buffer free [2]
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(hempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -245,6 +260,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>::NUM_THR
             mbar_init(&empty[s], 1);
             mbar_init(&ready[s], 4 * CG);
         }
+        for (int h = 0; h < Cfg::NHALO; ++h) mbar_init(&hempty[h], 1);
         for (int b = 0; b < Cfg::NBUF; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF * CG);
@@ -284,6 +300,56 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>::NUM_THR
         if (p.trace && lane == 0) p.trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
         int stage = 0;
         uint32_t phase = 0;
+        if constexpr (HALO) {
+            // one halo box per (tile, channel block) + the filter taps' weight
+            // k-blocks in groups of NSUB; the halo rides on the first group's barrier
+            int hcount = 0;
+            const int RS = p.R * p.S;
+            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+                const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
+                const int rt = m_blk * CG + (int)rank;            // this CTA's row tile
+                const int n = rt / p.tiles_per_img;               // (>= N: all-OOB box, rows masked)
+                const int p0 = (rt - n * p.tiles_per_img) * p.rpt;
+                const int brow = n_blk * BN + (int)rank * Cfg::BNL;
+                for (int cblk = 0; cblk < p.num_cblk; ++cblk, ++hcount) {
+                    const int hb = hcount & 1;
+                    const uint32_t hph = (hcount >> 1) & 1;
+                    for (int tap = 0; tap < RS;) {
+                        const int nsub = min(NSUB, RS - tap);
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        if (tap == 0) mbar_wait(&hempty[hb], hph ^ 1);
+                        if (elect_one()) {
+                            const int tx = nsub * Cfg::SUB_TX + (tap == 0 ? p.halo_tx : 0);
+                            if (p.probe == 2) {
+                                if (!PAIR_TX || rank == 0) mbar_arrive(&full[stage]);
+                            } else {
+                                if constexpr (PAIR_TX) {
+                                    const uint32_t fb = full0_leader + 8u * stage;
+                                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * tx);
+                                    if (tap == 0)
+                                        tma_load_4d_cg2(halo_buf + hb * Cfg::HALO_BYTES, &tm_a, fb, cblk * Cfg::LOAD_ROW,
+                                                        -p.pad, p0 - p.pad, n, pol_a);
+                                    for (int j = 0; j < nsub; ++j)
+                                        tma_load_2d_cg2(b_s8 + stage * Cfg::B_S8 + j * Cfg::B_SUB, &tm_b, fb,
+                                                        (tap + j) * p.row_bytes + cblk * Cfg::LOAD_ROW, brow, pol_b);
+                                } else {
+                                    mbar_arrive_expect_tx(&full[stage], tx);
+                                    if (tap == 0)
+                                        tma_load_4d(halo_buf + hb * Cfg::HALO_BYTES, &tm_a, &full[stage],
+                                                    cblk * Cfg::LOAD_ROW, -p.pad, p0 - p.pad, n, pol_a);
+                                    for (int j = 0; j < nsub; ++j)
+                                        tma_load_2d(b_s8 + stage * Cfg::B_S8 + j * Cfg::B_SUB, &tm_b, &full[stage],
+                                                    (tap + j) * p.row_bytes + cblk * Cfg::LOAD_ROW, brow, pol_b);
+                                }
+                            }
+                        }
+                        __syncwarp();
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        tap += nsub;
+                    }
+                }
+            }
+        } else
         for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
             const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
             const int m0 = m_blk * (BM * CG) + (int)rank * BM;   // this CTA's first output pixel
@@ -345,6 +411,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>::NUM_THR
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
+            int hcount = 0;
             for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++local) {
                 const int buf = local % Cfg::NBUF;
                 const uint32_t aphase = (local / Cfg::NBUF) & 1;
@@ -358,6 +425,62 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>::NUM_THR
                 }
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + buf * BN;
+                if constexpr (HALO) {
+                    // filter tap (r, s) reads the halo rows starting at r*Wp + s:
+                    // the duplicate-aware load of PAPER.md Alg. 1, with the
+                    // "genuine index" remap done by the UMMA descriptor start address
+                    const int RS = p.R * p.S;
+                    const uint32_t halo0 = smem_u32(halo_buf);
+                    for (int cblk = 0; cblk < p.num_cblk; ++cblk, ++hcount) {
+                        const int hb = hcount & 1;
+                        int r = 0, s = 0;
+                        for (int tap = 0; tap < RS;) {
+                            const int nsub = min(NSUB, RS - tap);
+                            mbar_wait(&full[stage], phase);
+                            tc_fence_after();
+                            if (elect_one()) {
+                                if (p.probe == 1) {
+                                    mbar_arrive(&empty[stage]);
+                                    if (tap + nsub == RS) mbar_arrive(&hempty[hb]);
+                                    if constexpr (CG == 2) {
+                                        mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
+                                        if (tap + nsub == RS) mbar_arrive_cluster(mapa_shared(smem_u32(&hempty[hb]), 1));
+                                    }
+                                } else {
+                                    const uint64_t bd0 = b_desc0 + (uint64_t)((stage * Cfg::B_S8) >> 4);
+                                    int rr = r, ss = s;
+#pragma unroll
+                                    for (int j = 0; j < NSUB; ++j) {
+                                        if (j < nsub) {
+                                            const uint32_t a_addr = halo0 + hb * Cfg::HALO_BYTES + (rr * p.Wp + ss) * KCH;
+                                            uint64_t ad = umma_desc_kmajor(a_addr, KCH);
+                                            if (p.desc_bo) ad |= (uint64_t)((a_addr >> 7) & 7) << 49;
+                                            const uint64_t bd = bd0 + (uint64_t)((j * Cfg::B_SUB) >> 4);
+#pragma unroll
+                                            for (int k = 0; k < KCH / 32; ++k) {
+                                                const uint32_t acc = (cblk | (tap + j) | k) != 0;
+                                                if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
+                                                else mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
+                                            }
+                                            if (++ss == p.S) { ss = 0; ++rr; }
+                                        }
+                                    }
+                                    if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
+                                    else mma_commit(&empty[stage]);
+                                    if (tap + nsub == RS) {        // last use of this halo buffer
+                                        if constexpr (CG == 2) mma_commit_cg2_mc(&hempty[hb], 0x3);
+                                        else mma_commit(&hempty[hb]);
+                                    }
+                                }
+                            }
+                            __syncwarp();
+                            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                            for (int j = 0; j < nsub; ++j)
+                                if (++s == p.S) { s = 0; ++r; }
+                            tap += nsub;
+                        }
+                    }
+                } else
                 for (int kb = 0; kb < p.num_kb; kb += NSUB) {
                     const int nsub = min(NSUB, p.num_kb - kb);
                     long long t0 = p.trace ? clock64() : 0;
@@ -433,7 +556,17 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>::NUM_THR
         for (int tile = tile0 + b * tstep; tile < p.num_tiles; tile += Cfg::NBUF * tstep, ++j) {
             const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
             const int mrow0 = m_blk * (BM * CG) + (int)rank * BM;
-            const int m = mrow0 + row;
+            int m = mrow0 + row;
+            if constexpr (HALO) {
+                // MMA row -> (output row within the tile, padded column); the
+                // S-1 right-most padded columns and rows past the tile are discarded
+                const int rt = m_blk * CG + (int)rank;
+                const int n = rt / p.tiles_per_img;
+                const int pl = row / p.Wp, qq = row - pl * p.Wp;
+                const int pp = (rt - n * p.tiles_per_img) * p.rpt + pl;
+                const bool ok = rt < p.m_tiles && pl < p.rpt && pp < p.P && qq < p.Q;
+                m = ok ? (n * p.P + pp) * p.Q + qq : p.M;
+            }
             if (OUT == OUT_TMA) {   // this warp's slab must have been read out by its previous store
                 if (lane == 0) tma_store_wait_read0();
                 __syncwarp();
@@ -446,83 +579,101 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>::NUM_THR
             }
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + b * BN + half * Cfg::EPI_COLS;
-#pragma unroll 1
-            for (int c = 0; c < Cfg::EPI_COLS / Cfg::CW; ++c) {
-                uint32_t v[Cfg::CW];
-                if constexpr (Cfg::CW == 16) tmem_ld_32x32b_x16(taddr + c * Cfg::CW, v);
-                else tmem_ld_32x32b_x32(taddr + c * Cfg::CW, v);
-                if (c == Cfg::EPI_COLS / Cfg::CW - 1) {  // this warp's columns are in registers
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if constexpr (CG == 2) mbar_arrive_cluster(acc_empty_leader);
-                        else mbar_arrive(&acc_empty[b]);
-                    }
+            // TMEM -> registers, software-pipelined: the load of chunk c+1 is in
+            // flight while chunk c is requantized (tcgen05.wait::ld waits for all
+            // of this thread's loads, so each wait covers exactly one chunk).
+            constexpr int NCH = Cfg::EPI_COLS / Cfg::CW;
+            auto release_acc = [&]() {   // every column of this warp is in registers
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2) mbar_arrive_cluster(acc_empty_leader);
+                    else mbar_arrive(&acc_empty[b]);
                 }
-                const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
-                const int col0 = n_blk * BN + ccol;
-                if (OUT == OUT_S32) {
-                    if (m < p.M) {
-                        int32_t *dst = p.y32 + (int64_t)m * p.K + col0;
-                        if (col0 + Cfg::CW <= p.K) {
+            };
+            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c) {
+                    const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
+                    const int col0 = n_blk * BN + ccol;
+                    if (OUT == OUT_S32) {
+                        if (m < p.M) {
+                            int32_t *dst = p.y32 + (int64_t)m * p.K + col0;
+                            if (col0 + Cfg::CW <= p.K) {
 #pragma unroll
-                            for (int q = 0; q < Cfg::CW; q += 4) {
-                                int4 t;
-                                t.x = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
-                                t.y = BITS == 4 ? ((int)v[q + 1] >> 8) : (int)v[q + 1];
-                                t.z = BITS == 4 ? ((int)v[q + 2] >> 8) : (int)v[q + 2];
-                                t.w = BITS == 4 ? ((int)v[q + 3] >> 8) : (int)v[q + 3];
-                                *reinterpret_cast<int4 *>(dst + q) = t;
+                                for (int q = 0; q < Cfg::CW; q += 4) {
+                                    int4 t;
+                                    t.x = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
+                                    t.y = BITS == 4 ? ((int)v[q + 1] >> 8) : (int)v[q + 1];
+                                    t.z = BITS == 4 ? ((int)v[q + 2] >> 8) : (int)v[q + 2];
+                                    t.w = BITS == 4 ? ((int)v[q + 3] >> 8) : (int)v[q + 3];
+                                    *reinterpret_cast<int4 *>(dst + q) = t;
+                                }
+                            } else {
+                                for (int q = 0; q < Cfg::CW && col0 + q < p.K; ++q)
+                                    dst[q] = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
+                            }
+                        }
+                    } else {
+                        uint32_t r[Cfg::CW];
+                        if (col0 + Cfg::CW <= p.K) {
+                            const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
+                            const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
+#pragma unroll
+                            for (int q = 0; q < Cfg::CW / 4; ++q) {
+                                const float4 sa = __ldg(s4 + q), sb = __ldg(h4 + q);
+                                const int x0 = BITS == 4 ? ((int)v[4 * q] >> 8) : (int)v[4 * q];
+                                const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
+                                const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
+                                const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
+                                r[4 * q] = requant_bits(x0, sa.x, sb.x, lo, hi);
+                                r[4 * q + 1] = requant_bits(x1, sa.y, sb.y, lo, hi);
+                                r[4 * q + 2] = requant_bits(x2, sa.z, sb.z, lo, hi);
+                                r[4 * q + 3] = requant_bits(x3, sa.w, sb.w, lo, hi);
                             }
                         } else {
-                            for (int q = 0; q < Cfg::CW && col0 + q < p.K; ++q)
-                                dst[q] = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
-                        }
-                    }
-                } else {
-                    uint32_t r[Cfg::CW];
-                    if (col0 + Cfg::CW <= p.K) {
-                        const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
-                        const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
 #pragma unroll
-                        for (int q = 0; q < Cfg::CW / 4; ++q) {
-                            const float4 sa = __ldg(s4 + q), sb = __ldg(h4 + q);
-                            const int x0 = BITS == 4 ? ((int)v[4 * q] >> 8) : (int)v[4 * q];
-                            const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
-                            const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
-                            const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
-                            r[4 * q] = requant_bits(x0, sa.x, sb.x, lo, hi);
-                            r[4 * q + 1] = requant_bits(x1, sa.y, sb.y, lo, hi);
-                            r[4 * q + 2] = requant_bits(x2, sa.z, sb.z, lo, hi);
-                            r[4 * q + 3] = requant_bits(x3, sa.w, sb.w, lo, hi);
+                            for (int q = 0; q < Cfg::CW; ++q) {
+                                const bool ok = col0 + q < p.K;  // columns past K are never stored
+                                const float sc = ok ? __ldg(p.scale + col0 + q) : 0.f;
+                                const float sh = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
+                                r[q] = requant_bits(BITS == 4 ? ((int)v[q] >> 8) : (int)v[q], sc, sh, lo, hi);
+                            }
                         }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < Cfg::CW; ++q) {
-                            const bool ok = col0 + q < p.K;  // columns past K are never stored
-                            const float sc = ok ? __ldg(p.scale + col0 + q) : 0.f;
-                            const float sh = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
-                            r[q] = requant_bits(BITS == 4 ? ((int)v[q] >> 8) : (int)v[q], sc, sh, lo, hi);
+                        uint4 pk;   // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
+                        if constexpr (BITS == 8) {
+                            pk = make_uint4(pack4_low_bytes(r[0], r[1], r[2], r[3]), pack4_low_bytes(r[4], r[5], r[6], r[7]),
+                                            pack4_low_bytes(r[8], r[9], r[10], r[11]),
+                                            pack4_low_bytes(r[12], r[13], r[14], r[15]));
+                        } else {
+                            pk = make_uint4(pack8_low_nibbles(r), pack8_low_nibbles(r + 8), pack8_low_nibbles(r + 16),
+                                            pack8_low_nibbles(r + 24));
+                        }
+                        const int sbyte = c * 16;                 // byte within this warp's slab row
+                        if constexpr (OUT == OUT_TMA) {
+                            uint8_t *sub = slab + (sbyte / Cfg::EPI_SUBW) * (32 * Cfg::EPI_SUBW);
+                            *reinterpret_cast<uint4 *>(sub + swz<Cfg::EPI_SUBW>(lane * Cfg::EPI_SUBW + sbyte % Cfg::EPI_SUBW)) = pk;
+                        } else {
+                            const int gbyte = n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + sbyte;
+                            if (m < p.M && gbyte < p.out_row)
+                                *reinterpret_cast<uint4 *>(p.y8 + (int64_t)m * p.out_row + gbyte) = pk;
                         }
                     }
-                    uint4 pk;   // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
-                    if constexpr (BITS == 8) {
-                        pk = make_uint4(pack4_low_bytes(r[0], r[1], r[2], r[3]), pack4_low_bytes(r[4], r[5], r[6], r[7]),
-                                        pack4_low_bytes(r[8], r[9], r[10], r[11]),
-                                        pack4_low_bytes(r[12], r[13], r[14], r[15]));
-                    } else {
-                        pk = make_uint4(pack8_low_nibbles(r), pack8_low_nibbles(r + 8), pack8_low_nibbles(r + 16),
-                                        pack8_low_nibbles(r + 24));
-                    }
-                    const int sbyte = c * 16;                 // byte within this warp's slab row
-                    if constexpr (OUT == OUT_TMA) {
-                        uint8_t *sub = slab + (sbyte / Cfg::EPI_SUBW) * (32 * Cfg::EPI_SUBW);
-                        *reinterpret_cast<uint4 *>(sub + swz<Cfg::EPI_SUBW>(lane * Cfg::EPI_SUBW + sbyte % Cfg::EPI_SUBW)) = pk;
-                    } else {
-                        const int gbyte = n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + sbyte;
-                        if (m < p.M && gbyte < p.out_row)
-                            *reinterpret_cast<uint4 *>(p.y8 + (int64_t)m * p.out_row + gbyte) = pk;
-                    }
+            };
+            uint32_t va[Cfg::CW], vb[Cfg::CW];
+            tmem_ld_issue<Cfg::CW>(taddr, va);
+            tmem_ld_wait_regs(va);
+#pragma unroll 1
+            for (int c = 0; c < NCH; c += 2) {
+                const bool more1 = c + 1 < NCH;
+                if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
+                else release_acc();
+                process(va, c);
+                if (more1) {
+                    tmem_ld_wait_regs(vb);
+                    const bool more2 = c + 2 < NCH;
+                    if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
+                    else release_acc();
+                    process(vb, c + 1);
+                    if (more2) tmem_ld_wait_regs(va);
                 }
             }
             if (OUT == OUT_TMA) {

@@ -22,9 +22,9 @@
 #include <vector>
 
 #include "../../include/convq.h"
-#include "conv.cuh"
 #include "pack.cuh"
 #include "peak.cuh"
+#include "plan.cuh"
 
 using namespace convq;
 
@@ -32,7 +32,9 @@ using namespace convq;
 static thread_local std::string g_err;
 static thread_local int g_status = CONV_Q_OK;
 
-static int set_err(int code, const char *fmt, ...) {
+namespace convq {
+int g_num_sms = 0;
+int set_err(int code, const char *fmt, ...) {
     char buf[512];
     va_list ap;
     va_start(ap, fmt);
@@ -42,11 +44,7 @@ static int set_err(int code, const char *fmt, ...) {
     g_status = code;
     return code;
 }
-#define CUDA_TRY(expr)                                                                              \
-    do {                                                                                            \
-        cudaError_t e_ = (expr);                                                                    \
-        if (e_ != cudaSuccess) return set_err(CONV_Q_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
-    } while (0)
+}  // namespace convq
 
 extern "C" const char *conv_q_last_error(void) { return g_err.c_str(); }
 extern "C" int conv_q_last_status(void) { return g_status; }
@@ -63,7 +61,6 @@ typedef CUresult (*PFN_encodeIm2col_t)(CUtensorMap *, CUtensorMapDataType, cuuin
                                        CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static PFN_encodeTiled_t g_encode_tiled = nullptr;
 static PFN_encodeIm2col_t g_encode_im2col = nullptr;
-static int g_num_sms = 0;
 static std::once_flag g_init_once;
 static int g_init_status = CONV_Q_OK;
 static std::string g_init_msg;
@@ -112,34 +109,10 @@ static CUtensorMapSwizzle swizzle_for(int span) {
 }
 
 // ============================================================== plan
-struct Cand {
-    int bn, kch, cg, nsub;  // N tile, channels per k-block, CTAs per tile, k-blocks per stage
-    int direct;             // packed output by direct stores (1) or smem staging + TMA store (0)
-};
-
-struct conv_q_plan_s {
-    int N, H, W, C, K, R, S, stride, pad, bits;
-    int P, Q;
-    int64_t M, Kg;
-    int row_bytes;     // C*bits/8
-    int out_row;       // K*bits/8
-    int relu = 0, out_mode = CONV_Q_OUT_PACKED;
-    cudaStream_t stream = nullptr;
-    std::vector<Cand> cands;
-    int sel = 0;
-    float tuned_us = -1.f;
-    int probe = 0;     // CONV_Q_PROBE (measurement only; results are garbage when != 0)
-    unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
-    // tensor-map cache (re-encoded when a pointer or the config changes)
-    CUtensorMap tm_a, tm_b, tm_y;
-    const void *c_x = nullptr, *c_w = nullptr, *c_y = nullptr;
-    int c_sel = -1, c_mode = -1;
-};
-
 static std::string cand_name(const conv_q_plan_s *p, int i) {
     char b[64];
-    snprintf(b, sizeof b, "bm%d_bn%d_kc%dx%d_c%d%s", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
-             p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "");
+    snprintf(b, sizeof b, "bm%d_bn%d_kc%dx%d_c%d%s%s", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
+             p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "", p->cands[i].halo ? "_h" : "");
     return b;
 }
 
@@ -187,25 +160,6 @@ static void cache_store_locked() {
     rename(tmp.c_str(), path);
 }
 
-static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
-
-// Whether a TileConfig fits shared memory (>= 2 stages) for both output modes.
-template <int BITS>
-static bool cand_fits(const Cand &c) {
-#define CONVQ_FIT(BN_, KC_, NS_, CG_)                                                        \
-    if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.cg == CG_)                         \
-        return (c.direct ? ConvCfg<BITS, BN_, KC_, OUT_DIRECT, CG_, NS_>::FITS                \
-                         : ConvCfg<BITS, BN_, KC_, OUT_TMA, CG_, NS_>::FITS) &&               \
-               ConvCfg<BITS, BN_, KC_, OUT_S32, CG_, NS_>::FITS;
-#define CONVQ_FITS_BN(KC_, NS_, CG_) CONVQ_FIT(64, KC_, NS_, CG_) CONVQ_FIT(128, KC_, NS_, CG_) CONVQ_FIT(256, KC_, NS_, CG_)
-    CONVQ_FITS_BN(128, 2, 1) CONVQ_FITS_BN(128, 1, 1) CONVQ_FITS_BN(64, 4, 1) CONVQ_FITS_BN(64, 1, 1)
-    CONVQ_FITS_BN(32, 4, 1) CONVQ_FITS_BN(32, 1, 1)
-    CONVQ_FITS_BN(128, 2, 2) CONVQ_FITS_BN(128, 1, 2) CONVQ_FITS_BN(64, 4, 2) CONVQ_FITS_BN(64, 1, 2)
-    CONVQ_FITS_BN(32, 4, 2) CONVQ_FITS_BN(32, 1, 2)
-#undef CONVQ_FITS_BN
-#undef CONVQ_FIT
-    return false;
-}
 
 static void enumerate_candidates(conv_q_plan_s *p) {
     p->cands.clear();
@@ -225,6 +179,21 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                     p->cands.push_back(cand);
                 }
             }
+    // duplicate-aware (halo) candidates: stride-1 INT8 R x S convolutions whose
+    // halo box (rows covering 128 MMA rows + the largest tap shift) fits 32 KB
+    const int Wp = p->W + 2 * p->pad;
+    if (p->bits == 8 && p->stride == 1 && p->R * p->S > 1 && Wp <= BM && p->C % 64 == 0) {
+        const int kch = p->C % 128 == 0 ? 128 : 64;
+        const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
+        if ((int64_t)halo_rows * Wp * kch <= 32768 && halo_rows <= 256)
+            for (int cg : {1, 2})
+                for (int bn : {64, 128, 256}) {
+                    if (bn > 64 && bn / 2 >= p->K) continue;
+                    Cand cand{bn, kch, cg, 3, 1};
+                    cand.halo = 1;
+                    if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                }
+    }
 }
 
 // Default pick before tuning: deepest K chunk, then the widest N tile whose
@@ -322,6 +291,7 @@ extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, 
     enumerate_candidates(p);
     p->sel = default_candidate(p);
     if (const char *pr = getenv("CONV_Q_PROBE")) p->probe = atoi(pr);
+    if (const char *bo = getenv("CONV_Q_DESC_BO")) p->desc_bo = atoi(bo);
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
         cache_load_locked();
@@ -393,76 +363,26 @@ extern "C" int conv_q_plan_info(const conv_q_plan_t *p, conv_q_info_t *info) {
     return CONV_Q_OK;
 }
 
-// ============================================================== launch
-template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB>
-static int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
-    using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG, NSUB>;
-    auto kern = conv_igemm_kernel<BITS, BN, KCH, OUT, CG, NSUB>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-        attr_set = true;
-    }
-    ConvParams prm;
-    prm.N = p->N; prm.H = p->H; prm.W = p->W; prm.C = p->C; prm.K = p->K; prm.R = p->R; prm.S = p->S;
-    prm.stride = p->stride; prm.pad = p->pad; prm.P = p->P; prm.Q = p->Q; prm.M = (int)p->M;
-    prm.row_bytes = p->row_bytes;
-    prm.num_cblk = p->C / KCH;
-    prm.num_kb = p->R * p->S * prm.num_cblk;
-    prm.n_tiles = (int)ceil_div(p->K, BN);
-    prm.num_tiles = (int)(ceil_div(p->M, BM * CG) * prm.n_tiles);
-    prm.relu = p->relu;
-    prm.probe = p->probe;
-    prm.trace = p->trace;
-    prm.scale = scale;
-    prm.y32 = static_cast<int32_t *>(y);
-    prm.y8 = static_cast<uint8_t *>(y);
-    prm.out_row = p->out_row;
-    const int clusters = std::min(prm.num_tiles, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(clusters * CG);
-    cfg.blockDim = dim3(Cfg::NUM_THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM;
-    cfg.stream = p->stream;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (griddepcontrol in the kernel)
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p->tm_a, p->tm_b, p->tm_y, prm));
-    return CONV_Q_OK;
-}
-
-template <int BITS, int OUT>
-static int dispatch_bn_kch(conv_q_plan_s *p, const float *scale, void *y) {
-    const Cand c = p->cands[p->sel];
-#define CONVQ_CASE(BN_, KC_, NS_, CG_)                                            \
-    if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.cg == CG_) {          \
-        if constexpr (ConvCfg<BITS, BN_, KC_, OUT, CG_, NS_>::FITS)             \
-            return launch_conv<BITS, BN_, KC_, OUT, CG_, NS_>(p, scale, y);     \
-        else                                                                    \
-            return set_err(CONV_Q_EUNSUPPORTED, "tile config exceeds shared memory"); \
-    }
-#define CONVQ_CASES_BN(KC_, NS_, CG_) \
-    CONVQ_CASE(64, KC_, NS_, CG_) CONVQ_CASE(128, KC_, NS_, CG_) CONVQ_CASE(256, KC_, NS_, CG_)
-    CONVQ_CASES_BN(128, 2, 1) CONVQ_CASES_BN(128, 1, 1) CONVQ_CASES_BN(64, 4, 1) CONVQ_CASES_BN(64, 1, 1)
-    CONVQ_CASES_BN(32, 4, 1) CONVQ_CASES_BN(32, 1, 1)
-    CONVQ_CASES_BN(128, 2, 2) CONVQ_CASES_BN(128, 1, 2) CONVQ_CASES_BN(64, 4, 2) CONVQ_CASES_BN(64, 1, 2)
-    CONVQ_CASES_BN(32, 4, 2) CONVQ_CASES_BN(32, 1, 2)
-#undef CONVQ_CASES_BN
-#undef CONVQ_CASE
-    return set_err(CONV_Q_EUNSUPPORTED, "no kernel instantiation for bn=%d kch=%d nsub=%d cg=%d", c.bn, c.kch,
-                   c.nsub, c.cg);
-}
-
 static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) {
     const Cand c = p->cands[p->sel];
     const int load_row = c.kch * p->bits / 8;
     const CUtensorMapSwizzle sw_ld = swizzle_for(load_row);
+    // A (halo mode): tiled 4-D box {KCH bytes, Wp, halo rows, 1} of the
+    // padded input starting at (w, h) = (-pad, p0-pad): the duplicate-free
+    // "genuine" data of PAPER.md section 3.1; OOB (padding) is zero-filled.
+    if (c.halo) {
+        const int Wp = p->W + 2 * p->pad;
+        const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
+        cuuint64_t dims[4] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->W, (cuuint64_t)p->H, (cuuint64_t)p->N};
+        cuuint64_t strides[3] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->row_bytes * p->W,
+                                 (cuuint64_t)p->row_bytes * p->W * p->H};
+        cuuint32_t box[4] = {(cuuint32_t)load_row, (cuuint32_t)Wp, (cuuint32_t)halo_rows, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = g_encode_tiled(&p->tm_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(x), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw_ld,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(x halo) failed: %d", (int)r);
+    } else
     // A: packed NHWC activations, im2col mode ("im2col layout"),
     // {C bytes, W, H, N}; the bounding box walks output pixels with the conv
     // stride; the corners make out-of-image taps read as zero (padding).
@@ -530,10 +450,8 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
     const bool s32 = p->out_mode == CONV_Q_OUT_S32;
     const bool direct = p->cands[p->sel].direct != 0;
     if (p->bits == 8)
-        return s32 ? dispatch_bn_kch<8, OUT_S32>(p, scale, y)
-                   : direct ? dispatch_bn_kch<8, OUT_DIRECT>(p, scale, y) : dispatch_bn_kch<8, OUT_TMA>(p, scale, y);
-    return s32 ? dispatch_bn_kch<4, OUT_S32>(p, scale, y)
-               : direct ? dispatch_bn_kch<4, OUT_DIRECT>(p, scale, y) : dispatch_bn_kch<4, OUT_TMA>(p, scale, y);
+        return s32 ? dispatch_conv_8_1(p, scale, y) : direct ? dispatch_conv_8_2(p, scale, y) : dispatch_conv_8_0(p, scale, y);
+    return s32 ? dispatch_conv_4_1(p, scale, y) : direct ? dispatch_conv_4_2(p, scale, y) : dispatch_conv_4_0(p, scale, y);
 }
 
 extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y,

@@ -1,0 +1,189 @@
+// plan.cuh -- internal (not part of the C ABI): the plan structure, the
+// TileConfig description and the templated launcher shared by the kernel
+// translation units (kern_*.cu) and the host library (convq.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/convq.h"
+#include "conv.cuh"
+
+namespace convq {
+
+int set_err(int code, const char *fmt, ...);   // thread-local last error (convq.cu)
+extern int g_num_sms;
+
+#define CUDA_TRY(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t e_ = (expr);                                                                    \
+        if (e_ != cudaSuccess) return set_err(CONV_Q_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+struct Cand {
+    int bn, kch, cg, nsub;  // N tile, channels per k-block, CTAs per tile, k-blocks per stage
+    int direct;             // packed output by direct stores (1) or smem staging + TMA store (0)
+    int halo = 0;           // duplicate-aware halo A operand (stride 1 only)
+};
+
+}  // namespace convq
+
+struct conv_q_plan_s {
+    using Cand = convq::Cand;
+    int N, H, W, C, K, R, S, stride, pad, bits;
+    int P, Q;
+    int64_t M, Kg;
+    int row_bytes;     // C*bits/8
+    int out_row;       // K*bits/8
+    int relu = 0, out_mode = CONV_Q_OUT_PACKED;
+    cudaStream_t stream = nullptr;
+    std::vector<Cand> cands;
+    int sel = 0;
+    float tuned_us = -1.f;
+    int probe = 0;     // CONV_Q_PROBE (measurement only; results are garbage when != 0)
+    int desc_bo = 0;   // CONV_Q_DESC_BO: UMMA base-offset field for row-shifted halo windows (measured: the
+                       // swizzle follows absolute smem address bits, so 0 is correct)
+    unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
+    // tensor-map cache (re-encoded when a pointer or the config changes)
+    CUtensorMap tm_a, tm_b, tm_y;
+    const void *c_x = nullptr, *c_w = nullptr, *c_y = nullptr;
+    int c_sel = -1, c_mode = -1;
+};
+
+
+namespace convq {
+
+// Whether a TileConfig fits shared memory (>= 2 stages) for both output modes.
+template <int BITS>
+inline bool cand_fits(const Cand &c) {
+    if (c.halo) {
+#define CONVQ_HFIT(BN_, KC_, CG_)                                                                   \
+        if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_)                                             \
+            return ConvCfg<BITS, BN_, KC_, OUT_DIRECT, CG_, 3, 1>::FITS && ConvCfg<BITS, BN_, KC_, OUT_S32, CG_, 3, 1>::FITS;
+        CONVQ_HFIT(64, 128, 1) CONVQ_HFIT(128, 128, 1) CONVQ_HFIT(256, 128, 1)
+        CONVQ_HFIT(64, 64, 1) CONVQ_HFIT(128, 64, 1) CONVQ_HFIT(256, 64, 1)
+        CONVQ_HFIT(64, 128, 2) CONVQ_HFIT(128, 128, 2) CONVQ_HFIT(256, 128, 2)
+        CONVQ_HFIT(64, 64, 2) CONVQ_HFIT(128, 64, 2) CONVQ_HFIT(256, 64, 2)
+#undef CONVQ_HFIT
+        return false;
+    }
+#define CONVQ_FIT(BN_, KC_, NS_, CG_)                                                        \
+    if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.cg == CG_)                         \
+        return (c.direct ? ConvCfg<BITS, BN_, KC_, OUT_DIRECT, CG_, NS_>::FITS                \
+                         : ConvCfg<BITS, BN_, KC_, OUT_TMA, CG_, NS_>::FITS) &&               \
+               ConvCfg<BITS, BN_, KC_, OUT_S32, CG_, NS_>::FITS;
+#define CONVQ_FITS_BN(KC_, NS_, CG_) CONVQ_FIT(64, KC_, NS_, CG_) CONVQ_FIT(128, KC_, NS_, CG_) CONVQ_FIT(256, KC_, NS_, CG_)
+    CONVQ_FITS_BN(128, 2, 1) CONVQ_FITS_BN(128, 1, 1) CONVQ_FITS_BN(64, 4, 1) CONVQ_FITS_BN(64, 1, 1)
+    CONVQ_FITS_BN(32, 4, 1) CONVQ_FITS_BN(32, 1, 1)
+    CONVQ_FITS_BN(128, 2, 2) CONVQ_FITS_BN(128, 1, 2) CONVQ_FITS_BN(64, 4, 2) CONVQ_FITS_BN(64, 1, 2)
+    CONVQ_FITS_BN(32, 4, 2) CONVQ_FITS_BN(32, 1, 2)
+#undef CONVQ_FITS_BN
+#undef CONVQ_FIT
+    return false;
+}
+
+
+// ============================================================== launch
+template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO = 0>
+inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
+    using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>;
+    auto kern = conv_igemm_kernel<BITS, BN, KCH, OUT, CG, NSUB, HALO>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+        attr_set = true;
+    }
+    ConvParams prm;
+    prm.N = p->N; prm.H = p->H; prm.W = p->W; prm.C = p->C; prm.K = p->K; prm.R = p->R; prm.S = p->S;
+    prm.stride = p->stride; prm.pad = p->pad; prm.P = p->P; prm.Q = p->Q; prm.M = (int)p->M;
+    prm.row_bytes = p->row_bytes;
+    prm.num_cblk = p->C / KCH;
+    prm.num_kb = p->R * p->S * prm.num_cblk;
+    prm.n_tiles = (int)ceil_div(p->K, BN);
+    prm.num_tiles = (int)(ceil_div(p->M, BM * CG) * prm.n_tiles);
+    prm.Wp = p->W + 2 * p->pad;
+    prm.rpt = std::max(1, std::min(p->P, BM / prm.Wp));
+    prm.tiles_per_img = (int)ceil_div(p->P, prm.rpt);
+    prm.m_tiles = p->N * prm.tiles_per_img;
+    const int halo_rows = (int)ceil_div(BM + (p->R - 1) * prm.Wp + p->S - 1, prm.Wp);
+    prm.halo_tx = halo_rows * prm.Wp * Cfg::LOAD_ROW;
+    prm.desc_bo = p->desc_bo;
+    if (HALO) prm.num_tiles = (int)(ceil_div(prm.m_tiles, CG) * prm.n_tiles);
+    prm.relu = p->relu;
+    prm.probe = p->probe;
+    prm.trace = p->trace;
+    prm.scale = scale;
+    prm.y32 = static_cast<int32_t *>(y);
+    prm.y8 = static_cast<uint8_t *>(y);
+    prm.out_row = p->out_row;
+    const int clusters = std::min(prm.num_tiles, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * CG);
+    cfg.blockDim = dim3(Cfg::NUM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = p->stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (griddepcontrol in the kernel)
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p->tm_a, p->tm_b, p->tm_y, prm));
+    return CONV_Q_OK;
+}
+
+template <int BITS, int OUT>
+inline int dispatch_bn_kch(conv_q_plan_s *p, const float *scale, void *y) {
+    const Cand c = p->cands[p->sel];
+    if (c.halo) {
+#define CONVQ_HCASE(BN_, KC_, CG_)                                                                 \
+        if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_) {                                          \
+            if constexpr (ConvCfg<BITS, BN_, KC_, OUT, CG_, 3, 1>::FITS)                           \
+                return launch_conv<BITS, BN_, KC_, OUT, CG_, 3, 1>(p, scale, y);                   \
+            else                                                                                   \
+                return set_err(CONV_Q_EUNSUPPORTED, "halo config unavailable for this output mode");  \
+        }
+        CONVQ_HCASE(64, 128, 1) CONVQ_HCASE(128, 128, 1) CONVQ_HCASE(256, 128, 1)
+        CONVQ_HCASE(64, 64, 1) CONVQ_HCASE(128, 64, 1) CONVQ_HCASE(256, 64, 1)
+        CONVQ_HCASE(64, 128, 2) CONVQ_HCASE(128, 128, 2) CONVQ_HCASE(256, 128, 2)
+        CONVQ_HCASE(64, 64, 2) CONVQ_HCASE(128, 64, 2) CONVQ_HCASE(256, 64, 2)
+#undef CONVQ_HCASE
+        return set_err(CONV_Q_EUNSUPPORTED, "no halo kernel for bn=%d kch=%d cg=%d", c.bn, c.kch, c.cg);
+    }
+#define CONVQ_CASE(BN_, KC_, NS_, CG_)                                            \
+    if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.cg == CG_) {          \
+        if constexpr (ConvCfg<BITS, BN_, KC_, OUT, CG_, NS_>::FITS)             \
+            return launch_conv<BITS, BN_, KC_, OUT, CG_, NS_>(p, scale, y);     \
+        else                                                                    \
+            return set_err(CONV_Q_EUNSUPPORTED, "tile config exceeds shared memory"); \
+    }
+#define CONVQ_CASES_BN(KC_, NS_, CG_) \
+    CONVQ_CASE(64, KC_, NS_, CG_) CONVQ_CASE(128, KC_, NS_, CG_) CONVQ_CASE(256, KC_, NS_, CG_)
+    CONVQ_CASES_BN(128, 2, 1) CONVQ_CASES_BN(128, 1, 1) CONVQ_CASES_BN(64, 4, 1) CONVQ_CASES_BN(64, 1, 1)
+    CONVQ_CASES_BN(32, 4, 1) CONVQ_CASES_BN(32, 1, 1)
+    CONVQ_CASES_BN(128, 2, 2) CONVQ_CASES_BN(128, 1, 2) CONVQ_CASES_BN(64, 4, 2) CONVQ_CASES_BN(64, 1, 2)
+    CONVQ_CASES_BN(32, 4, 2) CONVQ_CASES_BN(32, 1, 2)
+#undef CONVQ_CASES_BN
+#undef CONVQ_CASE
+    return set_err(CONV_Q_EUNSUPPORTED, "no kernel instantiation for bn=%d kch=%d nsub=%d cg=%d", c.bn, c.kch,
+                   c.nsub, c.cg);
+}
+
+
+// one explicit instantiation per translation unit (kern_b<BITS>_o<OUT>.cu)
+int dispatch_conv_8_0(conv_q_plan_s *p, const float *scale, void *y);
+int dispatch_conv_8_1(conv_q_plan_s *p, const float *scale, void *y);
+int dispatch_conv_8_2(conv_q_plan_s *p, const float *scale, void *y);
+int dispatch_conv_4_0(conv_q_plan_s *p, const float *scale, void *y);
+int dispatch_conv_4_1(conv_q_plan_s *p, const float *scale, void *y);
+int dispatch_conv_4_2(conv_q_plan_s *p, const float *scale, void *y);
+
+}  // namespace convq
