@@ -40,6 +40,17 @@ import numpy as np  # noqa: E402
 import workloads as wl  # noqa: E402
 
 METRIC = "images/s (ResNet-50 conv layers, INT8, fused requant-repack)"
+
+
+def metric_name(workload: str) -> str:
+    """BASELINE.json's images/s metric, labelled with the workload's network and precision."""
+    if workload == "resnet50_int8_b256":
+        return METRIC
+    if workload == "resnet18_int8_b1":
+        return "images/s (ResNet-18 conv layers, INT8, fused requant-repack)"
+    if workload == "resnet18_int4_b16":
+        return "images/s (ResNet-18 conv layers, INT4, fused requant-repack)"
+    return "images/s (single INT8 conv 56x56x64->64 3x3, fused requant-repack)"
 UNIT = "images/s"
 L2_BYTES = 126 * 1024 * 1024
 
@@ -360,7 +371,7 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(B_global / (ms_per_step * 1e-3), 2), "unit": UNIT,
+            "metric": metric_name(args.workload), "value": round(B_global / (ms_per_step * 1e-3), 2), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int8" if bits == 8 else "int4",
             "data": "synthetic (seeded N(0,1) fp16 input, uniform weight codes, random-init ResNet shapes)",
@@ -481,7 +492,7 @@ def run_reference(args):
     dt = time.perf_counter() - t
     imgs = macs / per_image_macs
     value = imgs / dt
-    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+    line = {"impl": "reference", "metric": metric_name(args.workload), "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic", "config": {"workload": args.workload, "description": desc, "per_gpu_batch": B,

@@ -77,8 +77,8 @@ typedef struct conv_q_info_s {
     int relu, out_mode;
     int num_candidates;       /* TileConfig candidates valid for this shape */
     int config_index;         /* currently selected candidate */
-    char config[64];          /* its name, e.g. "bm128_bn128_kc128_st4_c1" */
-    float tuned_us;           /* median time of the selected config if tuned, else -1 */
+    char config[64];          /* its name, e.g. "bm128_bn256_kc128x1_c1_st" (see conv_q_plan_candidate_name) */
+    float tuned_us;           /* per-launch time of the selected config if tuned, else -1 */
     int64_t macs;             /* M * K * Kg: multiply-accumulates of one run */
 } conv_q_info_t;
 
@@ -103,9 +103,15 @@ CONVQ_API conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, i
 /*
  * Run the plan: y = requant(conv(x, w), scale) (or raw s32 accumulators).
  * x, w, scale, y: device pointers in the layouts above, 16-byte aligned.
- * Never allocates; one launch of the implicit-GEMM kernel on the plan's stream.
+ * One launch of the implicit-GEMM kernel on the plan's stream.  Allocates
+ * only for a split-K config (name suffix "_k<s>": s CTAs share one output
+ * tile's K loop, and meet in a plan-owned s32 workspace of
+ * ceil(M/BM)*BM*K*4 bytes + counters, zeroed once and left zero by every run);
+ * that allocation happens at conv_q_plan_set_config / conv_q_plan_tune / the
+ * first run, never inside CUDA graph capture (EINVAL there).
  * Errors: EINVAL (NULL / misaligned pointer), ECUDA (no device, launch failure).
- * One run in flight per plan is allowed (the plan caches tensor maps).
+ * One run in flight per plan is allowed (the plan caches tensor maps and owns
+ * the split-K workspace).
  */
 CONVQ_API int conv_q_run(conv_q_plan_t *plan, const void *x, const void *w, const float *scale, void *y);
 
@@ -115,7 +121,11 @@ CONVQ_API int conv_q_plan_set_stream(conv_q_plan_t *plan, void *stream);
 /* relu in {0,1}; out_mode CONV_Q_OUT_PACKED or CONV_Q_OUT_S32. */
 CONVQ_API int conv_q_plan_set_epilogue(conv_q_plan_t *plan, int relu, int out_mode);
 
-/* TileConfig candidates: count, names, manual selection. */
+/* TileConfig candidates: count, names, manual selection.
+ * Name = bm<MMA rows>_bn<N tile>_kc<channels per k-block>x<k-blocks per stage>
+ *        _c<CTAs per tile (2 = cta_group::2 pair)>[_st: direct 16-byte stores,
+ *        else smem staging + TMA store][_h: duplicate-aware halo A operand]
+ *        [_k<s>: split-K over s work units]. */
 CONVQ_API int conv_q_plan_num_candidates(const conv_q_plan_t *plan);
 CONVQ_API int conv_q_plan_candidate_name(const conv_q_plan_t *plan, int index, char *buf, int buflen);
 CONVQ_API int conv_q_plan_set_config(conv_q_plan_t *plan, int index);
@@ -125,7 +135,9 @@ CONVQ_API int conv_q_plan_set_config(conv_q_plan_t *plan, int index);
  * scheduling of MMA instructions varies for different convolution sizes";
  * the B200 analog of the paper's exhaustive search, Table 1).
  * Times every candidate on the given (caller-owned, valid) buffers with CUDA
- * events -- `warmup` untimed runs then the median of `reps` -- selects the
+ * events -- `warmup` untimed runs, then 3 rounds of `reps` back-to-back
+ * launches (as in a layer sequence, where each launch's prologue overlaps the
+ * previous kernel), scored by the median round's mean -- selects the
  * fastest and records it in the in-process cache (and in the JSON file named
  * by $CONV_Q_CACHE, if set).  y is overwritten.  Synchronises the stream.
  * Returns the selected index (>= 0) or an error code.

@@ -23,7 +23,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libconvq.so")
+LIB_PATH = os.environ.get("CONV_Q_LIB") or os.path.join(_HERE, "libconvq.so")  # CONV_Q_LIB: A/B measurement of another build
 
 OK, EINVAL, EUNSUPPORTED, EOVERFLOW, ECUDA, ENOMEM = 0, -1, -2, -3, -4, -5
 OUT_PACKED, OUT_S32 = 0, 1

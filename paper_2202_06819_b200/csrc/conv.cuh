@@ -47,7 +47,7 @@ namespace convq {
 constexpr int BM = 128;
 // per-CTA trace counters (cycles): where the control loops wait
 enum { TR_PROD_EMPTY = 0, TR_MMA_FULL, TR_MMA_ACC, TR_EPI_ACC, TR_MMA_ISSUE, TR_TOTAL, TR_TILES, TR_T0, TR_T1,
-       TR_TPDL, TR_SLOTS = 10 };
+       TR_TPDL, TR_TFULL, TR_TACC, TR_SLOTS = 12 };
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -78,6 +78,14 @@ struct ConvParams {
     int32_t *y32;        // s32 output (OUT = OUT_S32)
     uint8_t *y8;         // packed output for direct stores (OUT = OUT_DIRECT)
     int out_row;         // packed output bytes per pixel row = K*BITS/8
+    // split-K (stream-K style work units, "the dimension of K is
+    // reduced"): a tile's k-blocks are cut into `splits` ranges processed by
+    // different CTAs; partial s32 sums meet in `ws` and the last arriving
+    // warp of each 32-row region requantizes.  splits = 1: plain tiles.
+    int splits;
+    int num_units;       // num_tiles * splits
+    int32_t *ws;         // [num_tiles*CG][4*EPB regions][EPI_COLS][32] partial sums (kept zero between runs)
+    unsigned *cnt;       // per-region arrival counters (kept zero between runs)
 };
 
 // Output path of the epilogue.
@@ -208,6 +216,62 @@ __device__ __forceinline__ uint32_t pack8_low_nibbles(const uint32_t *r) {
     uint32_t b45 = (r[4] & 0xFu) | ((r[5] << 4) & 0xF0u);
     uint32_t b67 = (r[6] & 0xFu) | ((r[7] << 4) & 0xF0u);
     return __byte_perm(__byte_perm(b01, b23, 0x0040), __byte_perm(b45, b67, 0x0040), 0x5410);
+}
+
+// Work unit -> (tile, k-block range).  splits == 1 (every non-split config)
+// takes the division-free branch: these run once per tile in the single-thread
+// control loops, where a few dozen extra instructions per tile show up on
+// layers with one k-block per tile.  split*num_kb < 2^31 is checked at plan time.
+__device__ __forceinline__ void unit_range(const ConvParams &p, int unit, int &tile, int &kb_lo, int &kb_hi) {
+    if (p.splits == 1) {
+        tile = unit;
+        kb_lo = 0;
+        kb_hi = p.num_kb;
+    } else {
+        tile = unit / p.splits;
+        const int split = unit - tile * p.splits;
+        kb_lo = split * p.num_kb / p.splits;
+        kb_hi = (split + 1) * p.num_kb / p.splits;
+    }
+}
+
+// Expand one k-block (A rows then B rows) with all loads of a thread issued
+// before its first store: ITEMS 16-byte pieces per thread in flight (ILP)
+// instead of one shared-memory round trip per piece.
+template <int KCH, int ROWS_A, int ROWS_B, int NTHR>
+__device__ __forceinline__ void expand_kblock(const uint8_t *a_src, uint8_t *a_dst, const uint8_t *b_src,
+                                              uint8_t *b_dst, int tid) {
+    constexpr int PW = KCH / 2, PPR = PW / 16;
+    constexpr int TA = ROWS_A * PPR, T = (ROWS_A + ROWS_B) * PPR;
+    constexpr int ITEMS = (T + NTHR - 1) / NTHR;
+    uint4 v[ITEMS];
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const int i = tid + k * NTHR;
+        if (T % NTHR == 0 || i < T) {
+            const bool a = i < TA;
+            const int ii = a ? i : i - TA;
+            const int row = ii / PPR, j = ii - row * PPR;
+            v[k] = *reinterpret_cast<const uint4 *>((a ? a_src : b_src) + swz<PW>(row * PW + j * 16));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < ITEMS; ++k) {
+        const int i = tid + k * NTHR;
+        if (T % NTHR == 0 || i < T) {
+            const bool a = i < TA;
+            const int ii = a ? i : i - TA;
+            const int row = ii / PPR, j = ii - row * PPR;
+            uint32_t o[8];
+            expand_s4(v[k].x, o[0], o[1]);
+            expand_s4(v[k].y, o[2], o[3]);
+            expand_s4(v[k].z, o[4], o[5]);
+            expand_s4(v[k].w, o[6], o[7]);
+            uint8_t *dst = a ? a_dst : b_dst;
+            *reinterpret_cast<uint4 *>(dst + swz<KCH>(row * KCH + (2 * j) * 16)) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4 *>(dst + swz<KCH>(row * KCH + (2 * j + 1) * 16)) = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+    }
 }
 
 template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO>
@@ -350,7 +414,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
             }
         } else
-        for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+        for (int unit = tile0; unit < p.num_units; unit += tstep) {
+            int tile, kb_lo, kb_hi;
+            unit_range(p, unit, tile, kb_lo, kb_hi);
             const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
             const int m0 = m_blk * (BM * CG) + (int)rank * BM;   // this CTA's first output pixel
             const int n0 = m0 / PQ, rem = m0 - n0 * PQ;
@@ -358,8 +424,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad;
             const int brow = n_blk * BN + (int)rank * Cfg::BNL;  // this CTA's B rows
             int r = 0, s = 0, cblk = 0, kcol = 0;
-            for (int kb = 0; kb < p.num_kb; kb += NSUB) {
-                const int nsub = min(NSUB, p.num_kb - kb);   // ragged last stage of a tile
+            if (kb_lo > 0) {                       // split-K unit: start mid-way through the taps
+                const int tap0 = kb_lo / p.num_cblk;
+                r = tap0 / p.S;
+                s = tap0 - r * p.S;
+                cblk = kb_lo - tap0 * p.num_cblk;
+                kcol = tap0 * p.row_bytes;
+            }
+            for (int kb = kb_lo; kb < kb_hi; kb += NSUB) {
+                const int nsub = min(NSUB, kb_hi - kb);   // ragged last stage of a tile
                 {
                     const long long t0 = p.trace ? clock64() : 0;
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -412,7 +485,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             uint32_t phase = 0;
             int local = 0;
             int hcount = 0;
-            for (int tile = tile0; tile < p.num_tiles; tile += tstep, ++local) {
+            for (int unit = tile0; unit < p.num_units; unit += tstep, ++local) {
+                int tile, kb_lo, kb_hi;
+                unit_range(p, unit, tile, kb_lo, kb_hi);
                 const int buf = local % Cfg::NBUF;
                 const uint32_t aphase = (local / Cfg::NBUF) & 1;
                 {
@@ -481,13 +556,14 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         }
                     }
                 } else
-                for (int kb = 0; kb < p.num_kb; kb += NSUB) {
-                    const int nsub = min(NSUB, p.num_kb - kb);
+                for (int kb = kb_lo; kb < kb_hi; kb += NSUB) {
+                    const int nsub = min(NSUB, kb_hi - kb);
                     long long t0 = p.trace ? clock64() : 0;
                     mbar_wait(BITS == 4 ? &ready[stage] : &full[stage], phase);
                     if (p.trace && lane == 0) {
                         const long long t1 = clock64();
                         atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
+                        if (local == 0 && kb == kb_lo) p.trace[blockIdx.x * TR_SLOTS + TR_TFULL] = globaltimer_ns();
                         t0 = t1;
                     }
                     tc_fence_after();
@@ -509,7 +585,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                     const uint64_t bd = bd0 + (uint64_t)((j * Cfg::B_SUB) >> 4);
 #pragma unroll
                                     for (int k = 0; k < KCH / 32; ++k) {
-                                        const uint32_t acc = (kb + j + k) != 0;
+                                        const uint32_t acc = (kb - kb_lo + j + k) != 0;
                                         if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
                                         else mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
                                     }
@@ -553,7 +629,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         const float hi = (float)((1 << (BITS - 1)) - 1);
         pdl_wait();
         int j = 0;
-        for (int tile = tile0 + b * tstep; tile < p.num_tiles; tile += Cfg::NBUF * tstep, ++j) {
+        for (int unit = tile0 + b * tstep; unit < p.num_units; unit += Cfg::NBUF * tstep, ++j) {
+            const int tile = p.splits == 1 ? unit : unit / p.splits;
             const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
             const int mrow0 = m_blk * (BM * CG) + (int)rank * BM;
             int m = mrow0 + row;
@@ -574,8 +651,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             {
                 const long long t0 = p.trace ? clock64() : 0;
                 mbar_wait(&acc_full[b], j & 1);
-                if (p.trace && lane == 0 && warp == Cfg::EPI_WARP0)
+                if (p.trace && lane == 0 && warp == Cfg::EPI_WARP0) {
                     atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_EPI_ACC, clock64() - t0);
+                    if (j == 0) p.trace[blockIdx.x * TR_SLOTS + TR_TACC] = globaltimer_ns();
+                }
             }
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + b * BN + half * Cfg::EPI_COLS;
@@ -659,6 +738,43 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     }
             };
             uint32_t va[Cfg::CW], vb[Cfg::CW];
+            bool emit = true;   // this warp writes the region's outputs
+            if (p.splits > 1) {
+                // split-K: add this partial into the region's workspace (column-major
+                // [col][32 rows], so each red instruction covers 128 contiguous bytes);
+                // the warp whose arrival completes the region requantizes the sum and
+                // leaves the workspace and counter zero for the next run.  s32
+                // addition is associative: bit-exact in any arrival order.
+                const int region = (tile * CG + (int)rank) * (4 * EPB) + half * 4 + quad;
+                int32_t *wsr = p.ws + (int64_t)region * (32 * Cfg::EPI_COLS) + lane;
+#pragma unroll 1
+                for (int c = 0; c < NCH; ++c) {
+                    tmem_ld_issue<Cfg::CW>(taddr + c * Cfg::CW, va);
+                    tmem_ld_wait_regs(va);
+#pragma unroll
+                    for (int q = 0; q < Cfg::CW; ++q) red_add_s32(wsr + (c * Cfg::CW + q) * 32, (int)va[q]);
+                }
+                release_acc();
+                __threadfence();
+                __syncwarp();
+                unsigned old = 0;
+                if (lane == 0) old = atomicAdd(p.cnt + region, 1u);
+                old = __shfl_sync(0xffffffffu, old, 0);
+                emit = old == (unsigned)(p.splits - 1);
+                if (emit) {
+                    __threadfence();
+#pragma unroll 1
+                    for (int c = 0; c < NCH; ++c) {
+#pragma unroll
+                        for (int q = 0; q < Cfg::CW; ++q) {
+                            va[q] = (uint32_t)__ldcg(wsr + (c * Cfg::CW + q) * 32);
+                            __stcg(wsr + (c * Cfg::CW + q) * 32, 0);
+                        }
+                        process(va, c);
+                    }
+                    if (lane == 0) p.cnt[region] = 0u;
+                }
+            } else {
             tmem_ld_issue<Cfg::CW>(taddr, va);
             tmem_ld_wait_regs(va);
 #pragma unroll 1
@@ -676,7 +792,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     if (more2) tmem_ld_wait_regs(va);
                 }
             }
-            if (OUT == OUT_TMA) {
+            }
+            if (OUT == OUT_TMA && emit) {
                 fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
                 __syncwarp();
                 if (lane == 0) {
@@ -696,16 +813,16 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             const uint32_t ready0 = CG == 2 ? mapa_shared(smem_u32(&ready[0]), 0) : 0;
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
-                for (int kb = 0; kb < p.num_kb; kb += NSUB) {
-                    const int nsub = min(NSUB, p.num_kb - kb);
+            for (int unit = tile0; unit < p.num_units; unit += tstep) {
+                int tile, kb_lo, kb_hi;
+                unit_range(p, unit, tile, kb_lo, kb_hi);
+                for (int kb = kb_lo; kb < kb_hi; kb += NSUB) {
+                    const int nsub = min(NSUB, kb_hi - kb);
                     mbar_wait(&full[stage], phase);
-                    for (int j = 0; j < nsub; ++j) {
-                        expand_tile<KCH>(a_pk + stage * Cfg::A_PK + j * Cfg::A_PK_SUB,
-                                         a_s8 + stage * Cfg::A_S8 + j * Cfg::A_SUB, BM, tid, 128);
-                        expand_tile<KCH>(b_pk + stage * Cfg::B_PK + j * Cfg::B_PK_SUB,
-                                         b_s8 + stage * Cfg::B_S8 + j * Cfg::B_SUB, Cfg::BNL, tid, 128);
-                    }
+                    for (int j = 0; j < nsub; ++j)
+                        expand_kblock<KCH, BM, Cfg::BNL, 128>(
+                            a_pk + stage * Cfg::A_PK + j * Cfg::A_PK_SUB, a_s8 + stage * Cfg::A_S8 + j * Cfg::A_SUB,
+                            b_pk + stage * Cfg::B_PK + j * Cfg::B_PK_SUB, b_s8 + stage * Cfg::B_S8 + j * Cfg::B_SUB, tid);
                     fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.mma
                     __syncwarp();
                     if (lane == 0) {

@@ -95,6 +95,7 @@ static void init_device() {
     g_encode_tiled = reinterpret_cast<PFN_encodeTiled_t>(f1);
     g_encode_im2col = reinterpret_cast<PFN_encodeIm2col_t>(f2);
 }
+static int ensure_ws(conv_q_plan_s *p);
 static int ensure_device() {
     std::call_once(g_init_once, init_device);
     if (g_init_status != CONV_Q_OK) return set_err(g_init_status, "%s", g_init_msg.c_str());
@@ -111,8 +112,10 @@ static CUtensorMapSwizzle swizzle_for(int span) {
 // ============================================================== plan
 static std::string cand_name(const conv_q_plan_s *p, int i) {
     char b[64];
-    snprintf(b, sizeof b, "bm%d_bn%d_kc%dx%d_c%d%s%s", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
-             p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "", p->cands[i].halo ? "_h" : "");
+    char k[16] = "";
+    if (p->cands[i].split > 1) snprintf(k, sizeof k, "_k%d", p->cands[i].split);
+    snprintf(b, sizeof b, "bm%d_bn%d_kc%dx%d_c%d%s%s%s", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
+             p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "", p->cands[i].halo ? "_h" : "", k);
     return b;
 }
 
@@ -177,6 +180,23 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                     const Cand cand{bn, kch, cg, nsub, direct};
                     if (!(p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand))) continue;
                     p->cands.push_back(cand);
+                    // split-K variants when the tiles fill fewer than two waves:
+                    // ~1 and ~2 work units per SM, each unit >= 2 stages of K
+                    const int64_t tiles = ceil_div(p->M, 128 * cg) * ceil_div(p->K, bn);
+                    const int64_t num_kb = (int64_t)p->R * p->S * (p->C / kch);
+                    const int sms = g_num_sms > 0 ? g_num_sms : 148;
+                    const int64_t ws = tiles * cg * 128 * bn * 4;
+                    if (tiles >= 2 * sms / cg || ws > ((int64_t)64 << 20) || 16 * num_kb >= ((int64_t)1 << 31)) continue;
+                    int last = 1;
+                    for (int waves : {1, 2}) {
+                        int sp = (int)std::min<int64_t>(ceil_div((int64_t)waves * sms / cg, tiles), 16);
+                        sp = (int)std::min<int64_t>(sp, num_kb / (2 * nsub));
+                        if (sp <= last) continue;
+                        Cand sc = cand;
+                        sc.split = sp;
+                        p->cands.push_back(sc);
+                        last = sp;
+                    }
                 }
             }
     // duplicate-aware (halo) candidates: stride-1 INT8 R x S convolutions whose
@@ -303,6 +323,10 @@ extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, 
                     p->tuned_us = it->second.second;
                 }
     }
+    if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK && ensure_ws(p) != CONV_Q_OK) {
+        delete p;
+        return nullptr;
+    }
     return p;
 }
 
@@ -340,6 +364,8 @@ extern "C" int conv_q_plan_set_config(conv_q_plan_t *p, int i) {
     if (i < 0 || i >= (int)p->cands.size()) return set_err(CONV_Q_EINVAL, "candidate %d out of range", i);
     p->sel = i;
     p->tuned_us = -1.f;
+    // allocate a split-K workspace now, so a later run may be graph-captured
+    if (p->cands[i].split > 1 && ensure_device() == CONV_Q_OK) return ensure_ws(p);
     return CONV_Q_OK;
 }
 
@@ -436,6 +462,36 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
 
 static bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
+// Split-K workspace for the selected config: partial sums + region counters,
+// zeroed once here and left zero by every run (the kernel's last arriving warp
+// clears what it consumed).  Grows only; never allocated during graph capture.
+static int ensure_ws(conv_q_plan_s *p) {
+    const Cand &c = p->cands[p->sel];
+    if (c.split <= 1) return CONV_Q_OK;
+    const int64_t tiles = ceil_div(p->M, 128 * c.cg) * ceil_div(p->K, c.bn);
+    const size_t need = (size_t)tiles * c.cg * 128 * c.bn * sizeof(int32_t);
+    const size_t cnt_need = (size_t)tiles * c.cg * 16 * sizeof(unsigned);   // <= 4 warps x 4 column parts
+    if (p->ws && p->ws_bytes >= need && p->cnt_bytes >= cnt_need) return CONV_Q_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(p->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+        return set_err(CONV_Q_EINVAL, "split-K workspace must be allocated before graph capture (run or select the config once first)");
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    if (p->ws) cudaFree(p->ws);
+    if (p->cnt) cudaFree(p->cnt);
+    p->ws = nullptr;
+    p->cnt = nullptr;
+    p->ws_bytes = p->cnt_bytes = 0;
+    CUDA_TRY(cudaMalloc(&p->ws, need));
+    CUDA_TRY(cudaMalloc(&p->cnt, cnt_need));
+    CUDA_TRY(cudaMemset(p->ws, 0, need));
+    CUDA_TRY(cudaMemset(p->cnt, 0, cnt_need));
+    CUDA_TRY(cudaDeviceSynchronize());
+    p->ws_bytes = need;
+    p->cnt_bytes = cnt_need;
+    return CONV_Q_OK;
+}
+
 extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y) {
     if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
     if (!x || !w || !scale || !y) return set_err(CONV_Q_EINVAL, "NULL tensor pointer");
@@ -443,6 +499,7 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
         return set_err(CONV_Q_EINVAL, "tensor pointers must be 16-byte aligned");
     int rc = ensure_device();
     if (rc) return rc;
+    if ((rc = ensure_ws(p))) return rc;
     if (p->c_x != x || p->c_w != w || p->c_y != y || p->c_sel != p->sel || p->c_mode != p->out_mode) {
         rc = encode_maps(p, x, w, y);
         if (rc) return rc;
@@ -465,26 +522,29 @@ extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, 
     CUDA_TRY(cudaEventCreate(&e1));
     int best = -1;
     float best_us = 0.f;
-    std::vector<float> ts(reps);
     const int saved = p->sel;
     for (int i = 0; i < (int)p->cands.size(); ++i) {
         p->sel = i;
         for (int k = 0; k < warmup; ++k)
             if ((rc = conv_q_run(p, x, w, scale, y))) break;
         if (rc) break;
-        for (int k = 0; k < reps; ++k) {
+        // back-to-back launches (as in a step, where PDL overlaps each
+        // launch's prologue with the previous kernel's tail): the mean over
+        // `reps` launches, median of 3 rounds
+        float rt[3];
+        for (int k = 0; k < 3 && !rc; ++k) {
             cudaEventRecord(e0, p->stream);
-            rc = conv_q_run(p, x, w, scale, y);
+            for (int j = 0; j < reps && !rc; ++j) rc = conv_q_run(p, x, w, scale, y);
             cudaEventRecord(e1, p->stream);
             if (rc) break;
             cudaEventSynchronize(e1);
             float ms = 0.f;
             cudaEventElapsedTime(&ms, e0, e1);
-            ts[k] = ms * 1000.f;
+            rt[k] = ms * 1000.f / reps;
         }
         if (rc) break;
-        std::sort(ts.begin(), ts.end());
-        float med = ts[reps / 2];
+        std::sort(rt, rt + 3);
+        float med = rt[1];
         if (best < 0 || med < best_us) {
             best = i;
             best_us = med;

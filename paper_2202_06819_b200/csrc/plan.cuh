@@ -29,6 +29,7 @@ struct Cand {
     int bn, kch, cg, nsub;  // N tile, channels per k-block, CTAs per tile, k-blocks per stage
     int direct;             // packed output by direct stores (1) or smem staging + TMA store (0)
     int halo = 0;           // duplicate-aware halo A operand (stride 1 only)
+    int split = 1;          // split-K work units per tile (1 = none)
 };
 
 }  // namespace convq
@@ -53,6 +54,14 @@ struct conv_q_plan_s {
     CUtensorMap tm_a, tm_b, tm_y;
     const void *c_x = nullptr, *c_w = nullptr, *c_y = nullptr;
     int c_sel = -1, c_mode = -1;
+    // split-K workspace (zero between runs; owned by the plan)
+    int32_t *ws = nullptr;
+    unsigned *cnt = nullptr;
+    size_t ws_bytes = 0, cnt_bytes = 0;
+    ~conv_q_plan_s() {
+        if (ws) cudaFree(ws);
+        if (cnt) cudaFree(cnt);
+    }
 };
 
 
@@ -114,6 +123,16 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.halo_tx = halo_rows * prm.Wp * Cfg::LOAD_ROW;
     prm.desc_bo = p->desc_bo;
     if (HALO) prm.num_tiles = (int)(ceil_div(prm.m_tiles, CG) * prm.n_tiles);
+    prm.splits = HALO ? 1 : p->cands[p->sel].split;
+    prm.num_units = prm.num_tiles * prm.splits;
+    prm.ws = p->ws;
+    prm.cnt = p->cnt;
+    if (prm.splits > 1) {
+        const size_t need = (size_t)prm.num_tiles * CG * 128 * BN * sizeof(int32_t);
+        const size_t regions = (size_t)prm.num_tiles * CG * 4 * Cfg::EPI_PER_BUF;
+        if (!p->ws || p->ws_bytes < need || p->cnt_bytes < regions * sizeof(unsigned))
+            return set_err(CONV_Q_EINVAL, "split-K workspace not allocated (select the config outside graph capture)");
+    }
     prm.relu = p->relu;
     prm.probe = p->probe;
     prm.trace = p->trace;
@@ -121,7 +140,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.y32 = static_cast<int32_t *>(y);
     prm.y8 = static_cast<uint8_t *>(y);
     prm.out_row = p->out_row;
-    const int clusters = std::min(prm.num_tiles, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
+    const int clusters = std::min(prm.num_units, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * CG);
     cfg.blockDim = dim3(Cfg::NUM_THREADS);

@@ -359,4 +359,9 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
            | ((uint32_t)(M >> 4) << 24);    // M >> 4
 }
 
+// Relaxed GPU-scope atomic add without return (RED): split-K partial sums.
+__device__ __forceinline__ void red_add_s32(int32_t *addr, int v) {
+    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
 }  // namespace convq

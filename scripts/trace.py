@@ -7,8 +7,9 @@ lib = cq.load()
 lib.conv_q_plan_set_trace.restype = ctypes.c_int
 lib.conv_q_plan_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 name = sys.argv[1]
-L = {l.name: l for l, _ in wl.resnet50_layers()}[name]
-N, bits = 256, 8
+net = os.environ.get("TRACE_NET", "resnet50")
+L = {l.name: l for l, _ in getattr(wl, net + "_layers")()}[name]
+N, bits = int(os.environ.get("TRACE_N", 256)), int(os.environ.get("TRACE_BITS", 8))
 g = wl.rng(9, 0)
 x, w, ss = wl.layer_inputs(g, L, N, bits)
 p = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
@@ -24,7 +25,7 @@ for cname in cfgs:
     for _ in range(10): p.run(xd, wd, sd, y)
     e1.record(); torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / 10 * 1000
-    tr = torch.zeros(148 * 10, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(148 * 12, dtype=torch.int64, device="cuda")
     h0, h1 = torch.cuda.Event(True), torch.cuda.Event(True)
     lib.conv_q_plan_set_trace(p._h, ctypes.c_void_p(tr.data_ptr()))
     torch.cuda.synchronize()
@@ -33,7 +34,7 @@ for cname in cfgs:
     h1.record()
     torch.cuda.synchronize()
     lib.conv_q_plan_set_trace(p._h, None)
-    t = tr.view(148, 10).double().cpu()
+    t = tr.view(148, 12).double().cpu()
     act = t[:, 5] > 0
     m = t[act].mean(0)
     s = "  ".join(f"{n}={m[i]/1965:6.1f}" for i, n in enumerate(names[:6]))
@@ -41,4 +42,4 @@ for cname in cfgs:
     base = t0.min()
     print(f"{cname:26s} {us:6.1f}us (traced run {h0.elapsed_time(h1)*1000:6.1f}) ctas={int(act.sum())} "
           f"tiles/cta={m[6]:.1f} {s} | start spread {(t0.max()-base)/1e3:.1f}us pdl_pass {(tp.min()-base)/1e3:.1f}.."
-          f"{(tp.max()-base)/1e3:.1f} end {(t1.min()-base)/1e3:.1f}..{(t1.max()-base)/1e3:.1f}us", flush=True)
+          f"{(tp.max()-base)/1e3:.1f} full1 {(t[act,10].min()-base)/1e3:.1f}..{(t[act,10].max()-base)/1e3:.1f} acc1 {(t[act,11].min()-base)/1e3:.1f}..{(t[act,11].max()-base)/1e3:.1f} end {(t1.min()-base)/1e3:.1f}..{(t1.max()-base)/1e3:.1f}us", flush=True)

@@ -220,3 +220,30 @@ def test_resnet18_chain_int8_b1(cq):
 def test_int8_peak_runs(cq):
     ops = cq.int8_peak(20000)
     assert 1e14 < ops < 6e15
+
+
+# ----------------------------------------------------------------- split-K
+@pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("L,N", [
+    (wl.Layer("l4.3x3", 7, 7, 512, 512, 3, 3, 1, 1), 1),         # ResNet-18 stage 5, batch 1
+    (wl.Layer("l3.s2", 28, 28, 128, 256, 3, 3, 2, 1), 1),        # stride-2 entry of stage 4
+    (wl.Layer("l4.ds", 14, 14, 256, 512, 1, 1, 2, 0), 2),        # 1x1 s2 downsample
+])
+def test_split_k_parity(cq, bits, L, N):
+    """Split-K work units (several CTAs per output tile, partial sums meeting
+    in the plan's workspace): every split candidate, three runs in a row (the
+    workspace must be left zero by each run), s32 and packed outputs."""
+    g = np.random.default_rng(77 + bits)
+    x, w, ss = wl.layer_inputs(g, L, N, bits)
+    ref32 = oracle.conv_s32(x, w, L.C, L.stride, L.pad, bits)
+    refq = oracle.requant(ref32, ss, True, bits)
+    plan = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits)
+    names = plan.candidates()
+    split = [i for i, n in enumerate(names) if "_k" in n]
+    assert split, names
+    for ci in split:
+        for rep in range(3):
+            got32 = run_conv(cq, L, N, bits, x, w, ss, True, True, ci, plan)
+            assert np.array_equal(got32, ref32), (names[ci], rep, first_diff(got32, ref32))
+            gotq = run_conv(cq, L, N, bits, x, w, ss, True, False, ci, plan)
+            assert np.array_equal(gotq, refq), (names[ci], rep, first_diff(gotq, refq))
