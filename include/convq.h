@@ -118,7 +118,8 @@ CONVQ_API int conv_q_run(conv_q_plan_t *plan, const void *x, const void *w, cons
 /* Stream for subsequent runs (a cudaStream_t; NULL = legacy default stream). */
 CONVQ_API int conv_q_plan_set_stream(conv_q_plan_t *plan, void *stream);
 
-/* relu in {0,1}; out_mode CONV_Q_OUT_PACKED or CONV_Q_OUT_S32. */
+/* relu in {0,1}; out_mode CONV_Q_OUT_PACKED or CONV_Q_OUT_S32.  Re-selects the
+ * tuning cache's config for (shape, relu, out_mode) when it holds one. */
 CONVQ_API int conv_q_plan_set_epilogue(conv_q_plan_t *plan, int relu, int out_mode);
 
 /* TileConfig candidates: count, names, manual selection.

@@ -231,6 +231,20 @@ static int default_candidate(const conv_q_plan_s *p) {
     return pick >= 0 ? pick : std::max(narrow, 0);
 }
 
+// Select the cached tuning result for the plan's shape + epilogue, if any
+// (the key includes relu / out_mode, so this runs again on set_epilogue).
+static void apply_cache(conv_q_plan_s *p) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    cache_load_locked();
+    auto it = g_cache.find(shape_key(p));
+    if (it == g_cache.end()) return;
+    for (size_t i = 0; i < p->cands.size(); ++i)
+        if (cand_name(p, (int)i) == it->second.first) {
+            p->sel = (int)i;
+            p->tuned_us = it->second.second;
+        }
+}
+
 extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, int S, int stride, int pad,
                                       int bits) {
     g_err.clear();
@@ -312,17 +326,7 @@ extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, 
     p->sel = default_candidate(p);
     if (const char *pr = getenv("CONV_Q_PROBE")) p->probe = atoi(pr);
     if (const char *bo = getenv("CONV_Q_DESC_BO")) p->desc_bo = atoi(bo);
-    {
-        std::lock_guard<std::mutex> lk(g_cache_mu);
-        cache_load_locked();
-        auto it = g_cache.find(shape_key(p));
-        if (it != g_cache.end())
-            for (size_t i = 0; i < p->cands.size(); ++i)
-                if (cand_name(p, (int)i) == it->second.first) {
-                    p->sel = (int)i;
-                    p->tuned_us = it->second.second;
-                }
-    }
+    apply_cache(p);
     if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK && ensure_ws(p) != CONV_Q_OK) {
         delete p;
         return nullptr;
@@ -344,6 +348,8 @@ extern "C" int conv_q_plan_set_epilogue(conv_q_plan_t *p, int relu, int out_mode
         return set_err(CONV_Q_EINVAL, "relu must be 0/1 and out_mode PACKED(0)/S32(1)");
     p->relu = relu;
     p->out_mode = out_mode;
+    apply_cache(p);
+    if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK) return ensure_ws(p);
     return CONV_Q_OK;
 }
 
