@@ -73,7 +73,6 @@ struct ConvParams {
     int tiles_per_img;   // ceil(P / rpt)
     int m_tiles;         // N * tiles_per_img
     int halo_tx;         // bytes of one halo TMA box
-    int desc_bo;         // 1: set the UMMA descriptor base offset for row-shifted windows
     const float *scale;  // [2K] scale then shift
     int32_t *y32;        // s32 output (OUT = OUT_S32)
     uint8_t *y8;         // packed output for direct stores (OUT = OUT_DIRECT)
@@ -114,7 +113,6 @@ struct ConvCfg {
     static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
     static constexpr int SUB_TX = ((HALO ? 0 : BM) + BNL) * LOAD_ROW;  // TMA bytes per k-block per CTA
     static constexpr int HALO_BYTES = HALO ? 32768 : 0;      // one halo buffer (budget; checked at plan time)
-    static constexpr int NHALO = HALO ? 2 : 0;
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUT_BYTES = OUT == OUT_TMA ? BM * OUT_ROW : 0;   // staging per TMEM buffer
     static constexpr int NUM_EPI = BITS == 8 ? 4 : 2;               // epilogue warpgroups
@@ -130,8 +128,15 @@ struct ConvCfg {
     static constexpr int CW = BITS == 8 ? 16 : 32;                  // columns per tcgen05.ld (16 B packed)
     static constexpr int SS_BYTES = 0;
     static constexpr int BAR_BYTES = 1024;
-    static constexpr int STAGES_FIT =
-        (SMEM_LIMIT - 1024 - BAR_BYTES - NBUF * (OUT_BYTES + SS_BYTES) - NHALO * HALO_BYTES) / STAGE_BYTES;
+    static constexpr int stages_with(int nhalo) {
+        return (SMEM_LIMIT - 1024 - BAR_BYTES - NBUF * (OUT_BYTES + SS_BYTES) - nhalo * HALO_BYTES) / STAGE_BYTES;
+    }
+    // halo buffers in flight: the halo load of tile t+NHALO-1 overlaps tiles
+    // t..t+NHALO-2, so more buffers hide more TMA latency; keep >= 2 tiles of
+    // weight stages ((9/NSUB) stages per tile, 3x3 filters)
+    static constexpr int HST = NSUB >= 9 ? 1 : (9 + NSUB - 1) / NSUB;
+    static constexpr int NHALO = !HALO ? 0 : stages_with(4) >= 2 * HST ? 4 : stages_with(3) >= 2 * HST ? 3 : 2;
+    static constexpr int STAGES_FIT = stages_with(NHALO);
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * HALO_BYTES + BAR_BYTES;
     static constexpr int TMEM_COLS = NBUF * BN < 32 ? 32 : NBUF * BN;
@@ -192,30 +197,37 @@ __device__ __forceinline__ void expand_tile(const uint8_t *src, uint8_t *dst, in
 
 // Requantize (section 3.2.2; DESIGN readings 4-5):
 //   y = clamp(rne(fmaf((float)acc, scale, shift)), lo, hi)
-// computed without the quarter-rate FRND/F2I conversions: clamp first (the
-// bounds are integers, so clamp-then-round == round-then-clamp, and NaN -> lo
-// through max.f32 either way), then add 1.5*2^23: for |u| <= 2^22 the IEEE
-// add rounds u to the nearest integer (ties to even) and leaves it, two's
-// complement, in the low mantissa bits.  Returns those bits; the caller
-// takes the low byte / nibble as the packed code.
-constexpr float RNE_MAGIC = 12582912.0f;  // 1.5 * 2^23
-__device__ __forceinline__ uint32_t requant_bits(int acc, float sc, float sh, float lo, float hi) {
-    float f = __int2float_rn(acc);
-    float u = __fmaf_rn(f, sc, sh);
-    u = fminf(fmaxf(u, lo), hi);
-    return __float_as_uint(__fadd_rn(u, RNE_MAGIC));
+// as I2FP, FFMA, max(., lo) (NaN -> lo, and the lower clamp: lo is an
+// integer, so rne(max(u, lo)) == max(rne(u), lo)), then one F2I with
+// round-to-nearest-even that saturates to s32; the upper clamp (and the
+// narrowing) is the saturation of the packing instruction below
+// (I2IP.S8/S4.SAT, lo >= -2^(b-1)).  Measured ~1.8x the outputs/clk of the
+// clamp-in-float + magic-add + byte-permute sequence (scripts/micro/epi_math.cu).
+__device__ __forceinline__ int requant_int(int acc, float sc, float sh, float lo) {
+    const float u = fmaxf(__fmaf_rn(__int2float_rn(acc), sc, sh), lo);
+    int r;
+    asm("cvt.rni.s32.f32 %0, %1;" : "=r"(r) : "f"(u));
+    return r;
 }
-// low bytes of four requant_bits results -> one packed s8 word
-__device__ __forceinline__ uint32_t pack4_low_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+// cvt.pack.sat.s8.s32.b32 d, a, b, c:  d = c << 16 | sat8(a) << 8 | sat8(b)
+__device__ __forceinline__ uint32_t pack2_s8(int a, int b, uint32_t c) {
+    uint32_t d;
+    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
 }
-// low nibbles of eight requant_bits results -> one packed s4 word
-__device__ __forceinline__ uint32_t pack8_low_nibbles(const uint32_t *r) {
-    uint32_t b01 = (r[0] & 0xFu) | ((r[1] << 4) & 0xF0u);
-    uint32_t b23 = (r[2] & 0xFu) | ((r[3] << 4) & 0xF0u);
-    uint32_t b45 = (r[4] & 0xFu) | ((r[5] << 4) & 0xF0u);
-    uint32_t b67 = (r[6] & 0xFu) | ((r[7] << 4) & 0xF0u);
-    return __byte_perm(__byte_perm(b01, b23, 0x0040), __byte_perm(b45, b67, 0x0040), 0x5410);
+// cvt.pack.sat.s4.s32.b32 d, a, b, c:  d = c << 8 | sat4(a) << 4 | sat4(b)
+__device__ __forceinline__ uint32_t pack2_s4(int a, int b, uint32_t c) {
+    uint32_t d;
+    asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+// four codes -> one packed s8 word (code 0 in byte 0), saturating to [-128, 127]
+__device__ __forceinline__ uint32_t pack4_sat_s8(int r0, int r1, int r2, int r3) {
+    return pack2_s8(r1, r0, pack2_s8(r3, r2, 0u));
+}
+// eight codes -> one packed s4 word (code 0 in the low nibble), saturating to [-8, 7]
+__device__ __forceinline__ uint32_t pack8_sat_s4(const int *r) {
+    return pack2_s4(r[1], r[0], pack2_s4(r[3], r[2], pack2_s4(r[5], r[4], pack2_s4(r[7], r[6], 0u))));
 }
 
 // Work unit -> (tile, k-block range).  splits == 1 (every non-split config)
@@ -293,15 +305,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][NSUB][BM*KCH/2]
     uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][NSUB][BNL*KCH/2]
     uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [NBUF][EPB][4 quads] slabs [EPI_NSUB][32][EPI_SUBW]
-    uint8_t *halo_buf = out_stage + Cfg::NBUF * (Cfg::OUT_BYTES + Cfg::SS_BYTES);   // HALO: [2][HALO_BYTES]
+    uint8_t *halo_buf = out_stage + Cfg::NBUF * (Cfg::OUT_BYTES + Cfg::SS_BYTES);   // HALO: [NHALO][HALO_BYTES]
     uint64_t *bars = reinterpret_cast<uint64_t *>(halo_buf + Cfg::NHALO * Cfg::HALO_BYTES);
     uint64_t *full = bars;                  // TMA -> (transform | MMA)
     uint64_t *empty = bars + STAGES;        // MMA -> TMA
     uint64_t *ready = bars + 2 * STAGES;    // transform -> MMA (INT4)
     uint64_t *acc_full = bars + 3 * STAGES; // MMA -> epilogue [NBUF]
     uint64_t *acc_empty = acc_full + 4;     // epilogue -> MMA [NBUF]
-    uint64_t *hempty = acc_empty + 4;       // HALO: MMA -> TMA, halo buffer free [2]
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(hempty + 2);
+    uint64_t *hempty = acc_empty + 4;       // HALO: MMA -> TMA, halo buffer free [NHALO <= 4]
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(hempty + 4);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -376,12 +388,16 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 const int p0 = (rt - n * p.tiles_per_img) * p.rpt;
                 const int brow = n_blk * BN + (int)rank * Cfg::BNL;
                 for (int cblk = 0; cblk < p.num_cblk; ++cblk, ++hcount) {
-                    const int hb = hcount & 1;
-                    const uint32_t hph = (hcount >> 1) & 1;
+                    const int hb = hcount % Cfg::NHALO;
+                    const uint32_t hph = (hcount / Cfg::NHALO) & 1;
                     for (int tap = 0; tap < RS;) {
                         const int nsub = min(NSUB, RS - tap);
-                        mbar_wait(&empty[stage], phase ^ 1);
-                        if (tap == 0) mbar_wait(&hempty[hb], hph ^ 1);
+                        {
+                            const long long t0 = p.trace ? clock64() : 0;
+                            mbar_wait(&empty[stage], phase ^ 1);
+                            if (tap == 0) mbar_wait(&hempty[hb], hph ^ 1);
+                            if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
+                        }
                         if (elect_one()) {
                             const int tx = nsub * Cfg::SUB_TX + (tap == 0 ? p.halo_tx : 0);
                             if (p.probe == 2) {
@@ -481,6 +497,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         if (rank == 0) {
             const uint64_t a_desc0 = umma_desc_kmajor(smem_u32(a_s8), KCH);
             const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(b_s8), KCH);
+            // HALO (3x3): descriptor start-address delta of tap t's window, (r*Wp + s)*KCH bytes
+            const uint64_t a_desc_h = umma_desc_kmajor(smem_u32(halo_buf), KCH);
+            uint32_t toff[9];
+#pragma unroll
+            for (int t = 0; t < 9; ++t) toff[t] = (uint32_t)(((t / 3) * p.Wp + (t % 3)) * KCH) >> 4;
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -503,56 +524,57 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 if constexpr (HALO) {
                     // filter tap (r, s) reads the halo rows starting at r*Wp + s:
                     // the duplicate-aware load of PAPER.md Alg. 1, with the
-                    // "genuine index" remap done by the UMMA descriptor start address
-                    const int RS = p.R * p.S;
-                    const uint32_t halo0 = smem_u32(halo_buf);
+                    // "genuine index" remap done by the UMMA descriptor start
+                    // address (3x3 filters; tap offsets precomputed in toff[])
+                    constexpr int RS = 9;
                     for (int cblk = 0; cblk < p.num_cblk; ++cblk, ++hcount) {
-                        const int hb = hcount & 1;
-                        int r = 0, s = 0;
-                        for (int tap = 0; tap < RS;) {
-                            const int nsub = min(NSUB, RS - tap);
+                        const int hb = hcount % Cfg::NHALO;
+                        const uint64_t ad_h = a_desc_h + (uint64_t)((hb * Cfg::HALO_BYTES) >> 4);
+#pragma unroll
+                        for (int g = 0; g < Cfg::HST; ++g) {
+                            long long t0 = p.trace ? clock64() : 0;
                             mbar_wait(&full[stage], phase);
+                            if (p.trace && lane == 0) {
+                                const long long t1 = clock64();
+                                atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
+                                t0 = t1;
+                            }
                             tc_fence_after();
                             if (elect_one()) {
                                 if (p.probe == 1) {
                                     mbar_arrive(&empty[stage]);
-                                    if (tap + nsub == RS) mbar_arrive(&hempty[hb]);
+                                    if (g == Cfg::HST - 1) mbar_arrive(&hempty[hb]);
                                     if constexpr (CG == 2) {
                                         mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
-                                        if (tap + nsub == RS) mbar_arrive_cluster(mapa_shared(smem_u32(&hempty[hb]), 1));
+                                        if (g == Cfg::HST - 1) mbar_arrive_cluster(mapa_shared(smem_u32(&hempty[hb]), 1));
                                     }
                                 } else {
                                     const uint64_t bd0 = b_desc0 + (uint64_t)((stage * Cfg::B_S8) >> 4);
-                                    int rr = r, ss = s;
 #pragma unroll
                                     for (int j = 0; j < NSUB; ++j) {
-                                        if (j < nsub) {
-                                            const uint32_t a_addr = halo0 + hb * Cfg::HALO_BYTES + (rr * p.Wp + ss) * KCH;
-                                            uint64_t ad = umma_desc_kmajor(a_addr, KCH);
-                                            if (p.desc_bo) ad |= (uint64_t)((a_addr >> 7) & 7) << 49;
+                                        const int t = g * NSUB + j;
+                                        if (t < RS) {
+                                            const uint64_t ad = ad_h + toff[t];
                                             const uint64_t bd = bd0 + (uint64_t)((j * Cfg::B_SUB) >> 4);
 #pragma unroll
                                             for (int k = 0; k < KCH / 32; ++k) {
-                                                const uint32_t acc = (cblk | (tap + j) | k) != 0;
+                                                const uint32_t acc = (cblk | t | k) != 0;
                                                 if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
                                                 else mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
                                             }
-                                            if (++ss == p.S) { ss = 0; ++rr; }
                                         }
                                     }
                                     if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
                                     else mma_commit(&empty[stage]);
-                                    if (tap + nsub == RS) {        // last use of this halo buffer
+                                    if (g == Cfg::HST - 1) {        // last use of this halo buffer
                                         if constexpr (CG == 2) mma_commit_cg2_mc(&hempty[hb], 0x3);
                                         else mma_commit(&hempty[hb]);
                                     }
                                 }
                             }
                             __syncwarp();
+                            if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                             if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                            for (int j = 0; j < nsub; ++j)
-                                if (++s == p.S) { s = 0; ++r; }
-                            tap += nsub;
                         }
                     }
                 } else
@@ -626,7 +648,6 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         uint8_t *slab = out_stage + b * Cfg::OUT_BYTES + (half * 4 + quad) * Cfg::SLAB;
         const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(&acc_empty[b]), 0) : 0;
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
-        const float hi = (float)((1 << (BITS - 1)) - 1);
         pdl_wait();
         int j = 0;
         for (int unit = tile0 + b * tstep; unit < p.num_units; unit += Cfg::NBUF * tstep, ++j) {
@@ -692,7 +713,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             }
                         }
                     } else {
-                        uint32_t r[Cfg::CW];
+                        int r[Cfg::CW];
                         if (col0 + Cfg::CW <= p.K) {
                             const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
                             const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
@@ -703,10 +724,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
                                 const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
                                 const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
-                                r[4 * q] = requant_bits(x0, sa.x, sb.x, lo, hi);
-                                r[4 * q + 1] = requant_bits(x1, sa.y, sb.y, lo, hi);
-                                r[4 * q + 2] = requant_bits(x2, sa.z, sb.z, lo, hi);
-                                r[4 * q + 3] = requant_bits(x3, sa.w, sb.w, lo, hi);
+                                r[4 * q] = requant_int(x0, sa.x, sb.x, lo);
+                                r[4 * q + 1] = requant_int(x1, sa.y, sb.y, lo);
+                                r[4 * q + 2] = requant_int(x2, sa.z, sb.z, lo);
+                                r[4 * q + 3] = requant_int(x3, sa.w, sb.w, lo);
                             }
                         } else {
 #pragma unroll
@@ -714,17 +735,17 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 const bool ok = col0 + q < p.K;  // columns past K are never stored
                                 const float sc = ok ? __ldg(p.scale + col0 + q) : 0.f;
                                 const float sh = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
-                                r[q] = requant_bits(BITS == 4 ? ((int)v[q] >> 8) : (int)v[q], sc, sh, lo, hi);
+                                r[q] = requant_int(BITS == 4 ? ((int)v[q] >> 8) : (int)v[q], sc, sh, lo);
                             }
                         }
                         uint4 pk;   // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
                         if constexpr (BITS == 8) {
-                            pk = make_uint4(pack4_low_bytes(r[0], r[1], r[2], r[3]), pack4_low_bytes(r[4], r[5], r[6], r[7]),
-                                            pack4_low_bytes(r[8], r[9], r[10], r[11]),
-                                            pack4_low_bytes(r[12], r[13], r[14], r[15]));
+                            pk = make_uint4(pack4_sat_s8(r[0], r[1], r[2], r[3]), pack4_sat_s8(r[4], r[5], r[6], r[7]),
+                                            pack4_sat_s8(r[8], r[9], r[10], r[11]),
+                                            pack4_sat_s8(r[12], r[13], r[14], r[15]));
                         } else {
-                            pk = make_uint4(pack8_low_nibbles(r), pack8_low_nibbles(r + 8), pack8_low_nibbles(r + 16),
-                                            pack8_low_nibbles(r + 24));
+                            pk = make_uint4(pack8_sat_s4(r), pack8_sat_s4(r + 8), pack8_sat_s4(r + 16),
+                                            pack8_sat_s4(r + 24));
                         }
                         const int sbyte = c * 16;                 // byte within this warp's slab row
                         if constexpr (OUT == OUT_TMA) {

@@ -202,17 +202,18 @@ static void enumerate_candidates(conv_q_plan_s *p) {
     // duplicate-aware (halo) candidates: stride-1 INT8 R x S convolutions whose
     // halo box (rows covering 128 MMA rows + the largest tap shift) fits 32 KB
     const int Wp = p->W + 2 * p->pad;
-    if (p->bits == 8 && p->stride == 1 && p->R * p->S > 1 && Wp <= BM && p->C % 64 == 0) {
+    if (p->bits == 8 && p->stride == 1 && p->R == 3 && p->S == 3 && Wp <= BM && p->C % 64 == 0) {
         const int kch = p->C % 128 == 0 ? 128 : 64;
         const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
         if ((int64_t)halo_rows * Wp * kch <= 32768 && halo_rows <= 256)
-            for (int cg : {1, 2})
-                for (int bn : {64, 128, 256}) {
-                    if (bn > 64 && bn / 2 >= p->K) continue;
-                    Cand cand{bn, kch, cg, 3, 1};
-                    cand.halo = 1;
-                    if (cand_fits<8>(cand)) p->cands.push_back(cand);
-                }
+            for (int nsub : {3, 1})
+                for (int cg : {1, 2})
+                    for (int bn : {64, 128, 256}) {
+                        if (bn > 64 && bn / 2 >= p->K) continue;
+                        Cand cand{bn, kch, cg, nsub, 1};
+                        cand.halo = 1;
+                        if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                    }
     }
 }
 
@@ -325,7 +326,6 @@ extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, 
     enumerate_candidates(p);
     p->sel = default_candidate(p);
     if (const char *pr = getenv("CONV_Q_PROBE")) p->probe = atoi(pr);
-    if (const char *bo = getenv("CONV_Q_DESC_BO")) p->desc_bo = atoi(bo);
     apply_cache(p);
     if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK && ensure_ws(p) != CONV_Q_OK) {
         delete p;
@@ -704,6 +704,29 @@ extern "C" CONVQ_API int conv_q_mma_pipe_probe(int groups, int G, int S, int n, 
     cudaFree(sink);
     if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "probe kernel failed: %s", cudaGetErrorString(e));
     *ops_per_s = 2.0 * 128 * n * 32 * (double)groups * G * g_num_sms / (ms * 1e-3);
+    return CONV_Q_OK;
+}
+
+// Measurement only: per-primitive single-thread cycles of the MMA warp (see micro_probe_kernel).
+extern "C" CONVQ_API int conv_q_micro_probe(int mode, int iters, int n, double *cycles_per_iter) {
+    if (mode < 0 || mode > 9 || iters < 1 || n < 16 || n > 256 || (n % 16) || !cycles_per_iter)
+        return set_err(CONV_Q_EINVAL, "bad probe arguments");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int smem = 1024 + (128 + 256) * 128 + 256;
+    void (*kerns[10])(int, int, long long *) = {micro_probe_kernel<0>, micro_probe_kernel<1>, micro_probe_kernel<2>,
+                                                micro_probe_kernel<3>, micro_probe_kernel<4>, micro_probe_kernel<5>,
+                                                micro_probe_kernel<6>, micro_probe_kernel<7>, micro_probe_kernel<8>,
+                                                micro_probe_kernel<9>};
+    CUDA_TRY(cudaFuncSetAttribute(kerns[mode], cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    long long *out = nullptr;
+    CUDA_TRY(cudaMalloc(&out, sizeof(long long)));
+    kerns[mode]<<<1, 128, smem>>>(iters, n, out);
+    long long h = 0;
+    cudaError_t e = cudaMemcpy(&h, out, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(out);
+    if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "probe kernel failed: %s", cudaGetErrorString(e));
+    *cycles_per_iter = (double)h / iters;
     return CONV_Q_OK;
 }
 

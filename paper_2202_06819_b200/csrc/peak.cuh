@@ -192,4 +192,98 @@ __global__ void __launch_bounds__(128, 1) mma_pipe_probe2_kernel(int groups, int
         tmem_dealloc_cg2<256>(tmem);
     }
 }
+// Measurement only: single-thread cost of the MMA warp's primitives, in SM
+// cycles per iteration (clock64), one CTA.  mode:
+//   0  mbarrier.try_wait on an already-completed phase (result consumed)
+//   1  mbarrier.test_wait on an already-completed phase
+//   2  tcgen05.mma M=128 N=n K=32, back to back (no commit)
+//   3  tcgen05.mma + tcgen05.commit (arrive on a barrier nobody waits for)
+//   4  tcgen05.commit alone
+//   5  G=4 x tcgen05.mma + commit + try_wait(completed barrier), as one stage
+//   6  like 5, but the try_wait of the *next* stage is issued before the MMAs
+template <int mode>
+__global__ void __launch_bounds__(128, 1) micro_probe_kernel(int iters, int n, long long *out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t *a = smem, *b = smem + 128 * 128;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(b + 256 * 128);
+    uint32_t *holder = reinterpret_cast<uint32_t *>(bars + 4);
+    for (int i = threadIdx.x; i < (128 + 256) * 128 / 16; i += blockDim.x)
+        reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+        mbar_arrive(&bars[0]);   // phase 0 of bars[0] complete
+    }
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) tmem_alloc<256>(holder);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *holder;
+    long long t = 0;
+    if (warp == 1) {
+        const uint32_t idesc = idesc_i8(128, n);
+        const uint64_t ad = umma_desc_kmajor(smem_u32(a), 128), bd = umma_desc_kmajor(smem_u32(b), 128);
+        uint32_t acc = 0;
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            if constexpr (mode == 7) {
+                acc += (uint32_t)it * 3u;
+            } else if constexpr (mode == 8) {
+                if (elect_one()) acc += 1u;
+                __syncwarp();
+            } else if constexpr (mode == 9) {
+                asm volatile("" ::: "memory");
+                acc += 1u;
+            } else if constexpr (mode == 0) {
+                acc += mbar_try_wait(&bars[0], 0) ? 1u : 0u;
+            } else if constexpr (mode == 1) {
+                uint32_t ok;
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                             "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(&bars[0])), "r"(0u) : "memory");
+                acc += ok;
+            } else if constexpr (mode == 2) {
+                if (elect_one()) mma_i8(tmem, ad, bd, idesc, it != 0);
+                __syncwarp();
+            } else if constexpr (mode == 3) {
+                if (elect_one()) { mma_i8(tmem, ad, bd, idesc, it != 0); mma_commit(&bars[1]); }
+                __syncwarp();
+            } else if constexpr (mode == 4) {
+                if (elect_one()) mma_commit(&bars[1]);
+                __syncwarp();
+            } else if constexpr (mode == 5) {
+                mbar_wait(&bars[0], 0);
+                tc_fence_after();
+                if (elect_one()) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) mma_i8(tmem, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
+                    mma_commit(&bars[1]);
+                }
+                __syncwarp();
+            } else {
+                const bool ready = mbar_try_wait(&bars[0], 0);
+                tc_fence_after();
+                if (elect_one()) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) mma_i8(tmem, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
+                    mma_commit(&bars[1]);
+                }
+                __syncwarp();
+                if (!ready) mbar_wait(&bars[0], 0);
+            }
+        }
+        t = clock64() - t0;
+        if (threadIdx.x == 32) out[0] = t + (acc == 12345 ? 1 : 0);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<256>(tmem);
+    }
+}
+
 }  // namespace convq

@@ -47,8 +47,6 @@ struct conv_q_plan_s {
     int sel = 0;
     float tuned_us = -1.f;
     int probe = 0;     // CONV_Q_PROBE (measurement only; results are garbage when != 0)
-    int desc_bo = 0;   // CONV_Q_DESC_BO: UMMA base-offset field for row-shifted halo windows (measured: the
-                       // swizzle follows absolute smem address bits, so 0 is correct)
     unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
     CUtensorMap tm_a, tm_b, tm_y;
@@ -71,13 +69,15 @@ namespace convq {
 template <int BITS>
 inline bool cand_fits(const Cand &c) {
     if (c.halo) {
-#define CONVQ_HFIT(BN_, KC_, CG_)                                                                   \
-        if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_)                                             \
-            return ConvCfg<BITS, BN_, KC_, OUT_DIRECT, CG_, 3, 1>::FITS && ConvCfg<BITS, BN_, KC_, OUT_S32, CG_, 3, 1>::FITS;
-        CONVQ_HFIT(64, 128, 1) CONVQ_HFIT(128, 128, 1) CONVQ_HFIT(256, 128, 1)
-        CONVQ_HFIT(64, 64, 1) CONVQ_HFIT(128, 64, 1) CONVQ_HFIT(256, 64, 1)
-        CONVQ_HFIT(64, 128, 2) CONVQ_HFIT(128, 128, 2) CONVQ_HFIT(256, 128, 2)
-        CONVQ_HFIT(64, 64, 2) CONVQ_HFIT(128, 64, 2) CONVQ_HFIT(256, 64, 2)
+#define CONVQ_HFIT(BN_, KC_, CG_, NS_)                                                              \
+        if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_ && c.nsub == NS_)                            \
+            return ConvCfg<BITS, BN_, KC_, OUT_DIRECT, CG_, NS_, 1>::FITS && ConvCfg<BITS, BN_, KC_, OUT_S32, CG_, NS_, 1>::FITS;
+#define CONVQ_HFIT_NS(BN_, KC_, CG_) CONVQ_HFIT(BN_, KC_, CG_, 3) CONVQ_HFIT(BN_, KC_, CG_, 1)
+        CONVQ_HFIT_NS(64, 128, 1) CONVQ_HFIT_NS(128, 128, 1) CONVQ_HFIT_NS(256, 128, 1)
+        CONVQ_HFIT_NS(64, 64, 1) CONVQ_HFIT_NS(128, 64, 1) CONVQ_HFIT_NS(256, 64, 1)
+        CONVQ_HFIT_NS(64, 128, 2) CONVQ_HFIT_NS(128, 128, 2) CONVQ_HFIT_NS(256, 128, 2)
+        CONVQ_HFIT_NS(64, 64, 2) CONVQ_HFIT_NS(128, 64, 2) CONVQ_HFIT_NS(256, 64, 2)
+#undef CONVQ_HFIT_NS
 #undef CONVQ_HFIT
         return false;
     }
@@ -121,7 +121,6 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.m_tiles = p->N * prm.tiles_per_img;
     const int halo_rows = (int)ceil_div(BM + (p->R - 1) * prm.Wp + p->S - 1, prm.Wp);
     prm.halo_tx = halo_rows * prm.Wp * Cfg::LOAD_ROW;
-    prm.desc_bo = p->desc_bo;
     if (HALO) prm.num_tiles = (int)(ceil_div(prm.m_tiles, CG) * prm.n_tiles);
     prm.splits = HALO ? 1 : p->cands[p->sel].split;
     prm.num_units = prm.num_tiles * prm.splits;
@@ -163,17 +162,19 @@ template <int BITS, int OUT>
 inline int dispatch_bn_kch(conv_q_plan_s *p, const float *scale, void *y) {
     const Cand c = p->cands[p->sel];
     if (c.halo) {
-#define CONVQ_HCASE(BN_, KC_, CG_)                                                                 \
-        if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_) {                                          \
-            if constexpr (ConvCfg<BITS, BN_, KC_, OUT, CG_, 3, 1>::FITS)                           \
-                return launch_conv<BITS, BN_, KC_, OUT, CG_, 3, 1>(p, scale, y);                   \
+#define CONVQ_HCASE(BN_, KC_, CG_, NS_)                                                            \
+        if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_ && c.nsub == NS_) {                         \
+            if constexpr (ConvCfg<BITS, BN_, KC_, OUT, CG_, NS_, 1>::FITS)                         \
+                return launch_conv<BITS, BN_, KC_, OUT, CG_, NS_, 1>(p, scale, y);                 \
             else                                                                                   \
                 return set_err(CONV_Q_EUNSUPPORTED, "halo config unavailable for this output mode");  \
         }
-        CONVQ_HCASE(64, 128, 1) CONVQ_HCASE(128, 128, 1) CONVQ_HCASE(256, 128, 1)
-        CONVQ_HCASE(64, 64, 1) CONVQ_HCASE(128, 64, 1) CONVQ_HCASE(256, 64, 1)
-        CONVQ_HCASE(64, 128, 2) CONVQ_HCASE(128, 128, 2) CONVQ_HCASE(256, 128, 2)
-        CONVQ_HCASE(64, 64, 2) CONVQ_HCASE(128, 64, 2) CONVQ_HCASE(256, 64, 2)
+#define CONVQ_HCASE_NS(BN_, KC_, CG_) CONVQ_HCASE(BN_, KC_, CG_, 3) CONVQ_HCASE(BN_, KC_, CG_, 1)
+        CONVQ_HCASE_NS(64, 128, 1) CONVQ_HCASE_NS(128, 128, 1) CONVQ_HCASE_NS(256, 128, 1)
+        CONVQ_HCASE_NS(64, 64, 1) CONVQ_HCASE_NS(128, 64, 1) CONVQ_HCASE_NS(256, 64, 1)
+        CONVQ_HCASE_NS(64, 128, 2) CONVQ_HCASE_NS(128, 128, 2) CONVQ_HCASE_NS(256, 128, 2)
+        CONVQ_HCASE_NS(64, 64, 2) CONVQ_HCASE_NS(128, 64, 2) CONVQ_HCASE_NS(256, 64, 2)
+#undef CONVQ_HCASE_NS
 #undef CONVQ_HCASE
         return set_err(CONV_Q_EUNSUPPORTED, "no halo kernel for bn=%d kch=%d cg=%d", c.bn, c.kch, c.cg);
     }
