@@ -1,6 +1,7 @@
 """Build libconvq.so in-tree with nvcc for sm_100a (no torch extension, no JIT).
 
-The kernel instantiations live in six translation units (kern_b{8,4}_o{0,1,2}.cu)
+The kernel instantiations live in eight translation units (kern_b{8,4}_o{0,1,2}.cu and
+the INT8 ReLU-specialised kern_b8_o{4,6}.cu)
 compiled in parallel, plus the host library convq.cu; objects are linked into
 one shared library with the CUDA runtime linked statically."""
 from __future__ import annotations
@@ -16,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libconvq.so")
-SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2)]
+SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2)] + ["kern_b8_o4.cu", "kern_b8_o6.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]

@@ -47,7 +47,7 @@ namespace convq {
 constexpr int BM = 128;
 // per-CTA trace counters (cycles): where the control loops wait
 enum { TR_PROD_EMPTY = 0, TR_MMA_FULL, TR_MMA_ACC, TR_EPI_ACC, TR_MMA_ISSUE, TR_TOTAL, TR_TILES, TR_T0, TR_T1,
-       TR_TPDL, TR_TFULL, TR_TACC, TR_SLOTS = 12 };
+       TR_TPDL, TR_TFULL, TR_TACC, TR_EPI_SLAB, TR_EPI_BODY, TR_EPI_STORE, TR_SLOTS = 15 };
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -90,7 +90,8 @@ struct ConvParams {
 // Output path of the epilogue.
 constexpr int OUT_TMA = 0;     // packed codes staged in smem, written by TMA stores
 constexpr int OUT_S32 = 1;     // raw int32 accumulators, direct global stores (debug / parity)
-constexpr int OUT_DIRECT = 2;  // packed codes, 16-byte direct global stores (no staging smem ->
+constexpr int OUT_DIRECT = 2;
+constexpr int OUT_RELU = 4;    // flag: INT8 ReLU-specialised epilogue (OUT_TMA | OUT_RELU, OUT_DIRECT | OUT_RELU)  // packed codes, 16-byte direct global stores (no staging smem ->
                                // deeper operand pipeline; L2 merges the row pieces)
 
 template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO = 0>
@@ -114,7 +115,9 @@ struct ConvCfg {
     static constexpr int SUB_TX = ((HALO ? 0 : BM) + BNL) * LOAD_ROW;  // TMA bytes per k-block per CTA
     static constexpr int HALO_BYTES = HALO ? 32768 : 0;      // one halo buffer (budget; checked at plan time)
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
-    static constexpr int OUT_BYTES = OUT == OUT_TMA ? BM * OUT_ROW : 0;   // staging per TMEM buffer
+    static constexpr int OUTP = OUT & 3;                     // output path
+    static constexpr bool RELU8 = BITS == 8 && (OUT & OUT_RELU) != 0;
+    static constexpr int OUT_BYTES = OUTP == OUT_TMA ? BM * OUT_ROW : 0;   // staging per TMEM buffer
     static constexpr int NUM_EPI = BITS == 8 ? 4 : 2;               // epilogue warpgroups
     // TMEM accumulator buffers: as many as the 512 columns allow (max 4), so
     // up to NBUF tiles are in the epilogue while the MMA fills the next one
@@ -150,7 +153,7 @@ struct ConvCfg {
     static constexpr int MMA_WARP = PROD_WARP + 1;
     static constexpr int NUM_THREADS = 32 * (MMA_WARP + 1);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
-    static constexpr bool FITS = STAGES >= 2 && (!HALO || (BITS == 8 && OUT != OUT_TMA));  // else never instantiated
+    static constexpr bool FITS = STAGES >= 2 && (!HALO || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
     static_assert(NSUB >= 1 && NSUB <= 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
@@ -208,6 +211,25 @@ __device__ __forceinline__ int requant_int(int acc, float sc, float sh, float lo
     int r;
     asm("cvt.rni.s32.f32 %0, %1;" : "=r"(r) : "f"(u));
     return r;
+}
+// ReLU, s8: lo = 0, hi = 127.  One F2I with round-to-nearest-even that
+// saturates to [-128, 127] (NaN -> 0 = lo), then the unsigned saturating pack
+// (pack4_sat_u8) takes negatives to 0: clamp(rne(u), 0, 127) exactly, in three
+// instructions per value instead of four.
+__device__ __forceinline__ int requant_relu_s8(int acc, float sc, float sh) {
+    const float u = __fmaf_rn(__int2float_rn(acc), sc, sh);
+    int r;
+    asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(r) : "f"(u));
+    return r;
+}
+// cvt.pack.sat.u8.s32.b32: as pack2_s8 with saturation to [0, 255]
+__device__ __forceinline__ uint32_t pack2_u8(int a, int b, uint32_t c) {
+    uint32_t d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t pack4_sat_u8(int r0, int r1, int r2, int r3) {
+    return pack2_u8(r1, r0, pack2_u8(r3, r2, 0u));
 }
 // cvt.pack.sat.s8.s32.b32 d, a, b, c:  d = c << 16 | sat8(a) << 8 | sat8(b)
 __device__ __forceinline__ uint32_t pack2_s8(int a, int b, uint32_t c) {
@@ -330,7 +352,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tm_a);
         tma_prefetch_desc(&tm_b);
-        if (OUT == OUT_TMA) tma_prefetch_desc(&tm_y);
+        if (Cfg::OUTP == OUT_TMA) tma_prefetch_desc(&tm_y);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -648,6 +670,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         uint8_t *slab = out_stage + b * Cfg::OUT_BYTES + (half * 4 + quad) * Cfg::SLAB;
         const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(&acc_empty[b]), 0) : 0;
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
+        constexpr bool relu8 = Cfg::RELU8;   // ReLU specialisation (p.relu == 1 guaranteed by the dispatch)
         pdl_wait();
         int j = 0;
         for (int unit = tile0 + b * tstep; unit < p.num_units; unit += Cfg::NBUF * tstep, ++j) {
@@ -665,7 +688,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 const bool ok = rt < p.m_tiles && pl < p.rpt && pp < p.P && qq < p.Q;
                 m = ok ? (n * p.P + pp) * p.Q + qq : p.M;
             }
-            if (OUT == OUT_TMA) {   // this warp's slab must have been read out by its previous store
+            if (Cfg::OUTP == OUT_TMA) {   // this warp's slab must have been read out by its previous store
                 if (lane == 0) tma_store_wait_read0();
                 __syncwarp();
             }
@@ -694,7 +717,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             auto process = [&](const uint32_t (&v)[Cfg::CW], const int c) {
                     const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
                     const int col0 = n_blk * BN + ccol;
-                    if (OUT == OUT_S32) {
+                    if (Cfg::OUTP == OUT_S32) {
                         if (m < p.M) {
                             int32_t *dst = p.y32 + (int64_t)m * p.K + col0;
                             if (col0 + Cfg::CW <= p.K) {
@@ -714,7 +737,18 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         }
                     } else {
                         int r[Cfg::CW];
-                        if (col0 + Cfg::CW <= p.K) {
+                        if (BITS == 8 && relu8 && col0 + Cfg::CW <= p.K) {
+                            const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
+                            const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
+#pragma unroll
+                            for (int q = 0; q < Cfg::CW / 4; ++q) {
+                                const float4 sa = __ldg(s4 + q), sb = __ldg(h4 + q);
+                                r[4 * q] = requant_relu_s8((int)v[4 * q], sa.x, sb.x);
+                                r[4 * q + 1] = requant_relu_s8((int)v[4 * q + 1], sa.y, sb.y);
+                                r[4 * q + 2] = requant_relu_s8((int)v[4 * q + 2], sa.z, sb.z);
+                                r[4 * q + 3] = requant_relu_s8((int)v[4 * q + 3], sa.w, sb.w);
+                            }
+                        } else if (col0 + Cfg::CW <= p.K) {
                             const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
                             const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
 #pragma unroll
@@ -735,20 +769,26 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 const bool ok = col0 + q < p.K;  // columns past K are never stored
                                 const float sc = ok ? __ldg(p.scale + col0 + q) : 0.f;
                                 const float sh = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
-                                r[q] = requant_int(BITS == 4 ? ((int)v[q] >> 8) : (int)v[q], sc, sh, lo);
+                                const int x = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
+                                r[q] = relu8 ? requant_relu_s8(x, sc, sh) : requant_int(x, sc, sh, lo);
                             }
                         }
                         uint4 pk;   // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
                         if constexpr (BITS == 8) {
-                            pk = make_uint4(pack4_sat_s8(r[0], r[1], r[2], r[3]), pack4_sat_s8(r[4], r[5], r[6], r[7]),
-                                            pack4_sat_s8(r[8], r[9], r[10], r[11]),
-                                            pack4_sat_s8(r[12], r[13], r[14], r[15]));
+                            if (relu8)   // codes from requant_relu_s8 (both paths): u8 saturation = the lo = 0 clamp
+                                pk = make_uint4(pack4_sat_u8(r[0], r[1], r[2], r[3]), pack4_sat_u8(r[4], r[5], r[6], r[7]),
+                                                pack4_sat_u8(r[8], r[9], r[10], r[11]),
+                                                pack4_sat_u8(r[12], r[13], r[14], r[15]));
+                            else
+                                pk = make_uint4(pack4_sat_s8(r[0], r[1], r[2], r[3]), pack4_sat_s8(r[4], r[5], r[6], r[7]),
+                                                pack4_sat_s8(r[8], r[9], r[10], r[11]),
+                                                pack4_sat_s8(r[12], r[13], r[14], r[15]));
                         } else {
                             pk = make_uint4(pack8_sat_s4(r), pack8_sat_s4(r + 8), pack8_sat_s4(r + 16),
                                             pack8_sat_s4(r + 24));
                         }
                         const int sbyte = c * 16;                 // byte within this warp's slab row
-                        if constexpr (OUT == OUT_TMA) {
+                        if constexpr (Cfg::OUTP == OUT_TMA) {
                             uint8_t *sub = slab + (sbyte / Cfg::EPI_SUBW) * (32 * Cfg::EPI_SUBW);
                             *reinterpret_cast<uint4 *>(sub + swz<Cfg::EPI_SUBW>(lane * Cfg::EPI_SUBW + sbyte % Cfg::EPI_SUBW)) = pk;
                         } else {
@@ -814,7 +854,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
             }
             }
-            if (OUT == OUT_TMA && emit) {
+            if (Cfg::OUTP == OUT_TMA && emit) {
                 fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
                 __syncwarp();
                 if (lane == 0) {
@@ -826,7 +866,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
             }
         }
-        if (OUT == OUT_TMA && lane == 0) tma_store_wait0();
+        if (Cfg::OUTP == OUT_TMA && lane == 0) tma_store_wait0();
     } else if (warp < Cfg::PROD_WARP) {
         // =========================== INT4 transform =========================
         if constexpr (BITS == 4) {

@@ -512,8 +512,11 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
     }
     const bool s32 = p->out_mode == CONV_Q_OUT_S32;
     const bool direct = p->cands[p->sel].direct != 0;
-    if (p->bits == 8)
-        return s32 ? dispatch_conv_8_1(p, scale, y) : direct ? dispatch_conv_8_2(p, scale, y) : dispatch_conv_8_0(p, scale, y);
+    if (p->bits == 8) {
+        if (s32) return dispatch_conv_8_1(p, scale, y);
+        if (p->relu) return direct ? dispatch_conv_8_6(p, scale, y) : dispatch_conv_8_4(p, scale, y);
+        return direct ? dispatch_conv_8_2(p, scale, y) : dispatch_conv_8_0(p, scale, y);
+    }
     return s32 ? dispatch_conv_4_1(p, scale, y) : direct ? dispatch_conv_4_2(p, scale, y) : dispatch_conv_4_0(p, scale, y);
 }
 

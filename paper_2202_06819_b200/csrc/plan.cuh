@@ -202,6 +202,8 @@ inline int dispatch_bn_kch(conv_q_plan_s *p, const float *scale, void *y) {
 int dispatch_conv_8_0(conv_q_plan_s *p, const float *scale, void *y);
 int dispatch_conv_8_1(conv_q_plan_s *p, const float *scale, void *y);
 int dispatch_conv_8_2(conv_q_plan_s *p, const float *scale, void *y);
+int dispatch_conv_8_4(conv_q_plan_s *p, const float *scale, void *y);   // OUT_TMA | OUT_RELU
+int dispatch_conv_8_6(conv_q_plan_s *p, const float *scale, void *y);   // OUT_DIRECT | OUT_RELU
 int dispatch_conv_4_0(conv_q_plan_s *p, const float *scale, void *y);
 int dispatch_conv_4_1(conv_q_plan_s *p, const float *scale, void *y);
 int dispatch_conv_4_2(conv_q_plan_s *p, const float *scale, void *y);

@@ -17,6 +17,7 @@ xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
 y = torch.empty((N, L.P, L.Q, L.K * bits // 8), dtype=torch.uint8, device="cuda")
 cfgs = sys.argv[2:] or p.candidates()
 names = ["prod_wait_empty", "mma_wait_full", "mma_wait_acc", "epi_wait_acc", "mma_issue", "total", "tiles"]
+enames = ["epi_slab", "epi_body", "epi_store"]
 for cname in cfgs:
     p.set_config(p.candidates().index(cname))
     for _ in range(3): p.run(xd, wd, sd, y)
@@ -25,7 +26,7 @@ for cname in cfgs:
     for _ in range(10): p.run(xd, wd, sd, y)
     e1.record(); torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / 10 * 1000
-    tr = torch.zeros(148 * 12, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(148 * 15, dtype=torch.int64, device="cuda")
     h0, h1 = torch.cuda.Event(True), torch.cuda.Event(True)
     lib.conv_q_plan_set_trace(p._h, ctypes.c_void_p(tr.data_ptr()))
     torch.cuda.synchronize()
@@ -34,10 +35,11 @@ for cname in cfgs:
     h1.record()
     torch.cuda.synchronize()
     lib.conv_q_plan_set_trace(p._h, None)
-    t = tr.view(148, 12).double().cpu()
+    t = tr.view(148, 15).double().cpu()
     act = t[:, 5] > 0
     m = t[act].mean(0)
     s = "  ".join(f"{n}={m[i]/1965:6.1f}" for i, n in enumerate(names[:6]))
+    s += "  " + "  ".join(f"{n}={m[12 + i]/1965:6.1f}" for i, n in enumerate(enames))
     t0 = t[act, 7]; t1 = t[act, 8]; tp = t[act, 9]
     base = t0.min()
     print(f"{cname:26s} {us:6.1f}us (traced run {h0.elapsed_time(h1)*1000:6.1f}) ctas={int(act.sum())} "
