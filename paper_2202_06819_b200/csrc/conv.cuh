@@ -129,7 +129,11 @@ struct ConvCfg {
     static constexpr int EPI_NSUB = EPI_ROW / EPI_SUBW;
     static constexpr int SLAB = 32 * EPI_ROW;                       // one warp's staging slab
     static constexpr int CW = BITS == 8 ? 16 : 32;                  // columns per tcgen05.ld (16 B packed)
-    static constexpr int SS_BYTES = 0;
+    // per TMEM buffer, two slots (tiles alternate): the tile's BN scales then BN
+    // shifts (fp32), bulk-copied from global one tile ahead by the buffer's
+    // first epilogue warp; the epilogue reads them with LDS (per-chunk global
+    // loads were the epilogue's top stall: L1-hit latency, 64-bit addressing)
+    static constexpr int SS_BYTES = OUTP == OUT_S32 ? 0 : 2 * 8 * BN;
     static constexpr int BAR_BYTES = 1024;
     static constexpr int stages_with(int nhalo) {
         return (SMEM_LIMIT - 1024 - BAR_BYTES - NBUF * (OUT_BYTES + SS_BYTES) - nhalo * HALO_BYTES) / STAGE_BYTES;
@@ -200,52 +204,48 @@ __device__ __forceinline__ void expand_tile(const uint8_t *src, uint8_t *dst, in
 
 // Requantize (section 3.2.2; DESIGN readings 4-5):
 //   y = clamp(rne(fmaf((float)acc, scale, shift)), lo, hi)
-// as I2FP, FFMA, max(., lo) (NaN -> lo, and the lower clamp: lo is an
-// integer, so rne(max(u, lo)) == max(rne(u), lo)), then one F2I with
-// round-to-nearest-even that saturates to s32; the upper clamp (and the
-// narrowing) is the saturation of the packing instruction below
-// (I2IP.S8/S4.SAT, lo >= -2^(b-1)).  Measured ~1.8x the outputs/clk of the
-// clamp-in-float + magic-add + byte-permute sequence (scripts/micro/epi_math.cu).
+// The float part is I2FP, FFMA and max(., lo) (NaN -> lo, and the lower clamp:
+// lo is an integer, so rne(max(u, lo)) == max(rne(u), lo)); rounding and the
+// upper clamp are done by the conversion to the packed code.
+__device__ __forceinline__ float requant_f(int acc, float sc, float sh, float lo) {
+    return fmaxf(__fmaf_rn(__int2float_rn(acc), sc, sh), lo);
+}
+// INT4: one F2I (round-to-nearest-even, saturating to s32) per code; the upper
+// clamp is the saturation of the s4 packing instruction (I2IP.S4.SAT).
 __device__ __forceinline__ int requant_int(int acc, float sc, float sh, float lo) {
-    const float u = fmaxf(__fmaf_rn(__int2float_rn(acc), sc, sh), lo);
     int r;
-    asm("cvt.rni.s32.f32 %0, %1;" : "=r"(r) : "f"(u));
+    asm("cvt.rni.s32.f32 %0, %1;" : "=r"(r) : "f"(requant_f(acc, sc, sh, lo)));
     return r;
 }
-// ReLU, s8: lo = 0, hi = 127.  One F2I with round-to-nearest-even that
-// saturates to [-128, 127] (NaN -> 0 = lo), then the unsigned saturating pack
-// (pack4_sat_u8) takes negatives to 0: clamp(rne(u), 0, 127) exactly, in three
-// instructions per value instead of four.
-__device__ __forceinline__ int requant_relu_s8(int acc, float sc, float sh) {
-    const float u = __fmaf_rn(__int2float_rn(acc), sc, sh);
-    int r;
-    asm("cvt.rni.sat.s8.f32 %0, %1;" : "=r"(r) : "f"(u));
-    return r;
-}
-// cvt.pack.sat.u8.s32.b32: as pack2_s8 with saturation to [0, 255]
-__device__ __forceinline__ uint32_t pack2_u8(int a, int b, uint32_t c) {
+// INT8: two codes -> two packed s8 bytes in ONE instruction.  The PTX pair
+// "cvt.rni.s32.f32 x2 ; cvt.pack.sat.s8.s32.b32" (kept adjacent in one asm
+// block) is fused by ptxas into F2IP.S8.F32 (round-to-nearest-even, saturate to
+// [-128, 127], pack with the upper bytes of c): d = c << 16 | q(a) << 8 | q(b).
+// Measured on B200 (scripts/micro/pipe_rates.cu, epi_rates.cu): the separate
+// F2I runs at 16 lanes/clk/SM -- the epilogue's old ceiling -- while F2IP and
+// I2FP run at 64, so a code now costs I2FP + FFMA + FMNMX + half an F2IP.
+__device__ __forceinline__ uint32_t pack2_f32_s8(float a, float b, uint32_t c) {
     uint32_t d;
-    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    asm("{\n .reg .s32 ia, ib;\n cvt.rni.s32.f32 ia, %1;\n cvt.rni.s32.f32 ib, %2;\n"
+        " cvt.pack.sat.s8.s32.b32 %0, ia, ib, %3;\n}" : "=r"(d) : "f"(a), "f"(b), "r"(c));
     return d;
 }
-__device__ __forceinline__ uint32_t pack4_sat_u8(int r0, int r1, int r2, int r3) {
-    return pack2_u8(r1, r0, pack2_u8(r3, r2, 0u));
+// four float values -> one packed s8 word (value 0 in byte 0)
+__device__ __forceinline__ uint32_t pack4_f32_s8(float u0, float u1, float u2, float u3) {
+    return pack2_f32_s8(u1, u0, pack2_f32_s8(u3, u2, 0u));
 }
-// cvt.pack.sat.s8.s32.b32 d, a, b, c:  d = c << 16 | sat8(a) << 8 | sat8(b)
-__device__ __forceinline__ uint32_t pack2_s8(int a, int b, uint32_t c) {
-    uint32_t d;
-    asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
+// ReLU on four packed s8 codes: PRMT with sign-replicating selectors gives
+// 0xFF for every negative byte; clear those bytes.  Two instructions per word.
+__device__ __forceinline__ uint32_t relu_s8x4(uint32_t w) {
+    uint32_t m;   // prmt.b32: selector nibble bit 3 = replicate the sign of the selected byte
+    asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(m) : "r"(w));
+    return w & ~m;
 }
 // cvt.pack.sat.s4.s32.b32 d, a, b, c:  d = c << 8 | sat4(a) << 4 | sat4(b)
 __device__ __forceinline__ uint32_t pack2_s4(int a, int b, uint32_t c) {
     uint32_t d;
     asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
     return d;
-}
-// four codes -> one packed s8 word (code 0 in byte 0), saturating to [-128, 127]
-__device__ __forceinline__ uint32_t pack4_sat_s8(int r0, int r1, int r2, int r3) {
-    return pack2_s8(r1, r0, pack2_s8(r3, r2, 0u));
 }
 // eight codes -> one packed s4 word (code 0 in the low nibble), saturating to [-8, 7]
 __device__ __forceinline__ uint32_t pack8_sat_s4(const int *r) {
@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][NSUB][BM*KCH/2]
     uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][NSUB][BNL*KCH/2]
     uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [NBUF][EPB][4 quads] slabs [EPI_NSUB][32][EPI_SUBW]
+    float *ss_stage = reinterpret_cast<float *>(out_stage + Cfg::NBUF * Cfg::OUT_BYTES);  // [NBUF][2 slots][2][BN]
     uint8_t *halo_buf = out_stage + Cfg::NBUF * (Cfg::OUT_BYTES + Cfg::SS_BYTES);   // HALO: [NHALO][HALO_BYTES]
     uint64_t *bars = reinterpret_cast<uint64_t *>(halo_buf + Cfg::NHALO * Cfg::HALO_BYTES);
     uint64_t *full = bars;                  // TMA -> (transform | MMA)
@@ -335,7 +336,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint64_t *acc_full = bars + 3 * STAGES; // MMA -> epilogue [NBUF]
     uint64_t *acc_empty = acc_full + 4;     // epilogue -> MMA [NBUF]
     uint64_t *hempty = acc_empty + 4;       // HALO: MMA -> TMA, halo buffer free [NHALO <= 4]
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(hempty + 4);
+    uint64_t *ss_full = hempty + 4;         // scale/shift bulk copy -> epilogue [NBUF][2 slots]
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(ss_full + 8);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -362,6 +364,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         for (int b = 0; b < Cfg::NBUF; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF * CG);
+            mbar_init(&ss_full[2 * b], 1);
+            mbar_init(&ss_full[2 * b + 1], 1);
         }
         fence_mbar_init();
     }
@@ -672,6 +676,24 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
         constexpr bool relu8 = Cfg::RELU8;   // ReLU specialisation (p.relu == 1 guaranteed by the dispatch)
         pdl_wait();
+        // scale/shift of the j-th tile of this buffer -> slot j & 1, issued by the
+        // buffer's first warp one tile ahead (when it starts tile j-1, every warp of
+        // the buffer has released tile j-2, whose slot this is)
+        const bool ss_smem = Cfg::OUTP != OUT_S32 && p.splits == 1;
+        const bool ss_issuer = ss_smem && half == 0 && quad == 0;
+        auto ss_issue = [&](int u, int jj) {
+            if (u < p.num_units && elect_one()) {
+                const int n0 = (u - (u / p.n_tiles) * p.n_tiles) * BN;
+                const uint32_t bytes = 4u * (uint32_t)min(BN, p.K - n0);
+                const uint32_t bar = smem_u32(&ss_full[2 * b + (jj & 1)]);
+                const uint32_t dst = smem_u32(ss_stage + (2 * b + (jj & 1)) * 2 * BN);
+                mbar_arrive_expect_tx_cluster(bar, 2 * bytes);
+                bulk_load_g2s(dst, p.scale + n0, bytes, bar);
+                bulk_load_g2s(dst + 4 * BN, p.scale + p.K + n0, bytes, bar);
+            }
+            __syncwarp();
+        };
+        if (ss_issuer) ss_issue(tile0 + b * tstep, 0);
         int j = 0;
         for (int unit = tile0 + b * tstep; unit < p.num_units; unit += Cfg::NBUF * tstep, ++j) {
             const int tile = p.splits == 1 ? unit : unit / p.splits;
@@ -701,6 +723,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
             }
             tc_fence_after();
+            if (ss_issuer) ss_issue(unit + Cfg::NBUF * tstep, j + 1);
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + b * BN + half * Cfg::EPI_COLS;
             // TMEM -> registers, software-pipelined: the load of chunk c+1 is in
             // flight while chunk c is requantized (tcgen05.wait::ld waits for all
@@ -714,7 +737,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     else mbar_arrive(&acc_empty[b]);
                 }
             };
-            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c) {
+            // scale/shift of this tile's columns: the buffer's smem slot (filled by
+            // the MMA warp's bulk copy) or, for split-K units, global memory
+            const float *ss_b = ss_stage + (2 * b + (j & 1)) * 2 * BN;
+            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag) {
+                    constexpr bool SMEM_SS = decltype(smem_tag)::value;
                     const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
                     const int col0 = n_blk * BN + ccol;
                     if (Cfg::OUTP == OUT_S32) {
@@ -736,54 +763,47 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             }
                         }
                     } else {
-                        int r[Cfg::CW];
-                        if (BITS == 8 && relu8 && col0 + Cfg::CW <= p.K) {
-                            const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
-                            const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
+                        // (smem slot: columns past K hold stale values; their codes are never stored)
+                        const bool full = SMEM_SS || col0 + Cfg::CW <= p.K;
+                        float sc[Cfg::CW], sh[Cfg::CW];
+                        if (full) {
+                            const float4 *s4 = reinterpret_cast<const float4 *>(SMEM_SS ? ss_b + ccol : p.scale + col0);
+                            const float4 *h4 = reinterpret_cast<const float4 *>(SMEM_SS ? ss_b + BN + ccol : p.scale + p.K + col0);
 #pragma unroll
                             for (int q = 0; q < Cfg::CW / 4; ++q) {
-                                const float4 sa = __ldg(s4 + q), sb = __ldg(h4 + q);
-                                r[4 * q] = requant_relu_s8((int)v[4 * q], sa.x, sb.x);
-                                r[4 * q + 1] = requant_relu_s8((int)v[4 * q + 1], sa.y, sb.y);
-                                r[4 * q + 2] = requant_relu_s8((int)v[4 * q + 2], sa.z, sb.z);
-                                r[4 * q + 3] = requant_relu_s8((int)v[4 * q + 3], sa.w, sb.w);
-                            }
-                        } else if (col0 + Cfg::CW <= p.K) {
-                            const float4 *s4 = reinterpret_cast<const float4 *>(p.scale + col0);
-                            const float4 *h4 = reinterpret_cast<const float4 *>(p.scale + p.K + col0);
-#pragma unroll
-                            for (int q = 0; q < Cfg::CW / 4; ++q) {
-                                const float4 sa = __ldg(s4 + q), sb = __ldg(h4 + q);
-                                const int x0 = BITS == 4 ? ((int)v[4 * q] >> 8) : (int)v[4 * q];
-                                const int x1 = BITS == 4 ? ((int)v[4 * q + 1] >> 8) : (int)v[4 * q + 1];
-                                const int x2 = BITS == 4 ? ((int)v[4 * q + 2] >> 8) : (int)v[4 * q + 2];
-                                const int x3 = BITS == 4 ? ((int)v[4 * q + 3] >> 8) : (int)v[4 * q + 3];
-                                r[4 * q] = requant_int(x0, sa.x, sb.x, lo);
-                                r[4 * q + 1] = requant_int(x1, sa.y, sb.y, lo);
-                                r[4 * q + 2] = requant_int(x2, sa.z, sb.z, lo);
-                                r[4 * q + 3] = requant_int(x3, sa.w, sb.w, lo);
+                                const float4 sa = SMEM_SS ? s4[q] : __ldg(s4 + q), sb = SMEM_SS ? h4[q] : __ldg(h4 + q);
+                                sc[4 * q] = sa.x; sc[4 * q + 1] = sa.y; sc[4 * q + 2] = sa.z; sc[4 * q + 3] = sa.w;
+                                sh[4 * q] = sb.x; sh[4 * q + 1] = sb.y; sh[4 * q + 2] = sb.z; sh[4 * q + 3] = sb.w;
                             }
                         } else {
 #pragma unroll
                             for (int q = 0; q < Cfg::CW; ++q) {
                                 const bool ok = col0 + q < p.K;  // columns past K are never stored
-                                const float sc = ok ? __ldg(p.scale + col0 + q) : 0.f;
-                                const float sh = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
-                                const int x = BITS == 4 ? ((int)v[q] >> 8) : (int)v[q];
-                                r[q] = relu8 ? requant_relu_s8(x, sc, sh) : requant_int(x, sc, sh, lo);
+                                sc[q] = ok ? __ldg(p.scale + col0 + q) : 0.f;
+                                sh[q] = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
                             }
                         }
                         uint4 pk;   // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
                         if constexpr (BITS == 8) {
-                            if (relu8)   // codes from requant_relu_s8 (both paths): u8 saturation = the lo = 0 clamp
-                                pk = make_uint4(pack4_sat_u8(r[0], r[1], r[2], r[3]), pack4_sat_u8(r[4], r[5], r[6], r[7]),
-                                                pack4_sat_u8(r[8], r[9], r[10], r[11]),
-                                                pack4_sat_u8(r[12], r[13], r[14], r[15]));
-                            else
-                                pk = make_uint4(pack4_sat_s8(r[0], r[1], r[2], r[3]), pack4_sat_s8(r[4], r[5], r[6], r[7]),
-                                                pack4_sat_s8(r[8], r[9], r[10], r[11]),
-                                                pack4_sat_s8(r[12], r[13], r[14], r[15]));
+                            // u = fma((float)acc, scale, shift); the F2IP pair conversion
+                            // rounds (RNE) and saturates to [-128, 127]; ReLU (lo = 0)
+                            // then clears the negative bytes of each packed word.  (Equal
+                            // to clamp(rne(u), lo, hi) for every finite u; u is never NaN
+                            // for finite scale/shift, the documented precondition.)
+                            float u[Cfg::CW];
+#pragma unroll
+                            for (int q = 0; q < Cfg::CW; ++q) u[q] = __fmaf_rn(__int2float_rn((int)v[q]), sc[q], sh[q]);
+                            uint32_t w4[4];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                w4[q] = pack4_f32_s8(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
+                                if (relu8 || p.relu) w4[q] = relu_s8x4(w4[q]);
+                            }
+                            pk = make_uint4(w4[0], w4[1], w4[2], w4[3]);
                         } else {
+                            int r[Cfg::CW];
+#pragma unroll
+                            for (int q = 0; q < Cfg::CW; ++q) r[q] = requant_int((int)v[q] >> 8, sc[q], sh[q], lo);
                             pk = make_uint4(pack8_sat_s4(r), pack8_sat_s4(r + 8), pack8_sat_s4(r + 16),
                                             pack8_sat_s4(r + 24));
                         }
@@ -831,28 +851,30 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             va[q] = (uint32_t)__ldcg(wsr + (c * Cfg::CW + q) * 32);
                             __stcg(wsr + (c * Cfg::CW + q) * 32, 0);
                         }
-                        process(va, c);
+                        process(va, c, std::false_type{});
                     }
                     if (lane == 0) p.cnt[region] = 0u;
                 }
             } else {
-            tmem_ld_issue<Cfg::CW>(taddr, va);
-            tmem_ld_wait_regs(va);
+                // the MMA warp's copy of this tile's scale/shift (long done by now)
+                if (Cfg::OUTP != OUT_S32) mbar_wait(&ss_full[2 * b + (j & 1)], (j >> 1) & 1);
+                tmem_ld_issue<Cfg::CW>(taddr, va);
+                tmem_ld_wait_regs(va);
 #pragma unroll 1
-            for (int c = 0; c < NCH; c += 2) {
-                const bool more1 = c + 1 < NCH;
-                if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
-                else release_acc();
-                process(va, c);
-                if (more1) {
-                    tmem_ld_wait_regs(vb);
-                    const bool more2 = c + 2 < NCH;
-                    if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
-                    else release_acc();
-                    process(vb, c + 1);
-                    if (more2) tmem_ld_wait_regs(va);
+                for (int c = 0; c < NCH; c += 2) {
+                    const bool more1 = c + 1 < NCH;
+                    if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
+                    process(va, c, std::true_type{});
+                    if (more1) {
+                        tmem_ld_wait_regs(vb);
+                        const bool more2 = c + 2 < NCH;
+                        if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
+                        process(vb, c + 1, std::true_type{});
+                        if (more2) tmem_ld_wait_regs(va);
+                    }
                 }
-            }
+                // TMEM columns and the scale/shift slot are both consumed
+                release_acc();
             }
             if (Cfg::OUTP == OUT_TMA && emit) {
                 fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)

@@ -280,6 +280,22 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// arrive + expect-tx on a barrier anywhere in the cluster (own CTA: the local address)
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+                 "r"(bytes)
+                 : "memory");
+}
+// 1-D bulk copy global -> shared memory of a CTA of the cluster (TMA, no tensor
+// map); bytes and both addresses 16-byte aligned; completes on `bar_cluster`
+// (a barrier in the destination CTA).
+__device__ __forceinline__ void bulk_load_g2s(uint32_t dst_cluster, const void *src, uint32_t bytes,
+                                              uint32_t bar_cluster) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     dst_cluster),
+                 "l"(src), "r"(bytes), "r"(bar_cluster)
+                 : "memory");
+}
 // CTA-pair TMA loads: data lands in this CTA's smem, the transaction bytes are
 // counted on the barrier at `bar_cluster` (the pair leader's barrier).
 __device__ __forceinline__ void tma_load_2d_cg2(void *dst, const CUtensorMap *m, uint32_t bar_cluster, int c0, int c1,
