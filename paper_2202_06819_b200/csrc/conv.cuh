@@ -65,6 +65,8 @@ struct ConvParams {
     int n_tiles;    // ceil(K / BN)
     int num_tiles;  // m_tiles * n_tiles
     int relu;
+    int rotate;          // rotate each CTA's k-block start (see the producer)
+    int a_gemm;          // 1x1 / stride 1 / pad 0: A is the input as a [M][C] matrix (tiled TMA, no im2col)
     int probe;           // measurement only: 0 normal, 1 = loads without MMAs, 2 = MMAs without loads
     unsigned long long *trace;  // measurement only: per-CTA wait-cycle counters (TRACE_SLOTS each), or null
     // duplicate-aware (halo) mode, stride 1 only:
@@ -129,11 +131,14 @@ struct ConvCfg {
     static constexpr int EPI_NSUB = EPI_ROW / EPI_SUBW;
     static constexpr int SLAB = 32 * EPI_ROW;                       // one warp's staging slab
     static constexpr int CW = BITS == 8 ? 16 : 32;                  // columns per tcgen05.ld (16 B packed)
-    // per TMEM buffer, two slots (tiles alternate): the tile's BN scales then BN
-    // shifts (fp32), bulk-copied from global one tile ahead by the buffer's
-    // first epilogue warp; the epilogue reads them with LDS (per-chunk global
-    // loads were the epilogue's top stall: L1-hit latency, 64-bit addressing)
-    static constexpr int SS_BYTES = OUTP == OUT_S32 ? 0 : 2 * 8 * BN;
+    // per TMEM buffer, three slots (tile j of the buffer uses slot j % 3): the
+    // tile's BN scales then BN shifts (fp32), bulk-copied from global one tile
+    // ahead by the buffer's first epilogue warp; the epilogue reads them with
+    // LDS (per-chunk global loads were the epilogue's top stall).  Three slots
+    // let every warp release its TMEM buffer before requantizing its last chunk:
+    // the copy for tile j+1 starts once the buffer's warps have released tile
+    // j-1, i.e. have finished tile j-2, the previous user of slot (j+1) % 3.
+    static constexpr int SS_BYTES = OUTP == OUT_S32 ? 0 : 3 * 8 * BN;
     static constexpr int BAR_BYTES = 1024;
     static constexpr int stages_with(int nhalo) {
         return (SMEM_LIMIT - 1024 - BAR_BYTES - NBUF * (OUT_BYTES + SS_BYTES) - nhalo * HALO_BYTES) / STAGE_BYTES;
@@ -327,7 +332,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][NSUB][BM*KCH/2]
     uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][NSUB][BNL*KCH/2]
     uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [NBUF][EPB][4 quads] slabs [EPI_NSUB][32][EPI_SUBW]
-    float *ss_stage = reinterpret_cast<float *>(out_stage + Cfg::NBUF * Cfg::OUT_BYTES);  // [NBUF][2 slots][2][BN]
+    float *ss_stage = reinterpret_cast<float *>(out_stage + Cfg::NBUF * Cfg::OUT_BYTES);  // [NBUF][3 slots][2][BN]
     uint8_t *halo_buf = out_stage + Cfg::NBUF * (Cfg::OUT_BYTES + Cfg::SS_BYTES);   // HALO: [NHALO][HALO_BYTES]
     uint64_t *bars = reinterpret_cast<uint64_t *>(halo_buf + Cfg::NHALO * Cfg::HALO_BYTES);
     uint64_t *full = bars;                  // TMA -> (transform | MMA)
@@ -336,8 +341,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint64_t *acc_full = bars + 3 * STAGES; // MMA -> epilogue [NBUF]
     uint64_t *acc_empty = acc_full + 4;     // epilogue -> MMA [NBUF]
     uint64_t *hempty = acc_empty + 4;       // HALO: MMA -> TMA, halo buffer free [NHALO <= 4]
-    uint64_t *ss_full = hempty + 4;         // scale/shift bulk copy -> epilogue [NBUF][2 slots]
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(ss_full + 8);
+    uint64_t *ss_full = hempty + 4;         // scale/shift bulk copy -> epilogue [NBUF][3 slots]
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(ss_full + 12);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -346,10 +351,12 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;     // position in the CTA pair
     const int tile0 = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
     const int tstep = CG == 2 ? (int)num_clusters_x() : (int)gridDim.x;
-    // INT8 pairs count both CTAs' TMA bytes on the leader's full barrier; INT4
-    // pairs expand locally, then both CTAs' transform warps arrive on the
-    // leader's ready barrier.
-    constexpr bool PAIR_TX = CG == 2 && BITS == 8;
+    // CTA pairs: every CTA's TMA loads complete on its OWN full barrier (a load
+    // that signals the peer CTA's barrier is serialised by the TMA unit -- one in
+    // flight, ~1000 cycles each, measured in scripts/micro/tma_bw.cu).  The
+    // follower relays each filled stage to the leader's `ready` barrier: INT4 by
+    // its transform warps (after expanding), INT8 by its otherwise idle MMA warp.
+    constexpr bool PAIR8 = CG == 2 && BITS == 8;
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tm_a);
@@ -358,14 +365,13 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
-            mbar_init(&ready[s], 4 * CG);
+            mbar_init(&ready[s], BITS == 4 ? 4 * CG : 1);
         }
         for (int h = 0; h < Cfg::NHALO; ++h) mbar_init(&hempty[h], 1);
         for (int b = 0; b < Cfg::NBUF; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF * CG);
-            mbar_init(&ss_full[2 * b], 1);
-            mbar_init(&ss_full[2 * b + 1], 1);
+            for (int k = 0; k < 3; ++k) mbar_init(&ss_full[3 * b + k], 1);
         }
         fence_mbar_init();
     }
@@ -397,7 +403,6 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         constexpr int B_LD = BITS == 4 ? Cfg::B_PK : Cfg::B_S8;
         constexpr int A_LD_SUB = BITS == 4 ? Cfg::A_PK_SUB : Cfg::A_SUB;
         constexpr int B_LD_SUB = BITS == 4 ? Cfg::B_PK_SUB : Cfg::B_SUB;
-        const uint32_t full0_leader = PAIR_TX ? mapa_shared(smem_u32(&full[0]), 0) : 0;
         pdl_wait();
         if (p.trace && lane == 0) p.trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
         int stage = 0;
@@ -427,18 +432,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         if (elect_one()) {
                             const int tx = nsub * Cfg::SUB_TX + (tap == 0 ? p.halo_tx : 0);
                             if (p.probe == 2) {
-                                if (!PAIR_TX || rank == 0) mbar_arrive(&full[stage]);
+                                mbar_arrive(&full[stage]);
                             } else {
-                                if constexpr (PAIR_TX) {
-                                    const uint32_t fb = full0_leader + 8u * stage;
-                                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * tx);
-                                    if (tap == 0)
-                                        tma_load_4d_cg2(halo_buf + hb * Cfg::HALO_BYTES, &tm_a, fb, cblk * Cfg::LOAD_ROW,
-                                                        -p.pad, p0 - p.pad, n, pol_a);
-                                    for (int j = 0; j < nsub; ++j)
-                                        tma_load_2d_cg2(b_s8 + stage * Cfg::B_S8 + j * Cfg::B_SUB, &tm_b, fb,
-                                                        (tap + j) * p.row_bytes + cblk * Cfg::LOAD_ROW, brow, pol_b);
-                                } else {
+                                {
                                     mbar_arrive_expect_tx(&full[stage], tx);
                                     if (tap == 0)
                                         tma_load_4d(halo_buf + hb * Cfg::HALO_BYTES, &tm_a, &full[stage],
@@ -465,14 +461,20 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             const int p0 = rem / p.Q, q0 = rem - p0 * p.Q;
             const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad;
             const int brow = n_blk * BN + (int)rank * Cfg::BNL;  // this CTA's B rows
+            // k-blocks in rotated order: CTA c starts at k-block (7c mod n) and wraps,
+            // so the persistent CTAs do not all stream the same weight rows at once
+            // (integer accumulation: any order is bit-exact)
             int r = 0, s = 0, cblk = 0, kcol = 0;
-            if (kb_lo > 0) {                       // split-K unit: start mid-way through the taps
-                const int tap0 = kb_lo / p.num_cblk;
+            auto seek = [&](int kb) {
+                const int tap0 = kb / p.num_cblk;
                 r = tap0 / p.S;
                 s = tap0 - r * p.S;
-                cblk = kb_lo - tap0 * p.num_cblk;
+                cblk = kb - tap0 * p.num_cblk;
                 kcol = tap0 * p.row_bytes;
-            }
+            };
+            const int nk = kb_hi - kb_lo;
+            int cur = kb_lo + (p.rotate ? (int)(((unsigned)(blockIdx.x / CG) * 7u) % (unsigned)nk) : 0);
+            if (cur > 0) seek(cur);
             for (int kb = kb_lo; kb < kb_hi; kb += NSUB) {
                 const int nsub = min(NSUB, kb_hi - kb);   // ragged last stage of a tile
                 {
@@ -483,9 +485,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 const bool issuer = elect_one();
                 if (issuer) {
                     if (p.probe == 2) {                       // measurement: no loads
-                        if (!PAIR_TX || rank == 0) mbar_arrive(&full[stage]);
-                    } else if (PAIR_TX) {
-                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * nsub * Cfg::SUB_TX);
+                        mbar_arrive(&full[stage]);
                     } else {
                         mbar_arrive_expect_tx(&full[stage], nsub * Cfg::SUB_TX);
                     }
@@ -494,18 +494,17 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     if (issuer && p.probe != 2) {
                         uint8_t *ad = a_dst + stage * A_LD + j * A_LD_SUB;
                         uint8_t *bd = b_dst + stage * B_LD + j * B_LD_SUB;
-                        if constexpr (PAIR_TX) {
-                            const uint32_t fb = full0_leader + 8u * stage;
-                            tma_load_im2col_4d_cg2(ad, &tm_a, fb, cblk * Cfg::LOAD_ROW, w0, h0, n0, (uint16_t)s,
-                                                   (uint16_t)r, pol_a);
-                            tma_load_2d_cg2(bd, &tm_b, fb, kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
-                        } else {
+                        if (p.a_gemm)
+                            tma_load_2d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, m0, pol_a);
+                        else
                             tma_load_im2col_4d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0, (uint16_t)s,
                                                (uint16_t)r, pol_a);
-                            tma_load_2d(bd, &tm_b, &full[stage], kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
-                        }
+                        tma_load_2d(bd, &tm_b, &full[stage], kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
                     }
-                    if (++cblk == p.num_cblk) {            // next filter tap (r, s)
+                    if (++cur == kb_hi) {                  // wrap to the unit's first k-block
+                        cur = kb_lo;
+                        seek(cur);
+                    } else if (++cblk == p.num_cblk) {     // next filter tap (r, s)
                         cblk = 0;
                         kcol += p.row_bytes;
                         if (++s == p.S) { s = 0; ++r; }
@@ -560,6 +559,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         for (int g = 0; g < Cfg::HST; ++g) {
                             long long t0 = p.trace ? clock64() : 0;
                             mbar_wait(&full[stage], phase);
+                            if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's half of the stage
                             if (p.trace && lane == 0) {
                                 const long long t1 = clock64();
                                 atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
@@ -608,6 +608,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     const int nsub = min(NSUB, kb_hi - kb);
                     long long t0 = p.trace ? clock64() : 0;
                     mbar_wait(BITS == 4 ? &ready[stage] : &full[stage], phase);
+                    if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's half of the stage
                     if (p.trace && lane == 0) {
                         const long long t1 = clock64();
                         atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
@@ -655,6 +656,28 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
                 __syncwarp();
             }
+        } else if constexpr (PAIR8) {
+            // follower CTA: relay every stage its own TMA loads filled to the
+            // leader's ready barrier (same stage sequence as the producer)
+            const uint32_t ready0 = mapa_shared(smem_u32(&ready[0]), 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int unit = tile0; unit < p.num_units; unit += tstep) {
+                int nst;
+                if constexpr (HALO) {
+                    nst = p.num_cblk * ((p.R * p.S + NSUB - 1) / NSUB);
+                } else {
+                    int tile, kb_lo, kb_hi;
+                    unit_range(p, unit, tile, kb_lo, kb_hi);
+                    nst = (kb_hi - kb_lo + NSUB - 1) / NSUB;
+                }
+                for (int i = 0; i < nst; ++i) {
+                    mbar_wait(&full[stage], phase);
+                    if (elect_one()) mbar_arrive_cluster(ready0 + 8u * stage);
+                    __syncwarp();
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
         }
     } else if (warp < Cfg::XF_WARP0) {
         // =========================== epilogue ===============================
@@ -676,18 +699,18 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
         constexpr bool relu8 = Cfg::RELU8;   // ReLU specialisation (p.relu == 1 guaranteed by the dispatch)
         pdl_wait();
-        // scale/shift of the j-th tile of this buffer -> slot j & 1, issued by the
-        // buffer's first warp one tile ahead (when it starts tile j-1, every warp of
-        // the buffer has released tile j-2, whose slot this is)
+        // scale/shift of the j-th tile of this buffer -> slot j % 3, issued by the
+        // buffer's first warp one tile ahead (see SS_BYTES)
         const bool ss_smem = Cfg::OUTP != OUT_S32 && p.splits == 1;
         const bool ss_issuer = ss_smem && half == 0 && quad == 0;
         auto ss_issue = [&](int u, int jj) {
             if (u < p.num_units && elect_one()) {
                 const int n0 = (u - (u / p.n_tiles) * p.n_tiles) * BN;
                 const uint32_t bytes = 4u * (uint32_t)min(BN, p.K - n0);
-                const uint32_t bar = smem_u32(&ss_full[2 * b + (jj & 1)]);
-                const uint32_t dst = smem_u32(ss_stage + (2 * b + (jj & 1)) * 2 * BN);
-                mbar_arrive_expect_tx_cluster(bar, 2 * bytes);
+                uint64_t *barp = &ss_full[3 * b + jj % 3];
+                const uint32_t bar = smem_u32(barp);
+                const uint32_t dst = smem_u32(ss_stage + (3 * b + jj % 3) * 2 * BN);
+                mbar_arrive_expect_tx(barp, 2 * bytes);
                 bulk_load_g2s(dst, p.scale + n0, bytes, bar);
                 bulk_load_g2s(dst + 4 * BN, p.scale + p.K + n0, bytes, bar);
             }
@@ -739,7 +762,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             };
             // scale/shift of this tile's columns: the buffer's smem slot (filled by
             // the MMA warp's bulk copy) or, for split-K units, global memory
-            const float *ss_b = ss_stage + (2 * b + (j & 1)) * 2 * BN;
+            const float *ss_b = ss_stage + (3 * b + j % 3) * 2 * BN;
             auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag) {
                     constexpr bool SMEM_SS = decltype(smem_tag)::value;
                     const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
@@ -857,24 +880,24 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
             } else {
                 // the MMA warp's copy of this tile's scale/shift (long done by now)
-                if (Cfg::OUTP != OUT_S32) mbar_wait(&ss_full[2 * b + (j & 1)], (j >> 1) & 1);
+                if (Cfg::OUTP != OUT_S32) mbar_wait(&ss_full[3 * b + j % 3], (j / 3) & 1);
                 tmem_ld_issue<Cfg::CW>(taddr, va);
                 tmem_ld_wait_regs(va);
 #pragma unroll 1
                 for (int c = 0; c < NCH; c += 2) {
                     const bool more1 = c + 1 < NCH;
                     if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
+                    else release_acc();   // every column of this warp is in registers
                     process(va, c, std::true_type{});
                     if (more1) {
                         tmem_ld_wait_regs(vb);
                         const bool more2 = c + 2 < NCH;
                         if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
+                        else release_acc();
                         process(vb, c + 1, std::true_type{});
                         if (more2) tmem_ld_wait_regs(va);
                     }
                 }
-                // TMEM columns and the scale/shift slot are both consumed
-                release_acc();
             }
             if (Cfg::OUTP == OUT_TMA && emit) {
                 fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)

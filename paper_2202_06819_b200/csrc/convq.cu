@@ -326,6 +326,7 @@ extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, 
     enumerate_candidates(p);
     p->sel = default_candidate(p);
     if (const char *pr = getenv("CONV_Q_PROBE")) p->probe = atoi(pr);
+    if (const char *ro = getenv("CONV_Q_ROTATE")) p->rotate = atoi(ro) ? 1 : 0;
     apply_cache(p);
     if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK && ensure_ws(p) != CONV_Q_OK) {
         delete p;
@@ -414,6 +415,17 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw_ld,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(x halo) failed: %d", (int)r);
+    } else if (p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0) {
+        // A (1x1, stride 1, no padding): the im2col matrix IS the input viewed
+        // as [N*H*W][C bytes]; a plain tiled 2-D load of BM rows
+        cuuint64_t dims[2] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->M};
+        cuuint64_t strides[1] = {(cuuint64_t)p->row_bytes};
+        cuuint32_t box[2] = {(cuuint32_t)load_row, (cuuint32_t)BM};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = g_encode_tiled(&p->tm_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(x), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw_ld,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(x 1x1) failed: %d", (int)r);
     } else
     // A: packed NHWC activations, im2col mode ("im2col layout"),
     // {C bytes, W, H, N}; the bounding box walks output pixels with the conv

@@ -46,6 +46,7 @@ struct conv_q_plan_s {
     std::vector<Cand> cands;
     int sel = 0;
     float tuned_us = -1.f;
+    int rotate = 0;    // CONV_Q_ROTATE=1: rotate each CTA's k-block start (A/B measurement)
     int probe = 0;     // CONV_Q_PROBE (measurement only; results are garbage when != 0)
     unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
@@ -133,6 +134,8 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
             return set_err(CONV_Q_EINVAL, "split-K workspace not allocated (select the config outside graph capture)");
     }
     prm.relu = p->relu;
+    prm.rotate = p->rotate;
+    prm.a_gemm = p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0 && !HALO;
     prm.probe = p->probe;
     prm.trace = p->trace;
     prm.scale = scale;

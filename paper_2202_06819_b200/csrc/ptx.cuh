@@ -277,14 +277,12 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
 }
+// Arrive on a barrier of another CTA of the cluster.  Default semantics
+// (release at CTA scope), as CUTLASS's ClusterBarrier::arrive: the explicit
+// .release.cluster form makes ptxas emit MEMBAR.ALL.GPU before the arrive,
+// ~1000 cycles with TMA traffic in flight -- it serialised CTA-pair pipelines.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-// arrive + expect-tx on a barrier anywhere in the cluster (own CTA: the local address)
-__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
-                 "r"(bytes)
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 1-D bulk copy global -> shared memory of a CTA of the cluster (TMA, no tensor
 // map); bytes and both addresses 16-byte aligned; completes on `bar_cluster`
