@@ -100,13 +100,22 @@ template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO = 0>
 struct ConvCfg {
     // CG = CTAs per tile (1, or 2 = a CTA pair running tcgen05.mma.cta_group::2
     // with M = 256: each CTA stages its own 128 A rows and BN/2 B rows).
-    // HALO = 1: duplicate-aware A operand (section 3.1, Alg. 1):
+    // HALO bit 0: duplicate-aware A operand (section 3.1, Alg. 1):
     // per (tile, channel block) ONE halo box of the padded input is loaded and
     // every filter tap reads its A rows as a shifted window of it.
+    // HALO bit 1 (WS): weight-stationary -- every tile of a persistent CTA has the
+    // same N block (grid = a multiple of the N-tile count), so the CTA loads its
+    // BN x R*S*C weight block ONCE into a resident region and the pipeline
+    // stages carry only activations (with bit 0: one halo box per stage).
+    static constexpr bool HA = (HALO & 1) != 0;
+    static constexpr bool WS = (HALO & 2) != 0;
+    static constexpr int WSB = WS ? 65536 : 0;               // resident weight region (budget; plan-time check)
+    static constexpr int HBOX = WS && HA ? (KCH == 64 ? 20480 : 32768) : 0;   // WS halo stage (budget)
+    static constexpr int B_TILE = BN / CG * KCH;             // one resident k-block of this CTA's weight rows
     static constexpr int BNL = BN / CG;                     // B rows staged per CTA
     static constexpr int LOAD_ROW = KCH * BITS / 8;        // packed bytes per row per k-block
-    static constexpr int A_SUB = HALO ? 0 : BM * KCH;       // s8 A sub-tile bytes (one k-block)
-    static constexpr int B_SUB = BNL * KCH;
+    static constexpr int A_SUB = HA ? HBOX : BM * KCH;      // s8 A sub-tile bytes (one k-block / WS halo box)
+    static constexpr int B_SUB = WS ? 0 : BNL * KCH;
     static constexpr int A_S8 = NSUB * A_SUB;               // per stage
     static constexpr int B_S8 = NSUB * B_SUB;
     static constexpr int A_PK_SUB = BITS == 4 ? BM * LOAD_ROW : 0;
@@ -114,8 +123,8 @@ struct ConvCfg {
     static constexpr int A_PK = NSUB * A_PK_SUB;
     static constexpr int B_PK = NSUB * B_PK_SUB;
     static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
-    static constexpr int SUB_TX = ((HALO ? 0 : BM) + BNL) * LOAD_ROW;  // TMA bytes per k-block per CTA
-    static constexpr int HALO_BYTES = HALO ? 32768 : 0;      // one halo buffer (budget; checked at plan time)
+    static constexpr int SUB_TX = ((HA ? 0 : BM) + (WS ? 0 : BNL)) * LOAD_ROW;  // TMA bytes per k-block per CTA
+    static constexpr int HALO_BYTES = HA && !WS ? 32768 : 0;  // one halo buffer (budget; checked at plan time)
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUTP = OUT & 3;                     // output path
     static constexpr bool RELU8 = BITS == 8 && (OUT & OUT_RELU) != 0;
@@ -141,16 +150,16 @@ struct ConvCfg {
     static constexpr int SS_BYTES = OUTP == OUT_S32 ? 0 : 3 * 8 * BN;
     static constexpr int BAR_BYTES = 1024;
     static constexpr int stages_with(int nhalo) {
-        return (SMEM_LIMIT - 1024 - BAR_BYTES - NBUF * (OUT_BYTES + SS_BYTES) - nhalo * HALO_BYTES) / STAGE_BYTES;
+        return (SMEM_LIMIT - 1024 - BAR_BYTES - WSB - NBUF * (OUT_BYTES + SS_BYTES) - nhalo * HALO_BYTES) / STAGE_BYTES;
     }
     // halo buffers in flight: the halo load of tile t+NHALO-1 overlaps tiles
     // t..t+NHALO-2, so more buffers hide more TMA latency; keep >= 2 tiles of
     // weight stages ((9/NSUB) stages per tile, 3x3 filters)
     static constexpr int HST = NSUB >= 9 ? 1 : (9 + NSUB - 1) / NSUB;
-    static constexpr int NHALO = !HALO ? 0 : stages_with(4) >= 2 * HST ? 4 : stages_with(3) >= 2 * HST ? 3 : 2;
+    static constexpr int NHALO = !HA || WS ? 0 : stages_with(4) >= 2 * HST ? 4 : stages_with(3) >= 2 * HST ? 3 : 2;
     static constexpr int STAGES_FIT = stages_with(NHALO);
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * HALO_BYTES + BAR_BYTES;
+    static constexpr int SMEM = 1024 + WSB + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * HALO_BYTES + BAR_BYTES;
     static constexpr int TMEM_COLS = NBUF * BN < 32 ? 32 : NBUF * BN;
     // Warp layout: epilogue warpgroups first, then (INT4) the transform
     // warpgroup, then the TMA producer and the MMA issuer as the two highest
@@ -162,7 +171,8 @@ struct ConvCfg {
     static constexpr int MMA_WARP = PROD_WARP + 1;
     static constexpr int NUM_THREADS = 32 * (MMA_WARP + 1);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
-    static constexpr bool FITS = STAGES >= 2 && (!HALO || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU));  // else never instantiated
+    static constexpr bool FITS = STAGES >= 2 && (!HA || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
+                                 (!WS || (BITS == 8 && (!HA || NSUB == 1)));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
     static_assert(NSUB >= 1 && NSUB <= 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
@@ -327,7 +337,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 
     // ---- carve shared memory (every tile 1024-byte aligned; identical offsets
     // in both CTAs of a pair, as cta_group::2 descriptors require)
-    uint8_t *a_s8 = smem;                               // [STAGES][NSUB][BM*KCH]
+    constexpr bool HA = Cfg::HA, WS = Cfg::WS;
+    uint8_t *b_res = smem;                              // WS: [num_kb][BN rows][KCH] resident weights
+    uint8_t *a_s8 = smem + Cfg::WSB;                    // [STAGES][NSUB][BM*KCH] (WS halo: [STAGES][HBOX])
     uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][NSUB][BNL*KCH]
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][NSUB][BM*KCH/2]
     uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][NSUB][BNL*KCH/2]
@@ -341,6 +353,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint64_t *acc_full = bars + 3 * STAGES; // MMA -> epilogue [NBUF]
     uint64_t *acc_empty = acc_full + 4;     // epilogue -> MMA [NBUF]
     uint64_t *hempty = acc_empty + 4;       // HALO: MMA -> TMA, halo buffer free [NHALO <= 4]
+    uint64_t *bfull = hempty;               // WS (no separate halo buffers): resident weights loaded
     uint64_t *ss_full = hempty + 4;         // scale/shift bulk copy -> epilogue [NBUF][3 slots]
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(ss_full + 12);
 
@@ -368,6 +381,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             mbar_init(&ready[s], BITS == 4 ? 4 * CG : 1);
         }
         for (int h = 0; h < Cfg::NHALO; ++h) mbar_init(&hempty[h], 1);
+        if (WS) mbar_init(bfull, 1);
+        if (WS && CG == 2) mbar_init(&hempty[1], 1);   // leader: the follower's weight block is loaded
         for (int b = 0; b < Cfg::NBUF; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF * CG);
@@ -407,7 +422,43 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         if (p.trace && lane == 0) p.trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
         int stage = 0;
         uint32_t phase = 0;
-        if constexpr (HALO) {
+        if constexpr (WS) {
+            // weight-stationary: this CTA's BN x (R*S*C) weight block, once, as
+            // num_kb k-block tiles [BN rows][KCH] (tap-major k order)
+            if (tile0 < p.num_tiles && elect_one()) {
+                const int brow = (tile0 % p.n_tiles) * BN + (int)rank * Cfg::BNL;
+                mbar_arrive_expect_tx(bfull, (uint32_t)(p.num_kb * Cfg::BNL * Cfg::LOAD_ROW));
+                for (int kb = 0; kb < p.num_kb; ++kb) {
+                    const int tap = kb / p.num_cblk, cb = kb - tap * p.num_cblk;
+                    tma_load_2d(b_res + kb * Cfg::B_TILE, &tm_b, bfull, tap * p.row_bytes + cb * Cfg::LOAD_ROW, brow,
+                                pol_b);
+                }
+            }
+            __syncwarp();
+        }
+        if constexpr (WS && HA) {
+            // one stage = one halo box per (tile, channel block); no weights
+            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+                const int m_blk = tile / p.n_tiles;
+                const int rt = m_blk * CG + (int)rank;            // this CTA's row tile
+                const int n = rt / p.tiles_per_img;               // (>= N: all-OOB box, rows masked)
+                const int p0 = (rt - n * p.tiles_per_img) * p.rpt;
+                for (int cblk = 0; cblk < p.num_cblk; ++cblk) {
+                    {
+                        const long long t0 = p.trace ? clock64() : 0;
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
+                    }
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&full[stage], p.halo_tx);
+                        tma_load_4d(a_s8 + stage * Cfg::A_S8, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, -p.pad,
+                                    p0 - p.pad, n, pol_a);
+                    }
+                    __syncwarp();
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        } else if constexpr (HA) {
             // one halo box per (tile, channel block) + the filter taps' weight
             // k-blocks in groups of NSUB; the halo rides on the first group's barrier
             int hcount = 0;
@@ -473,7 +524,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 kcol = tap0 * p.row_bytes;
             };
             const int nk = kb_hi - kb_lo;
-            int cur = kb_lo + (p.rotate ? (int)(((unsigned)(blockIdx.x / CG) * 7u) % (unsigned)nk) : 0);
+            int cur = kb_lo + (p.rotate && !WS ? (int)(((unsigned)(blockIdx.x / CG) * 7u) % (unsigned)nk) : 0);
             if (cur > 0) seek(cur);
             for (int kb = kb_lo; kb < kb_hi; kb += NSUB) {
                 const int nsub = min(NSUB, kb_hi - kb);   // ragged last stage of a tile
@@ -499,7 +550,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         else
                             tma_load_im2col_4d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0, (uint16_t)s,
                                                (uint16_t)r, pol_a);
-                        tma_load_2d(bd, &tm_b, &full[stage], kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
+                        if (!WS) tma_load_2d(bd, &tm_b, &full[stage], kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
                     }
                     if (++cur == kb_hi) {                  // wrap to the unit's first k-block
                         cur = kb_lo;
@@ -527,6 +578,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             uint32_t toff[9];
 #pragma unroll
             for (int t = 0; t < 9; ++t) toff[t] = (uint32_t)(((t / 3) * p.Wp + (t % 3)) * KCH) >> 4;
+            const uint64_t b_desc_res = umma_desc_kmajor(smem_u32(b_res), KCH);   // WS: resident k-block 0
+            if (WS) mbar_wait(bfull, 0);
+            if (WS && CG == 2) mbar_wait(&hempty[1], 0);   // the follower's weight rows
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -546,7 +600,45 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + buf * BN;
-                if constexpr (HALO) {
+                if constexpr (WS && HA) {
+                    // one stage = this tile's halo box of channel block cblk; tap t
+                    // reads it at row offset r*Wp + s, its weights from the resident
+                    // k-block t*num_cblk + cblk
+                    for (int cblk = 0; cblk < p.num_cblk; ++cblk) {
+                        long long t0 = p.trace ? clock64() : 0;
+                        mbar_wait(&full[stage], phase);
+                        if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's halo box
+                        if (p.trace && lane == 0) {
+                            const long long t1 = clock64();
+                            atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
+                            t0 = t1;
+                        }
+                        tc_fence_after();
+                        if (p.probe == 1) {
+                            if (elect_one()) {
+                                mbar_arrive(&empty[stage]);
+                                if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
+                            }
+                        } else if (elect_one()) {
+                            const uint64_t ad_s = a_desc0 + (uint64_t)((stage * Cfg::A_S8) >> 4);
+#pragma unroll
+                            for (int t = 0; t < 9; ++t) {
+                                const uint64_t ad = ad_s + toff[t];
+                                const uint64_t bd = b_desc_res + (uint64_t)(((t * p.num_cblk + cblk) * Cfg::B_TILE) >> 4);
+#pragma unroll
+                                for (int k = 0; k < KCH / 32; ++k) {
+                                    if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                    else mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                }
+                            }
+                            if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
+                            else mma_commit(&empty[stage]);
+                        }
+                        __syncwarp();
+                        if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                } else if constexpr (HA) {
                     // filter tap (r, s) reads the halo rows starting at r*Wp + s:
                     // the duplicate-aware load of PAPER.md Alg. 1, with the
                     // "genuine index" remap done by the UMMA descriptor start
@@ -631,7 +723,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             for (int j = 0; j < NSUB; ++j) {
                                 if (j < nsub) {
                                     const uint64_t ad = ad0 + (uint64_t)((j * Cfg::A_SUB) >> 4);
-                                    const uint64_t bd = bd0 + (uint64_t)((j * Cfg::B_SUB) >> 4);
+                                    const uint64_t bd = WS ? b_desc_res + (uint64_t)(((kb + j) * Cfg::B_TILE) >> 4)
+                                                           : bd0 + (uint64_t)((j * Cfg::B_SUB) >> 4);
 #pragma unroll
                                     for (int k = 0; k < KCH / 32; ++k) {
                                         const uint32_t acc = (kb - kb_lo + j + k) != 0;
@@ -660,11 +753,18 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             // follower CTA: relay every stage its own TMA loads filled to the
             // leader's ready barrier (same stage sequence as the producer)
             const uint32_t ready0 = mapa_shared(smem_u32(&ready[0]), 0);
+            if (WS) {   // this CTA's weight rows are resident -> tell the leader
+                mbar_wait(bfull, 0);
+                if (elect_one()) mbar_arrive_cluster(mapa_shared(smem_u32(&hempty[1]), 0));
+                __syncwarp();
+            }
             int stage = 0;
             uint32_t phase = 0;
             for (int unit = tile0; unit < p.num_units; unit += tstep) {
                 int nst;
-                if constexpr (HALO) {
+                if constexpr (WS && HA) {
+                    nst = p.num_cblk;
+                } else if constexpr (HA) {
                     nst = p.num_cblk * ((p.R * p.S + NSUB - 1) / NSUB);
                 } else {
                     int tile, kb_lo, kb_hi;
@@ -723,7 +823,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
             const int mrow0 = m_blk * (BM * CG) + (int)rank * BM;
             int m = mrow0 + row;
-            if constexpr (HALO) {
+            if constexpr (HA) {
                 // MMA row -> (output row within the tile, padded column); the
                 // S-1 right-most padded columns and rows past the tile are discarded
                 const int rt = m_blk * CG + (int)rank;

@@ -116,6 +116,7 @@ static std::string cand_name(const conv_q_plan_s *p, int i) {
     if (p->cands[i].split > 1) snprintf(k, sizeof k, "_k%d", p->cands[i].split);
     snprintf(b, sizeof b, "bm%d_bn%d_kc%dx%d_c%d%s%s%s", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
              p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "", p->cands[i].halo ? "_h" : "", k);
+    if (p->cands[i].ws) return std::string(b) + "_w";
     return b;
 }
 
@@ -215,10 +216,36 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                         if (cand_fits<8>(cand)) p->cands.push_back(cand);
                     }
     }
+    // weight-stationary candidates (INT8): the CTA's whole (BN/CG) x R*S*C
+    // weight block stays resident in 64 KB of shared memory, stages carry only
+    // activations (halo boxes for stride-1 3x3, im2col / tiled rows otherwise)
+    if (p->bits == 8) {
+        const int kch = p->C % 128 == 0 ? 128 : p->C % 64 == 0 ? 64 : 0;
+        const int sms = g_num_sms > 0 ? g_num_sms : 148;
+        if (kch)
+            for (int cg : {1, 2})
+                for (int direct : {0, 1})
+                    for (int bn : {64, 128, 256}) {
+                        if (bn > 64 && bn / 2 >= p->K) continue;
+                        if ((int64_t)(bn / cg) * p->R * p->S * p->C > 65536 || ceil_div(p->K, bn) > sms / cg) continue;
+                        for (int nsub : {1, 2}) {
+                            Cand cand{bn, kch, cg, nsub, direct};
+                            cand.ws = 1;
+                            if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                        }
+                        if (p->stride == 1 && p->R == 3 && p->S == 3 && Wp <= BM && direct) {
+                            const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
+                            if ((int64_t)halo_rows * Wp * kch <= (kch == 64 ? 20480 : 32768) && halo_rows <= 256) {
+                                Cand cand{bn, kch, cg, 1, direct};
+                                cand.ws = 1;
+                                cand.halo = 1;
+                                if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                            }
+                        }
+                    }
+    }
 }
 
-// Default pick before tuning: deepest K chunk, then the widest N tile whose
-// tile count still fills one wave of SMs (else the narrowest tile).
 static int default_candidate(const conv_q_plan_s *p) {
     const int64_t m_tiles = ceil_div(p->M, BM);
     const int sms = g_num_sms > 0 ? g_num_sms : 148;

@@ -29,8 +29,20 @@ struct Cand {
     int bn, kch, cg, nsub;  // N tile, channels per k-block, CTAs per tile, k-blocks per stage
     int direct;             // packed output by direct stores (1) or smem staging + TMA store (0)
     int halo = 0;           // duplicate-aware halo A operand (stride 1 only)
+    int ws = 0;             // weight-stationary: resident weight block per CTA (INT8, CG = 1)
     int split = 1;          // split-K work units per tile (1 = none)
 };
+
+// weight-stationary instantiations (BN, KCH, NSUB, halo, CG)
+#define CONVQ_WS_LIST(X)                                                                        \
+    X(64, 64, 1, 1, 1) X(64, 128, 1, 1, 1) X(128, 64, 1, 1, 1) X(128, 128, 1, 1, 1)            \
+    X(64, 64, 1, 1, 2) X(64, 128, 1, 1, 2) X(128, 64, 1, 1, 2) X(128, 128, 1, 1, 2)            \
+    X(64, 64, 1, 0, 1) X(128, 64, 1, 0, 1) X(256, 64, 1, 0, 1)                                \
+    X(64, 128, 1, 0, 1) X(128, 128, 1, 0, 1) X(256, 128, 1, 0, 1)                             \
+    X(64, 64, 2, 0, 1) X(128, 64, 2, 0, 1) X(256, 64, 2, 0, 1)                                \
+    X(64, 128, 2, 0, 1) X(128, 128, 2, 0, 1) X(256, 128, 2, 0, 1)                             \
+    X(64, 64, 1, 0, 2) X(128, 64, 1, 0, 2) X(256, 64, 1, 0, 2)                                \
+    X(64, 128, 1, 0, 2) X(128, 128, 1, 0, 2) X(256, 128, 1, 0, 2)
 
 }  // namespace convq
 
@@ -69,6 +81,17 @@ namespace convq {
 // Whether a TileConfig fits shared memory (>= 2 stages) for both output modes.
 template <int BITS>
 inline bool cand_fits(const Cand &c) {
+    if (c.ws) {
+        if (BITS != 8) return false;
+#define CONVQ_WFIT(BN_, KC_, NS_, H_, CG_)                                                             \
+        if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.halo == H_ && c.cg == CG_)               \
+            return (c.direct ? ConvCfg<BITS, BN_, KC_, OUT_DIRECT, CG_, NS_, 2 + H_>::FITS              \
+                             : ConvCfg<BITS, BN_, KC_, OUT_TMA, CG_, NS_, 2 + H_>::FITS) &&             \
+                   ConvCfg<BITS, BN_, KC_, OUT_S32, CG_, NS_, 2 + H_>::FITS;
+        CONVQ_WS_LIST(CONVQ_WFIT)
+#undef CONVQ_WFIT
+        return false;
+    }
     if (c.halo) {
 #define CONVQ_HFIT(BN_, KC_, CG_, NS_)                                                              \
         if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_ && c.nsub == NS_)                            \
@@ -122,7 +145,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.m_tiles = p->N * prm.tiles_per_img;
     const int halo_rows = (int)ceil_div(BM + (p->R - 1) * prm.Wp + p->S - 1, prm.Wp);
     prm.halo_tx = halo_rows * prm.Wp * Cfg::LOAD_ROW;
-    if (HALO) prm.num_tiles = (int)(ceil_div(prm.m_tiles, CG) * prm.n_tiles);
+    if (HALO & 1) prm.num_tiles = (int)(ceil_div(prm.m_tiles, CG) * prm.n_tiles);
     prm.splits = HALO ? 1 : p->cands[p->sel].split;
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = p->ws;
@@ -135,14 +158,18 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     }
     prm.relu = p->relu;
     prm.rotate = p->rotate;
-    prm.a_gemm = p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0 && !HALO;
+    prm.a_gemm = p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0 && !(HALO & 1);
     prm.probe = p->probe;
     prm.trace = p->trace;
     prm.scale = scale;
     prm.y32 = static_cast<int32_t *>(y);
     prm.y8 = static_cast<uint8_t *>(y);
     prm.out_row = p->out_row;
-    const int clusters = std::min(prm.num_units, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
+    int clusters = std::min(prm.num_units, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
+    if (HALO & 2) {   // weight-stationary: every CTA keeps one N block -> a multiple of the N-tile count
+        clusters = clusters / prm.n_tiles * prm.n_tiles;
+        if (clusters < 1) return set_err(CONV_Q_EUNSUPPORTED, "weight-stationary config needs n_tiles <= SMs");
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * CG);
     cfg.blockDim = dim3(Cfg::NUM_THREADS);
@@ -164,6 +191,20 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
 template <int BITS, int OUT>
 inline int dispatch_bn_kch(conv_q_plan_s *p, const float *scale, void *y) {
     const Cand c = p->cands[p->sel];
+    if (c.ws) {
+        if constexpr (BITS == 8) {
+#define CONVQ_WCASE(BN_, KC_, NS_, H_, CG_)                                                        \
+            if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.halo == H_ && c.cg == CG_) {     \
+                if constexpr (ConvCfg<BITS, BN_, KC_, OUT, CG_, NS_, 2 + H_>::FITS)                \
+                    return launch_conv<BITS, BN_, KC_, OUT, CG_, NS_, 2 + H_>(p, scale, y);        \
+                else                                                                               \
+                    return set_err(CONV_Q_EUNSUPPORTED, "weight-stationary config unavailable for this output mode"); \
+            }
+            CONVQ_WS_LIST(CONVQ_WCASE)
+#undef CONVQ_WCASE
+        }
+        return set_err(CONV_Q_EUNSUPPORTED, "no weight-stationary kernel for bn=%d kch=%d nsub=%d", c.bn, c.kch, c.nsub);
+    }
     if (c.halo) {
 #define CONVQ_HCASE(BN_, KC_, CG_, NS_)                                                            \
         if (c.bn == BN_ && c.kch == KC_ && c.cg == CG_ && c.nsub == NS_) {                         \
