@@ -983,7 +983,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 if (Cfg::OUTP != OUT_S32) mbar_wait(&ss_full[3 * b + j % 3], (j / 3) & 1);
                 tmem_ld_issue<Cfg::CW>(taddr, va);
                 tmem_ld_wait_regs(va);
-#pragma unroll 1
+#pragma unroll
                 for (int c = 0; c < NCH; c += 2) {
                     const bool more1 = c + 1 < NCH;
                     if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
