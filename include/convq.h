@@ -80,6 +80,15 @@ typedef struct conv_q_info_s {
     char config[64];          /* its name, e.g. "bm128_bn256_kc128x1_c1_st" (see conv_q_plan_candidate_name) */
     float tuned_us;           /* per-launch time of the selected config if tuned, else -1 */
     int64_t macs;             /* M * K * Kg: multiply-accumulates of one run */
+    /* (ABI 1.01) tensor shapes conv_q_run expects, in bytes of the innermost dim:
+     *   x [x_dims[0]][x_dims[1]][x_dims[2]][x_dims[3] bytes]
+     *   w [w_dims[0]][w_dims[1]][w_dims[2]][w_dims[3] bytes]
+     * (== [N][H][W][C*bits/8] and [K][R][S][C*bits/8] for conv_q_plan; the
+     * s2d tensors for conv_q_plan_s2d, whose other fields describe the
+     * caller's stride-2 conv). */
+    int s2d;
+    int x_dims[4];
+    int w_dims[4];
 } conv_q_info_t;
 
 /*
@@ -99,6 +108,36 @@ typedef struct conv_q_info_s {
  */
 CONVQ_API conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, int S,
                            int stride, int pad, int bits);
+
+/*
+ * Stem convolution (ABI 1.01): a stride-2 R x S convolution with pad `pad`
+ * over an image with few channels (C <= 4 for bits = 8, C <= 8 for bits = 4),
+ * e.g. ResNet's conv1 7x7/2 over RGB -- the same operation and output
+ * (P = (H+2pad-R)/2 + 1, y packed NHWC [N][P][Q][K*bits/8]) as
+ * conv_q_plan(N,H,W,C,K,R,S,2,pad,bits) on the channel-padded input, computed
+ * as a stride-1 convolution over a space-to-depth(2) view (DESIGN.md s6
+ * "stem"): no 32-channel padding of C=3 (10.7x wasted MMA work and operand
+ * bytes at 7x7/2) and 128/64-byte operand rows instead of 32-byte ones.
+ *   x : conv_q_s2d_quantize output, [N][ceil(H/2)][Q + S2P - 1][16 B]
+ *       (info.x_dims; 16-byte s2d pixels = 2x2 input pixels x 4 (s8) / 8 (s4)
+ *       channel codes, index (2*dh+dw)*CP + c, zero borders)
+ *   w : conv_q_s2d_pack_weights output, [K][R2][1][S2P*16 B] (info.w_dims)
+ * conv_q_run / _tune / _set_epilogue / _set_config / _info work as for any
+ * plan.  Errors: as conv_q_plan, plus EUNSUPPORTED when C exceeds the phase
+ * width or the filter needs more than 8 s2d taps in W.
+ */
+CONVQ_API conv_q_plan_t *conv_q_plan_s2d(int N, int H, int W, int C, int K, int R, int S, int pad, int bits);
+
+/* fp16 NHWC image [N][H][W][C] (device) -> the plan's s2d tensor xs (device,
+ * info.x_dims bytes, 16-byte aligned), quantized exactly as conv_q_quantize:
+ * q = clamp(rne(fp32(x) * inv_scale), lo, hi), NaN -> lo.  Errors: EINVAL. */
+CONVQ_API int conv_q_s2d_quantize(const conv_q_plan_t *plan, const void *x_fp16, float inv_scale, void *xs,
+                                  void *stream);
+
+/* int8 KRSC codes [K][R][S][C] (device, the caller's unpadded C) -> the plan's
+ * window weights (device, info.w_dims bytes).  Once per model. */
+CONVQ_API int conv_q_s2d_pack_weights(const conv_q_plan_t *plan, const int8_t *w_krsc, void *w_packed,
+                                      void *stream);
 
 /*
  * Run the plan: y = requant(conv(x, w), scale) (or raw s32 accumulators).

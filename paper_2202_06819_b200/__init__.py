@@ -19,7 +19,7 @@ from dataclasses import dataclass
 
 __all__ = [
     "ConvQError", "ConvPlan", "PlanInfo", "load", "quantize", "pack_weights", "padded_channels",
-    "int8_peak", "out_dim", "OUT_PACKED", "OUT_S32",
+    "int8_peak", "out_dim", "OUT_PACKED", "OUT_S32", "StemPlan",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -42,7 +42,8 @@ class _Info(ctypes.Structure):
         ("M", ctypes.c_int64), ("Kg", ctypes.c_int64), ("x_bytes", ctypes.c_int64), ("w_bytes", ctypes.c_int64),
         ("y_bytes", ctypes.c_int64), ("y_s32_bytes", ctypes.c_int64), ("relu", ctypes.c_int),
         ("out_mode", ctypes.c_int), ("num_candidates", ctypes.c_int), ("config_index", ctypes.c_int),
-        ("config", ctypes.c_char * 64), ("tuned_us", ctypes.c_float), ("macs", ctypes.c_int64)]
+        ("config", ctypes.c_char * 64), ("tuned_us", ctypes.c_float), ("macs", ctypes.c_int64),
+        ("s2d", ctypes.c_int), ("x_dims", ctypes.c_int * 4), ("w_dims", ctypes.c_int * 4)]
 
 
 @dataclass
@@ -51,6 +52,7 @@ class PlanInfo:
     P: int; Q: int; M: int; Kg: int
     x_bytes: int; w_bytes: int; y_bytes: int; y_s32_bytes: int
     relu: int; out_mode: int; num_candidates: int; config_index: int; config: str; tuned_us: float; macs: int
+    s2d: int; x_dims: tuple; w_dims: tuple
 
 
 _lib = None
@@ -96,6 +98,12 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.conv_q_padded_channels.argtypes = [i, i]
     lib.conv_q_pack_weights.restype = i
     lib.conv_q_pack_weights.argtypes = [vp, i, i, i, i, i, vp, vp]
+    lib.conv_q_plan_s2d.restype = vp
+    lib.conv_q_plan_s2d.argtypes = [i] * 9
+    lib.conv_q_s2d_quantize.restype = i
+    lib.conv_q_s2d_quantize.argtypes = [vp, vp, f, vp, vp]
+    lib.conv_q_s2d_pack_weights.restype = i
+    lib.conv_q_s2d_pack_weights.argtypes = [vp, vp, vp, vp]
     lib.conv_q_last_status.restype = i
     lib.conv_q_last_status.argtypes = []
     lib.conv_q_last_error.restype = ctypes.c_char_p
@@ -184,6 +192,7 @@ class ConvPlan:
         _check(load().conv_q_plan_info(self._h, ctypes.byref(inf)))
         d = {n: getattr(inf, n) for n, _ in _Info._fields_}
         d["config"] = inf.config.decode()
+        d["x_dims"], d["w_dims"] = tuple(inf.x_dims), tuple(inf.w_dims)
         return PlanInfo(**d)
 
     # -- sizes (bytes)
@@ -218,6 +227,58 @@ class ConvPlan:
         return _check(lib.conv_q_plan_tune(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)),
                                            ctypes.c_void_p(_ptr(scale)), ctypes.c_void_p(_ptr(y)),
                                            warmup, reps))
+
+
+class StemPlan(ConvPlan):
+    """conv_q_plan_s2d: a stride-2 stem conv (C <= 4 s8 / 8 s4, e.g. ResNet conv1
+    7x7/2 over RGB) run as a stride-1 conv over a space-to-depth(2) view.
+    Same output as ConvPlan(N,H,W,C',K,R,S,2,pad,bits) on the channel-padded
+    input; inputs come from quantize() / pack_weights() of this class."""
+
+    def __init__(self, N, H, W, C, K, R, S, pad, bits, relu=False, out_mode=OUT_PACKED):
+        lib = load()
+        h = lib.conv_q_plan_s2d(N, H, W, C, K, R, S, pad, bits)
+        if not h:
+            raise ConvQError(lib.conv_q_last_status(), lib.conv_q_last_error().decode())
+        self._h = ctypes.c_void_p(h)
+        self.N, self.H, self.W, self.C, self.K = N, H, W, C, K
+        self.R, self.S, self.stride, self.pad, self.bits = R, S, 2, pad, bits
+        self.P, self.Q = out_dim(H, R, 2, pad), out_dim(W, S, 2, pad)
+        self.set_epilogue(relu, out_mode)
+        inf = self.info()
+        self.x_dims, self.w_dims = inf.x_dims, inf.w_dims
+
+    @property
+    def x_bytes(self):
+        d = self.x_dims
+        return d[0] * d[1] * d[2] * d[3]
+
+    @property
+    def w_bytes(self):
+        d = self.w_dims
+        return d[0] * d[1] * d[2] * d[3]
+
+    def quantize(self, x_fp16, inv_scale: float, out=None, stream=None):
+        """fp16 NHWC image [N,H,W,C] -> the s2d tensor (uint8, x_dims)."""
+        import torch
+        assert x_fp16.dtype == torch.float16 and x_fp16.is_contiguous()
+        assert tuple(x_fp16.shape) == (self.N, self.H, self.W, self.C)
+        if out is None:
+            out = torch.empty(self.x_dims, dtype=torch.uint8, device=x_fp16.device)
+        _check(load().conv_q_s2d_quantize(self._h, ctypes.c_void_p(x_fp16.data_ptr()), float(inv_scale),
+                                          ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream(stream))))
+        return out
+
+    def pack_weights(self, w_codes, out=None, stream=None):
+        """int8 KRSC codes [K,R,S,C] (device) -> window weights (uint8, w_dims)."""
+        import torch
+        assert w_codes.dtype == torch.int8 and w_codes.is_contiguous()
+        assert tuple(w_codes.shape) == (self.K, self.R, self.S, self.C)
+        if out is None:
+            out = torch.empty(self.w_dims, dtype=torch.uint8, device=w_codes.device)
+        _check(load().conv_q_s2d_pack_weights(self._h, ctypes.c_void_p(w_codes.data_ptr()),
+                                              ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream(stream))))
+        return out
 
 
 def quantize(x_fp16, inv_scale: float, bits: int, out=None, stream=None):

@@ -55,8 +55,19 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
 
+// n / d for 0 <= n < 2^31 by multiply-high + shift (divisors fixed per launch;
+// the single-thread control loops run several per tile, and a runtime integer
+// division is ~20 dependent instructions).  m, s from make_fastdiv (plan.cuh).
+struct FastDiv {
+    uint32_t d, m, s;
+    __device__ __forceinline__ int div(int n) const {
+        return (int)((__umulhi((uint32_t)n, m) + (uint32_t)n) >> s);
+    }
+};
+
 struct ConvParams {
     int N, H, W, C, K, R, S, stride, pad;
+    int pad_w;      // left padding of the im2col W walk (= pad, or 0 for the space-to-depth stem's window view)
     int P, Q;
     int M;          // N*P*Q
     int row_bytes;  // packed bytes per input pixel row = C*BITS/8
@@ -67,7 +78,9 @@ struct ConvParams {
     int relu;
     int rotate;          // rotate each CTA's k-block start (see the producer)
     int a_gemm;          // 1x1 / stride 1 / pad 0: A is the input as a [M][C] matrix (tiled TMA, no im2col)
-    int probe;           // measurement only: 0 normal, 1 = loads without MMAs, 2 = MMAs without loads
+    int probe;           // measurement only (bits): 1 = no MMAs, 2 = no loads, 4 = no epilogue work
+    int epi_wait;        // epilogue acc_full wait: 0 spin, 1 suspend-time hint, 2 nanosleep back-off
+    unsigned epi_wait_ns;
     unsigned long long *trace;  // measurement only: per-CTA wait-cycle counters (TRACE_SLOTS each), or null
     // duplicate-aware (halo) mode, stride 1 only:
     int Wp;              // padded input width W + 2 pad = MMA-row pitch of an output row
@@ -87,6 +100,7 @@ struct ConvParams {
     int num_units;       // num_tiles * splits
     int32_t *ws;         // [num_tiles*CG][4*EPB regions][EPI_COLS][32] partial sums (kept zero between runs)
     unsigned *cnt;       // per-region arrival counters (kept zero between runs)
+    FastDiv fd_ntiles, fd_PQ, fd_Q, fd_cblk, fd_S, fd_tpi, fd_splits, fd_Wp;
 };
 
 // Output path of the epilogue.
@@ -277,10 +291,10 @@ __device__ __forceinline__ void unit_range(const ConvParams &p, int unit, int &t
         kb_lo = 0;
         kb_hi = p.num_kb;
     } else {
-        tile = unit / p.splits;
+        tile = p.fd_splits.div(unit);
         const int split = unit - tile * p.splits;
-        kb_lo = split * p.num_kb / p.splits;
-        kb_hi = (split + 1) * p.num_kb / p.splits;
+        kb_lo = p.fd_splits.div(split * p.num_kb);
+        kb_hi = p.fd_splits.div((split + 1) * p.num_kb);
     }
 }
 
@@ -439,9 +453,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         if constexpr (WS && HA) {
             // one stage = one halo box per (tile, channel block); no weights
             for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
-                const int m_blk = tile / p.n_tiles;
+                const int m_blk = p.fd_ntiles.div(tile);
                 const int rt = m_blk * CG + (int)rank;            // this CTA's row tile
-                const int n = rt / p.tiles_per_img;               // (>= N: all-OOB box, rows masked)
+                const int n = p.fd_tpi.div(rt);                   // (>= N: all-OOB box, rows masked)
                 const int p0 = (rt - n * p.tiles_per_img) * p.rpt;
                 for (int cblk = 0; cblk < p.num_cblk; ++cblk) {
                     {
@@ -464,9 +478,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             int hcount = 0;
             const int RS = p.R * p.S;
             for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
-                const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
+                const int m_blk = p.fd_ntiles.div(tile), n_blk = tile - m_blk * p.n_tiles;
                 const int rt = m_blk * CG + (int)rank;            // this CTA's row tile
-                const int n = rt / p.tiles_per_img;               // (>= N: all-OOB box, rows masked)
+                const int n = p.fd_tpi.div(rt);                   // (>= N: all-OOB box, rows masked)
                 const int p0 = (rt - n * p.tiles_per_img) * p.rpt;
                 const int brow = n_blk * BN + (int)rank * Cfg::BNL;
                 for (int cblk = 0; cblk < p.num_cblk; ++cblk, ++hcount) {
@@ -482,7 +496,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         }
                         if (elect_one()) {
                             const int tx = nsub * Cfg::SUB_TX + (tap == 0 ? p.halo_tx : 0);
-                            if (p.probe == 2) {
+                            if (p.probe & 2) {
                                 mbar_arrive(&full[stage]);
                             } else {
                                 {
@@ -506,19 +520,19 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         for (int unit = tile0; unit < p.num_units; unit += tstep) {
             int tile, kb_lo, kb_hi;
             unit_range(p, unit, tile, kb_lo, kb_hi);
-            const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
+            const int m_blk = p.fd_ntiles.div(tile), n_blk = tile - m_blk * p.n_tiles;
             const int m0 = m_blk * (BM * CG) + (int)rank * BM;   // this CTA's first output pixel
-            const int n0 = m0 / PQ, rem = m0 - n0 * PQ;
-            const int p0 = rem / p.Q, q0 = rem - p0 * p.Q;
-            const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad;
+            const int n0 = p.fd_PQ.div(m0), rem = m0 - n0 * PQ;
+            const int p0 = p.fd_Q.div(rem), q0 = rem - p0 * p.Q;
+            const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad_w;
             const int brow = n_blk * BN + (int)rank * Cfg::BNL;  // this CTA's B rows
             // k-blocks in rotated order: CTA c starts at k-block (7c mod n) and wraps,
             // so the persistent CTAs do not all stream the same weight rows at once
             // (integer accumulation: any order is bit-exact)
             int r = 0, s = 0, cblk = 0, kcol = 0;
             auto seek = [&](int kb) {
-                const int tap0 = kb / p.num_cblk;
-                r = tap0 / p.S;
+                const int tap0 = p.fd_cblk.div(kb);
+                r = p.fd_S.div(tap0);
                 s = tap0 - r * p.S;
                 cblk = kb - tap0 * p.num_cblk;
                 kcol = tap0 * p.row_bytes;
@@ -535,14 +549,14 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
                 const bool issuer = elect_one();
                 if (issuer) {
-                    if (p.probe == 2) {                       // measurement: no loads
+                    if (p.probe & 2) {                       // measurement: no loads
                         mbar_arrive(&full[stage]);
                     } else {
                         mbar_arrive_expect_tx(&full[stage], nsub * Cfg::SUB_TX);
                     }
                 }
                 for (int j = 0; j < nsub; ++j) {
-                    if (issuer && p.probe != 2) {
+                    if (issuer && !(p.probe & 2)) {
                         uint8_t *ad = a_dst + stage * A_LD + j * A_LD_SUB;
                         uint8_t *bd = b_dst + stage * B_LD + j * B_LD_SUB;
                         if (p.a_gemm)
@@ -614,7 +628,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             t0 = t1;
                         }
                         tc_fence_after();
-                        if (p.probe == 1) {
+                        if (p.probe & 1) {
                             if (elect_one()) {
                                 mbar_arrive(&empty[stage]);
                                 if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
@@ -659,7 +673,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             }
                             tc_fence_after();
                             if (elect_one()) {
-                                if (p.probe == 1) {
+                                if (p.probe & 1) {
                                     mbar_arrive(&empty[stage]);
                                     if (g == Cfg::HST - 1) mbar_arrive(&hempty[hb]);
                                     if constexpr (CG == 2) {
@@ -709,7 +723,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     }
                     tc_fence_after();
                     if (elect_one()) {
-                        if (p.probe == 1) {                // measurement: no MMAs
+                        if (p.probe & 1) {                // measurement: no MMAs
                             if constexpr (CG == 2) {
                                 mbar_arrive(&empty[stage]);
                                 mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
@@ -805,7 +819,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         const bool ss_issuer = ss_smem && half == 0 && quad == 0;
         auto ss_issue = [&](int u, int jj) {
             if (u < p.num_units && elect_one()) {
-                const int n0 = (u - (u / p.n_tiles) * p.n_tiles) * BN;
+                const int n0 = (u - p.fd_ntiles.div(u) * p.n_tiles) * BN;
                 const uint32_t bytes = 4u * (uint32_t)min(BN, p.K - n0);
                 uint64_t *barp = &ss_full[3 * b + jj % 3];
                 const uint32_t bar = smem_u32(barp);
@@ -816,19 +830,19 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             }
             __syncwarp();
         };
-        if (ss_issuer) ss_issue(tile0 + b * tstep, 0);
+        if (ss_issuer && !(p.probe & 4)) ss_issue(tile0 + b * tstep, 0);
         int j = 0;
         for (int unit = tile0 + b * tstep; unit < p.num_units; unit += Cfg::NBUF * tstep, ++j) {
-            const int tile = p.splits == 1 ? unit : unit / p.splits;
-            const int m_blk = tile / p.n_tiles, n_blk = tile - m_blk * p.n_tiles;
+            const int tile = p.splits == 1 ? unit : p.fd_splits.div(unit);
+            const int m_blk = p.fd_ntiles.div(tile), n_blk = tile - m_blk * p.n_tiles;
             const int mrow0 = m_blk * (BM * CG) + (int)rank * BM;
             int m = mrow0 + row;
             if constexpr (HA) {
                 // MMA row -> (output row within the tile, padded column); the
                 // S-1 right-most padded columns and rows past the tile are discarded
                 const int rt = m_blk * CG + (int)rank;
-                const int n = rt / p.tiles_per_img;
-                const int pl = row / p.Wp, qq = row - pl * p.Wp;
+                const int n = p.fd_tpi.div(rt);
+                const int pl = p.fd_Wp.div(row), qq = row - pl * p.Wp;
                 const int pp = (rt - n * p.tiles_per_img) * p.rpt + pl;
                 const bool ok = rt < p.m_tiles && pl < p.rpt && pp < p.P && qq < p.Q;
                 m = ok ? (n * p.P + pp) * p.Q + qq : p.M;
@@ -839,13 +853,21 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             }
             {
                 const long long t0 = p.trace ? clock64() : 0;
-                mbar_wait(&acc_full[b], j & 1);
+                mbar_wait_relaxed(&acc_full[b], j & 1, p.epi_wait, p.epi_wait_ns);
                 if (p.trace && lane == 0 && warp == Cfg::EPI_WARP0) {
                     atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_EPI_ACC, clock64() - t0);
                     if (j == 0) p.trace[blockIdx.x * TR_SLOTS + TR_TACC] = globaltimer_ns();
                 }
             }
             tc_fence_after();
+            if (p.probe & 4) {   // measurement: release the accumulator untouched
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2) mbar_arrive_cluster(acc_empty_leader);
+                    else mbar_arrive(&acc_empty[b]);
+                }
+                continue;
+            }
             if (ss_issuer) ss_issue(unit + Cfg::NBUF * tstep, j + 1);
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + b * BN + half * Cfg::EPI_COLS;
             // TMEM -> registers, software-pipelined: the load of chunk c+1 is in

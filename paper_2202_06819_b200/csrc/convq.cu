@@ -48,7 +48,7 @@ int set_err(int code, const char *fmt, ...) {
 
 extern "C" const char *conv_q_last_error(void) { return g_err.c_str(); }
 extern "C" int conv_q_last_status(void) { return g_status; }
-extern "C" int conv_q_version(void) { return 100; }
+extern "C" int conv_q_version(void) { return 101; }
 
 // ============================================================== driver entry points
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -124,7 +124,7 @@ static std::string shape_key(const conv_q_plan_s *p) {
     char b[160];
     snprintf(b, sizeof b, "N%d_H%d_W%d_C%d_K%d_R%d_S%d_st%d_p%d_b%d_sm%d_m%d_r%d", p->N, p->H, p->W, p->C, p->K, p->R,
              p->S, p->stride, p->pad, p->bits, g_num_sms, p->out_mode, p->relu);
-    return b;
+    return p->s2d ? std::string(b) + "_s2d" : std::string(b);
 }
 
 // in-process tuning cache, optionally mirrored to $CONV_Q_CACHE (one JSON object)
@@ -273,6 +273,8 @@ static void apply_cache(conv_q_plan_s *p) {
         }
 }
 
+static conv_q_plan_t *finish_plan(conv_q_plan_s *p);
+
 extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, int S, int stride, int pad,
                                       int bits) {
     g_err.clear();
@@ -334,25 +336,36 @@ extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, 
                 (long long)bound);
         return nullptr;
     }
-    const int64_t M = (int64_t)N * P * Q;
-    if (M > 2147483647LL - 256) {
-        set_err(CONV_Q_EUNSUPPORTED, "N*P*Q = %lld exceeds the 32-bit GEMM row index", (long long)M);
-        return nullptr;
-    }
     auto *p = new (std::nothrow) conv_q_plan_s();
     if (!p) {
         set_err(CONV_Q_ENOMEM, "plan allocation failed");
         return nullptr;
     }
     p->N = N; p->H = H; p->W = W; p->C = C; p->K = K; p->R = R; p->S = S;
-    p->stride = stride; p->pad = pad; p->bits = bits;
-    p->P = (int)P; p->Q = (int)Q; p->M = M; p->Kg = Kg;
-    p->row_bytes = C * bits / 8;
-    p->out_row = K * bits / 8;
+    p->stride = stride; p->pad = p->pad_hi = pad; p->bits = bits;
+    p->P = (int)P; p->Q = (int)Q;
+    p->o_H = H; p->o_W = W; p->o_C = C; p->o_R = R; p->o_S = S; p->o_stride = stride; p->o_pad = pad;
+    p->xs_W = W;
+    return finish_plan(p);
+}
+
+// Common tail of plan creation: GEMM sizes, candidates, default / cached pick.
+static conv_q_plan_t *finish_plan(conv_q_plan_s *p) {
+    p->M = (int64_t)p->N * p->P * p->Q;
+    p->Kg = (int64_t)p->R * p->S * p->C;
+    if (p->M > 2147483647LL - 256) {
+        set_err(CONV_Q_EUNSUPPORTED, "N*P*Q = %lld exceeds the 32-bit GEMM row index", (long long)p->M);
+        delete p;
+        return nullptr;
+    }
+    p->row_bytes = p->C * p->bits / 8;
+    p->out_row = p->K * p->bits / 8;
     std::call_once(g_init_once, init_device);  // SM count for the default pick; errors surface at run
     enumerate_candidates(p);
     p->sel = default_candidate(p);
     if (const char *pr = getenv("CONV_Q_PROBE")) p->probe = atoi(pr);
+    if (const char *ew = getenv("CONV_Q_EPI_WAIT")) p->epi_wait = atoi(ew);
+    if (const char *en = getenv("CONV_Q_EPI_WAIT_NS")) p->epi_wait_ns = (unsigned)atoi(en);
     if (const char *ro = getenv("CONV_Q_ROTATE")) p->rotate = atoi(ro) ? 1 : 0;
     apply_cache(p);
     if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK && ensure_ws(p) != CONV_Q_OK) {
@@ -360,6 +373,76 @@ extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, 
         return nullptr;
     }
     return p;
+}
+
+static int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// Stride-2 stem conv as a stride-1 conv over a space-to-depth(2) view (pack.cuh):
+// s2d tap rows jr in [0, R2) at s2d row p - PL + jr; in W the S2P consecutive
+// s2d pixels q - PL .. q - PL + S2P - 1 form ONE k-block row of S2P*16 bytes,
+// read through an im2col map whose W stride is one s2d pixel (16 B), i.e.
+// overlapping windows of the stored tensor (no bytes duplicated in HBM).
+extern "C" conv_q_plan_t *conv_q_plan_s2d(int N, int H, int W, int C, int K, int R, int S, int pad, int bits) {
+    g_err.clear();
+    g_status = CONV_Q_OK;
+    if (N < 1 || H < 1 || W < 1 || C < 1 || K < 1 || R < 1 || S < 1) {
+        set_err(CONV_Q_EINVAL, "every dimension must be >= 1");
+        return nullptr;
+    }
+    if (bits != 4 && bits != 8) {
+        set_err(CONV_Q_EINVAL, "bits must be 4 or 8, got %d", bits);
+        return nullptr;
+    }
+    if (pad < 0 || pad > 64) {
+        set_err(CONV_Q_EINVAL, "pad %d outside [0,64]", pad);
+        return nullptr;
+    }
+    const int CP = bits == 8 ? 4 : 8;
+    if (C > CP) {
+        set_err(CONV_Q_EUNSUPPORTED, "s2d stem: C=%d > %d channels per 16-byte s2d pixel phase", C, CP);
+        return nullptr;
+    }
+    if (((int64_t)K * bits) % 128) {
+        set_err(CONV_Q_EUNSUPPORTED, "K*bits (%lld) must be a multiple of 128", (long long)K * bits);
+        return nullptr;
+    }
+    const int64_t P = floor_div(H + 2 * pad - R, 2) + 1, Q = floor_div(W + 2 * pad - S, 2) + 1;
+    if (P < 1 || Q < 1) {
+        set_err(CONV_Q_EINVAL, "output is empty (P=%lld, Q=%lld)", (long long)P, (long long)Q);
+        return nullptr;
+    }
+    const int PL = (pad + 1) / 2;                             // -floor(-pad/2)
+    const int R2 = floor_div(R - 1 - pad, 2) + PL + 1;
+    const int S2 = floor_div(S - 1 - pad, 2) + PL + 1;
+    int S2P = 2;
+    while (S2P < S2) S2P *= 2;
+    if (S2P > 8) {
+        set_err(CONV_Q_EUNSUPPORTED, "s2d stem: %d s2d taps in W exceed one 128-byte k-block", S2);
+        return nullptr;
+    }
+    const int H2 = (H + 1) / 2;
+    const int pad_hi = (int)P - 1 + R2 - H2 - PL;
+    if (R2 > 64 || pad_hi - (R2 - 1) < -128 || pad_hi > 127) {
+        set_err(CONV_Q_EUNSUPPORTED, "s2d stem: filter / padding outside the im2col corner range");
+        return nullptr;
+    }
+    const int64_t Kg = (int64_t)R2 * S2P * 16 * 8 / bits;
+    if (Kg * (int64_t)(1 << 14) > 2147483647LL) {
+        set_err(CONV_Q_EOVERFLOW, "s2d stem: accumulator bound exceeds int32");
+        return nullptr;
+    }
+    auto *p = new (std::nothrow) conv_q_plan_s();
+    if (!p) {
+        set_err(CONV_Q_ENOMEM, "plan allocation failed");
+        return nullptr;
+    }
+    p->s2d = 1;
+    p->N = N; p->H = H2; p->W = (int)Q; p->C = S2P * 16 * 8 / bits; p->K = K; p->R = R2; p->S = 1;
+    p->stride = 1; p->pad = PL; p->pad_hi = pad_hi; p->bits = bits;
+    p->P = (int)P; p->Q = (int)Q;
+    p->xs_W = (int)Q + S2P - 1;
+    p->o_H = H; p->o_W = W; p->o_C = C; p->o_R = R; p->o_S = S; p->o_stride = 2; p->o_pad = pad;
+    return finish_plan(p);
 }
 
 extern "C" void conv_q_plan_destroy(conv_q_plan_t *p) { delete p; }
@@ -406,10 +489,14 @@ extern "C" int conv_q_plan_set_config(conv_q_plan_t *p, int i) {
 extern "C" int conv_q_plan_info(const conv_q_plan_t *p, conv_q_info_t *info) {
     if (!p || !info) return set_err(CONV_Q_EINVAL, "NULL argument");
     memset(info, 0, sizeof *info);
-    info->N = p->N; info->H = p->H; info->W = p->W; info->C = p->C; info->K = p->K;
-    info->R = p->R; info->S = p->S; info->stride = p->stride; info->pad = p->pad; info->bits = p->bits;
+    info->N = p->N; info->H = p->o_H; info->W = p->o_W; info->C = p->o_C; info->K = p->K;
+    info->R = p->o_R; info->S = p->o_S; info->stride = p->o_stride; info->pad = p->o_pad; info->bits = p->bits;
     info->P = p->P; info->Q = p->Q; info->M = p->M; info->Kg = p->Kg;
-    info->x_bytes = (int64_t)p->N * p->H * p->W * p->row_bytes;
+    info->s2d = p->s2d;
+    info->x_dims[0] = p->N; info->x_dims[1] = p->H; info->x_dims[2] = p->xs_W;
+    info->x_dims[3] = p->s2d ? 16 : p->row_bytes;
+    info->w_dims[0] = p->K; info->w_dims[1] = p->R; info->w_dims[2] = p->S; info->w_dims[3] = p->row_bytes;
+    info->x_bytes = (int64_t)info->x_dims[0] * info->x_dims[1] * info->x_dims[2] * info->x_dims[3];
     info->w_bytes = (int64_t)p->K * p->R * p->S * p->row_bytes;
     info->y_bytes = p->M * p->out_row;
     info->y_s32_bytes = p->M * p->K * 4;
@@ -442,6 +529,22 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw_ld,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(x halo) failed: %d", (int)r);
+    } else if (p->s2d) {
+        // A (s2d stem): {window bytes, Q windows, H2, N}; window q starts at stored
+        // column q and spans S2P s2d pixels, so the W stride is ONE s2d pixel
+        // (16 B) while a "pixel" is row_bytes wide: overlapping windows.  H
+        // walks the R2 tap rows with corners (-PL, pad_hi - (R2-1)); out-of-
+        // image rows are zero-filled; columns are zero in the stored borders.
+        cuuint64_t dims[4] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->Q, (cuuint64_t)p->H, (cuuint64_t)p->N};
+        cuuint64_t strides[3] = {16, (cuuint64_t)16 * p->xs_W, (cuuint64_t)16 * p->xs_W * p->H};
+        int lower[2] = {0, -p->pad};
+        int upper[2] = {0, p->pad_hi - (p->R - 1)};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = g_encode_im2col(&p->tm_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(x), dims, strides,
+                                     lower, upper, (cuuint32_t)load_row, (cuuint32_t)BM, estr,
+                                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw_ld, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeIm2col(x s2d windows) failed: %d", (int)r);
     } else if (p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0) {
         // A (1x1, stride 1, no padding): the im2col matrix IS the input viewed
         // as [N*H*W][C bytes]; a plain tiled 2-D load of BM rows
@@ -688,6 +791,48 @@ extern "C" int conv_q_pack_weights(const int8_t *w, int K, int R, int S, int C, 
         pack_weights_kernel<8><<<grid, 256, 0, st>>>(w, static_cast<uint4 *>(wp), n_out_vec);
     else
         pack_weights_kernel<4><<<grid, 256, 0, st>>>(w, static_cast<uint4 *>(wp), n_out_vec);
+    CUDA_TRY(cudaGetLastError());
+    return CONV_Q_OK;
+}
+
+// s2d stem input / weights (pack.cuh s2d_quantize_kernel / s2d_weights_kernel)
+extern "C" int conv_q_s2d_quantize(const conv_q_plan_t *p, const void *x_fp16, float inv_scale, void *xs,
+                                   void *stream) {
+    if (!p || !x_fp16 || !xs) return set_err(CONV_Q_EINVAL, "NULL argument");
+    if (!p->s2d) return set_err(CONV_Q_EINVAL, "plan was not created by conv_q_plan_s2d");
+    if (!aligned16(xs)) return set_err(CONV_Q_EINVAL, "xs must be 16-byte aligned");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int64_t total = (int64_t)p->N * p->H * p->xs_W;
+    const int grid = grid_for(total, 256);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int PL = p->pad;
+    if (p->bits == 8)
+        s2d_quantize_kernel<8><<<grid, 256, 0, st>>>(static_cast<const __half *>(x_fp16), static_cast<uint4 *>(xs),
+                                                     p->N, p->o_H, p->o_W, p->o_C, p->H, p->xs_W, PL, inv_scale);
+    else
+        s2d_quantize_kernel<4><<<grid, 256, 0, st>>>(static_cast<const __half *>(x_fp16), static_cast<uint4 *>(xs),
+                                                     p->N, p->o_H, p->o_W, p->o_C, p->H, p->xs_W, PL, inv_scale);
+    CUDA_TRY(cudaGetLastError());
+    return CONV_Q_OK;
+}
+
+extern "C" int conv_q_s2d_pack_weights(const conv_q_plan_t *p, const int8_t *w_krsc, void *w_packed, void *stream) {
+    if (!p || !w_krsc || !w_packed) return set_err(CONV_Q_EINVAL, "NULL argument");
+    if (!p->s2d) return set_err(CONV_Q_EINVAL, "plan was not created by conv_q_plan_s2d");
+    if (!aligned16(w_packed)) return set_err(CONV_Q_EINVAL, "w_packed must be 16-byte aligned");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int S2P = p->row_bytes / 16;
+    const int64_t total = (int64_t)p->K * p->R * S2P;
+    const int grid = grid_for(total, 256);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (p->bits == 8)
+        s2d_weights_kernel<8><<<grid, 256, 0, st>>>(w_krsc, static_cast<uint4 *>(w_packed), p->K, p->o_R, p->o_S,
+                                                    p->o_C, p->R, S2P, p->pad, p->o_pad);
+    else
+        s2d_weights_kernel<4><<<grid, 256, 0, st>>>(w_krsc, static_cast<uint4 *>(w_packed), p->K, p->o_R, p->o_S,
+                                                    p->o_C, p->R, S2P, p->pad, p->o_pad);
     CUDA_TRY(cudaGetLastError());
     return CONV_Q_OK;
 }

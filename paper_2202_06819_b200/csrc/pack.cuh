@@ -165,4 +165,102 @@ __global__ void __launch_bounds__(256) pack_weights_kernel(const int8_t *__restr
     }
 }
 
+// ---------------------------------------------------------------- s2d stem
+// ResNet-style stem (a stride-2 R x S conv over an image with C <= 4 (s8) /
+// 8 (s4) channels) run as a stride-1 conv over a space-to-depth(2) view
+// (conv_q_plan_s2d, "stem").  One s2d pixel (h2, w2) is
+// 16 bytes: the 2x2 input pixels (2*h2+dh, 2*w2+dw) x CP channels, code index
+// (2*dh + dw)*CP + c, zero where the pixel or channel does not exist.
+// Stored column xc holds s2d column xc - PL (zero outside [0, ceil(W/2))), so
+// the S2P-pixel windows the conv reads never leave the row.
+template <int BITS>
+__global__ void __launch_bounds__(256) s2d_quantize_kernel(const __half *__restrict__ x, uint4 *__restrict__ y,
+                                                          int N, int H, int W, int C, int H2, int XW, int PL,
+                                                          float inv_scale) {
+    constexpr int CP = BITS == 8 ? 4 : 8;      // channels per phase (16 bytes = 4 phases)
+    const float lo = -(float)(1 << (BITS - 1)), hi = (float)((1 << (BITS - 1)) - 1);
+    const int64_t total = (int64_t)N * H2 * XW;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        const int xc = (int)(o % XW);
+        const int64_t t = o / XW;
+        const int h2 = (int)(t % H2);
+        const int n = (int)(t / H2);
+        const int w2 = xc - PL;
+        int q[4 * CP];
+#pragma unroll
+        for (int i = 0; i < 4 * CP; ++i) q[i] = 0;
+        if (w2 >= 0 && 2 * w2 < W) {
+#pragma unroll
+            for (int dh = 0; dh < 2; ++dh) {
+                const int h = 2 * h2 + dh;
+                if (h >= H) continue;
+#pragma unroll
+                for (int dw = 0; dw < 2; ++dw) {
+                    const int w = 2 * w2 + dw;
+                    if (w >= W) continue;
+                    const __half *src = x + (((int64_t)n * H + h) * W + w) * C;
+#pragma unroll
+                    for (int c = 0; c < CP; ++c)
+                        if (c < C) q[(2 * dh + dw) * CP + c] = quant1(src[c], inv_scale, lo, hi);
+                }
+            }
+        }
+        uint32_t out[4];
+        if constexpr (BITS == 8) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) out[k] = pack4_s8(q[4 * k], q[4 * k + 1], q[4 * k + 2], q[4 * k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int u[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) u[i] = q[8 * k + i];
+                out[k] = pack8_s4(u);
+            }
+        }
+        y[o] = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+}
+
+// Stem weights (once per model): int8 codes [K][R][S][C] -> [K][R2][S2P*16 bytes].
+// Window tap (jr, js), phase (dh, dw), channel c holds w[k, r, s, c] with
+// r = 2*(jr - PL) + dh + pad, s = 2*(js - PL) + dw + pad (0 outside the filter),
+// so sum over the window of x_s2d * w_s2d == the stride-2 conv's sum.
+template <int BITS>
+__global__ void __launch_bounds__(256) s2d_weights_kernel(const int8_t *__restrict__ w, uint4 *__restrict__ y,
+                                                         int K, int R, int S, int C, int R2, int S2P, int PL,
+                                                         int pad) {
+    constexpr int CP = BITS == 8 ? 4 : 8;
+    const int64_t total = (int64_t)K * R2 * S2P;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        const int js = (int)(o % S2P);
+        const int64_t t = o / S2P;
+        const int jr = (int)(t % R2);
+        const int k = (int)(t / R2);
+        int q[4 * CP];
+#pragma unroll
+        for (int e = 0; e < 4 * CP; ++e) {
+            const int ph = e / CP, c = e % CP;
+            const int r = 2 * (jr - PL) + (ph >> 1) + pad, s = 2 * (js - PL) + (ph & 1) + pad;
+            q[e] = (c < C && r >= 0 && r < R && s >= 0 && s < S) ? (int)w[(((int64_t)k * R + r) * S + s) * C + c] : 0;
+        }
+        uint32_t out[4];
+        if constexpr (BITS == 8) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) out[kk] = pack4_s8(q[4 * kk], q[4 * kk + 1], q[4 * kk + 2], q[4 * kk + 3]);
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                int u[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) u[i] = q[8 * kk + i];
+                out[kk] = pack8_s4(u);
+            }
+        }
+        y[o] = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+}
+
 }  // namespace convq

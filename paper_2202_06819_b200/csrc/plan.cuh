@@ -25,6 +25,19 @@ extern int g_num_sms;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// FastDiv constants: s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1; then
+// n / d == (umulhi(n, m) + n) >> s for 0 <= n < 2^31 (checked exhaustively at
+// the boundaries by tests/test_abi_cpu.py's emulation).
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d < 1 ? 1 : d;
+    uint32_t s = 0;
+    while ((1ull << s) < f.d) ++s;
+    f.s = s;
+    f.m = (uint32_t)((((1ull << 32) * ((1ull << s) - f.d)) / f.d) + 1);
+    return f;
+}
+
 struct Cand {
     int bn, kch, cg, nsub;  // N tile, channels per k-block, CTAs per tile, k-blocks per stage
     int direct;             // packed output by direct stores (1) or smem staging + TMA store (0)
@@ -51,6 +64,12 @@ struct conv_q_plan_s {
     int N, H, W, C, K, R, S, stride, pad, bits;
     int P, Q;
     int64_t M, Kg;
+    // space-to-depth stem (conv_q_plan_s2d): the fields above describe the
+    // stride-1 window convolution the kernel runs; o_* the caller's conv
+    int s2d = 0;
+    int pad_hi = 0;    // bottom padding of the H walk (= pad unless s2d)
+    int xs_W = 0;      // s2d: stored columns of the s2d tensor (zero borders included)
+    int o_H = 0, o_W = 0, o_C = 0, o_R = 0, o_S = 0, o_stride = 0, o_pad = 0;
     int row_bytes;     // C*bits/8
     int out_row;       // K*bits/8
     int relu = 0, out_mode = CONV_Q_OUT_PACKED;
@@ -60,6 +79,8 @@ struct conv_q_plan_s {
     float tuned_us = -1.f;
     int rotate = 0;    // CONV_Q_ROTATE=1: rotate each CTA's k-block start (A/B measurement)
     int probe = 0;     // CONV_Q_PROBE (measurement only; results are garbage when != 0)
+    int epi_wait = 0;  // CONV_Q_EPI_WAIT / _NS: how epilogue warps wait for accumulators (A/B)
+    unsigned epi_wait_ns = 0;
     unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
     CUtensorMap tm_a, tm_b, tm_y;
@@ -133,7 +154,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     }
     ConvParams prm;
     prm.N = p->N; prm.H = p->H; prm.W = p->W; prm.C = p->C; prm.K = p->K; prm.R = p->R; prm.S = p->S;
-    prm.stride = p->stride; prm.pad = p->pad; prm.P = p->P; prm.Q = p->Q; prm.M = (int)p->M;
+    prm.stride = p->stride; prm.pad = p->pad; prm.pad_w = p->s2d ? 0 : p->pad; prm.P = p->P; prm.Q = p->Q; prm.M = (int)p->M;
     prm.row_bytes = p->row_bytes;
     prm.num_cblk = p->C / KCH;
     prm.num_kb = p->R * p->S * prm.num_cblk;
@@ -156,10 +177,20 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
         if (!p->ws || p->ws_bytes < need || p->cnt_bytes < regions * sizeof(unsigned))
             return set_err(CONV_Q_EINVAL, "split-K workspace not allocated (select the config outside graph capture)");
     }
+    prm.fd_ntiles = make_fastdiv(prm.n_tiles);
+    prm.fd_PQ = make_fastdiv(p->P * p->Q);
+    prm.fd_Q = make_fastdiv(p->Q);
+    prm.fd_cblk = make_fastdiv(prm.num_cblk);
+    prm.fd_S = make_fastdiv(p->S);
+    prm.fd_tpi = make_fastdiv(prm.tiles_per_img);
+    prm.fd_splits = make_fastdiv(prm.splits);
+    prm.fd_Wp = make_fastdiv(prm.Wp);
     prm.relu = p->relu;
     prm.rotate = p->rotate;
     prm.a_gemm = p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0 && !(HALO & 1);
     prm.probe = p->probe;
+    prm.epi_wait = p->epi_wait;
+    prm.epi_wait_ns = p->epi_wait_ns;
     prm.trace = p->trace;
     prm.scale = scale;
     prm.y32 = static_cast<int32_t *>(y);

@@ -57,6 +57,32 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint (ns): the thread sleeps in the barrier
+// unit until the phase completes or the hint expires, instead of re-polling
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+    return ok != 0;
+}
+// Wait used by warps off the critical control path (the epilogue): mode 1 =
+// suspend-time hint, mode 2 = polling with __nanosleep back-off, else spin.
+__device__ __forceinline__ void mbar_wait_relaxed(uint64_t *bar, uint32_t parity, int mode, uint32_t ns) {
+    if (mode == 1) {
+        while (!mbar_try_wait_hint(bar, parity, ns)) {
+        }
+    } else if (mode == 2) {
+        while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+    } else {
+        while (!mbar_try_wait(bar, parity)) {
+        }
+    }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 #ifdef CONVQ_HANG_CHECK
     long long spins = 0;

@@ -1,0 +1,7 @@
+export PROBE_CFG=bm128_bn64_kc64x2_c1_w,bm128_bn64_kc64x1_c1_w,bm128_bn256_kc64x2_c1_w,bm128_bn128_kc128x1_c1_st,bm128_bn128_kc128x3_c1_st_h,bm256_bn128_kc128x3_c2_st_h,bm128_bn256_kc128x1_c1
+export PROBE_MODES=0,7
+for w in "0 0" "1 1000000" "1 2000" "2 100" "2 400"; do
+  set -- $w
+  echo "=== EPI_WAIT=$1 NS=$2"
+  CONV_Q_EPI_WAIT=$1 CONV_Q_EPI_WAIT_NS=$2 timeout 600 python scripts/probe.py stem l1.b0.c1 l1.b0.c3 l2.b0.c2 l3.b1.c2 l4.b0.c3
+done

@@ -11,14 +11,24 @@ sys.path.insert(0, %r)
 import torch, numpy as np
 import paper_2202_06819_b200 as cq, workloads as wl
 name, N, bits = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
-L = {l.name: l for l, _ in wl.resnet50_layers()}[name]
 g = wl.rng(9, 0)
-x, w, ss = wl.layer_inputs(g, L, N, bits)
-p = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
-xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
-y = torch.empty((N, L.P, L.Q, L.K * bits // 8), dtype=torch.uint8, device="cuda")
+if name == "stem":
+    p = cq.StemPlan(N, 224, 224, 3, 64, 7, 7, 3, bits, relu=True)
+    xd = torch.from_numpy(wl.random_bytes(g, p.x_dims)).cuda()
+    wd = torch.from_numpy(wl.random_bytes(g, p.w_dims)).cuda()
+    sd = torch.cat([torch.full((64,), 0.01), torch.zeros(64)]).cuda()
+    y = torch.empty((N, 112, 112, 64 * bits // 8), dtype=torch.uint8, device="cuda")
+else:
+    L = {l.name: l for l, _ in wl.resnet50_layers()}[name]
+    x, w, ss = wl.layer_inputs(g, L, N, bits)
+    p = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
+    xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
+    y = torch.empty((N, L.P, L.Q, L.K * bits // 8), dtype=torch.uint8, device="cuda")
 res = {}
+flt = os.environ.get("PROBE_CFG", "")
 for i, cname in enumerate(p.candidates()):
+    if flt and cname not in flt.split(","):
+        continue
     p.set_config(i)
     for _ in range(3): p.run(xd, wd, sd, y)
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
@@ -30,15 +40,20 @@ print(json.dumps(res))
 ''' % ROOT
 for name in sys.argv[1:]:
     out = {}
-    for mode in (0, 1, 2):
+    MODES = [int(m) for m in os.environ.get('PROBE_MODES', '0,1,2,3,4,7').split(',')]
+    for mode in MODES:
         env = dict(os.environ, CONV_Q_PROBE=str(mode))
         r = subprocess.run([sys.executable, "-c", CODE, name, "256", "8"], env=env, capture_output=True, text=True)
         out[mode] = r.stdout.strip() or r.stderr[-400:]
     print(name)
     import json
     d = {m: json.loads(v) if v.startswith("{") else v for m, v in out.items()}
-    if all(isinstance(v, dict) for v in d.values()):
+    if all(isinstance(v, dict) for v in d.values()) and len(d) < 6:
+        for c in d[MODES[0]]:
+            print(f"  {c:26s} " + "  ".join(f"probe{m} {d[m][c]:7.1f}" for m in MODES) + " us")
+    elif all(isinstance(v, dict) for v in d.values()):
         for c in d[0]:
-            print(f"  {c:24s} normal {d[0][c]:8.1f}us  loads-only {d[1][c]:8.1f}us  mma-only {d[2][c]:8.1f}us")
+            print(f"  {c:26s} normal {d[0][c]:7.1f}  noMMA {d[1][c]:7.1f}  noLoad {d[2][c]:7.1f}  "
+                  f"ctrl+epi {d[3][c]:7.1f}  noEpi {d[4][c]:7.1f}  ctrl-only {d[7][c]:7.1f} us")
     else:
         print(d)

@@ -22,14 +22,22 @@ ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 table = {"resnet50": [l for l, _ in wl.resnet50_layers()], "resnet18": [l for l, _ in wl.resnet18_layers()],
          "table1": wl.paper_table1_layers()}[a.workload]
-L = {l.name: l for l in table}[a.layer]
 g = wl.rng(9, 0)
-x, w, ss = wl.layer_inputs(g, L, a.batch, a.bits)
-p = cq.ConvPlan(a.batch, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, a.bits, relu=True)
+if a.layer == "stem":   # ResNet conv1 through the s2d StemPlan
+    L = "stem conv1 7x7/2 224x224x3->64 (s2d)"
+    p = cq.StemPlan(a.batch, 224, 224, 3, 64, 7, 7, 3, a.bits, relu=True)
+    xd = torch.from_numpy(wl.random_bytes(g, p.x_dims)).cuda()
+    wd = torch.from_numpy(wl.random_bytes(g, p.w_dims)).cuda()
+    sd = torch.cat([torch.full((64,), 0.01), torch.zeros(64)]).cuda()
+    y = torch.empty((a.batch, 112, 112, 64 * a.bits // 8), dtype=torch.uint8, device="cuda")
+else:
+    L = {l.name: l for l in table}[a.layer]
+    x, w, ss = wl.layer_inputs(g, L, a.batch, a.bits)
+    p = cq.ConvPlan(a.batch, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, a.bits, relu=True)
+    xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
+    y = torch.empty((a.batch, L.P, L.Q, L.K * a.bits // 8), dtype=torch.uint8, device="cuda")
 if a.config:
     p.set_config(p.candidates().index(a.config))
-xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
-y = torch.empty((a.batch, L.P, L.Q, L.K * a.bits // 8), dtype=torch.uint8, device="cuda")
 for _ in range(a.reps):
     p.run(xd, wd, sd, y)
 torch.cuda.synchronize()

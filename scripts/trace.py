@@ -8,13 +8,20 @@ lib.conv_q_plan_set_trace.restype = ctypes.c_int
 lib.conv_q_plan_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 name = sys.argv[1]
 net = os.environ.get("TRACE_NET", "resnet50")
-L = {l.name: l for l, _ in getattr(wl, net + "_layers")()}[name]
 N, bits = int(os.environ.get("TRACE_N", 256)), int(os.environ.get("TRACE_BITS", 8))
 g = wl.rng(9, 0)
-x, w, ss = wl.layer_inputs(g, L, N, bits)
-p = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
-xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
-y = torch.empty((N, L.P, L.Q, L.K * bits // 8), dtype=torch.uint8, device="cuda")
+if name == "stem":   # ResNet conv1 through the s2d StemPlan
+    p = cq.StemPlan(N, 224, 224, 3, 64, 7, 7, 3, bits, relu=True)
+    xd = torch.from_numpy(wl.random_bytes(g, p.x_dims)).cuda()
+    wd = torch.from_numpy(wl.random_bytes(g, p.w_dims)).cuda()
+    sd = torch.cat([torch.full((64,), 0.01), torch.zeros(64)]).cuda()
+    y = torch.empty((N, 112, 112, 64 * bits // 8), dtype=torch.uint8, device="cuda")
+else:
+    L = {l.name: l for l, _ in getattr(wl, net + "_layers")()}[name]
+    x, w, ss = wl.layer_inputs(g, L, N, bits)
+    p = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
+    xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
+    y = torch.empty((N, L.P, L.Q, L.K * bits // 8), dtype=torch.uint8, device="cuda")
 cfgs = sys.argv[2:] or p.candidates()
 names = ["prod_wait_empty", "mma_wait_full", "mma_wait_acc", "epi_wait_acc", "mma_issue", "total", "tiles"]
 enames = ["epi_slab", "epi_body", "epi_store"]

@@ -38,7 +38,7 @@ def test_library_exports_every_header_symbol(lib):
     out = os.popen(f"nm -D --defined-only {cq.LIB_PATH}").read()
     exported = set(re.findall(r" T (conv_q_\w+)", out))
     assert set(header_symbols()) <= exported
-    assert lib.conv_q_version() == 100
+    assert lib.conv_q_version() == 101
 
 
 @pytest.mark.parametrize("args,code", [
@@ -83,6 +83,35 @@ def test_plan_info_gemm_view(lib):
     assert p.candidates()[i.config_index] == i.config
 
 
+def test_stem_s2d_plan_geometry(lib):
+    """ResNet conv1 7x7/2 p3 over 224x224x3 as a stride-1 conv over the s2d view:
+    same P, Q and output bytes as the direct conv; 4 s2d tap rows x one 64-byte
+    window (4 s2d pixels x 16 B) per row -> Kg = 4*64 (vs 49*32 = 1568 with
+    C padded to 32); the s2d tensor holds Q+3 stored columns."""
+    p = cq.StemPlan(256, 224, 224, 3, 64, 7, 7, 3, 8)
+    i = p.info()
+    assert (i.H, i.W, i.C, i.R, i.S, i.stride, i.pad) == (224, 224, 3, 7, 7, 2, 3) and i.s2d == 1
+    assert (i.P, i.Q, i.M) == (112, 112, 256 * 112 * 112)
+    assert i.Kg == 4 * 64 and i.y_bytes == 256 * 112 * 112 * 64
+    assert i.x_dims == (256, 112, 115, 16) and i.w_dims == (64, 4, 1, 64)
+    assert i.x_bytes == 256 * 112 * 115 * 16
+    assert p.macs == 256 * 112 * 112 * 64 * 7 * 7 * 3                     # useful MACs
+    q = cq.StemPlan(16, 224, 224, 3, 64, 7, 7, 3, 4)                       # INT4: 8 nibbles per phase
+    assert q.info().w_dims == (64, 4, 1, 64) and q.info().Kg == 4 * 128
+    r = cq.StemPlan(1, 33, 29, 3, 32, 3, 3, 1, 8)                          # odd sizes, 3x3/2 p1
+    assert (r.info().P, r.info().Q) == (17, 15)
+    assert r.info().w_dims == (32, 2, 1, 32) and r.info().x_dims == (1, 17, 16, 16)
+    for args, code in (((1, 224, 224, 5, 64, 7, 7, 3, 8), cq.EUNSUPPORTED),   # C > 4 channels per phase (s8)
+                       ((1, 224, 224, 3, 40, 7, 7, 3, 8), cq.EUNSUPPORTED),   # K*bits % 128
+                       ((1, 224, 224, 3, 64, 19, 19, 9, 8), cq.EUNSUPPORTED),  # > 8 s2d taps in W
+                       ((0, 224, 224, 3, 64, 7, 7, 3, 8), cq.EINVAL)):
+        with pytest.raises(cq.ConvQError) as ei:
+            cq.StemPlan(*args)
+        assert ei.value.code == code, args
+    i0 = cq.ConvPlan(1, 8, 8, 64, 64, 3, 3, 1, 1, 8).info()
+    assert i0.s2d == 0 and i0.x_dims == (1, 8, 8, 64) and i0.w_dims == (64, 3, 3, 64)
+
+
 def test_candidates_and_selection(lib):
     p = cq.ConvPlan(32, 14, 14, 256, 256, 3, 3, 1, 1, 8)
     names = p.candidates()
@@ -123,3 +152,22 @@ def test_no_cpu_fallback(lib):
                           ctypes.c_void_p(addr)) == cq.EINVAL
     assert lib.conv_q_run(p._h, ctypes.c_void_p(addr + 4), ctypes.c_void_p(addr), ctypes.c_void_p(addr),
                           ctypes.c_void_p(addr)) == cq.EINVAL
+
+
+def test_fastdiv_constants_exact():
+    """The kernels' control loops divide by per-launch constants with
+    q = (umulhi(n, m) + n) >> s, s = ceil(log2 d), m = floor(2^32 (2^s - d)/d) + 1
+    (plan.cuh make_fastdiv).  Exact for every 0 <= n < 2^31 at the boundaries
+    that can fail (multiples of d and their neighbours, the top of the range)."""
+    import random
+    rnd = random.Random(6819)
+    ds = list(range(1, 2100)) + [rnd.randrange(1, 2 ** 31) for _ in range(2000)] + \
+        [2 ** k + e for k in range(31) for e in (-1, 0, 1) if 2 ** k + e >= 1]
+    for d in ds:
+        s = (d - 1).bit_length()
+        m = ((1 << 32) * ((1 << s) - d)) // d + 1
+        assert m < 1 << 32
+        top = (2 ** 31 - 1) // d * d
+        for n in {0, 1, d - 1, d, d + 1, 2 ** 31 - 1, top, top - 1, rnd.randrange(0, 2 ** 31)}:
+            if 0 <= n < 2 ** 31:
+                assert (((n * m) >> 32) + n) >> s == n // d, (d, n)

@@ -247,3 +247,74 @@ def test_split_k_parity(cq, bits, L, N):
             assert np.array_equal(got32, ref32), (names[ci], rep, first_diff(got32, ref32))
             gotq = run_conv(cq, L, N, bits, x, w, ss, True, False, ci, plan)
             assert np.array_equal(gotq, refq), (names[ci], rep, first_diff(gotq, refq))
+
+
+# ----------------------------------------------------------------- s2d stem
+@pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("N,H,W,C,K,R,S,pad", [
+    (2, 30, 38, 3, 64, 7, 7, 3),      # ResNet conv1 geometry, small image, several tiles + ragged tail
+    (1, 33, 29, 3, 64, 7, 7, 3),      # odd H/W: last s2d row/column half empty
+    (1, 21, 19, 3, 128, 3, 3, 1),     # 3x3/2 p1 stem (2 s2d taps)
+    (2, 16, 16, 1, 64, 5, 5, 2),      # C=1, 5x5/2 p2
+])
+def test_stem_s2d_parity(cq, bits, N, H, W, C, K, R, S, pad):
+    """StemPlan (s2d quantize + window weights + stride-1 conv) == the oracle's
+    direct stride-2 conv on the channel-padded quantized image, every config,
+    s32 accumulators and requantized bytes."""
+    g = np.random.default_rng(6819 + 7 * H + bits)
+    x = (g.standard_normal((N, H, W, C)) * 2).astype(np.float16)
+    inv = 127 / 4 if bits == 8 else 7 / 3
+    wv = wl.weight_values(g, K, R, S, C, bits)
+    Cp = oracle.padded_channels(C, bits)
+    w_pad = np.zeros((K, R, S, Cp), dtype=np.int8)
+    w_pad[..., :C] = wv
+    xq = oracle.quantize(x, inv, bits)
+    wq = oracle.pack(w_pad, bits)
+    ss = wl.scale_shift(g, K, R * S * C, 40.0 if bits == 8 else 3.0, wl.uniform_code_std(bits), bits)
+    ref32 = oracle.conv_s32(xq, wq, Cp, 2, pad, bits)
+    refq = oracle.requant(ref32, ss, True, bits)
+    plan = cq.StemPlan(N, H, W, C, K, R, S, pad, bits)
+    xs = plan.quantize(dev(x), inv)
+    wp = plan.pack_weights(dev(wv))
+    sd = dev(ss)
+    P, Q = plan.P, plan.Q
+    assert ref32.shape == (N, P, Q, K)
+    for ci, name in enumerate(plan.candidates()):
+        plan.set_config(ci)
+        plan.set_epilogue(True, cq.OUT_S32)
+        y32 = torch.full((N, P, Q, K), -7777777, dtype=torch.int32, device="cuda")
+        plan.run(xs, wp, sd, y32)
+        torch.cuda.synchronize()
+        got32 = y32.cpu().numpy()
+        assert np.array_equal(got32, ref32), (name, first_diff(got32, ref32))
+        plan.set_epilogue(True, cq.OUT_PACKED)
+        yq = torch.full((N, P, Q, K * bits // 8), 0xA5, dtype=torch.uint8, device="cuda")
+        plan.run(xs, wp, sd, yq)
+        torch.cuda.synchronize()
+        assert np.array_equal(yq.cpu().numpy(), refq), (name, first_diff(yq.cpu().numpy(), refq))
+
+
+@pytest.mark.parametrize("bits", [8, 4])
+def test_stem_s2d_fullsize_sampled(cq, bits):
+    """ResNet-50 conv1 at 224x224, batch 32 (the bench's launch configuration
+    shape per image): sampled output pixels vs the oracle, computed one by one."""
+    N, K = 32, 64
+    g = np.random.default_rng(99 + bits)
+    x = g.standard_normal((N, 224, 224, 3)).astype(np.float16)
+    inv = 127 / 4 if bits == 8 else 7 / 3
+    wv = wl.weight_values(g, K, 7, 7, 3, bits)
+    w_pad = np.zeros((K, 7, 7, 32), dtype=np.int8)
+    w_pad[..., :3] = wv
+    ss = wl.scale_shift(g, K, 147, 40.0 if bits == 8 else 3.0, wl.uniform_code_std(bits), bits)
+    plan = cq.StemPlan(N, 224, 224, 3, K, 7, 7, 3, bits, relu=True)
+    plan.tune(plan.quantize(dev(x), inv), plan.pack_weights(dev(wv)), dev(ss),
+              torch.empty((N, 112, 112, K * bits // 8), dtype=torch.uint8, device="cuda"), warmup=1, reps=2)
+    xs = plan.quantize(dev(x), inv)
+    y = torch.empty((N, 112, 112, K * bits // 8), dtype=torch.uint8, device="cuda")
+    plan.run(xs, plan.pack_weights(dev(wv)), dev(ss), y)
+    torch.cuda.synchronize()
+    M = N * 112 * 112
+    pix = np.unique(np.concatenate([g.integers(0, M, 3000), [0, 111, 112 * 112 - 1, M - 1, 112 * 111]]))
+    ref = oracle.conv_q(oracle.quantize(x, inv, bits), oracle.pack(w_pad, bits), 32, 2, 3, bits, ss, True, pix=pix)
+    got = y.cpu().numpy().reshape(M, -1)[pix]
+    assert np.array_equal(got, ref), first_diff(got, ref)
