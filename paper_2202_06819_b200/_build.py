@@ -15,12 +15,16 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build_obj")
-LIB = os.path.join(HERE, "libconvq.so")
+# CONVQ_INSTRUMENT=1: the measurement build (wait-cycle trace + probe modes,
+# scripts/trace.py / probe.py) -> libconvq_instr.so, loaded via CONV_Q_LIB
+INSTR = os.environ.get("CONVQ_INSTRUMENT") == "1"
+OBJ = os.path.join(HERE, "build_obj_instr" if INSTR else "build_obj")
+LIB = os.path.join(HERE, "libconvq_instr.so" if INSTR else "libconvq.so")
 SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2)] + ["kern_b8_o4.cu", "kern_b8_o6.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]
+NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"] + \
+    (["-DCONVQ_INSTRUMENT"] if INSTR else [])
 
 
 def _deps():

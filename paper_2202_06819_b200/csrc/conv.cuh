@@ -45,6 +45,11 @@
 namespace convq {
 
 constexpr int BM = 128;
+#ifdef CONVQ_INSTRUMENT
+constexpr bool kInstrument = true;
+#else
+constexpr bool kInstrument = false;
+#endif
 // per-CTA trace counters (cycles): where the control loops wait
 enum { TR_PROD_EMPTY = 0, TR_MMA_FULL, TR_MMA_ACC, TR_EPI_ACC, TR_MMA_ISSUE, TR_TOTAL, TR_TILES, TR_T0, TR_T1,
        TR_TPDL, TR_TFULL, TR_TACC, TR_EPI_SLAB, TR_EPI_BODY, TR_EPI_STORE, TR_SLOTS = 15 };
@@ -80,6 +85,7 @@ struct ConvParams {
     int a_gemm;          // 1x1 / stride 1 / pad 0: A is the input as a [M][C] matrix (tiled TMA, no im2col)
     int probe;           // measurement only (bits): 1 = no MMAs, 2 = no loads, 4 = no epilogue work
     int epi_wait;        // epilogue acc_full wait: 0 spin, 1 suspend-time hint, 2 nanosleep back-off
+    int epi_ld32;        // INT8 epilogue: 32-column TMEM loads (1) or pipelined 16-column loads (0)
     unsigned epi_wait_ns;
     unsigned long long *trace;  // measurement only: per-CTA wait-cycle counters (TRACE_SLOTS each), or null
     // duplicate-aware (halo) mode, stride 1 only:
@@ -342,6 +348,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     conv_igemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_y, const ConvParams p) {
     using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>;
+    // measurement hooks (wait-cycle trace, probe modes) exist only in the
+    // CONVQ_INSTRUMENT build (libconvq_instr.so); compiled out otherwise
+    unsigned long long *const trace = kInstrument ? p.trace : nullptr;
+    const int probe = kInstrument ? p.probe : 0;
     static_assert(Cfg::FITS, "tile does not fit shared memory");
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -373,8 +383,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const long long t_start = p.trace ? clock64() : 0;
-    if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * TR_SLOTS + TR_T0] = globaltimer_ns();
+    const long long t_start = trace ? clock64() : 0;
+    if (trace && threadIdx.x == 0) trace[blockIdx.x * TR_SLOTS + TR_T0] = globaltimer_ns();
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;     // position in the CTA pair
     const int tile0 = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
     const int tstep = CG == 2 ? (int)num_clusters_x() : (int)gridDim.x;
@@ -433,7 +443,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         constexpr int A_LD_SUB = BITS == 4 ? Cfg::A_PK_SUB : Cfg::A_SUB;
         constexpr int B_LD_SUB = BITS == 4 ? Cfg::B_PK_SUB : Cfg::B_SUB;
         pdl_wait();
-        if (p.trace && lane == 0) p.trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
+        if (trace && lane == 0) trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
         int stage = 0;
         uint32_t phase = 0;
         if constexpr (WS) {
@@ -459,9 +469,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 const int p0 = (rt - n * p.tiles_per_img) * p.rpt;
                 for (int cblk = 0; cblk < p.num_cblk; ++cblk) {
                     {
-                        const long long t0 = p.trace ? clock64() : 0;
+                        const long long t0 = trace ? clock64() : 0;
                         mbar_wait(&empty[stage], phase ^ 1);
-                        if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
+                        if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
                     }
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&full[stage], p.halo_tx);
@@ -489,14 +499,14 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     for (int tap = 0; tap < RS;) {
                         const int nsub = min(NSUB, RS - tap);
                         {
-                            const long long t0 = p.trace ? clock64() : 0;
+                            const long long t0 = trace ? clock64() : 0;
                             mbar_wait(&empty[stage], phase ^ 1);
                             if (tap == 0) mbar_wait(&hempty[hb], hph ^ 1);
-                            if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
+                            if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
                         }
                         if (elect_one()) {
                             const int tx = nsub * Cfg::SUB_TX + (tap == 0 ? p.halo_tx : 0);
-                            if (p.probe & 2) {
+                            if (probe & 2) {
                                 mbar_arrive(&full[stage]);
                             } else {
                                 {
@@ -526,54 +536,39 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             const int p0 = p.fd_Q.div(rem), q0 = rem - p0 * p.Q;
             const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad_w;
             const int brow = n_blk * BN + (int)rank * Cfg::BNL;  // this CTA's B rows
-            // k-blocks in rotated order: CTA c starts at k-block (7c mod n) and wraps,
-            // so the persistent CTAs do not all stream the same weight rows at once
-            // (integer accumulation: any order is bit-exact)
-            int r = 0, s = 0, cblk = 0, kcol = 0;
-            auto seek = [&](int kb) {
-                const int tap0 = p.fd_cblk.div(kb);
-                r = p.fd_S.div(tap0);
-                s = tap0 - r * p.S;
-                cblk = kb - tap0 * p.num_cblk;
-                kcol = tap0 * p.row_bytes;
-            };
             const int nk = kb_hi - kb_lo;
-            int cur = kb_lo + (p.rotate && !WS ? (int)(((unsigned)(blockIdx.x / CG) * 7u) % (unsigned)nk) : 0);
-            if (cur > 0) seek(cur);
-            for (int kb = kb_lo; kb < kb_hi; kb += NSUB) {
-                const int nsub = min(NSUB, kb_hi - kb);   // ragged last stage of a tile
+            // optional rotated k-block order (CTA c starts at k-block 7c mod nk; any
+            // order is bit-exact for integer accumulation)
+            const int rot = (p.rotate && !WS) ? (int)(((unsigned)(blockIdx.x / CG) * 7u) % (unsigned)nk) : 0;
+            for (int kb = 0; kb < nk; kb += NSUB) {
+                const int nsub = min(NSUB, nk - kb);   // ragged last stage of a tile
                 {
-                    const long long t0 = p.trace ? clock64() : 0;
+                    const long long t0 = trace ? clock64() : 0;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
+                    if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
                 }
-                const bool issuer = elect_one();
-                if (issuer) {
-                    if (p.probe & 2) {                       // measurement: no loads
-                        mbar_arrive(&full[stage]);
-                    } else {
-                        mbar_arrive_expect_tx(&full[stage], nsub * Cfg::SUB_TX);
-                    }
+                if (elect_one()) {
+                    if (probe & 2) mbar_arrive(&full[stage]);   // measurement: no loads
+                    else mbar_arrive_expect_tx(&full[stage], nsub * Cfg::SUB_TX);
                 }
-                for (int j = 0; j < nsub; ++j) {
-                    if (issuer && !(p.probe & 2)) {
-                        uint8_t *ad = a_dst + stage * A_LD + j * A_LD_SUB;
-                        uint8_t *bd = b_dst + stage * B_LD + j * B_LD_SUB;
-                        if (p.a_gemm)
-                            tma_load_2d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, m0, pol_a);
-                        else
-                            tma_load_im2col_4d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0, (uint16_t)s,
-                                               (uint16_t)r, pol_a);
-                        if (!WS) tma_load_2d(bd, &tm_b, &full[stage], kcol + cblk * Cfg::LOAD_ROW, brow, pol_b);
-                    }
-                    if (++cur == kb_hi) {                  // wrap to the unit's first k-block
-                        cur = kb_lo;
-                        seek(cur);
-                    } else if (++cblk == p.num_cblk) {     // next filter tap (r, s)
-                        cblk = 0;
-                        kcol += p.row_bytes;
-                        if (++s == p.S) { s = 0; ++r; }
-                    }
+                __syncwarp();
+                // lane j issues the loads of the stage's j-th k-block: the (tap,
+                // channel block) decomposition and the TMA issue run lane-parallel
+                // instead of NSUB times through one thread
+                if (lane < nsub && !(probe & 2)) {
+                    int k = kb + lane + rot;
+                    if (k >= nk) k -= nk;
+                    k += kb_lo;
+                    const int tap = p.fd_cblk.div(k), cblk = k - tap * p.num_cblk;
+                    const int r = p.fd_S.div(tap), s = tap - r * p.S;
+                    uint8_t *ad = a_dst + stage * A_LD + lane * A_LD_SUB;
+                    uint8_t *bd = b_dst + stage * B_LD + lane * B_LD_SUB;
+                    if (p.a_gemm)
+                        tma_load_2d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, m0, pol_a);
+                    else
+                        tma_load_im2col_4d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0, (uint16_t)s,
+                                           (uint16_t)r, pol_a);
+                    if (!WS) tma_load_2d(bd, &tm_b, &full[stage], tap * p.row_bytes + cblk * Cfg::LOAD_ROW, brow, pol_b);
                 }
                 __syncwarp();
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -605,11 +600,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 const int buf = local % Cfg::NBUF;
                 const uint32_t aphase = (local / Cfg::NBUF) & 1;
                 {
-                    const long long t0 = p.trace ? clock64() : 0;
+                    const long long t0 = trace ? clock64() : 0;
                     mbar_wait(&acc_empty[buf], aphase ^ 1);
-                    if (p.trace && lane == 0) {
-                        atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_ACC, clock64() - t0);
-                        atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_TILES, 1ull);
+                    if (trace && lane == 0) {
+                        atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ACC, clock64() - t0);
+                        atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_TILES, 1ull);
                     }
                 }
                 tc_fence_after();
@@ -619,16 +614,16 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     // reads it at row offset r*Wp + s, its weights from the resident
                     // k-block t*num_cblk + cblk
                     for (int cblk = 0; cblk < p.num_cblk; ++cblk) {
-                        long long t0 = p.trace ? clock64() : 0;
+                        long long t0 = trace ? clock64() : 0;
                         mbar_wait(&full[stage], phase);
                         if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's halo box
-                        if (p.trace && lane == 0) {
+                        if (trace && lane == 0) {
                             const long long t1 = clock64();
-                            atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
+                            atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
                             t0 = t1;
                         }
                         tc_fence_after();
-                        if (p.probe & 1) {
+                        if (probe & 1) {
                             if (elect_one()) {
                                 mbar_arrive(&empty[stage]);
                                 if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
@@ -649,7 +644,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             else mma_commit(&empty[stage]);
                         }
                         __syncwarp();
-                        if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
+                        if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 } else if constexpr (HA) {
@@ -663,17 +658,17 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         const uint64_t ad_h = a_desc_h + (uint64_t)((hb * Cfg::HALO_BYTES) >> 4);
 #pragma unroll
                         for (int g = 0; g < Cfg::HST; ++g) {
-                            long long t0 = p.trace ? clock64() : 0;
+                            long long t0 = trace ? clock64() : 0;
                             mbar_wait(&full[stage], phase);
                             if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's half of the stage
-                            if (p.trace && lane == 0) {
+                            if (trace && lane == 0) {
                                 const long long t1 = clock64();
-                                atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
+                                atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
                                 t0 = t1;
                             }
                             tc_fence_after();
                             if (elect_one()) {
-                                if (p.probe & 1) {
+                                if (probe & 1) {
                                     mbar_arrive(&empty[stage]);
                                     if (g == Cfg::HST - 1) mbar_arrive(&hempty[hb]);
                                     if constexpr (CG == 2) {
@@ -705,25 +700,25 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 }
                             }
                             __syncwarp();
-                            if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
+                            if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                             if (++stage == STAGES) { stage = 0; phase ^= 1; }
                         }
                     }
                 } else
                 for (int kb = kb_lo; kb < kb_hi; kb += NSUB) {
                     const int nsub = min(NSUB, kb_hi - kb);
-                    long long t0 = p.trace ? clock64() : 0;
+                    long long t0 = trace ? clock64() : 0;
                     mbar_wait(BITS == 4 ? &ready[stage] : &full[stage], phase);
                     if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's half of the stage
-                    if (p.trace && lane == 0) {
+                    if (trace && lane == 0) {
                         const long long t1 = clock64();
-                        atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
-                        if (local == 0 && kb == kb_lo) p.trace[blockIdx.x * TR_SLOTS + TR_TFULL] = globaltimer_ns();
+                        atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
+                        if (local == 0 && kb == kb_lo) trace[blockIdx.x * TR_SLOTS + TR_TFULL] = globaltimer_ns();
                         t0 = t1;
                     }
                     tc_fence_after();
                     if (elect_one()) {
-                        if (p.probe & 1) {                // measurement: no MMAs
+                        if (probe & 1) {                // measurement: no MMAs
                             if constexpr (CG == 2) {
                                 mbar_arrive(&empty[stage]);
                                 mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
@@ -753,7 +748,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         }
                     }
                     __syncwarp();
-                    if (p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
+                    if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 // accumulator ready for the epilogue (of both CTAs)
@@ -830,7 +825,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             }
             __syncwarp();
         };
-        if (ss_issuer && !(p.probe & 4)) ss_issue(tile0 + b * tstep, 0);
+        if (ss_issuer && !(probe & 4)) ss_issue(tile0 + b * tstep, 0);
         int j = 0;
         for (int unit = tile0 + b * tstep; unit < p.num_units; unit += Cfg::NBUF * tstep, ++j) {
             const int tile = p.splits == 1 ? unit : p.fd_splits.div(unit);
@@ -847,20 +842,16 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 const bool ok = rt < p.m_tiles && pl < p.rpt && pp < p.P && qq < p.Q;
                 m = ok ? (n * p.P + pp) * p.Q + qq : p.M;
             }
-            if (Cfg::OUTP == OUT_TMA) {   // this warp's slab must have been read out by its previous store
-                if (lane == 0) tma_store_wait_read0();
-                __syncwarp();
-            }
             {
-                const long long t0 = p.trace ? clock64() : 0;
+                const long long t0 = trace ? clock64() : 0;
                 mbar_wait_relaxed(&acc_full[b], j & 1, p.epi_wait, p.epi_wait_ns);
-                if (p.trace && lane == 0 && warp == Cfg::EPI_WARP0) {
-                    atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_EPI_ACC, clock64() - t0);
-                    if (j == 0) p.trace[blockIdx.x * TR_SLOTS + TR_TACC] = globaltimer_ns();
+                if (trace && lane == 0 && warp == Cfg::EPI_WARP0) {
+                    atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_EPI_ACC, clock64() - t0);
+                    if (j == 0) trace[blockIdx.x * TR_SLOTS + TR_TACC] = globaltimer_ns();
                 }
             }
             tc_fence_after();
-            if (p.probe & 4) {   // measurement: release the accumulator untouched
+            if (probe & 4) {   // measurement: release the accumulator untouched
                 __syncwarp();
                 if (lane == 0) {
                     if constexpr (CG == 2) mbar_arrive_cluster(acc_empty_leader);
@@ -954,6 +945,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         }
                         const int sbyte = c * 16;                 // byte within this warp's slab row
                         if constexpr (Cfg::OUTP == OUT_TMA) {
+                            if (c == 0) {   // the slab must have been read out by this warp's previous store
+                                if (lane == 0) tma_store_wait_read0();   // (waited as late as possible)
+                                __syncwarp();
+                            }
                             uint8_t *sub = slab + (sbyte / Cfg::EPI_SUBW) * (32 * Cfg::EPI_SUBW);
                             *reinterpret_cast<uint4 *>(sub + swz<Cfg::EPI_SUBW>(lane * Cfg::EPI_SUBW + sbyte % Cfg::EPI_SUBW)) = pk;
                         } else {
@@ -1003,6 +998,22 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             } else {
                 // the MMA warp's copy of this tile's scale/shift (long done by now)
                 if (Cfg::OUTP != OUT_S32) mbar_wait(&ss_full[3 * b + j % 3], (j / 3) & 1);
+                if constexpr (BITS == 8 && NCH % 2 == 0) {
+                  if (p.epi_ld32) {
+                    // 32 columns per tcgen05.ld (two 16-byte output pieces): half
+                    // the exposed TMEM-load round trips of the 16-column loop
+                    uint32_t v32[32];
+#pragma unroll
+                    for (int c = 0; c < NCH; c += 2) {
+                        tmem_ld_issue<32>(taddr + c * Cfg::CW, v32);
+                        tmem_ld_wait_regs(v32);
+                        if (c + 2 >= NCH) release_acc();
+                        process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c, std::true_type{});
+                        process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[16]), c + 1, std::true_type{});
+                    }
+                    goto epi_stored;
+                  }
+                }
                 tmem_ld_issue<Cfg::CW>(taddr, va);
                 tmem_ld_wait_regs(va);
 #pragma unroll
@@ -1021,6 +1032,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     }
                 }
             }
+        epi_stored:
             if (Cfg::OUTP == OUT_TMA && emit) {
                 fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
                 __syncwarp();
@@ -1066,9 +1078,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     tc_fence_before();
     if constexpr (CG == 2) cluster_sync();   // the pair's MMAs and remote arrivals are complete
     else __syncthreads();
-    if (p.trace && threadIdx.x == 0) {
-        atomicAdd(p.trace + blockIdx.x * TR_SLOTS + TR_TOTAL, clock64() - t_start);
-        p.trace[blockIdx.x * TR_SLOTS + TR_T1] = globaltimer_ns();
+    if (trace && threadIdx.x == 0) {
+        atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_TOTAL, clock64() - t_start);
+        trace[blockIdx.x * TR_SLOTS + TR_T1] = globaltimer_ns();
     }
     if (warp == Cfg::MMA_WARP) {
         tc_fence_after();

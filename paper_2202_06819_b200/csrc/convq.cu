@@ -366,6 +366,7 @@ static conv_q_plan_t *finish_plan(conv_q_plan_s *p) {
     if (const char *pr = getenv("CONV_Q_PROBE")) p->probe = atoi(pr);
     if (const char *ew = getenv("CONV_Q_EPI_WAIT")) p->epi_wait = atoi(ew);
     if (const char *en = getenv("CONV_Q_EPI_WAIT_NS")) p->epi_wait_ns = (unsigned)atoi(en);
+    if (const char *el = getenv("CONV_Q_EPI_LD32")) p->epi_ld32 = atoi(el);
     if (const char *ro = getenv("CONV_Q_ROTATE")) p->rotate = atoi(ro) ? 1 : 0;
     apply_cache(p);
     if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK && ensure_ws(p) != CONV_Q_OK) {
@@ -961,6 +962,9 @@ extern "C" CONVQ_API int conv_q_mma_pipe_probe2(int groups, int G, int S, int n,
 // caller passes a device buffer of >= 8 * grid u64 (zeroed), or NULL to stop.
 extern "C" CONVQ_API int conv_q_plan_set_trace(conv_q_plan_t *p, void *counters) {
     if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+#ifndef CONVQ_INSTRUMENT
+    if (counters) return set_err(CONV_Q_EUNSUPPORTED, "tracing needs the CONVQ_INSTRUMENT build (libconvq_instr.so)");
+#endif
     p->trace = static_cast<unsigned long long *>(counters);
     return CONV_Q_OK;
 }

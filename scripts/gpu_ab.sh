@@ -1,7 +1,5 @@
-# A/B the in-tree build against scratch/libconvq_old.so on the same box
-for i in 1 2; do
-  for lib in ${AB_LIBS:-scratch/libconvq_old.so paper_2202_06819_b200/libconvq.so}; do
-    CONV_Q_LIB=$PWD/$lib timeout 600 python bench.py --no-cpu-baseline --no-e2e --no-stem --no-k7 ${AB_ARGS} > gpurun_out/ab.json 2> gpurun_out/ab_$i_$(basename $lib).err
-    echo "$lib $(python -c 'import json;d=json.load(open("gpurun_out/ab.json"));print(d["value"], d["ms_per_step"])')"
-  done
-done
+# A/B of epilogue TMEM load width (probe.py normal mode only), then parity
+export PROBE_CFG=bm128_bn64_kc64x2_c1_w,bm128_bn64_kc64x1_c1_w,bm128_bn128_kc64x1_c1_w,bm128_bn256_kc64x2_c1_w,bm128_bn128_kc128x1_c1_st,bm128_bn256_kc128x1_c1,bm256_bn256_kc128x2_c2_st,bm128_bn256_kc128x2_c1_w,bm128_bn128_kc128x1_c1_w,bm256_bn128_kc128x3_c2_st_h
+export PROBE_MODES=0
+for v in 0 1; do echo "== EPI_LD32=$v"; CONV_Q_EPI_LD32=$v timeout 600 python scripts/probe.py stem l1.b0.c1 l1.b0.c3 l2.b0.c3 l3.b1.c3 l3.b1.c2 l4.b0.c3 l2.b1.c2; done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3

@@ -5,6 +5,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# probe modes exist only in the measurement build (CONVQ_INSTRUMENT=1 python paper_2202_06819_b200/_build.py)
+os.environ.setdefault("CONV_Q_LIB", os.path.join(ROOT, "paper_2202_06819_b200", "libconvq_instr.so"))
 CODE = r'''
 import os, sys, json
 sys.path.insert(0, %r)

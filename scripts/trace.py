@@ -1,5 +1,7 @@
 """Per-CTA wait attribution for a layer/config: python scripts/trace.py l3.b1.c2 [config...]"""
 import ctypes, os, sys
+# measurement build (CONVQ_INSTRUMENT=1 python paper_2202_06819_b200/_build.py)
+os.environ.setdefault("CONV_Q_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2202_06819_b200", "libconvq_instr.so"))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2202_06819_b200 as cq, workloads as wl
