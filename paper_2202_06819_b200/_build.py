@@ -18,13 +18,15 @@ CSRC = os.path.join(HERE, "csrc")
 # CONVQ_INSTRUMENT=1: the measurement build (wait-cycle trace + probe modes,
 # scripts/trace.py / probe.py) -> libconvq_instr.so, loaded via CONV_Q_LIB
 INSTR = os.environ.get("CONVQ_INSTRUMENT") == "1"
-OBJ = os.path.join(HERE, "build_obj_instr" if INSTR else "build_obj")
-LIB = os.path.join(HERE, "libconvq_instr.so" if INSTR else "libconvq.so")
+_SFX = ("_instr" if INSTR else "") + (f"_wg{os.environ['CONVQ_EPI_WG8']}" if os.environ.get("CONVQ_EPI_WG8") else "")
+OBJ = os.path.join(HERE, "build_obj" + _SFX)
+LIB = os.path.join(HERE, f"libconvq{_SFX}.so")
 SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2)] + ["kern_b8_o4.cu", "kern_b8_o6.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"] + \
-    (["-DCONVQ_INSTRUMENT"] if INSTR else [])
+    (["-DCONVQ_INSTRUMENT"] if INSTR else []) + \
+    ([f"-DCONVQ_EPI_WG8={os.environ['CONVQ_EPI_WG8']}"] if os.environ.get("CONVQ_EPI_WG8") else [])
 
 
 def _deps():

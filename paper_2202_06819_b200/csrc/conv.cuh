@@ -85,7 +85,6 @@ struct ConvParams {
     int a_gemm;          // 1x1 / stride 1 / pad 0: A is the input as a [M][C] matrix (tiled TMA, no im2col)
     int probe;           // measurement only (bits): 1 = no MMAs, 2 = no loads, 4 = no epilogue work
     int epi_wait;        // epilogue acc_full wait: 0 spin, 1 suspend-time hint, 2 nanosleep back-off
-    int epi_ld32;        // INT8 epilogue: 32-column TMEM loads (1) or pipelined 16-column loads (0)
     unsigned epi_wait_ns;
     unsigned long long *trace;  // measurement only: per-CTA wait-cycle counters (TRACE_SLOTS each), or null
     // duplicate-aware (halo) mode, stride 1 only:
@@ -115,6 +114,18 @@ constexpr int OUT_S32 = 1;     // raw int32 accumulators, direct global stores (
 constexpr int OUT_DIRECT = 2;
 constexpr int OUT_RELU = 4;    // flag: INT8 ReLU-specialised epilogue (OUT_TMA | OUT_RELU, OUT_DIRECT | OUT_RELU)  // packed codes, 16-byte direct global stores (no staging smem ->
                                // deeper operand pipeline; L2 merges the row pieces)
+
+// Epilogue warpgroups (INT8: CONVQ_EPI_WG8, default 4; INT4: 2) and TMEM
+// accumulator buffers (512 columns / BN, at most 4, at most one per warpgroup);
+// shared with the host's TMA-store box computation (convq.cu).
+#ifndef CONVQ_EPI_WG8
+#define CONVQ_EPI_WG8 4
+#endif
+constexpr int epi_warpgroups(int bits) { return bits == 8 ? CONVQ_EPI_WG8 : 2; }
+constexpr int tmem_buffers(int bits, int bn) {
+    return (512 / bn) < epi_warpgroups(bits) ? ((512 / bn) < 4 ? 512 / bn : 4)
+                                              : (epi_warpgroups(bits) < 4 ? epi_warpgroups(bits) : 4);
+}
 
 template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO = 0>
 struct ConvCfg {
@@ -149,10 +160,10 @@ struct ConvCfg {
     static constexpr int OUTP = OUT & 3;                     // output path
     static constexpr bool RELU8 = BITS == 8 && (OUT & OUT_RELU) != 0;
     static constexpr int OUT_BYTES = OUTP == OUT_TMA ? BM * OUT_ROW : 0;   // staging per TMEM buffer
-    static constexpr int NUM_EPI = BITS == 8 ? 4 : 2;               // epilogue warpgroups
+    static constexpr int NUM_EPI = epi_warpgroups(BITS);            // epilogue warpgroups
     // TMEM accumulator buffers: as many as the 512 columns allow (max 4), so
     // up to NBUF tiles are in the epilogue while the MMA fills the next one
-    static constexpr int NBUF = (512 / BN) < NUM_EPI ? (512 / BN) : NUM_EPI;
+    static constexpr int NBUF = tmem_buffers(BITS, BN);
     static constexpr int EPI_PER_BUF = NUM_EPI / NBUF;              // warpgroups per TMEM buffer
     static constexpr int EPI_COLS = BN / EPI_PER_BUF;               // columns one warp drains (of its 32 rows)
     static constexpr int EPI_ROW = EPI_COLS * BITS / 8;             // packed bytes of one row of a warp's slab
@@ -901,24 +912,25 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     } else {
                         // (smem slot: columns past K hold stale values; their codes are never stored)
                         const bool full = SMEM_SS || col0 + Cfg::CW <= p.K;
-                        float sc[Cfg::CW], sh[Cfg::CW];
-                        if (full) {
-                            const float4 *s4 = reinterpret_cast<const float4 *>(SMEM_SS ? ss_b + ccol : p.scale + col0);
-                            const float4 *h4 = reinterpret_cast<const float4 *>(SMEM_SS ? ss_b + BN + ccol : p.scale + p.K + col0);
+                        const float4 *s4 = reinterpret_cast<const float4 *>(SMEM_SS ? ss_b + ccol : p.scale + col0);
+                        const float4 *h4 = reinterpret_cast<const float4 *>(SMEM_SS ? ss_b + BN + ccol : p.scale + p.K + col0);
+                        // scale / shift of columns 4q..4q+3 of this chunk
+                        auto ss4 = [&](int q, float4 &sa, float4 &sb) {
+                            if (full) {
+                                sa = SMEM_SS ? s4[q] : __ldg(s4 + q);
+                                sb = SMEM_SS ? h4[q] : __ldg(h4 + q);
+                            } else {
+                                float t[8];
 #pragma unroll
-                            for (int q = 0; q < Cfg::CW / 4; ++q) {
-                                const float4 sa = SMEM_SS ? s4[q] : __ldg(s4 + q), sb = SMEM_SS ? h4[q] : __ldg(h4 + q);
-                                sc[4 * q] = sa.x; sc[4 * q + 1] = sa.y; sc[4 * q + 2] = sa.z; sc[4 * q + 3] = sa.w;
-                                sh[4 * q] = sb.x; sh[4 * q + 1] = sb.y; sh[4 * q + 2] = sb.z; sh[4 * q + 3] = sb.w;
+                                for (int e = 0; e < 4; ++e) {
+                                    const bool ok = col0 + 4 * q + e < p.K;  // columns past K are never stored
+                                    t[e] = ok ? __ldg(p.scale + col0 + 4 * q + e) : 0.f;
+                                    t[4 + e] = ok ? __ldg(p.scale + p.K + col0 + 4 * q + e) : 0.f;
+                                }
+                                sa = make_float4(t[0], t[1], t[2], t[3]);
+                                sb = make_float4(t[4], t[5], t[6], t[7]);
                             }
-                        } else {
-#pragma unroll
-                            for (int q = 0; q < Cfg::CW; ++q) {
-                                const bool ok = col0 + q < p.K;  // columns past K are never stored
-                                sc[q] = ok ? __ldg(p.scale + col0 + q) : 0.f;
-                                sh[q] = ok ? __ldg(p.scale + p.K + col0 + q) : 0.f;
-                            }
-                        }
+                        };
                         uint4 pk;   // 16 packed bytes = this chunk (16 s8 or 32 s4 columns)
                         if constexpr (BITS == 8) {
                             // u = fma((float)acc, scale, shift); the F2IP pair conversion
@@ -926,20 +938,31 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             // then clears the negative bytes of each packed word.  (Equal
                             // to clamp(rne(u), lo, hi) for every finite u; u is never NaN
                             // for finite scale/shift, the documented precondition.)
-                            float u[Cfg::CW];
-#pragma unroll
-                            for (int q = 0; q < Cfg::CW; ++q) u[q] = __fmaf_rn(__int2float_rn((int)v[q]), sc[q], sh[q]);
+                            // Four columns at a time: 8 scale/shift registers live, not 32.
                             uint32_t w4[4];
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                w4[q] = pack4_f32_s8(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]);
+                                float4 sa, sb;
+                                ss4(q, sa, sb);
+                                const float u0 = __fmaf_rn(__int2float_rn((int)v[4 * q]), sa.x, sb.x);
+                                const float u1 = __fmaf_rn(__int2float_rn((int)v[4 * q + 1]), sa.y, sb.y);
+                                const float u2 = __fmaf_rn(__int2float_rn((int)v[4 * q + 2]), sa.z, sb.z);
+                                const float u3 = __fmaf_rn(__int2float_rn((int)v[4 * q + 3]), sa.w, sb.w);
+                                w4[q] = pack4_f32_s8(u0, u1, u2, u3);
                                 if (relu8 || p.relu) w4[q] = relu_s8x4(w4[q]);
                             }
                             pk = make_uint4(w4[0], w4[1], w4[2], w4[3]);
                         } else {
                             int r[Cfg::CW];
 #pragma unroll
-                            for (int q = 0; q < Cfg::CW; ++q) r[q] = requant_int((int)v[q] >> 8, sc[q], sh[q], lo);
+                            for (int q = 0; q < Cfg::CW / 4; ++q) {
+                                float4 sa, sb;
+                                ss4(q, sa, sb);
+                                r[4 * q] = requant_int((int)v[4 * q] >> 8, sa.x, sb.x, lo);
+                                r[4 * q + 1] = requant_int((int)v[4 * q + 1] >> 8, sa.y, sb.y, lo);
+                                r[4 * q + 2] = requant_int((int)v[4 * q + 2] >> 8, sa.z, sb.z, lo);
+                                r[4 * q + 3] = requant_int((int)v[4 * q + 3] >> 8, sa.w, sb.w, lo);
+                            }
                             pk = make_uint4(pack8_sat_s4(r), pack8_sat_s4(r + 8), pack8_sat_s4(r + 16),
                                             pack8_sat_s4(r + 24));
                         }
@@ -999,9 +1022,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 // the MMA warp's copy of this tile's scale/shift (long done by now)
                 if (Cfg::OUTP != OUT_S32) mbar_wait(&ss_full[3 * b + j % 3], (j / 3) & 1);
                 if constexpr (BITS == 8 && NCH % 2 == 0) {
-                  if (p.epi_ld32) {
                     // 32 columns per tcgen05.ld (two 16-byte output pieces): half
-                    // the exposed TMEM-load round trips of the 16-column loop
+                    // the exposed TMEM-load round trips of a 16-column loop
                     uint32_t v32[32];
 #pragma unroll
                     for (int c = 0; c < NCH; c += 2) {
@@ -1011,28 +1033,26 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c, std::true_type{});
                         process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[16]), c + 1, std::true_type{});
                     }
-                    goto epi_stored;
-                  }
-                }
-                tmem_ld_issue<Cfg::CW>(taddr, va);
-                tmem_ld_wait_regs(va);
+                } else {
+                    tmem_ld_issue<Cfg::CW>(taddr, va);
+                    tmem_ld_wait_regs(va);
 #pragma unroll
-                for (int c = 0; c < NCH; c += 2) {
-                    const bool more1 = c + 1 < NCH;
-                    if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
-                    else release_acc();   // every column of this warp is in registers
-                    process(va, c, std::true_type{});
-                    if (more1) {
-                        tmem_ld_wait_regs(vb);
-                        const bool more2 = c + 2 < NCH;
-                        if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
-                        else release_acc();
-                        process(vb, c + 1, std::true_type{});
-                        if (more2) tmem_ld_wait_regs(va);
+                    for (int c = 0; c < NCH; c += 2) {
+                        const bool more1 = c + 1 < NCH;
+                        if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
+                        else release_acc();   // every column of this warp is in registers
+                        process(va, c, std::true_type{});
+                        if (more1) {
+                            tmem_ld_wait_regs(vb);
+                            const bool more2 = c + 2 < NCH;
+                            if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
+                            else release_acc();
+                            process(vb, c + 1, std::true_type{});
+                            if (more2) tmem_ld_wait_regs(va);
+                        }
                     }
                 }
             }
-        epi_stored:
             if (Cfg::OUTP == OUT_TMA && emit) {
                 fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
                 __syncwarp();

@@ -366,7 +366,6 @@ static conv_q_plan_t *finish_plan(conv_q_plan_s *p) {
     if (const char *pr = getenv("CONV_Q_PROBE")) p->probe = atoi(pr);
     if (const char *ew = getenv("CONV_Q_EPI_WAIT")) p->epi_wait = atoi(ew);
     if (const char *en = getenv("CONV_Q_EPI_WAIT_NS")) p->epi_wait_ns = (unsigned)atoi(en);
-    if (const char *el = getenv("CONV_Q_EPI_LD32")) p->epi_ld32 = atoi(el);
     if (const char *ro = getenv("CONV_Q_ROTATE")) p->rotate = atoi(ro) ? 1 : 0;
     apply_cache(p);
     if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK && ensure_ws(p) != CONV_Q_OK) {
@@ -589,8 +588,8 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
     // layer's x; PAPER.md:261 layout consistency).  Unused in S32 mode.
     if (p->out_mode == CONV_Q_OUT_PACKED && !c.direct) {
         // one box = one epilogue warp's 32-row slab (or a 128-byte column block of it)
-        const int num_epi = p->bits == 8 ? 4 : 2;
-        const int nbuf = std::min(512 / c.bn, num_epi);
+        const int num_epi = epi_warpgroups(p->bits);
+        const int nbuf = tmem_buffers(p->bits, c.bn);
         const int epb = num_epi / nbuf;
         const int epi_row = c.bn / epb * p->bits / 8;
         const int subw = epi_row < 128 ? epi_row : 128;

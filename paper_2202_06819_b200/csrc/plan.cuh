@@ -81,7 +81,6 @@ struct conv_q_plan_s {
     int probe = 0;     // CONV_Q_PROBE (measurement only; results are garbage when != 0)
     int epi_wait = 0;  // CONV_Q_EPI_WAIT / _NS: how epilogue warps wait for accumulators (A/B)
     unsigned epi_wait_ns = 0;
-    int epi_ld32 = 1;  // CONV_Q_EPI_LD32=0: 16-column pipelined TMEM loads (A/B)
     unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
     CUtensorMap tm_a, tm_b, tm_y;
@@ -191,7 +190,6 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.a_gemm = p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0 && !(HALO & 1);
     prm.probe = p->probe;
     prm.epi_wait = p->epi_wait;
-    prm.epi_ld32 = p->epi_ld32;
     prm.epi_wait_ns = p->epi_wait_ns;
     prm.trace = p->trace;
     prm.scale = scale;
