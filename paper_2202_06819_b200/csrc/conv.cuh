@@ -453,24 +453,26 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         constexpr int B_LD = BITS == 4 ? Cfg::B_PK : Cfg::B_S8;
         constexpr int A_LD_SUB = BITS == 4 ? Cfg::A_PK_SUB : Cfg::A_SUB;
         constexpr int B_LD_SUB = BITS == 4 ? Cfg::B_PK_SUB : Cfg::B_SUB;
-        pdl_wait();
-        if (trace && lane == 0) trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
         int stage = 0;
         uint32_t phase = 0;
         if constexpr (WS) {
             // weight-stationary: this CTA's BN x (R*S*C) weight block, once, as
-            // num_kb k-block tiles [BN rows][KCH] (tap-major k order)
+            // num_kb k-block tiles [BN rows][KCH] (tap-major k order).  Weights
+            // are constant across layers' launches, so this load is issued
+            // BEFORE the PDL wait and overlaps the previous kernel's tail.
             if (tile0 < p.num_tiles && elect_one()) {
-                const int brow = (tile0 % p.n_tiles) * BN + (int)rank * Cfg::BNL;
+                const int brow = (tile0 - p.fd_ntiles.div(tile0) * p.n_tiles) * BN + (int)rank * Cfg::BNL;
                 mbar_arrive_expect_tx(bfull, (uint32_t)(p.num_kb * Cfg::BNL * Cfg::LOAD_ROW));
                 for (int kb = 0; kb < p.num_kb; ++kb) {
-                    const int tap = kb / p.num_cblk, cb = kb - tap * p.num_cblk;
+                    const int tap = p.fd_cblk.div(kb), cb = kb - tap * p.num_cblk;
                     tma_load_2d(b_res + kb * Cfg::B_TILE, &tm_b, bfull, tap * p.row_bytes + cb * Cfg::LOAD_ROW, brow,
                                 pol_b);
                 }
             }
             __syncwarp();
         }
+        pdl_wait();   // activations (the previous layer's output) only after this
+        if (trace && lane == 0) trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
         if constexpr (WS && HA) {
             // one stage = one halo box per (tile, channel block); no weights
             for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
@@ -818,7 +820,6 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(&acc_empty[b]), 0) : 0;
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
         constexpr bool relu8 = Cfg::RELU8;   // ReLU specialisation (p.relu == 1 guaranteed by the dispatch)
-        pdl_wait();
         // scale/shift of the j-th tile of this buffer -> slot j % 3, issued by the
         // buffer's first warp one tile ahead (see SS_BYTES)
         const bool ss_smem = Cfg::OUTP != OUT_S32 && p.splits == 1;
@@ -836,7 +837,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             }
             __syncwarp();
         };
-        if (ss_issuer && !(probe & 4)) ss_issue(tile0 + b * tstep, 0);
+        if (ss_issuer && !(probe & 4)) ss_issue(tile0 + b * tstep, 0);   // constants: before the PDL wait
+        pdl_wait();   // outputs are written only after the previous kernel completed
         int j = 0;
         for (int unit = tile0 + b * tstep; unit < p.num_units; unit += Cfg::NBUF * tstep, ++j) {
             const int tile = p.splits == 1 ? unit : p.fd_splits.div(unit);
