@@ -276,6 +276,14 @@ __device__ __forceinline__ uint32_t pack2_f32_s8(float a, float b, uint32_t c) {
         " cvt.pack.sat.s8.s32.b32 %0, ia, ib, %3;\n}" : "=r"(d) : "f"(a), "f"(b), "r"(c));
     return d;
 }
+// (a0, a1) * (b0, b1) + (c0, c1) with ONE packed fp32 FMA (sm_100 FFMA2): two
+// independent IEEE round-to-nearest fmas, bit-identical to two __fmaf_rn.
+__device__ __forceinline__ void fma2_rn(float a0, float a1, float b0, float b1, float c0, float c1, float &d0,
+                                        float &d1) {
+    asm("{\n .reg .b64 a, b, c, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n mov.b64 c, {%6, %7};\n"
+        " fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
+        : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
 // four float values -> one packed s8 word (value 0 in byte 0)
 __device__ __forceinline__ uint32_t pack4_f32_s8(float u0, float u1, float u2, float u3) {
     return pack2_f32_s8(u1, u0, pack2_f32_s8(u3, u2, 0u));
@@ -946,10 +954,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             for (int q = 0; q < 4; ++q) {
                                 float4 sa, sb;
                                 ss4(q, sa, sb);
-                                const float u0 = __fmaf_rn(__int2float_rn((int)v[4 * q]), sa.x, sb.x);
-                                const float u1 = __fmaf_rn(__int2float_rn((int)v[4 * q + 1]), sa.y, sb.y);
-                                const float u2 = __fmaf_rn(__int2float_rn((int)v[4 * q + 2]), sa.z, sb.z);
-                                const float u3 = __fmaf_rn(__int2float_rn((int)v[4 * q + 3]), sa.w, sb.w);
+                                float u0, u1, u2, u3;
+                                fma2_rn(__int2float_rn((int)v[4 * q]), __int2float_rn((int)v[4 * q + 1]), sa.x, sa.y,
+                                        sb.x, sb.y, u0, u1);
+                                fma2_rn(__int2float_rn((int)v[4 * q + 2]), __int2float_rn((int)v[4 * q + 3]), sa.z,
+                                        sa.w, sb.z, sb.w, u2, u3);
                                 w4[q] = pack4_f32_s8(u0, u1, u2, u3);
                                 if (relu8 || p.relu) w4[q] = relu_s8x4(w4[q]);
                             }

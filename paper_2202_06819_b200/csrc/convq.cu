@@ -804,15 +804,17 @@ extern "C" int conv_q_s2d_quantize(const conv_q_plan_t *p, const void *x_fp16, f
     int rc = ensure_device();
     if (rc) return rc;
     const int64_t total = (int64_t)p->N * p->H * p->xs_W;
-    const int grid = grid_for(total, 256);
+    // one thread per stored s2d pixel (no grid-stride loop: every thread's loads
+    // are in flight at once; the kernel is a single HBM pass)
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 1 << 30);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int PL = p->pad;
-    if (p->bits == 8)
-        s2d_quantize_kernel<8><<<grid, 256, 0, st>>>(static_cast<const __half *>(x_fp16), static_cast<uint4 *>(xs),
-                                                     p->N, p->o_H, p->o_W, p->o_C, p->H, p->xs_W, PL, inv_scale);
-    else
-        s2d_quantize_kernel<4><<<grid, 256, 0, st>>>(static_cast<const __half *>(x_fp16), static_cast<uint4 *>(xs),
-                                                     p->N, p->o_H, p->o_W, p->o_C, p->H, p->xs_W, PL, inv_scale);
+    // (even W keeps every row's 6*W-byte offset 4-byte aligned)
+    const bool c3 = p->o_C == 3 && p->o_W % 2 == 0 && (reinterpret_cast<uintptr_t>(x_fp16) & 3) == 0;
+    auto kern = p->bits == 8 ? (c3 ? s2d_quantize_kernel<8, true> : s2d_quantize_kernel<8, false>)
+                             : (c3 ? s2d_quantize_kernel<4, true> : s2d_quantize_kernel<4, false>);
+    kern<<<grid, 256, 0, st>>>(static_cast<const __half *>(x_fp16), static_cast<uint4 *>(xs), p->N, p->o_H, p->o_W,
+                               p->o_C, p->H, p->xs_W, PL, inv_scale);
     CUDA_TRY(cudaGetLastError());
     return CONV_Q_OK;
 }

@@ -173,7 +173,9 @@ __global__ void __launch_bounds__(256) pack_weights_kernel(const int8_t *__restr
 // (2*dh + dw)*CP + c, zero where the pixel or channel does not exist.
 // Stored column xc holds s2d column xc - PL (zero outside [0, ceil(W/2))), so
 // the S2P-pixel windows the conv reads never leave the row.
-template <int BITS>
+// C3 = true: the RGB fast path (C == 3): the two pixels of a row are 12
+// contiguous, 4-byte aligned bytes -> three 32-bit read-only loads per row.
+template <int BITS, bool C3>
 __global__ void __launch_bounds__(256) s2d_quantize_kernel(const __half *__restrict__ x, uint4 *__restrict__ y,
                                                           int N, int H, int W, int C, int H2, int XW, int PL,
                                                           float inv_scale) {
@@ -190,7 +192,21 @@ __global__ void __launch_bounds__(256) s2d_quantize_kernel(const __half *__restr
         int q[4 * CP];
 #pragma unroll
         for (int i = 0; i < 4 * CP; ++i) q[i] = 0;
-        if (w2 >= 0 && 2 * w2 < W) {
+        if (C3 && w2 >= 0 && 2 * w2 + 1 < W) {
+#pragma unroll
+            for (int dh = 0; dh < 2; ++dh) {
+                const int h = 2 * h2 + dh;
+                if (h >= H) continue;
+                const uint32_t *src = reinterpret_cast<const uint32_t *>(x + (((int64_t)n * H + h) * W + 2 * w2) * 3);
+                const uint32_t a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
+                const uint32_t hv[3] = {a, b, c};   // halves: (p0c0 p0c1) (p0c2 p1c0) (p1c1 p1c2)
+#pragma unroll
+                for (int e = 0; e < 6; ++e) {
+                    const unsigned short bits = (unsigned short)(e & 1 ? hv[e >> 1] >> 16 : hv[e >> 1] & 0xFFFFu);
+                    q[(2 * dh + e / 3) * CP + e % 3] = quant1(__ushort_as_half(bits), inv_scale, lo, hi);
+                }
+            }
+        } else if (w2 >= 0 && 2 * w2 < W) {
 #pragma unroll
             for (int dh = 0; dh < 2; ++dh) {
                 const int h = 2 * h2 + dh;

@@ -256,6 +256,7 @@ def test_split_k_parity(cq, bits, L, N):
     (1, 33, 29, 3, 64, 7, 7, 3),      # odd H/W: last s2d row/column half empty
     (1, 21, 19, 3, 128, 3, 3, 1),     # 3x3/2 p1 stem (2 s2d taps)
     (2, 16, 16, 1, 64, 5, 5, 2),      # C=1, 5x5/2 p2
+    (1, 26, 32, 3, 64, 7, 7, 3),      # even W: the vectorised C=3 quantize path, odd H
 ])
 def test_stem_s2d_parity(cq, bits, N, H, W, C, K, R, S, pad):
     """StemPlan (s2d quantize + window weights + stride-1 conv) == the oracle's
