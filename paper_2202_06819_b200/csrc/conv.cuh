@@ -140,12 +140,17 @@ struct ConvCfg {
     // stages carry only activations (with bit 0: one halo box per stage).
     static constexpr bool HA = (HALO & 1) != 0;
     static constexpr bool WS = (HALO & 2) != 0;
+    // HALO bit 2 (S2H, with WS): the s2d stem's window operand -- one tiled box of
+    // consecutive 16-byte s2d pixels per tile; tap row jr and K step kk read it
+    // through a SWIZZLE_NONE descriptor at pixel offset jr*Wp + 2*kk, LBO = 16 B
+    static constexpr bool S2H = (HALO & 4) != 0;
+    static constexpr bool HB = HA || S2H;                    // stage = one halo box
     static constexpr int WSB = WS ? 65536 : 0;               // resident weight region (budget; plan-time check)
-    static constexpr int HBOX = WS && HA ? (KCH == 64 ? 20480 : 32768) : 0;   // WS halo stage (budget)
+    static constexpr int HBOX = WS && HB ? (KCH == 64 ? 20480 : 32768) : 0;   // WS halo stage (budget)
     static constexpr int B_TILE = BN / CG * KCH;             // one resident k-block of this CTA's weight rows
     static constexpr int BNL = BN / CG;                     // B rows staged per CTA
     static constexpr int LOAD_ROW = KCH * BITS / 8;        // packed bytes per row per k-block
-    static constexpr int A_SUB = HA ? HBOX : BM * KCH;      // s8 A sub-tile bytes (one k-block / WS halo box)
+    static constexpr int A_SUB = HB ? HBOX : BM * KCH;      // s8 A sub-tile bytes (one k-block / WS halo box)
     static constexpr int B_SUB = WS ? 0 : BNL * KCH;
     static constexpr int A_S8 = NSUB * A_SUB;               // per stage
     static constexpr int B_S8 = NSUB * B_SUB;
@@ -154,7 +159,7 @@ struct ConvCfg {
     static constexpr int A_PK = NSUB * A_PK_SUB;
     static constexpr int B_PK = NSUB * B_PK_SUB;
     static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
-    static constexpr int SUB_TX = ((HA ? 0 : BM) + (WS ? 0 : BNL)) * LOAD_ROW;  // TMA bytes per k-block per CTA
+    static constexpr int SUB_TX = ((HB ? 0 : BM) + (WS ? 0 : BNL)) * LOAD_ROW;  // TMA bytes per k-block per CTA
     static constexpr int HALO_BYTES = HA && !WS ? 32768 : 0;  // one halo buffer (budget; checked at plan time)
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUTP = OUT & 3;                     // output path
@@ -202,8 +207,9 @@ struct ConvCfg {
     static constexpr int MMA_WARP = PROD_WARP + 1;
     static constexpr int NUM_THREADS = 32 * (MMA_WARP + 1);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
-    static constexpr bool FITS = STAGES >= 2 && (!HA || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
-                                 (!WS || (BITS == 8 && (!HA || NSUB == 1)));  // else never instantiated
+    static constexpr bool FITS = STAGES >= 2 && (!HB || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
+                                 (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
+                                 (!S2H || (WS && !HA && KCH == 64));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
     static_assert(NSUB >= 1 && NSUB <= 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
@@ -380,7 +386,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 
     // ---- carve shared memory (every tile 1024-byte aligned; identical offsets
     // in both CTAs of a pair, as cta_group::2 descriptors require)
-    constexpr bool HA = Cfg::HA, WS = Cfg::WS;
+    constexpr bool HA = Cfg::HA, WS = Cfg::WS, S2H = Cfg::S2H;
     uint8_t *b_res = smem;                              // WS: [num_kb][BN rows][KCH] resident weights
     uint8_t *a_s8 = smem + Cfg::WSB;                    // [STAGES][NSUB][BM*KCH] (WS halo: [STAGES][HBOX])
     uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][NSUB][BNL*KCH]
@@ -481,7 +487,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         }
         pdl_wait();   // activations (the previous layer's output) only after this
         if (trace && lane == 0) trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
-        if constexpr (WS && HA) {
+        if constexpr (WS && (HA || S2H)) {
             // one stage = one halo box per (tile, channel block); no weights
             for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
                 const int m_blk = p.fd_ntiles.div(tile);
@@ -496,7 +502,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     }
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&full[stage], p.halo_tx);
-                        tma_load_4d(a_s8 + stage * Cfg::A_S8, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, -p.pad,
+                        tma_load_4d(a_s8 + stage * Cfg::A_S8, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, -p.pad_w,
                                     p0 - p.pad, n, pol_a);
                     }
                     __syncwarp();
@@ -630,7 +636,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + buf * BN;
-                if constexpr (WS && HA) {
+                if constexpr (WS && (HA || S2H)) {
                     // one stage = this tile's halo box of channel block cblk; tap t
                     // reads it at row offset r*Wp + s, its weights from the resident
                     // k-block t*num_cblk + cblk
@@ -649,7 +655,22 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 mbar_arrive(&empty[stage]);
                                 if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
                             }
-                        } else if (elect_one()) {
+                        } else if (S2H && elect_one()) {
+                            // s2d window: tap row jr, K step kk = s2d pixels 2kk, 2kk+1 of
+                            // every row's window -> box pixel offset jr*Wp + 2kk
+                            const uint64_t ad_s = umma_desc_kmajor_none(smem_u32(a_s8) + stage * Cfg::A_S8, 16, 128);
+                            for (int jr = 0; jr < p.R; ++jr) {
+                                const uint64_t bd = b_desc_res + (uint64_t)((jr * Cfg::B_TILE) >> 4);
+#pragma unroll
+                                for (int kk = 0; kk < 2; ++kk) {
+                                    const uint64_t ad = ad_s + (uint64_t)(jr * p.Wp + 2 * kk);
+                                    if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad, bd + 2 * kk, Cfg::IDESC, (jr | kk) != 0);
+                                    else mma_i8(d_tmem, ad, bd + 2 * kk, Cfg::IDESC, (jr | kk) != 0);
+                                }
+                            }
+                            if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
+                            else mma_commit(&empty[stage]);
+                        } else if (!S2H && elect_one()) {
                             const uint64_t ad_s = a_desc0 + (uint64_t)((stage * Cfg::A_S8) >> 4);
 #pragma unroll
                             for (int t = 0; t < 9; ++t) {
@@ -792,7 +813,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             uint32_t phase = 0;
             for (int unit = tile0; unit < p.num_units; unit += tstep) {
                 int nst;
-                if constexpr (WS && HA) {
+                if constexpr (WS && (HA || S2H)) {
                     nst = p.num_cblk;
                 } else if constexpr (HA) {
                     nst = p.num_cblk * ((p.R * p.S + NSUB - 1) / NSUB);
@@ -853,7 +874,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             const int m_blk = p.fd_ntiles.div(tile), n_blk = tile - m_blk * p.n_tiles;
             const int mrow0 = m_blk * (BM * CG) + (int)rank * BM;
             int m = mrow0 + row;
-            if constexpr (HA) {
+            if constexpr (HA || S2H) {
                 // MMA row -> (output row within the tile, padded column); the
                 // S-1 right-most padded columns and rows past the tile are discarded
                 const int rt = m_blk * CG + (int)rank;

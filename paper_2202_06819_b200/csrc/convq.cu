@@ -246,6 +246,24 @@ static void enumerate_candidates(conv_q_plan_s *p) {
     }
 }
 
+// s2d stem window-halo candidates (cand.halo = 4, weight-stationary, BN = 64):
+// one tiled box of (rows covering 128 MMA rows + 3 tap rows) x Wp stored s2d
+// pixels per tile; needs the 64-byte window (S2P = 4) and a box <= 20 KB
+static void enumerate_s2d_halo(conv_q_plan_s *p) {
+    if (!p->s2d || p->bits != 8 || p->row_bytes != 64 || p->xs_W > BM || p->K % 64) return;
+    const int Wp = p->xs_W;
+    const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + 3, Wp);
+    if ((int64_t)halo_rows * Wp * 16 > 20480 || halo_rows > 256) return;
+    const int sms = g_num_sms > 0 ? g_num_sms : 148;
+    for (int cg : {1, 2}) {
+        if (ceil_div(p->K, 64) > sms / cg) continue;
+        Cand c{64, 64, cg, 1, 1};
+        c.ws = 1;
+        c.halo = 4;
+        if (cand_fits<8>(c)) p->cands.push_back(c);
+    }
+}
+
 static int default_candidate(const conv_q_plan_s *p) {
     const int64_t m_tiles = ceil_div(p->M, BM);
     const int sms = g_num_sms > 0 ? g_num_sms : 148;
@@ -362,6 +380,7 @@ static conv_q_plan_t *finish_plan(conv_q_plan_s *p) {
     p->out_row = p->K * p->bits / 8;
     std::call_once(g_init_once, init_device);  // SM count for the default pick; errors surface at run
     enumerate_candidates(p);
+    enumerate_s2d_halo(p);
     p->sel = default_candidate(p);
     if (const char *pr = getenv("CONV_Q_PROBE")) p->probe = atoi(pr);
     if (const char *ew = getenv("CONV_Q_EPI_WAIT")) p->epi_wait = atoi(ew);
@@ -517,7 +536,21 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
     // A (halo mode): tiled 4-D box {KCH bytes, Wp, halo rows, 1} of the
     // padded input starting at (w, h) = (-pad, p0-pad): the duplicate-free
     // "genuine" data of PAPER.md section 3.1; OOB (padding) is zero-filled.
-    if (c.halo) {
+    if (c.halo == 4) {
+        // A (s2d window halo): tiled box {16 B, Wp stored pixels, halo rows, 1}
+        // of the stored s2d tensor [N][H2][Wp][16 B] at (0, 0, p0 - PL, n); rows
+        // outside [0, H2) are zero-filled, columns are in bounds by construction
+        const int Wp = p->xs_W;
+        const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + 3, Wp);
+        cuuint64_t dims[4] = {16, (cuuint64_t)Wp, (cuuint64_t)p->H, (cuuint64_t)p->N};
+        cuuint64_t strides[3] = {16, (cuuint64_t)16 * Wp, (cuuint64_t)16 * Wp * p->H};
+        cuuint32_t box[4] = {16, (cuuint32_t)Wp, (cuuint32_t)halo_rows, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = g_encode_tiled(&p->tm_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(x), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(x s2d halo) failed: %d", (int)r);
+    } else if (c.halo) {
         const int Wp = p->W + 2 * p->pad;
         const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
         cuuint64_t dims[4] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->W, (cuuint64_t)p->H, (cuuint64_t)p->N};

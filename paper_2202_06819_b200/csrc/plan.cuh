@@ -55,7 +55,8 @@ struct Cand {
     X(64, 64, 2, 0, 1) X(128, 64, 2, 0, 1) X(256, 64, 2, 0, 1)                                \
     X(64, 128, 2, 0, 1) X(128, 128, 2, 0, 1) X(256, 128, 2, 0, 1)                             \
     X(64, 64, 1, 0, 2) X(128, 64, 1, 0, 2) X(256, 64, 1, 0, 2)                                \
-    X(64, 128, 1, 0, 2) X(128, 128, 1, 0, 2) X(256, 128, 1, 0, 2)
+    X(64, 128, 1, 0, 2) X(128, 128, 1, 0, 2) X(256, 128, 1, 0, 2)                             \
+    X(64, 64, 1, 4, 1) X(64, 64, 1, 4, 2)
 
 }  // namespace convq
 
@@ -160,13 +161,13 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.num_kb = p->R * p->S * prm.num_cblk;
     prm.n_tiles = (int)ceil_div(p->K, BN);
     prm.num_tiles = (int)(ceil_div(p->M, BM * CG) * prm.n_tiles);
-    prm.Wp = p->W + 2 * p->pad;
+    prm.Wp = p->s2d ? p->xs_W : p->W + 2 * p->pad;   // MMA-row pitch of an output row (halo modes)
     prm.rpt = std::max(1, std::min(p->P, BM / prm.Wp));
     prm.tiles_per_img = (int)ceil_div(p->P, prm.rpt);
     prm.m_tiles = p->N * prm.tiles_per_img;
-    const int halo_rows = (int)ceil_div(BM + (p->R - 1) * prm.Wp + p->S - 1, prm.Wp);
-    prm.halo_tx = halo_rows * prm.Wp * Cfg::LOAD_ROW;
-    if (HALO & 1) prm.num_tiles = (int)(ceil_div(prm.m_tiles, CG) * prm.n_tiles);
+    const int halo_rows = (int)ceil_div(BM + (p->R - 1) * prm.Wp + ((HALO & 4) ? 3 : p->S - 1), prm.Wp);
+    prm.halo_tx = halo_rows * prm.Wp * ((HALO & 4) ? 16 : Cfg::LOAD_ROW);   // S2H box: whole 16-byte s2d pixels
+    if (HALO & 5) prm.num_tiles = (int)(ceil_div(prm.m_tiles, CG) * prm.n_tiles);
     prm.splits = HALO ? 1 : p->cands[p->sel].split;
     prm.num_units = prm.num_tiles * prm.splits;
     prm.ws = p->ws;

@@ -390,6 +390,16 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t smem_addr, uint32_
     uint64_t sbo = (8ull * row_bytes) >> 4;
     return (uint64_t)((smem_addr & 0x3FFFF) >> 4) | (1ull << 16) | (sbo << 32) | (1ull << 46) | (layout << 61);
 }
+// K-major, SWIZZLE_NONE (layout type 0): core matrices of 8 rows x 16 B with
+// rows 16 B apart; LBO = byte distance between the two 16-byte K chunks of a
+// 32-byte MMA K step, SBO = between 8-row groups (CUTLASS mma_sm100_desc:
+// ((8,m),(T,2)):((1T,SBO),(1,LBO))).  The s2d stem's window operand uses
+// LBO = 16 B: consecutive MMA rows AND consecutive K chunks are consecutive
+// 16-byte s2d pixels, i.e. overlapping rows of one halo box.
+__device__ __forceinline__ uint64_t umma_desc_kmajor_none(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((smem_addr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+           (1ull << 46);
+}
 // Instruction descriptor for kind::i8: D s32, A s8, B s8, both K-major.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4)                        // D format: S32
