@@ -85,6 +85,7 @@ struct ConvParams {
     int a_gemm;          // 1x1 / stride 1 / pad 0: A is the input as a [M][C] matrix (tiled TMA, no im2col)
     int probe;           // measurement only (bits): 1 = no MMAs, 2 = no loads, 4 = no epilogue work
     int epi_wait;        // epilogue acc_full wait: 0 spin, 1 suspend-time hint, 2 nanosleep back-off
+    int out_policy;      // L2 policy of the packed output stores: 0 none, 1 evict_last, 2 evict_first
     unsigned epi_wait_ns;
     unsigned long long *trace;  // measurement only: per-CTA wait-cycle counters (TRACE_SLOTS each), or null
     // duplicate-aware (halo) mode, stride 1 only:
@@ -848,6 +849,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         uint8_t *slab = out_stage + b * Cfg::OUT_BYTES + (half * 4 + quad) * Cfg::SLAB;
         const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(&acc_empty[b]), 0) : 0;
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
+        const uint64_t out_pol = p.out_policy == 1 ? policy_evict_last() : p.out_policy == 2 ? policy_evict_first() : 0;
         constexpr bool relu8 = Cfg::RELU8;   // ReLU specialisation (p.relu == 1 guaranteed by the dispatch)
         // scale/shift of the j-th tile of this buffer -> slot j % 3, issued by the
         // buffer's first warp one tile ahead (see SS_BYTES)
@@ -1008,8 +1010,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             *reinterpret_cast<uint4 *>(sub + swz<Cfg::EPI_SUBW>(lane * Cfg::EPI_SUBW + sbyte % Cfg::EPI_SUBW)) = pk;
                         } else {
                             const int gbyte = n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + sbyte;
-                            if (m < p.M && gbyte < p.out_row)
-                                *reinterpret_cast<uint4 *>(p.y8 + (int64_t)m * p.out_row + gbyte) = pk;
+                            if (m < p.M && gbyte < p.out_row) {
+                                uint8_t *dst = p.y8 + (int64_t)m * p.out_row + gbyte;
+                                if (p.out_policy) st_global_v4_hint(dst, pk, out_pol);
+                                else *reinterpret_cast<uint4 *>(dst) = pk;
+                            }
                         }
                     }
             };
@@ -1090,9 +1095,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 __syncwarp();
                 if (lane == 0) {
 #pragma unroll
-                    for (int s = 0; s < Cfg::EPI_NSUB; ++s)
-                        tma_store_2d(&tm_y, slab + s * (32 * Cfg::EPI_SUBW),
-                                     n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + s * Cfg::EPI_SUBW, mrow0 + quad * 32);
+                    for (int s = 0; s < Cfg::EPI_NSUB; ++s) {
+                        const int c0 = n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + s * Cfg::EPI_SUBW, c1 = mrow0 + quad * 32;
+                        if (p.out_policy) tma_store_2d_hint(&tm_y, slab + s * (32 * Cfg::EPI_SUBW), c0, c1, out_pol);
+                        else tma_store_2d(&tm_y, slab + s * (32 * Cfg::EPI_SUBW), c0, c1);
+                    }
                     tma_store_commit();
                 }
             }

@@ -82,6 +82,7 @@ struct conv_q_plan_s {
     int probe = 0;     // CONV_Q_PROBE (measurement only; results are garbage when != 0)
     int epi_wait = 0;  // CONV_Q_EPI_WAIT / _NS: how epilogue warps wait for accumulators (A/B)
     unsigned epi_wait_ns = 0;
+    int out_policy = 1; // CONV_Q_OUT_POLICY: L2 hint on output stores (0 none, 1 evict_last = default: the next layer reads them, 2 evict_first)
     unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
     CUtensorMap tm_a, tm_b, tm_y;
@@ -191,6 +192,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.a_gemm = p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0 && !(HALO & 1);
     prm.probe = p->probe;
     prm.epi_wait = p->epi_wait;
+    prm.out_policy = p->out_policy;
     prm.epi_wait_ns = p->epi_wait_ns;
     prm.trace = p->trace;
     prm.scale = scale;
