@@ -88,6 +88,7 @@ struct ConvParams {
     int out_policy;      // L2 policy of the packed output stores: 0 none, 1 evict_last, 2 evict_first
     unsigned epi_wait_ns;
     unsigned long long *trace;  // measurement only: per-CTA wait-cycle counters (TRACE_SLOTS each), or null
+    unsigned long long *tl;     // measurement only: CTA 0's event timeline (clock64), [64 regions][256], or null
     // duplicate-aware (halo) mode, stride 1 only:
     int Wp;              // padded input width W + 2 pad = MMA-row pitch of an output row
     int rpt;             // output rows per 128-row tile
@@ -377,6 +378,12 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     // measurement hooks (wait-cycle trace, probe modes) exist only in the
     // CONVQ_INSTRUMENT build (libconvq_instr.so); compiled out otherwise
     unsigned long long *const trace = kInstrument ? p.trace : nullptr;
+    // timeline (instrumented build, CTA 0): region 0 producer after each empty
+    // wait, 1/2/3 MMA warp per tile after acc_empty / first full wait / acc_full
+    // commit, 4+w / 24+w epilogue warp w per tile after acc_full / after its store
+    unsigned long long *const tl = kInstrument && blockIdx.x == 0 ? p.tl : nullptr;
+#define CONVQ_TL(region, idx) \
+    do { if (tl && lane == 0) tl[(region) * 256 + ((idx) & 255)] = (unsigned long long)clock64(); } while (0)
     const int probe = kInstrument ? p.probe : 0;
     static_assert(Cfg::FITS, "tile does not fit shared memory");
     constexpr int STAGES = Cfg::STAGES;
@@ -470,6 +477,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         constexpr int B_LD_SUB = BITS == 4 ? Cfg::B_PK_SUB : Cfg::B_SUB;
         int stage = 0;
         uint32_t phase = 0;
+        int tl_n = 0;
         if constexpr (WS) {
             // weight-stationary: this CTA's BN x (R*S*C) weight block, once, as
             // num_kb k-block tiles [BN rows][KCH] (tap-major k order).  Weights
@@ -501,6 +509,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         mbar_wait(&empty[stage], phase ^ 1);
                         if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
                     }
+                    CONVQ_TL(0, tl_n++);
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&full[stage], p.halo_tx);
                         tma_load_4d(a_s8 + stage * Cfg::A_S8, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, -p.pad_w,
@@ -575,6 +584,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_PROD_EMPTY, clock64() - t0);
                 }
+                CONVQ_TL(0, tl_n++);
                 if (elect_one()) {
                     if (probe & 2) mbar_arrive(&full[stage]);   // measurement: no loads
                     else mbar_arrive_expect_tx(&full[stage], nsub * Cfg::SUB_TX);
@@ -630,6 +640,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 {
                     const long long t0 = trace ? clock64() : 0;
                     mbar_wait(&acc_empty[buf], aphase ^ 1);
+                    CONVQ_TL(1, local);
                     if (trace && lane == 0) {
                         atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ACC, clock64() - t0);
                         atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_TILES, 1ull);
@@ -645,6 +656,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         long long t0 = trace ? clock64() : 0;
                         mbar_wait(&full[stage], phase);
                         if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's halo box
+                        if (cblk == 0) CONVQ_TL(2, local);
                         if (trace && lane == 0) {
                             const long long t1 = clock64();
                             atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
@@ -753,6 +765,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     long long t0 = trace ? clock64() : 0;
                     mbar_wait(BITS == 4 ? &ready[stage] : &full[stage], phase);
                     if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's half of the stage
+                    if (kb == kb_lo) CONVQ_TL(2, local);
                     if (trace && lane == 0) {
                         const long long t1 = clock64();
                         atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
@@ -800,6 +813,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     else mma_commit(&acc_full[buf]);
                 }
                 __syncwarp();
+                CONVQ_TL(3, local);
             }
         } else if constexpr (PAIR8) {
             // follower CTA: relay every stage its own TMA loads filled to the
@@ -889,6 +903,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             {
                 const long long t0 = trace ? clock64() : 0;
                 mbar_wait_relaxed(&acc_full[b], j & 1, p.epi_wait, p.epi_wait_ns);
+                CONVQ_TL(4 + warp, j);
                 if (trace && lane == 0 && warp == Cfg::EPI_WARP0) {
                     atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_EPI_ACC, clock64() - t0);
                     if (j == 0) trace[blockIdx.x * TR_SLOTS + TR_TACC] = globaltimer_ns();
@@ -1103,8 +1118,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     tma_store_commit();
                 }
             }
+            CONVQ_TL(24 + warp, j);
         }
         if (Cfg::OUTP == OUT_TMA && lane == 0) tma_store_wait0();
+#undef CONVQ_TL
     } else if (warp < Cfg::PROD_WARP) {
         // =========================== INT4 transform =========================
         if constexpr (BITS == 4) {

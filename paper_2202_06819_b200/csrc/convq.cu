@@ -1003,3 +1003,14 @@ extern "C" CONVQ_API int conv_q_plan_set_trace(conv_q_plan_t *p, void *counters)
     p->trace = static_cast<unsigned long long *>(counters);
     return CONV_Q_OK;
 }
+
+// Measurement only: CTA 0's event timeline (clock64 per event, [64][256] u64,
+// zeroed by the caller; see conv.cuh CONVQ_TL), or NULL to stop.
+extern "C" CONVQ_API int conv_q_plan_set_timeline(conv_q_plan_t *p, void *buf) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+#ifndef CONVQ_INSTRUMENT
+    if (buf) return set_err(CONV_Q_EUNSUPPORTED, "timelines need the CONVQ_INSTRUMENT build (libconvq_instr.so)");
+#endif
+    p->tl = static_cast<unsigned long long *>(buf);
+    return CONV_Q_OK;
+}

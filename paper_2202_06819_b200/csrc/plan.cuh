@@ -84,6 +84,7 @@ struct conv_q_plan_s {
     unsigned epi_wait_ns = 0;
     int out_policy = 1; // CONV_Q_OUT_POLICY: L2 hint on output stores (0 none, 1 evict_last = default: the next layer reads them, 2 evict_first)
     unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
+    unsigned long long *tl = nullptr;     // conv_q_plan_set_timeline (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
     CUtensorMap tm_a, tm_b, tm_y;
     const void *c_x = nullptr, *c_w = nullptr, *c_y = nullptr;
@@ -195,6 +196,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.out_policy = p->out_policy;
     prm.epi_wait_ns = p->epi_wait_ns;
     prm.trace = p->trace;
+    prm.tl = p->tl;
     prm.scale = scale;
     prm.y32 = static_cast<int32_t *>(y);
     prm.y8 = static_cast<uint8_t *>(y);
