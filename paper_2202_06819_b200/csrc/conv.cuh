@@ -45,6 +45,10 @@
 namespace convq {
 
 constexpr int BM = 128;
+#ifndef CONVQ_MMA_1T
+#define CONVQ_MMA_1T 0
+#endif
+constexpr bool kMma1T = CONVQ_MMA_1T != 0;
 #ifdef CONVQ_INSTRUMENT
 constexpr bool kInstrument = true;
 #else
@@ -617,7 +621,14 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         // Whole warp (converged) waits; one elected lane issues the MMAs and
         // commits.  Descriptors: base + byte offset >> 4 in the start-address
         // field (addresses < 2^18, so the 14-bit field never carries).
-        if (rank == 0) {
+        // CONVQ_MMA_1T=1 (measured slower: the compiler cannot keep the descriptors
+        // in uniform registers and emits an R2UR waterfall per MMA): the MMA loop on lane 0 alone -- no
+        // elect / warp-sync / divergence checks per stage on this single-thread
+        // critical path (the per-tile control loop is serialised with the MMA
+        // execution; see profiles/r01_timeline_cta0.txt)
+        auto mma_elect = [&]() { return kMma1T ? true : elect_one(); };
+        auto mma_sync = [&]() { if (!kMma1T) __syncwarp(); };
+        if (rank == 0 && (!kMma1T || lane == 0)) {
             const uint64_t a_desc0 = umma_desc_kmajor(smem_u32(a_s8), KCH);
             const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(b_s8), KCH);
             // HALO (3x3): descriptor start-address delta of tap t's window, (r*Wp + s)*KCH bytes
@@ -664,11 +675,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         }
                         tc_fence_after();
                         if (probe & 1) {
-                            if (elect_one()) {
+                            if (mma_elect()) {
                                 mbar_arrive(&empty[stage]);
                                 if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
                             }
-                        } else if (S2H && elect_one()) {
+                        } else if (S2H && mma_elect()) {
                             // s2d window: tap row jr, K step kk = s2d pixels 2kk, 2kk+1 of
                             // every row's window -> box pixel offset jr*Wp + 2kk
                             const uint64_t ad_s = umma_desc_kmajor_none(smem_u32(a_s8) + stage * Cfg::A_S8, 16, 128);
@@ -683,7 +694,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             }
                             if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
                             else mma_commit(&empty[stage]);
-                        } else if (!S2H && elect_one()) {
+                        } else if (!S2H && mma_elect()) {
                             const uint64_t ad_s = a_desc0 + (uint64_t)((stage * Cfg::A_S8) >> 4);
 #pragma unroll
                             for (int t = 0; t < 9; ++t) {
@@ -698,7 +709,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
                             else mma_commit(&empty[stage]);
                         }
-                        __syncwarp();
+                        mma_sync();
                         if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -722,7 +733,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 t0 = t1;
                             }
                             tc_fence_after();
-                            if (elect_one()) {
+                            if (mma_elect()) {
                                 if (probe & 1) {
                                     mbar_arrive(&empty[stage]);
                                     if (g == Cfg::HST - 1) mbar_arrive(&hempty[hb]);
@@ -754,7 +765,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                     }
                                 }
                             }
-                            __syncwarp();
+                            mma_sync();
                             if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                             if (++stage == STAGES) { stage = 0; phase ^= 1; }
                         }
@@ -773,7 +784,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         t0 = t1;
                     }
                     tc_fence_after();
-                    if (elect_one()) {
+                    if (mma_elect()) {
                         if (probe & 1) {                // measurement: no MMAs
                             if constexpr (CG == 2) {
                                 mbar_arrive(&empty[stage]);
@@ -803,16 +814,16 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             else mma_commit(&empty[stage]);
                         }
                     }
-                    __syncwarp();
+                    mma_sync();
                     if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 // accumulator ready for the epilogue (of both CTAs)
-                if (elect_one()) {
+                if (mma_elect()) {
                     if constexpr (CG == 2) mma_commit_cg2_mc(&acc_full[buf], 0x3);
                     else mma_commit(&acc_full[buf]);
                 }
-                __syncwarp();
+                mma_sync();
                 CONVQ_TL(3, local);
             }
         } else if constexpr (PAIR8) {
@@ -845,6 +856,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
             }
         }
+        __syncwarp();   // reconverge the MMA warp (lane 0 ran the loop alone) before the aligned barriers
     } else if (warp < Cfg::XF_WARP0) {
         // =========================== epilogue ===============================
         // Every warp works on its own: TMEM buffer b (every other tile) is
