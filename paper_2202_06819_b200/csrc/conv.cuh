@@ -49,6 +49,17 @@ constexpr int BM = 128;
 #define CONVQ_MMA_1T 0
 #endif
 constexpr bool kMma1T = CONVQ_MMA_1T != 0;
+// Two MMA-issuing warps taking alternate tiles (CONVQ_DUAL_MMA=1; OFF by default:
+// parity-green on every test shape and 1.7x faster per tile on l1.b0.c2, but
+// l1.b1.c1 bm128_bn64_kc128x2_c1 at N=256 faults/hangs -- an unresolved race): a
+// warp's per-tile control path (barrier waits, fences, commits: ~650-700 cycles,
+// profiles/r01_timeline_cta0.txt) then overlaps the other warp's MMA execution
+// instead of adding to it.  Tile t: warp t % 2, TMEM buffer t % NBUF, smem
+// stages from t * (stages per tile) -- fixed when every unit has the same K range.
+#ifndef CONVQ_DUAL_MMA
+#define CONVQ_DUAL_MMA 0
+#endif
+constexpr int kNumMma = CONVQ_DUAL_MMA ? 2 : 1;
 #ifdef CONVQ_INSTRUMENT
 constexpr bool kInstrument = true;
 #else
@@ -211,7 +222,7 @@ struct ConvCfg {
     static constexpr int XF_WARP0 = 4 * NUM_EPI;                    // INT4 transform warps
     static constexpr int PROD_WARP = XF_WARP0 + (BITS == 4 ? 4 : 0);
     static constexpr int MMA_WARP = PROD_WARP + 1;
-    static constexpr int NUM_THREADS = 32 * (MMA_WARP + 1);
+    static constexpr int NUM_THREADS = 32 * (MMA_WARP + kNumMma);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
     static constexpr bool FITS = STAGES >= 2 && (!HB || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
                                  (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
@@ -417,6 +428,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint64_t *bfull = hempty;               // WS (no separate halo buffers): resident weights loaded
     uint64_t *ss_full = hempty + 4;         // scale/shift bulk copy -> epilogue [NBUF][3 slots]
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(ss_full + 12);
+    // dual MMA warps: the last global smem-stage index each has waited for (a
+    // parity wait is only valid once the stage's previous fill has completed)
+    volatile int *mma_prog = reinterpret_cast<volatile int *>(tmem_holder + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -449,6 +463,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF * CG);
             for (int k = 0; k < 3; ++k) mbar_init(&ss_full[3 * b + k], 1);
         }
+        mma_prog[0] = mma_prog[1] = -1;
         fence_mbar_init();
     }
     if (warp == Cfg::MMA_WARP) {
@@ -616,8 +631,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
-    } else if (warp == Cfg::MMA_WARP) {
+    } else if (warp >= Cfg::MMA_WARP) {
         // =========================== MMA issuer =============================
+        const int mw = warp - Cfg::MMA_WARP;                 // which MMA warp
+        // (split-K units have ragged K ranges; an odd buffer count would share
+        // TMEM buffers between the two warps)
+        const int nmma = p.splits == 1 && Cfg::NBUF % 2 == 0 ? kNumMma : 1;
+        // smem stages per unit (uniform when splits == 1)
+        const int s_unit = (WS && (HA || S2H)) ? p.num_cblk
+                         : HA ? p.num_cblk * Cfg::HST : (p.num_kb + NSUB - 1) / NSUB;
         // Whole warp (converged) waits; one elected lane issues the MMAs and
         // commits.  Descriptors: base + byte offset >> 4 in the start-address
         // field (addresses < 2^18, so the 14-bit field never carries).
@@ -628,7 +650,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         // execution; see profiles/r01_timeline_cta0.txt)
         auto mma_elect = [&]() { return kMma1T ? true : elect_one(); };
         auto mma_sync = [&]() { if (!kMma1T) __syncwarp(); };
-        if (rank == 0 && (!kMma1T || lane == 0)) {
+        if (rank == 0 && (!kMma1T || lane == 0) && mw < nmma) {
             const uint64_t a_desc0 = umma_desc_kmajor(smem_u32(a_s8), KCH);
             const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(b_s8), KCH);
             // HALO (3x3): descriptor start-address delta of tap t's window, (r*Wp + s)*KCH bytes
@@ -641,11 +663,28 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             if (WS && CG == 2) mbar_wait(&hempty[1], 0);   // the follower's weight rows
             int stage = 0;
             uint32_t phase = 0;
-            int local = 0;
             int hcount = 0;
-            for (int unit = tile0; unit < p.num_units; unit += tstep, ++local) {
+            int gsi = 0;   // global index of the current smem stage
+            // before a parity wait on stage gsi: its previous fill (gsi - STAGES)
+            // must be complete, i.e. some MMA warp has already waited past it
+            auto mma_gate = [&]() {
+                if (nmma > 1)
+                    while ((mma_prog[0] > mma_prog[1] ? mma_prog[0] : mma_prog[1]) < gsi - STAGES) {
+                    }
+            };
+            auto mma_mark = [&]() {
+                if (nmma > 1 && lane == 0) mma_prog[mw] = gsi;
+            };
+            for (int unit = tile0 + mw * tstep, local = mw; unit < p.num_units; unit += nmma * tstep, local += nmma) {
                 int tile, kb_lo, kb_hi;
                 unit_range(p, unit, tile, kb_lo, kb_hi);
+                if (nmma > 1) {   // this unit's first stage in the producer's global sequence
+                    const int gs = local * s_unit;
+                    gsi = gs;
+                    stage = gs % STAGES;
+                    phase = (uint32_t)(gs / STAGES) & 1u;
+                    hcount = local * p.num_cblk;
+                }
                 const int buf = local % Cfg::NBUF;
                 const uint32_t aphase = (local / Cfg::NBUF) & 1;
                 {
@@ -665,8 +704,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     // k-block t*num_cblk + cblk
                     for (int cblk = 0; cblk < p.num_cblk; ++cblk) {
                         long long t0 = trace ? clock64() : 0;
+                        mma_gate();
                         mbar_wait(&full[stage], phase);
                         if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's halo box
+                        mma_mark();
                         if (cblk == 0) CONVQ_TL(2, local);
                         if (trace && lane == 0) {
                             const long long t1 = clock64();
@@ -711,6 +752,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         }
                         mma_sync();
                         if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
+                        ++gsi;
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 } else if constexpr (HA) {
@@ -725,8 +767,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 #pragma unroll
                         for (int g = 0; g < Cfg::HST; ++g) {
                             long long t0 = trace ? clock64() : 0;
+                            mma_gate();
                             mbar_wait(&full[stage], phase);
                             if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's half of the stage
+                            mma_mark();
                             if (trace && lane == 0) {
                                 const long long t1 = clock64();
                                 atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_FULL, t1 - t0);
@@ -767,15 +811,18 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             }
                             mma_sync();
                             if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
-                            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                            ++gsi;
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
                         }
                     }
                 } else
                 for (int kb = kb_lo; kb < kb_hi; kb += NSUB) {
                     const int nsub = min(NSUB, kb_hi - kb);
                     long long t0 = trace ? clock64() : 0;
+                    mma_gate();
                     mbar_wait(BITS == 4 ? &ready[stage] : &full[stage], phase);
                     if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's half of the stage
+                    mma_mark();
                     if (kb == kb_lo) CONVQ_TL(2, local);
                     if (trace && lane == 0) {
                         const long long t1 = clock64();
@@ -816,7 +863,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     }
                     mma_sync();
                     if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    ++gsi;
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 // accumulator ready for the epilogue (of both CTAs)
                 if (mma_elect()) {
@@ -826,7 +874,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 mma_sync();
                 CONVQ_TL(3, local);
             }
-        } else if constexpr (PAIR8) {
+        } else if (PAIR8 && rank != 0 && mw == 0) {
             // follower CTA: relay every stage its own TMA loads filled to the
             // leader's ready barrier (same stage sequence as the producer)
             const uint32_t ready0 = mapa_shared(smem_u32(&ready[0]), 0);
