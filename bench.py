@@ -350,6 +350,35 @@ def run_ours(args):
                "copies": "double-buffered on a copy stream, overlapped with the previous step" if pipelined
                          else "serial"}
 
+    # ---- optional final gather: the ranks' last-layer packed
+    # outputs concatenated on every rank with one NCCL all_gather over NVLink,
+    # timed separately from the compute (no collective inside the step)
+    gather = None
+    if args.gather:
+        y_last = outs[-1]
+        y_all = torch.empty((world * y_last.shape[0],) + tuple(y_last.shape[1:]), dtype=y_last.dtype, device=dev)
+        def do_gather():
+            if world > 1:
+                dist.all_gather_into_tensor(y_all, y_last)
+            else:
+                y_all.copy_(y_last)
+        for _ in range(3):
+            do_gather()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(torch.cuda.current_stream())
+        for _ in range(10):
+            do_gather()
+        g1.record(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        tg = torch.tensor([g0.elapsed_time(g1) / 10], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        gather = {"ms": round(float(tg.item()), 4), "bytes_total": int(y_all.numel()),
+                  "op": "all_gather_into_tensor (NCCL)" if world > 1 else "copy (1 rank)"}
+
     # ---- stem conv1 (timed separately, not part of the step):
     # the s2d StemPlan = fused quantize + space-to-depth of the fp16 image, then
     # the stride-1 window conv (no 3 -> 32 channel padding)
@@ -456,7 +485,7 @@ def run_ours(args):
                          "gbs": round(B * 56 * 56 * 64 * (2 + bits / 8) / (quant_ms * 1e-3) / 1e9, 1),
                          "hbm_peak_gbs": hbm_peak},
             "gpu_launches": args.steps * (len(layers) + 1),
-            "clocks": clocks, "e2e": e2e, "stem": stem, "cpu_baseline": cpu,
+            "clocks": clocks, "e2e": e2e, "stem": stem, "gather": gather, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
         if args.layers_out:
@@ -585,6 +614,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=90.0)
     ap.add_argument("--layers-out", default="")
+    ap.add_argument("--gather", action="store_true",
+                    help="also time the optional final all_gather of the last layer's output (reported separately)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
