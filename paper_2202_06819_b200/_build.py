@@ -18,7 +18,8 @@ CSRC = os.path.join(HERE, "csrc")
 # CONVQ_INSTRUMENT=1: the measurement build (wait-cycle trace + probe modes,
 # scripts/trace.py / probe.py) -> libconvq_instr.so, loaded via CONV_Q_LIB
 INSTR = os.environ.get("CONVQ_INSTRUMENT") == "1"
-_SFX = ("_instr" if INSTR else "") + (f"_wg{os.environ['CONVQ_EPI_WG8']}" if os.environ.get("CONVQ_EPI_WG8") else "")
+_SFX = ("_instr" if INSTR else "") + (f"_wg{os.environ['CONVQ_EPI_WG8']}" if os.environ.get("CONVQ_EPI_WG8") else "") + \
+    ("_dual" if os.environ.get("CONVQ_DUAL_MMA") == "1" else "")
 OBJ = os.path.join(HERE, "build_obj" + _SFX)
 LIB = os.path.join(HERE, f"libconvq{_SFX}.so")
 SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2)] + ["kern_b8_o4.cu", "kern_b8_o6.cu"]
@@ -26,7 +27,8 @@ SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"] + \
     (["-DCONVQ_INSTRUMENT"] if INSTR else []) + \
-    ([f"-DCONVQ_EPI_WG8={os.environ['CONVQ_EPI_WG8']}"] if os.environ.get("CONVQ_EPI_WG8") else [])
+    ([f"-DCONVQ_EPI_WG8={os.environ['CONVQ_EPI_WG8']}"] if os.environ.get("CONVQ_EPI_WG8") else []) + \
+    (["-DCONVQ_DUAL_MMA=1"] if os.environ.get("CONVQ_DUAL_MMA") == "1" else [])
 
 
 def _deps():
