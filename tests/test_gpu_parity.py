@@ -217,6 +217,48 @@ def test_resnet18_chain_int8_b1(cq):
         assert np.array_equal(outs_gpu[-1], outs_ref[-1]), (i, L)
 
 
+def test_resnet18_chain_int4_b16(cq):
+    """cfg3: ResNet-18 convs INT4 (packed s4, s4 -> s8 on chip) batch 16, each y is
+    the next x byte-for-byte, every output byte compared."""
+    layers = wl.resnet18_layers()
+    g = wl.rng(3, 0)
+    x0 = wl.random_bytes(g, (16, 56, 56, 64 * 4 // 8))
+    outs_gpu, outs_ref = [], []
+    for i, (L, src) in enumerate(layers):
+        gi = wl.rng(3, i + 1)
+        wv = wl.random_bytes(gi, (L.K, L.R, L.S, L.C * 4 // 8))
+        sd = wl.uniform_code_std(4)
+        ss = wl.scale_shift(gi, L.K, L.R * L.S * L.C, sd * 0.5, sd, 4)
+        xin_g = x0 if src < 0 else outs_gpu[src]
+        xin_r = x0 if src < 0 else outs_ref[src]
+        outs_gpu.append(run_conv(cq, L, 16, 4, xin_g, wv, ss, relu=True))
+        outs_ref.append(oracle.conv_q(xin_r, wv, L.C, L.stride, L.pad, 4, ss, True))
+        assert np.array_equal(outs_gpu[-1], outs_ref[-1]), (i, L, first_diff(outs_gpu[-1], outs_ref[-1]))
+
+
+@pytest.mark.parametrize("bits,name", [(8, "l1.b0.c3"), (8, "l3.b1.c3"), (8, "l2.b1.c2"), (8, "l4.b0.c2")])
+def test_resnet50_fullsize_tuned_sampled(cq, bits, name):
+    """The bench's launch configuration: batch 256 with the tile config conv_q_plan_tune
+    picks (a7), sampled output pixels vs the oracle."""
+    L = dict((l.name, l) for l, _ in wl.resnet50_layers())[name]
+    N = 256
+    g = wl.rng(4, 7)
+    x, w, ss = wl.layer_inputs(g, L, N, bits)
+    plan = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
+    xd, wd, sd = dev(x), dev(w), dev(ss)
+    y = torch.full((N, L.P, L.Q, L.K * bits // 8), 0xA5, dtype=torch.uint8, device="cuda")
+    plan.tune(xd, wd, sd, y, warmup=1, reps=2)
+    y.fill_(0xA5)
+    plan.run(xd, wd, sd, y)
+    torch.cuda.synchronize()
+    got = y.cpu().numpy().reshape(-1, L.K * bits // 8)
+    M = N * L.P * L.Q
+    pix = np.unique(np.concatenate([np.arange(0, 40), np.arange(M - 40, M),
+                                    g.integers(0, M, 96)])).astype(np.int64)
+    ref = oracle.conv_q(x, w, L.C, L.stride, L.pad, bits, ss, True, pix=pix)
+    assert np.array_equal(got[pix], ref), (plan.info().config, first_diff(got[pix], ref))
+
+
 def test_int8_peak_runs(cq):
     ops = cq.int8_peak(20000)
     assert 1e14 < ops < 6e15
