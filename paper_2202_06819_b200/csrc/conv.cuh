@@ -162,8 +162,14 @@ struct ConvCfg {
     // through a SWIZZLE_NONE descriptor at pixel offset jr*Wp + 2*kk, LBO = 16 B
     static constexpr bool S2H = (HALO & 4) != 0;
     static constexpr bool HB = HA || S2H;                    // stage = one halo box
+    // HALO bit 3 (MT2, weight-stationary halo modes): a work unit is TWO 128-row
+    // m-groups -- one halo box covering both, MMAs into two BN-column TMEM halves,
+    // one accumulator round trip (barrier waits, commits) per 256 rows: the MMA
+    // warp's per-tile control path (~650 cycles) is amortised over twice the work
+    static constexpr int MT = (HALO & 8) ? 2 : 1;
+    static constexpr int TBW = MT * BN;                      // TMEM columns of one accumulator buffer
     static constexpr int WSB = WS ? 65536 : 0;               // resident weight region (budget; plan-time check)
-    static constexpr int HBOX = WS && HB ? (KCH == 64 ? 20480 : 32768) : 0;   // WS halo stage (budget)
+    static constexpr int HBOX = WS && HB ? (KCH == 64 && MT == 1 ? 20480 : 32768) : 0;   // WS halo stage (budget)
     static constexpr int B_TILE = BN / CG * KCH;             // one resident k-block of this CTA's weight rows
     static constexpr int BNL = BN / CG;                     // B rows staged per CTA
     static constexpr int LOAD_ROW = KCH * BITS / 8;        // packed bytes per row per k-block
@@ -185,7 +191,7 @@ struct ConvCfg {
     static constexpr int NUM_EPI = epi_warpgroups(BITS);            // epilogue warpgroups
     // TMEM accumulator buffers: as many as the 512 columns allow (max 4), so
     // up to NBUF tiles are in the epilogue while the MMA fills the next one
-    static constexpr int NBUF = tmem_buffers(BITS, BN);
+    static constexpr int NBUF = tmem_buffers(BITS, TBW);
     static constexpr int EPI_PER_BUF = NUM_EPI / NBUF;              // warpgroups per TMEM buffer
     static constexpr int EPI_COLS = BN / EPI_PER_BUF;               // columns one warp drains (of its 32 rows)
     static constexpr int EPI_ROW = EPI_COLS * BITS / 8;             // packed bytes of one row of a warp's slab
@@ -213,7 +219,7 @@ struct ConvCfg {
     static constexpr int STAGES_FIT = stages_with(NHALO);
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
     static constexpr int SMEM = 1024 + WSB + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * HALO_BYTES + BAR_BYTES;
-    static constexpr int TMEM_COLS = NBUF * BN < 32 ? 32 : NBUF * BN;
+    static constexpr int TMEM_COLS = NBUF * TBW < 32 ? 32 : NBUF * TBW;
     // Warp layout: epilogue warpgroups first, then (INT4) the transform
     // warpgroup, then the TMA producer and the MMA issuer as the two highest
     // warp ids -- the SMSP arbiter favours higher warp ids, so the two
@@ -226,7 +232,8 @@ struct ConvCfg {
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
     static constexpr bool FITS = STAGES >= 2 && (!HB || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
                                  (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
-                                 (!S2H || (WS && !HA && KCH == 64));  // else never instantiated
+                                 (!S2H || (WS && !HA && KCH == 64)) &&
+                                 (MT == 1 || (WS && HB && CG == 1));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
     static_assert(NSUB >= 1 && NSUB <= 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
@@ -697,7 +704,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     }
                 }
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + buf * BN;
+                const uint32_t d_tmem = tmem_base + buf * Cfg::TBW;
                 if constexpr (WS && (HA || S2H)) {
                     // one stage = this tile's halo box of channel block cblk; tap t
                     // reads it at row offset r*Wp + s, its weights from the resident
@@ -724,13 +731,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             // s2d window: tap row jr, K step kk = s2d pixels 2kk, 2kk+1 of
                             // every row's window -> box pixel offset jr*Wp + 2kk
                             const uint64_t ad_s = umma_desc_kmajor_none(smem_u32(a_s8) + stage * Cfg::A_S8, 16, 128);
+#pragma unroll
+                            for (int g = 0; g < Cfg::MT; ++g)   // MT2: m-group g = box pixels from 128 g
                             for (int jr = 0; jr < p.R; ++jr) {
                                 const uint64_t bd = b_desc_res + (uint64_t)((jr * Cfg::B_TILE) >> 4);
 #pragma unroll
                                 for (int kk = 0; kk < 2; ++kk) {
-                                    const uint64_t ad = ad_s + (uint64_t)(jr * p.Wp + 2 * kk);
-                                    if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad, bd + 2 * kk, Cfg::IDESC, (jr | kk) != 0);
-                                    else mma_i8(d_tmem, ad, bd + 2 * kk, Cfg::IDESC, (jr | kk) != 0);
+                                    const uint64_t ad = ad_s + (uint64_t)(g * BM + jr * p.Wp + 2 * kk);
+                                    if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad, bd + 2 * kk, Cfg::IDESC, (jr | kk) != 0);
+                                    else mma_i8(d_tmem + g * BN, ad, bd + 2 * kk, Cfg::IDESC, (jr | kk) != 0);
                                 }
                             }
                             if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
@@ -738,13 +747,16 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         } else if (!S2H && mma_elect()) {
                             const uint64_t ad_s = a_desc0 + (uint64_t)((stage * Cfg::A_S8) >> 4);
 #pragma unroll
+#pragma unroll
+                            for (int g = 0; g < Cfg::MT; ++g)   // MT2: m-group g = halo rows from 128 g
+#pragma unroll
                             for (int t = 0; t < 9; ++t) {
-                                const uint64_t ad = ad_s + toff[t];
+                                const uint64_t ad = ad_s + toff[t] + (uint64_t)((g * BM * KCH) >> 4);
                                 const uint64_t bd = b_desc_res + (uint64_t)(((t * p.num_cblk + cblk) * Cfg::B_TILE) >> 4);
 #pragma unroll
                                 for (int k = 0; k < KCH / 32; ++k) {
-                                    if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
-                                    else mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                    if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                    else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
                                 }
                             }
                             if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
@@ -950,16 +962,18 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             const int m_blk = p.fd_ntiles.div(tile), n_blk = tile - m_blk * p.n_tiles;
             const int mrow0 = m_blk * (BM * CG) + (int)rank * BM;
             int m = mrow0 + row;
-            if constexpr (HA || S2H) {
-                // MMA row -> (output row within the tile, padded column); the
-                // S-1 right-most padded columns and rows past the tile are discarded
+            // halo modes: MMA row r of the unit -> (output row within the tile,
+            // padded column); the S-1 right-most padded columns and rows past the
+            // tile are discarded (m = M)
+            auto halo_m = [&](int r) {
                 const int rt = m_blk * CG + (int)rank;
                 const int n = p.fd_tpi.div(rt);
-                const int pl = p.fd_Wp.div(row), qq = row - pl * p.Wp;
+                const int pl = p.fd_Wp.div(r), qq = r - pl * p.Wp;
                 const int pp = (rt - n * p.tiles_per_img) * p.rpt + pl;
                 const bool ok = rt < p.m_tiles && pl < p.rpt && pp < p.P && qq < p.Q;
-                m = ok ? (n * p.P + pp) * p.Q + qq : p.M;
-            }
+                return ok ? (n * p.P + pp) * p.Q + qq : p.M;
+            };
+            if constexpr (HA || S2H) m = halo_m(row);
             {
                 const long long t0 = trace ? clock64() : 0;
                 mbar_wait_relaxed(&acc_full[b], j & 1, p.epi_wait, p.epi_wait_ns);
@@ -979,7 +993,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 continue;
             }
             if (ss_issuer) ss_issue(unit + Cfg::NBUF * tstep, j + 1);
-            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + b * BN + half * Cfg::EPI_COLS;
+            const uint32_t taddr0 = tmem_base + ((uint32_t)(quad * 32) << 16) + b * Cfg::TBW + half * Cfg::EPI_COLS;
             // TMEM -> registers, software-pipelined: the load of chunk c+1 is in
             // flight while chunk c is requantized (tcgen05.wait::ld waits for all
             // of this thread's loads, so each wait covers exactly one chunk).
@@ -1094,6 +1108,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     }
             };
             uint32_t va[Cfg::CW], vb[Cfg::CW];
+            uint32_t taddr = taddr0;
             bool emit = true;   // this warp writes the region's outputs
             if (p.splits > 1) {
                 // split-K: add this partial into the region's workspace (column-major
@@ -1133,34 +1148,40 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             } else {
                 // the MMA warp's copy of this tile's scale/shift (long done by now)
                 if (Cfg::OUTP != OUT_S32) mbar_wait(&ss_full[3 * b + j % 3], (j / 3) & 1);
-                if constexpr (BITS == 8 && NCH % 2 == 0) {
-                    // 32 columns per tcgen05.ld (two 16-byte output pieces): half
-                    // the exposed TMEM-load round trips of a 16-column loop
-                    uint32_t v32[32];
+                // MT2: the unit's two m-groups sit in TMEM columns [g*BN, (g+1)*BN)
+                for (int g = 0; g < Cfg::MT; ++g) {
+                    taddr = taddr0 + g * BN;
+                    if constexpr (Cfg::MT > 1) m = halo_m(g * BM + row);
+                    const bool last = g == Cfg::MT - 1;
+                    if constexpr (BITS == 8 && NCH % 2 == 0) {
+                        // 32 columns per tcgen05.ld (two 16-byte output pieces): half
+                        // the exposed TMEM-load round trips of a 16-column loop
+                        uint32_t v32[32];
 #pragma unroll
-                    for (int c = 0; c < NCH; c += 2) {
-                        tmem_ld_issue<32>(taddr + c * Cfg::CW, v32);
-                        tmem_ld_wait_regs(v32);
-                        if (c + 2 >= NCH) release_acc();
-                        process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c, std::true_type{});
-                        process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[16]), c + 1, std::true_type{});
-                    }
-                } else {
-                    tmem_ld_issue<Cfg::CW>(taddr, va);
-                    tmem_ld_wait_regs(va);
+                        for (int c = 0; c < NCH; c += 2) {
+                            tmem_ld_issue<32>(taddr + c * Cfg::CW, v32);
+                            tmem_ld_wait_regs(v32);
+                            if (last && c + 2 >= NCH) release_acc();
+                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c, std::true_type{});
+                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[16]), c + 1, std::true_type{});
+                        }
+                    } else {
+                        tmem_ld_issue<Cfg::CW>(taddr, va);
+                        tmem_ld_wait_regs(va);
 #pragma unroll
-                    for (int c = 0; c < NCH; c += 2) {
-                        const bool more1 = c + 1 < NCH;
-                        if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
-                        else release_acc();   // every column of this warp is in registers
-                        process(va, c, std::true_type{});
-                        if (more1) {
-                            tmem_ld_wait_regs(vb);
-                            const bool more2 = c + 2 < NCH;
-                            if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
-                            else release_acc();
-                            process(vb, c + 1, std::true_type{});
-                            if (more2) tmem_ld_wait_regs(va);
+                        for (int c = 0; c < NCH; c += 2) {
+                            const bool more1 = c + 1 < NCH;
+                            if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
+                            else if (last) release_acc();   // every column of this warp is in registers
+                            process(va, c, std::true_type{});
+                            if (more1) {
+                                tmem_ld_wait_regs(vb);
+                                const bool more2 = c + 2 < NCH;
+                                if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
+                                else if (last) release_acc();
+                                process(vb, c + 1, std::true_type{});
+                                if (more2) tmem_ld_wait_regs(va);
+                            }
                         }
                     }
                 }

@@ -116,7 +116,7 @@ static std::string cand_name(const conv_q_plan_s *p, int i) {
     if (p->cands[i].split > 1) snprintf(k, sizeof k, "_k%d", p->cands[i].split);
     snprintf(b, sizeof b, "bm%d_bn%d_kc%dx%d_c%d%s%s%s", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
              p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "", p->cands[i].halo ? "_h" : "", k);
-    if (p->cands[i].ws) return std::string(b) + "_w";
+    if (p->cands[i].ws) return std::string(b) + "_w" + ((p->cands[i].halo & 8) ? "_m2" : "");
     return b;
 }
 
@@ -241,6 +241,14 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                                 cand.halo = 1;
                                 if (cand_fits<8>(cand)) p->cands.push_back(cand);
                             }
+                            // MT2 (one CTA, two m-groups per accumulator round trip)
+                            const int rows2 = (int)ceil_div(2 * BM + (p->R - 1) * Wp + p->S - 1, Wp);
+                            if (cg == 1 && (int64_t)rows2 * Wp * kch <= 32768 && rows2 <= 256) {
+                                Cand cand{bn, kch, 1, 1, direct};
+                                cand.ws = 1;
+                                cand.halo = 1 | 8;
+                                if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                            }
                         }
                     }
     }
@@ -260,6 +268,14 @@ static void enumerate_s2d_halo(conv_q_plan_s *p) {
         Cand c{64, 64, cg, 1, 1};
         c.ws = 1;
         c.halo = 4;
+        if (cand_fits<8>(c)) p->cands.push_back(c);
+    }
+    // MT2: two 128-row m-groups per accumulator round trip (box <= 32 KB)
+    const int rows2 = (int)ceil_div(2 * BM + (p->R - 1) * Wp + 3, Wp);
+    if ((int64_t)rows2 * Wp * 16 <= 32768 && ceil_div(p->K, 64) <= sms) {
+        Cand c{64, 64, 1, 1, 1};
+        c.ws = 1;
+        c.halo = 4 | 8;
         if (cand_fits<8>(c)) p->cands.push_back(c);
     }
 }
@@ -537,12 +553,13 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
     // A (halo mode): tiled 4-D box {KCH bytes, Wp, halo rows, 1} of the
     // padded input starting at (w, h) = (-pad, p0-pad): the duplicate-free
     // "genuine" data of PAPER.md section 3.1; OOB (padding) is zero-filled.
-    if (c.halo == 4) {
+    const int mt = (c.halo & 8) ? 2 : 1;   // MT2: the box covers two 128-row m-groups
+    if (c.halo & 4) {
         // A (s2d window halo): tiled box {16 B, Wp stored pixels, halo rows, 1}
         // of the stored s2d tensor [N][H2][Wp][16 B] at (0, 0, p0 - PL, n); rows
         // outside [0, H2) are zero-filled, columns are in bounds by construction
         const int Wp = p->xs_W;
-        const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + 3, Wp);
+        const int halo_rows = (int)ceil_div(mt * BM + (p->R - 1) * Wp + 3, Wp);
         cuuint64_t dims[4] = {16, (cuuint64_t)Wp, (cuuint64_t)p->H, (cuuint64_t)p->N};
         cuuint64_t strides[3] = {16, (cuuint64_t)16 * Wp, (cuuint64_t)16 * Wp * p->H};
         cuuint32_t box[4] = {16, (cuuint32_t)Wp, (cuuint32_t)halo_rows, 1};
@@ -553,7 +570,7 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
         if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(x s2d halo) failed: %d", (int)r);
     } else if (c.halo) {
         const int Wp = p->W + 2 * p->pad;
-        const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
+        const int halo_rows = (int)ceil_div(mt * BM + (p->R - 1) * Wp + p->S - 1, Wp);
         cuuint64_t dims[4] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->W, (cuuint64_t)p->H, (cuuint64_t)p->N};
         cuuint64_t strides[3] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->row_bytes * p->W,
                                  (cuuint64_t)p->row_bytes * p->W * p->H};

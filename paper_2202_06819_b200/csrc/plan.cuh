@@ -56,7 +56,8 @@ struct Cand {
     X(64, 128, 2, 0, 1) X(128, 128, 2, 0, 1) X(256, 128, 2, 0, 1)                             \
     X(64, 64, 1, 0, 2) X(128, 64, 1, 0, 2) X(256, 64, 1, 0, 2)                                \
     X(64, 128, 1, 0, 2) X(128, 128, 1, 0, 2) X(256, 128, 1, 0, 2)                             \
-    X(64, 64, 1, 4, 1) X(64, 64, 1, 4, 2)
+    X(64, 64, 1, 4, 1) X(64, 64, 1, 4, 2)                                                      \
+    X(64, 64, 1, 9, 1) X(64, 64, 1, 12, 1)
 
 }  // namespace convq
 
@@ -164,10 +165,11 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.n_tiles = (int)ceil_div(p->K, BN);
     prm.num_tiles = (int)(ceil_div(p->M, BM * CG) * prm.n_tiles);
     prm.Wp = p->s2d ? p->xs_W : p->W + 2 * p->pad;   // MMA-row pitch of an output row (halo modes)
-    prm.rpt = std::max(1, std::min(p->P, BM / prm.Wp));
+    constexpr int MTV = (HALO & 8) ? 2 : 1;   // MT2: a unit = two 128-row m-groups
+    prm.rpt = std::max(1, std::min(p->P, MTV * BM / prm.Wp));
     prm.tiles_per_img = (int)ceil_div(p->P, prm.rpt);
     prm.m_tiles = p->N * prm.tiles_per_img;
-    const int halo_rows = (int)ceil_div(BM + (p->R - 1) * prm.Wp + ((HALO & 4) ? 3 : p->S - 1), prm.Wp);
+    const int halo_rows = (int)ceil_div(MTV * BM + (p->R - 1) * prm.Wp + ((HALO & 4) ? 3 : p->S - 1), prm.Wp);
     prm.halo_tx = halo_rows * prm.Wp * ((HALO & 4) ? 16 : Cfg::LOAD_ROW);   // S2H box: whole 16-byte s2d pixels
     if (HALO & 5) prm.num_tiles = (int)(ceil_div(prm.m_tiles, CG) * prm.n_tiles);
     prm.splits = HALO ? 1 : p->cands[p->sel].split;
