@@ -233,7 +233,7 @@ struct ConvCfg {
     static constexpr bool FITS = STAGES >= 2 && (!HB || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
                                  (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
                                  (!S2H || (WS && !HA && KCH == 64)) &&
-                                 (MT == 1 || (WS && HB && CG == 1));  // else never instantiated
+                                 (MT == 1 || (WS && HB));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
     static_assert(NSUB >= 1 && NSUB <= 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");

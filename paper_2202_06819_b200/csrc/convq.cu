@@ -243,8 +243,8 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                             }
                             // MT2 (one CTA, two m-groups per accumulator round trip)
                             const int rows2 = (int)ceil_div(2 * BM + (p->R - 1) * Wp + p->S - 1, Wp);
-                            if (cg == 1 && (int64_t)rows2 * Wp * kch <= 32768 && rows2 <= 256) {
-                                Cand cand{bn, kch, 1, 1, direct};
+                            if ((int64_t)rows2 * Wp * kch <= 32768 && rows2 <= 256) {
+                                Cand cand{bn, kch, cg, 1, direct};
                                 cand.ws = 1;
                                 cand.halo = 1 | 8;
                                 if (cand_fits<8>(cand)) p->cands.push_back(cand);
@@ -272,12 +272,14 @@ static void enumerate_s2d_halo(conv_q_plan_s *p) {
     }
     // MT2: two 128-row m-groups per accumulator round trip (box <= 32 KB)
     const int rows2 = (int)ceil_div(2 * BM + (p->R - 1) * Wp + 3, Wp);
-    if ((int64_t)rows2 * Wp * 16 <= 32768 && ceil_div(p->K, 64) <= sms) {
-        Cand c{64, 64, 1, 1, 1};
-        c.ws = 1;
-        c.halo = 4 | 8;
-        if (cand_fits<8>(c)) p->cands.push_back(c);
-    }
+    if ((int64_t)rows2 * Wp * 16 <= 32768)
+        for (int cg : {1, 2}) {
+            if (ceil_div(p->K, 64) > sms / cg) continue;
+            Cand c{64, 64, cg, 1, 1};
+            c.ws = 1;
+            c.halo = 4 | 8;
+            if (cand_fits<8>(c)) p->cands.push_back(c);
+        }
 }
 
 static int default_candidate(const conv_q_plan_s *p) {

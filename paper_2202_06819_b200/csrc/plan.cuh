@@ -57,7 +57,7 @@ struct Cand {
     X(64, 64, 1, 0, 2) X(128, 64, 1, 0, 2) X(256, 64, 1, 0, 2)                                \
     X(64, 128, 1, 0, 2) X(128, 128, 1, 0, 2) X(256, 128, 1, 0, 2)                             \
     X(64, 64, 1, 4, 1) X(64, 64, 1, 4, 2)                                                      \
-    X(64, 64, 1, 9, 1) X(64, 64, 1, 12, 1)
+    X(64, 64, 1, 9, 1) X(64, 64, 1, 12, 1) X(64, 64, 1, 9, 2) X(64, 64, 1, 12, 2)
 
 }  // namespace convq
 
