@@ -583,7 +583,7 @@ def run_reference(args):
     value = imgs / dt
     line = {"impl": "reference", "metric": metric_name(args.workload), "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": f"int{bits}",
             "data": "synthetic", "config": {"workload": args.workload, "description": desc, "per_gpu_batch": B,
                                             "bits": bits},
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": nthreads, "kind": "oracle",
