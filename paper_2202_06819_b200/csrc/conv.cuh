@@ -50,8 +50,7 @@ constexpr int BM = 128;
 #endif
 constexpr bool kMma1T = CONVQ_MMA_1T != 0;
 // Two MMA-issuing warps taking alternate tiles (CONVQ_DUAL_MMA=1; OFF by default:
-// parity-green on every test shape and 1.7x faster per tile on l1.b0.c2, but
-// l1.b1.c1 bm128_bn64_kc128x2_c1 at N=256 faults/hangs -- an unresolved race): a
+// parity-green, but the ResNet-50 step measured no faster -- 1.40 vs 1.34-1.38 ms): a
 // warp's per-tile control path (barrier waits, fences, commits: ~650-700 cycles,
 // profiles/r01_timeline_cta0.txt) then overlaps the other warp's MMA execution
 // instead of adding to it.  Tile t: warp t % 2, TMEM buffer t % NBUF, smem
@@ -435,9 +434,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint64_t *bfull = hempty;               // WS (no separate halo buffers): resident weights loaded
     uint64_t *ss_full = hempty + 4;         // scale/shift bulk copy -> epilogue [NBUF][3 slots]
     uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(ss_full + 12);
-    // dual MMA warps: the last global smem-stage index each has waited for (a
-    // parity wait is only valid once the stage's previous fill has completed)
-    volatile int *mma_prog = reinterpret_cast<volatile int *>(tmem_holder + 1);
+    // dual MMA warps: per smem stage, the last global stage index whose fill an
+    // MMA warp has waited for.  A parity wait on a stage is only valid once the
+    // stage's PREVIOUS fill has completed -- and TMA fills of different stages
+    // can complete out of order, so this is tracked per stage.
+    volatile int *stage_done = reinterpret_cast<volatile int *>(tmem_holder + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             mbar_init(&acc_empty[b], 4 * Cfg::EPI_PER_BUF * CG);
             for (int k = 0; k < 3; ++k) mbar_init(&ss_full[3 * b + k], 1);
         }
-        mma_prog[0] = mma_prog[1] = -1;
+        for (int i = 0; i < STAGES; ++i) stage_done[i] = -1;
         fence_mbar_init();
     }
     if (warp == Cfg::MMA_WARP) {
@@ -672,15 +673,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             uint32_t phase = 0;
             int hcount = 0;
             int gsi = 0;   // global index of the current smem stage
-            // before a parity wait on stage gsi: its previous fill (gsi - STAGES)
-            // must be complete, i.e. some MMA warp has already waited past it
+            // before a parity wait on stage gsi: the stage's previous fill (gsi - STAGES)
+            // must be complete, i.e. its consumer has already waited past it
             auto mma_gate = [&]() {
                 if (nmma > 1)
-                    while ((mma_prog[0] > mma_prog[1] ? mma_prog[0] : mma_prog[1]) < gsi - STAGES) {
+                    while (stage_done[stage] < gsi - STAGES) {
                     }
             };
             auto mma_mark = [&]() {
-                if (nmma > 1 && lane == 0) mma_prog[mw] = gsi;
+                if (nmma > 1 && lane == 0) stage_done[stage] = gsi;
             };
             for (int unit = tile0 + mw * tstep, local = mw; unit < p.num_units; unit += nmma * tstep, local += nmma) {
                 int tile, kb_lo, kb_hi;

@@ -1,15 +1,6 @@
-# dual-MMA race hunt: every candidate of l1.b1.c1 at N=256 and a few N for the first failing one
+# dual-MMA build: the previously failing configs at N=256, full parity suite, then the bench
 export CONV_Q_LIB=$PWD/paper_2202_06819_b200/libconvq_dual.so
-python - <<'PY'
-import subprocess, sys
-sys.path.insert(0, ".")
-import paper_2202_06819_b200 as cq
-p = cq.ConvPlan(256, 56, 56, 256, 64, 1, 1, 1, 0, 8, relu=True)
-for c in p.candidates():
-    r = subprocess.run([sys.executable, "scripts/check_cfg.py", "l1.b1.c1", c, "256"], capture_output=True, text=True, timeout=None) if False else None
-    try:
-        r = subprocess.run([sys.executable, "scripts/check_cfg.py", "l1.b1.c1", c, "256"], capture_output=True, text=True, timeout=40)
-        print(c, r.stdout.strip().splitlines()[-1] if r.stdout.strip() else ("rc=%d " % r.returncode) + r.stderr.strip().splitlines()[-1][:100], flush=True)
-    except subprocess.TimeoutExpired:
-        print(c, "HANG (40 s)", flush=True)
-PY
+for c in bm128_bn64_kc128x2_c1 bm128_bn64_kc128x2_c1_w; do for i in 1 2 3; do timeout 60 python scripts/check_cfg.py l1.b1.c1 $c 256 2>&1 | tail -1; done; done
+timeout 60 python scripts/check_cfg.py l2.b0.c1 bm128_bn64_kc128x2_c1_w 256 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 900 python bench.py --no-cpu-baseline --no-k7 --layers-out gpurun_out/layers_dual.json > gpurun_out/bench_dual.json 2> gpurun_out/bench_dual.err; echo bench=$?; head -c 300 gpurun_out/bench_dual.json
