@@ -174,14 +174,15 @@ struct ConvCfg {
     static constexpr int LOAD_ROW = KCH * BITS / 8;        // packed bytes per row per k-block
     static constexpr int A_SUB = HB ? HBOX : BM * KCH;      // s8 A sub-tile bytes (one k-block / WS halo box)
     static constexpr int B_SUB = WS ? 0 : BNL * KCH;
-    static constexpr int A_S8 = NSUB * A_SUB;               // per stage
+    static constexpr int AMT = HB ? 1 : MT;                 // A sub-tiles per k-block (generic MT2: one per m-group)
+    static constexpr int A_S8 = NSUB * AMT * A_SUB;         // per stage
     static constexpr int B_S8 = NSUB * B_SUB;
     static constexpr int A_PK_SUB = BITS == 4 ? BM * LOAD_ROW : 0;
     static constexpr int B_PK_SUB = BITS == 4 ? BNL * LOAD_ROW : 0;
     static constexpr int A_PK = NSUB * A_PK_SUB;
     static constexpr int B_PK = NSUB * B_PK_SUB;
     static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
-    static constexpr int SUB_TX = ((HB ? 0 : BM) + (WS ? 0 : BNL)) * LOAD_ROW;  // TMA bytes per k-block per CTA
+    static constexpr int SUB_TX = ((HB ? 0 : AMT * BM) + (WS ? 0 : BNL)) * LOAD_ROW;  // TMA bytes per k-block per CTA
     static constexpr int HALO_BYTES = HA && !WS ? 32768 : 0;  // one halo buffer (budget; checked at plan time)
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUTP = OUT & 3;                     // output path
@@ -232,7 +233,7 @@ struct ConvCfg {
     static constexpr bool FITS = STAGES >= 2 && (!HB || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
                                  (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
                                  (!S2H || (WS && !HA && KCH == 64)) &&
-                                 (MT == 1 || (WS && HB));  // else never instantiated
+                                 (MT == 1 || (WS && HB) || (WS && BITS == 8 && CG == 1 && OUTP != OUT_TMA));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
     static_assert(NSUB >= 1 && NSUB <= 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
@@ -595,10 +596,18 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             int tile, kb_lo, kb_hi;
             unit_range(p, unit, tile, kb_lo, kb_hi);
             const int m_blk = p.fd_ntiles.div(tile), n_blk = tile - m_blk * p.n_tiles;
-            const int m0 = m_blk * (BM * CG) + (int)rank * BM;   // this CTA's first output pixel
-            const int n0 = p.fd_PQ.div(m0), rem = m0 - n0 * PQ;
-            const int p0 = p.fd_Q.div(rem), q0 = rem - p0 * p.Q;
-            const int h0 = p0 * p.stride - p.pad, w0 = q0 * p.stride - p.pad_w;
+            const int m0 = m_blk * (BM * CG * Cfg::AMT) + (int)rank * BM;   // this CTA's first output pixel
+            // MT2: m-group g starts at row m0 + 128 g (its own im2col origin)
+            int n0g[Cfg::AMT], h0g[Cfg::AMT], w0g[Cfg::AMT];
+#pragma unroll
+            for (int g = 0; g < Cfg::AMT; ++g) {
+                const int mg = m0 + g * BM;
+                const int n0 = p.fd_PQ.div(mg), rem = mg - n0 * PQ;
+                const int p0 = p.fd_Q.div(rem), q0 = rem - p0 * p.Q;
+                n0g[g] = n0;
+                h0g[g] = p0 * p.stride - p.pad;
+                w0g[g] = q0 * p.stride - p.pad_w;
+            }
             const int brow = n_blk * BN + (int)rank * Cfg::BNL;  // this CTA's B rows
             const int nk = kb_hi - kb_lo;
             // optional rotated k-block order (CTA c starts at k-block 7c mod nk; any
@@ -626,13 +635,16 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     k += kb_lo;
                     const int tap = p.fd_cblk.div(k), cblk = k - tap * p.num_cblk;
                     const int r = p.fd_S.div(tap), s = tap - r * p.S;
-                    uint8_t *ad = a_dst + stage * A_LD + lane * A_LD_SUB;
                     uint8_t *bd = b_dst + stage * B_LD + lane * B_LD_SUB;
-                    if (p.a_gemm)
-                        tma_load_2d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, m0, pol_a);
-                    else
-                        tma_load_im2col_4d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0, h0, n0, (uint16_t)s,
-                                           (uint16_t)r, pol_a);
+#pragma unroll
+                    for (int g = 0; g < Cfg::AMT; ++g) {
+                        uint8_t *ad = a_dst + stage * A_LD + (lane * Cfg::AMT + g) * A_LD_SUB;
+                        if (p.a_gemm)
+                            tma_load_2d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, m0 + g * BM, pol_a);
+                        else
+                            tma_load_im2col_4d(ad, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, w0g[g], h0g[g], n0g[g],
+                                               (uint16_t)s, (uint16_t)r, pol_a);
+                    }
                     if (!WS) tma_load_2d(bd, &tm_b, &full[stage], tap * p.row_bytes + cblk * Cfg::LOAD_ROW, brow, pol_b);
                 }
                 __syncwarp();
@@ -858,14 +870,17 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 #pragma unroll
                             for (int j = 0; j < NSUB; ++j) {
                                 if (j < nsub) {
-                                    const uint64_t ad = ad0 + (uint64_t)((j * Cfg::A_SUB) >> 4);
                                     const uint64_t bd = WS ? b_desc_res + (uint64_t)(((kb + j) * Cfg::B_TILE) >> 4)
                                                            : bd0 + (uint64_t)((j * Cfg::B_SUB) >> 4);
 #pragma unroll
-                                    for (int k = 0; k < KCH / 32; ++k) {
-                                        const uint32_t acc = (kb - kb_lo + j + k) != 0;
-                                        if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
-                                        else mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
+                                    for (int g = 0; g < Cfg::AMT; ++g) {   // MT2: m-group g -> TMEM columns g*BN
+                                        const uint64_t ad = ad0 + (uint64_t)(((j * Cfg::AMT + g) * Cfg::A_SUB) >> 4);
+#pragma unroll
+                                        for (int k = 0; k < KCH / 32; ++k) {
+                                            const uint32_t acc = (kb - kb_lo + j + k) != 0;
+                                            if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
+                                            else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
+                                        }
                                     }
                                 }
                             }
@@ -961,7 +976,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         for (int unit = tile0 + b * tstep; unit < p.num_units; unit += Cfg::NBUF * tstep, ++j) {
             const int tile = p.splits == 1 ? unit : p.fd_splits.div(unit);
             const int m_blk = p.fd_ntiles.div(tile), n_blk = tile - m_blk * p.n_tiles;
-            const int mrow0 = m_blk * (BM * CG) + (int)rank * BM;
+            const int mrow0 = m_blk * (BM * CG * Cfg::AMT) + (int)rank * BM;
             int m = mrow0 + row;
             // halo modes: MMA row r of the unit -> (output row within the tile,
             // padded column); the S-1 right-most padded columns and rows past the
@@ -1152,7 +1167,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 // MT2: the unit's two m-groups sit in TMEM columns [g*BN, (g+1)*BN)
                 for (int g = 0; g < Cfg::MT; ++g) {
                     taddr = taddr0 + g * BN;
-                    if constexpr (Cfg::MT > 1) m = halo_m(g * BM + row);
+                    if constexpr (Cfg::MT > 1) m = (HA || S2H) ? halo_m(g * BM + row) : mrow0 + g * BM + row;
                     const bool last = g == Cfg::MT - 1;
                     if constexpr (BITS == 8 && NCH % 2 == 0) {
                         // 32 columns per tcgen05.ld (two 16-byte output pieces): half

@@ -115,7 +115,7 @@ static std::string cand_name(const conv_q_plan_s *p, int i) {
     char k[16] = "";
     if (p->cands[i].split > 1) snprintf(k, sizeof k, "_k%d", p->cands[i].split);
     snprintf(b, sizeof b, "bm%d_bn%d_kc%dx%d_c%d%s%s%s", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
-             p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "", p->cands[i].halo ? "_h" : "", k);
+             p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "", (p->cands[i].halo & 5) ? "_h" : "", k);
     if (p->cands[i].ws) return std::string(b) + "_w" + ((p->cands[i].halo & 8) ? "_m2" : "");
     return b;
 }
@@ -231,6 +231,12 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                         for (int nsub : {1, 2}) {
                             Cand cand{bn, kch, cg, nsub, direct};
                             cand.ws = 1;
+                            if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                        }
+                        if (direct && cg == 1 && bn <= 128) {   // MT2: two 128-row m-groups per unit
+                            Cand cand{bn, kch, 1, 1, 1};
+                            cand.ws = 1;
+                            cand.halo = 8;
                             if (cand_fits<8>(cand)) p->cands.push_back(cand);
                         }
                         if (p->stride == 1 && p->R == 3 && p->S == 3 && Wp <= BM && direct) {
@@ -570,7 +576,7 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(x s2d halo) failed: %d", (int)r);
-    } else if (c.halo) {
+    } else if (c.halo & 1) {
         const int Wp = p->W + 2 * p->pad;
         const int halo_rows = (int)ceil_div(mt * BM + (p->R - 1) * Wp + p->S - 1, Wp);
         cuuint64_t dims[4] = {(cuuint64_t)p->row_bytes, (cuuint64_t)p->W, (cuuint64_t)p->H, (cuuint64_t)p->N};

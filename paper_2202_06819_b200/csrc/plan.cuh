@@ -57,7 +57,8 @@ struct Cand {
     X(64, 64, 1, 0, 2) X(128, 64, 1, 0, 2) X(256, 64, 1, 0, 2)                                \
     X(64, 128, 1, 0, 2) X(128, 128, 1, 0, 2) X(256, 128, 1, 0, 2)                             \
     X(64, 64, 1, 4, 1) X(64, 64, 1, 4, 2)                                                      \
-    X(64, 64, 1, 9, 1) X(64, 64, 1, 12, 1) X(64, 64, 1, 9, 2) X(64, 64, 1, 12, 2)
+    X(64, 64, 1, 9, 1) X(64, 64, 1, 12, 1) X(64, 64, 1, 9, 2) X(64, 64, 1, 12, 2)                 \
+    X(64, 64, 1, 8, 1) X(64, 128, 1, 8, 1) X(128, 64, 1, 8, 1) X(128, 128, 1, 8, 1)
 
 }  // namespace convq
 
@@ -163,7 +164,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.num_cblk = p->C / KCH;
     prm.num_kb = p->R * p->S * prm.num_cblk;
     prm.n_tiles = (int)ceil_div(p->K, BN);
-    prm.num_tiles = (int)(ceil_div(p->M, BM * CG) * prm.n_tiles);
+    prm.num_tiles = (int)(ceil_div(p->M, BM * CG * ((HALO & 5) ? 1 : ((HALO & 8) ? 2 : 1))) * prm.n_tiles);   // generic MT2: 256-row units
     prm.Wp = p->s2d ? p->xs_W : p->W + 2 * p->pad;   // MMA-row pitch of an output row (halo modes)
     constexpr int MTV = (HALO & 8) ? 2 : 1;   // MT2: a unit = two 128-row m-groups
     prm.rpt = std::max(1, std::min(p->P, MTV * BM / prm.Wp));
