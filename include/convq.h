@@ -165,7 +165,9 @@ CONVQ_API int conv_q_plan_set_epilogue(conv_q_plan_t *plan, int relu, int out_mo
  * Name = bm<MMA rows>_bn<N tile>_kc<channels per k-block>x<k-blocks per stage>
  *        _c<CTAs per tile (2 = cta_group::2 pair)>[_st: direct 16-byte stores,
  *        else smem staging + TMA store][_h: duplicate-aware halo A operand]
- *        [_k<s>: split-K over s work units]. */
+ *        [_k<s>: split-K over s work units][_w: weight-stationary (the CTA's
+ *        weight block resident in shared memory)][_m2: a work unit is two
+ *        128-row m-groups sharing one accumulator round trip]. */
 CONVQ_API int conv_q_plan_num_candidates(const conv_q_plan_t *plan);
 CONVQ_API int conv_q_plan_candidate_name(const conv_q_plan_t *plan, int index, char *buf, int buflen);
 CONVQ_API int conv_q_plan_set_config(conv_q_plan_t *plan, int index);
