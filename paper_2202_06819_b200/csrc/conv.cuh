@@ -233,7 +233,7 @@ struct ConvCfg {
     static constexpr bool FITS = STAGES >= 2 && (!HB || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
                                  (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
                                  (!S2H || (WS && !HA && KCH == 64)) &&
-                                 (MT == 1 || (WS && HB) || (WS && BITS == 8 && CG == 1 && OUTP != OUT_TMA));  // else never instantiated
+                                 (MT == 1 || (WS && HB) || (WS && BITS == 8 && CG == 1));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
     static_assert(NSUB >= 1 && NSUB <= 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
@@ -1126,6 +1126,23 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             uint32_t va[Cfg::CW], vb[Cfg::CW];
             uint32_t taddr = taddr0;
             bool emit = true;   // this warp writes the region's outputs
+            // TMA store of this warp's staged slab (m-group g's 32 rows)
+            auto store_slab = [&](int g) {
+                if (Cfg::OUTP == OUT_TMA && emit) {
+                    fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
+                    __syncwarp();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int s = 0; s < Cfg::EPI_NSUB; ++s) {
+                            const int c0 = n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + s * Cfg::EPI_SUBW;
+                            const int c1 = mrow0 + g * BM + quad * 32;
+                            if (p.out_policy) tma_store_2d_hint(&tm_y, slab + s * (32 * Cfg::EPI_SUBW), c0, c1, out_pol);
+                            else tma_store_2d(&tm_y, slab + s * (32 * Cfg::EPI_SUBW), c0, c1);
+                        }
+                        tma_store_commit();
+                    }
+                }
+            };
             if (p.splits > 1) {
                 // split-K: add this partial into the region's workspace (column-major
                 // [col][32 rows], so each red instruction covers 128 contiguous bytes);
@@ -1200,21 +1217,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             }
                         }
                     }
+                    if constexpr (Cfg::MT > 1) store_slab(g);   // the slab is reused by the next group
                 }
             }
-            if (Cfg::OUTP == OUT_TMA && emit) {
-                fence_proxy_async_smem();  // st.shared -> visible to the TMA (async proxy)
-                __syncwarp();
-                if (lane == 0) {
-#pragma unroll
-                    for (int s = 0; s < Cfg::EPI_NSUB; ++s) {
-                        const int c0 = n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + s * Cfg::EPI_SUBW, c1 = mrow0 + quad * 32;
-                        if (p.out_policy) tma_store_2d_hint(&tm_y, slab + s * (32 * Cfg::EPI_SUBW), c0, c1, out_pol);
-                        else tma_store_2d(&tm_y, slab + s * (32 * Cfg::EPI_SUBW), c0, c1);
-                    }
-                    tma_store_commit();
-                }
-            }
+            if constexpr (Cfg::MT == 1) store_slab(0);
             CONVQ_TL(24 + warp, j);
         }
         if (Cfg::OUTP == OUT_TMA && lane == 0) tma_store_wait0();

@@ -233,8 +233,8 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                             cand.ws = 1;
                             if (cand_fits<8>(cand)) p->cands.push_back(cand);
                         }
-                        if (direct && cg == 1 && bn <= 128) {   // MT2: two 128-row m-groups per unit
-                            Cand cand{bn, kch, 1, 1, 1};
+                        if (cg == 1 && bn <= 128) {   // MT2: two 128-row m-groups per unit
+                            Cand cand{bn, kch, 1, 1, direct};
                             cand.ws = 1;
                             cand.halo = 8;
                             if (cand_fits<8>(cand)) p->cands.push_back(cand);
@@ -648,7 +648,7 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
     if (p->out_mode == CONV_Q_OUT_PACKED && !c.direct) {
         // one box = one epilogue warp's 32-row slab (or a 128-byte column block of it)
         const int num_epi = epi_warpgroups(p->bits);
-        const int nbuf = tmem_buffers(p->bits, c.bn);
+        const int nbuf = tmem_buffers(p->bits, ((c.halo & 8) ? 2 : 1) * c.bn);   // the kernel's rule (MT2: 2*BN TMEM columns per buffer)
         const int epb = num_epi / nbuf;
         const int epi_row = c.bn / epb * p->bits / 8;
         const int subw = epi_row < 128 ? epi_row : 128;
