@@ -70,6 +70,8 @@ def _load():
         lib.oracle_conv_q.restype = i32
         lib.oracle_conv_q.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, i64, i64, i32,
                                       vp, i32, vp, i64, vp, i32]
+        lib.oracle_maxpool.restype = i32
+        lib.oracle_maxpool.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, i32, vp, i32]
         _lib = lib
     return _lib
 
@@ -191,6 +193,7 @@ def requant(acc: np.ndarray, scale_shift: np.ndarray, relu: bool, bits: int,
     K = acc.shape[-1]
     ss = np.ascontiguousarray(scale_shift, dtype=np.float32)
     assert ss.size == 2 * K
+    assert K <= 8192, "oracle_requant packs one row in an 8192-code buffer"
     M = acc.size // K
     out = np.empty((M, K * bits // 8), dtype=np.uint8)
     _load().oracle_requant(_ptr(acc), M, K, _ptr(ss), int(bool(relu)), bits, _ptr(out),
@@ -204,3 +207,19 @@ def conv_q(x: np.ndarray, w: np.ndarray, C: int, stride: int, pad: int, bits: in
     """One whole layer: conv_s32 -> requant -> pack."""
     acc = conv_s32(x, w, C, stride, pad, bits, pix=pix, nthreads=nthreads)
     return requant(acc, scale_shift, relu, bits, nthreads=nthreads)
+
+
+def maxpool(x: np.ndarray, C: int, R: int, stride: int, pad: int, bits: int,
+            nthreads: int | None = None) -> np.ndarray:
+    """R x R max pooling of packed NHWC codes, padding never wins (the ResNet
+    stem's 3x3/2 pool; section 1)."""
+    x = np.ascontiguousarray(x, dtype=np.uint8)
+    N, H, W, nb = x.shape
+    assert nb == C * bits // 8 and C <= 4096
+    P, Q = out_dim(H, R, stride, pad), out_dim(W, R, stride, pad)
+    y = np.empty((N, P, Q, nb), dtype=np.uint8)
+    rc = _load().oracle_maxpool(_ptr(x), N, H, W, C, R, stride, pad, bits, _ptr(y),
+                                nthreads or default_threads())
+    if rc != 0:
+        raise ValueError("oracle_maxpool: a window has no in-range tap")
+    return y

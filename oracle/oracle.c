@@ -27,7 +27,12 @@
  *                          explicit GEMM for 1x1, all-ones tap counts
  *                          (SPEC.md:76 -> 4C/6C/9C), identity 1x1, zero in
  *   oracle_requant_value   pinned: closed forms (scale 1 -> saturating cast,
- *                          scale 0.5 ties -> even, ReLU, 2^-k shifts)
+ *                          scale 0.5 ties -> even, ReLU, 2^-k shifts) and
+ *                          40 000 adversarial near-tie (acc, scale, shift)
+ *                          triples vs an exact-rational single-rounding
+ *                          evaluation (separates fmaf from mul-then-add)
+ *   oracle_maxpool         pinned: torch max_pool2d (float64, library) on the
+ *                          unpacked codes; all-equal / one-hot windows
  */
 #include <math.h>
 #include <stdint.h>
@@ -275,4 +280,45 @@ ORACLE_API int oracle_conv_q(const uint8_t *x, const uint8_t *w,
     oracle_requant(acc, M, K, scale_shift, relu, bits, y, nthreads);
     free(acc);
     return rc;
+}
+
+/* ------------------------------------------------------------------------
+ * Max pooling over packed codes (the pooling glue between the stem conv and
+ * layer1 of ResNet; section 1 evaluates
+ * "ResNet-18 and ResNet-50", whose stem is conv1 -> 3x3/2 max pool).
+ *   y[n,p,q,c] = max over the in-range taps (r,s) of x[n, p*st-pad+r, q*st-pad+s, c]
+ * Out-of-range taps are skipped (the padding never wins; torch semantics).
+ * Quantization is monotone, so the max of the codes is the code of the max.
+ * Output spatial size: floor form (reading 6).  Returns -1 if some window has
+ * no in-range tap (not possible for pad < R), else 0.
+ * ---------------------------------------------------------------------- */
+ORACLE_API int oracle_maxpool(const uint8_t *x, int64_t N, int64_t H, int64_t W, int64_t C,
+                              int64_t R, int64_t stride, int64_t pad, int bits,
+                              uint8_t *y, int nthreads)
+{
+    int64_t P = oracle_out_dim(H, R, stride, pad);
+    int64_t Q = oracle_out_dim(W, R, stride, pad);
+    int64_t row_bytes = C * bits / 8;
+    int empty = 0;
+#pragma omp parallel for num_threads(nthreads) schedule(static) reduction(| : empty)
+    for (int64_t m = 0; m < N * P * Q; ++m) {
+        int64_t n = m / (P * Q), p = (m / Q) % P, q = m % Q;
+        int8_t best[4096], v[4096];
+        int any = 0;
+        for (int64_t r = 0; r < R; ++r) {
+            int64_t h = p * stride - pad + r;
+            if (h < 0 || h >= H) continue;
+            for (int64_t s = 0; s < R; ++s) {
+                int64_t w = q * stride - pad + s;
+                if (w < 0 || w >= W) continue;
+                oracle_unpack(x + ((n * H + h) * W + w) * row_bytes, C, bits, v);
+                for (int64_t c = 0; c < C; ++c)
+                    if (!any || v[c] > best[c]) best[c] = v[c];
+                any = 1;
+            }
+        }
+        if (!any) { empty |= 1; memset(best, 0, (size_t)C); }
+        oracle_pack(best, C, bits, y + m * row_bytes);
+    }
+    return empty ? -1 : 0;
 }

@@ -280,6 +280,39 @@ def test_requant_int_to_float_rounding():
     assert round(Fraction(acc, 1 << 25)) == -1
 
 
+@pytest.mark.parametrize("relu", [False, True])
+def test_requant_single_rounding_fma_exact(relu):
+    """Reading 5 (PAPER.md:200 s3.2.2 epilogue order): the
+    multiply-add rounds ONCE.  40 000 adversarial (acc, scale, shift) triples
+    whose exact value sits within half an ulp of a half-integer (a quarter of
+    them exact ties) are evaluated with exact rationals and one binary32
+    rounding (tests/exact_fp.py); the oracle must match every one, and the
+    set must contain cases where mul-then-add (two roundings) gives another
+    code -- so a two-rounding oracle fails this pin."""
+    import exact_fp
+    g = np.random.default_rng(2202)
+    acc, scale, shift = exact_fp.near_tie_cases(g, 40000, 8)
+    n = acc.size
+    # one case per output channel of a 1 x 8000 accumulator row (vectorised oracle calls)
+    got = np.concatenate([
+        oracle.unpack(oracle.requant(acc[i:i + 8000].astype(np.int32).reshape(1, -1),
+                                     np.concatenate([scale[i:i + 8000], shift[i:i + 8000]]), relu, 8), 8000, 8)[0]
+        for i in range(0, n, 8000)])
+    ref = np.array([exact_fp.requant_exact(int(a), float(s), float(h), relu, 8)
+                    for a, s, h in zip(acc, scale, shift)])
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, (bad[:5], acc[bad[:5]], scale[bad[:5]], shift[bad[:5]], got[bad[:5]], ref[bad[:5]])
+    two = exact_fp.requant_two_roundings(acc, scale, shift, relu, 8)
+    differ = int(np.count_nonzero(two != ref))
+    assert differ >= 500, differ                  # the pin separates fmaf from mul-then-add
+    # exact ties (float64 evaluation is exact for these short operands): round
+    # half to even decides, and every tie lands on an even code
+    f = acc.astype(np.float64) * scale.astype(np.float64) + shift.astype(np.float64)
+    ties = (np.arange(n) % 4 == 0) & (f - np.floor(f) == 0.5)
+    assert np.count_nonzero(ties) >= n // 5
+    assert np.all(ref[ties] % 2 == 0)
+
+
 def test_requant_pack_rows():
     acc = np.array([[1, -1, 200, -200, 3, 4, 5, 6]], np.int32)
     ss = np.concatenate([np.ones(8), np.zeros(8)]).astype(np.float32)
@@ -303,3 +336,35 @@ def test_accumulator_bits_paper():
     assert bits_required(8, 8, 256) == 25
     assert channels_to_saturate(32, 4, 4, 9) == 932068
     assert channels_to_saturate(16, 4, 4, 1) == 128
+
+
+# ---------------------------------------------------------------- max pool (NEXT-2 glue)
+@pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("N,H,W,C,R,st,pad", [(2, 9, 8, 64, 3, 2, 1), (1, 12, 12, 32, 3, 2, 1),
+                                               (1, 7, 5, 32, 2, 2, 0), (1, 6, 6, 64, 3, 1, 1)])
+def test_maxpool_matches_torch(bits, N, H, W, C, R, st, pad):
+    """Library cross-check: torch max_pool2d (float64, -inf padding) on the
+    unpacked codes, repacked by the (pinned) pack."""
+    g = np.random.default_rng(31 + H)
+    x = wl.random_bytes(g, (N, H, W, C * bits // 8))
+    got = oracle.maxpool(x, C, R, st, pad, bits)
+    xt = torch.from_numpy(oracle.unpack(x, C, bits).astype(np.float64)).permute(0, 3, 1, 2)
+    ref = torch.nn.functional.max_pool2d(xt, R, st, pad).permute(0, 2, 3, 1).numpy().astype(np.int8)
+    assert got.shape[:3] == ref.shape[:3]
+    assert np.array_equal(oracle.unpack(got, C, bits), ref)
+
+
+def test_maxpool_closed_forms():
+    """All-equal input -> the same code everywhere (padding never wins, even for
+    the most negative code); a single maximum reaches exactly the windows that
+    cover it."""
+    x = np.full((1, 5, 5, 32), 0x80, np.uint8)                # every code -128
+    assert np.all(oracle.maxpool(x, 32, 3, 2, 1, 8) == 0x80)
+    x = np.zeros((1, 6, 6, 32), np.uint8)
+    x[0, 3, 2, 5] = 100
+    y = oracle.unpack(oracle.maxpool(x, 32, 3, 2, 1, 8), 32, 8)
+    hit = {(p, q) for p in range(3) for q in range(3) if abs(2 * p - 3) <= 1 and abs(2 * q - 2) <= 1}
+    for p in range(3):
+        for q in range(3):
+            assert y[0, p, q, 5] == (100 if (p, q) in hit else 0)
+    assert np.all(np.delete(y, 5, axis=3) == 0)
