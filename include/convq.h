@@ -215,6 +215,19 @@ CONVQ_API int conv_q_padded_channels(int C, int bits);
 CONVQ_API int conv_q_pack_weights(const int8_t *w_krsc, int K, int R, int S, int C, int bits,
                         void *w_packed, void *stream);
 
+/*
+ * R x R max pooling of packed codes (ABI 1.02; the pooling glue of a ResNet
+ * stem: conv1 -> 3x3/2 max pool -> layer1; the networks of
+ * PAPER.md:40 section 1).  x: device packed NHWC [N][H][W][C*bits/8];
+ * y: device packed NHWC [N][P][Q][C*bits/8], P = (H+2pad-R)/stride + 1 (floor),
+ * Q likewise.  y[n,p,q,c] = max of x[n, p*stride-pad+r, q*stride-pad+s, c] over
+ * the in-range taps (padding never wins); max of signed codes, exact.
+ * Errors: EINVAL (NULL / misaligned pointer, dims < 1, pad not in [0,R),
+ * empty output), EUNSUPPORTED (C*bits not a multiple of 128), ECUDA.
+ */
+CONVQ_API int conv_q_maxpool(const void *x, int N, int H, int W, int C, int R, int stride, int pad, int bits,
+                             void *y, void *stream);
+
 /* Thread-local status code of the last failed call on this thread (0 if none). */
 CONVQ_API int conv_q_last_status(void);
 

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 
 __all__ = [
     "ConvQError", "ConvPlan", "PlanInfo", "load", "quantize", "pack_weights", "padded_channels",
-    "int8_peak", "out_dim", "OUT_PACKED", "OUT_S32", "StemPlan",
+    "int8_peak", "out_dim", "OUT_PACKED", "OUT_S32", "StemPlan", "maxpool",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -110,6 +110,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.conv_q_last_error.argtypes = []
     lib.conv_q_version.restype = i
     lib.conv_q_version.argtypes = []
+    lib.conv_q_maxpool.restype = i
+    lib.conv_q_maxpool.argtypes = [vp, i, i, i, i, i, i, i, i, vp, vp]
     lib.conv_q_int8_peak.restype = i
     lib.conv_q_int8_peak.argtypes = [i, ctypes.POINTER(ctypes.c_double)]
     _lib = lib
@@ -158,6 +160,7 @@ class ConvPlan:
         self.N, self.H, self.W, self.C, self.K = N, H, W, C, K
         self.R, self.S, self.stride, self.pad, self.bits = R, S, stride, pad, bits
         self.P, self.Q = out_dim(H, R, stride, pad), out_dim(W, S, stride, pad)
+        self._need = None
         self.set_epilogue(relu, out_mode)
 
     def __del__(self):
@@ -170,6 +173,7 @@ class ConvPlan:
     def set_epilogue(self, relu: bool, out_mode: int = OUT_PACKED):
         _check(load().conv_q_plan_set_epilogue(self._h, int(bool(relu)), out_mode))
         self.relu, self.out_mode = bool(relu), out_mode
+        self._need = None
 
     def set_stream(self, stream):
         _check(load().conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
@@ -186,6 +190,25 @@ class ConvPlan:
 
     def set_config(self, index: int):
         _check(load().conv_q_plan_set_config(self._h, index))
+
+    def _check_buffers(self, x, w, scale, y):
+        """Sizes / dtypes / contiguity of torch tensors against the plan (raw
+        integer addresses are passed through unchecked)."""
+        if self._need is None:
+            inf = self.info()
+            self._need = (inf.x_bytes, inf.w_bytes, inf.y_s32_bytes if self.out_mode == OUT_S32 else inf.y_bytes,
+                          2 * inf.K)
+        nx, nw, ny, nss = self._need
+        for name, t, n in (("x", x, nx), ("w", w, nw), ("y", y, ny)):
+            if isinstance(t, int):
+                continue
+            if not t.is_contiguous() or t.numel() * t.element_size() < n:
+                raise ConvQError(EINVAL, f"{name}: need a contiguous buffer of >= {n} bytes, got "
+                                         f"{t.numel() * t.element_size()} (contiguous={t.is_contiguous()})")
+        if not isinstance(scale, int):
+            import torch
+            if scale.dtype != torch.float32 or not scale.is_contiguous() or scale.numel() < nss:
+                raise ConvQError(EINVAL, f"scale: need {nss} contiguous float32 values (scale then shift)")
 
     def info(self) -> PlanInfo:
         inf = _Info()
@@ -215,6 +238,7 @@ class ConvPlan:
     # -- execution
     def run(self, x, w, scale, y, stream=None):
         """y <- requant(conv(x, w)) on `stream` (default: torch's current stream)."""
+        self._check_buffers(x, w, scale, y)
         lib = load()
         _check(lib.conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
         _check(lib.conv_q_run(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)),
@@ -222,6 +246,7 @@ class ConvPlan:
         return y
 
     def tune(self, x, w, scale, y, warmup=3, reps=10, stream=None) -> int:
+        self._check_buffers(x, w, scale, y)
         lib = load()
         _check(lib.conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
         return _check(lib.conv_q_plan_tune(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)),
@@ -244,6 +269,7 @@ class StemPlan(ConvPlan):
         self.N, self.H, self.W, self.C, self.K = N, H, W, C, K
         self.R, self.S, self.stride, self.pad, self.bits = R, S, 2, pad, bits
         self.P, self.Q = out_dim(H, R, 2, pad), out_dim(W, S, 2, pad)
+        self._need = None
         self.set_epilogue(relu, out_mode)
         inf = self.info()
         self.x_dims, self.w_dims = inf.x_dims, inf.w_dims
@@ -303,6 +329,20 @@ def pack_weights(w_codes, bits: int, out=None, stream=None):
         out = torch.empty((K, R, S, C * bits // 8), dtype=torch.uint8, device=w_codes.device)
     _check(load().conv_q_pack_weights(ctypes.c_void_p(w_codes.data_ptr()), K, R, S, C, bits,
                                       ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def maxpool(x, C: int, R: int, stride: int, pad: int, bits: int, out=None, stream=None):
+    """R x R max pooling of packed NHWC codes (conv_q_maxpool): uint8 [N,H,W,C*bits/8]."""
+    import torch
+    N, H, W, nb = x.shape
+    assert x.dtype == torch.uint8 and x.is_contiguous() and nb == C * bits // 8
+    P, Q = out_dim(H, R, stride, pad), out_dim(W, R, stride, pad)
+    if out is None:
+        out = torch.empty((N, P, Q, nb), dtype=torch.uint8, device=x.device)
+    assert out.dtype == torch.uint8 and out.is_contiguous() and tuple(out.shape) == (N, P, Q, nb)
+    _check(load().conv_q_maxpool(ctypes.c_void_p(x.data_ptr()), N, H, W, C, R, stride, pad, bits,
+                                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream(stream))))
     return out
 
 

@@ -48,7 +48,7 @@ int set_err(int code, const char *fmt, ...) {
 
 extern "C" const char *conv_q_last_error(void) { return g_err.c_str(); }
 extern "C" int conv_q_last_status(void) { return g_status; }
-extern "C" int conv_q_version(void) { return 101; }
+extern "C" int conv_q_version(void) { return 102; }
 
 // ============================================================== driver entry points
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -304,6 +304,7 @@ static int default_candidate(const conv_q_plan_s *p) {
 // Select the cached tuning result for the plan's shape + epilogue, if any
 // (the key includes relu / out_mode, so this runs again on set_epilogue).
 static void apply_cache(conv_q_plan_s *p) {
+    if (p->user_sel) return;   // an explicit conv_q_plan_set_config / _tune pick is sticky
     std::lock_guard<std::mutex> lk(g_cache_mu);
     cache_load_locked();
     auto it = g_cache.find(shape_key(p));
@@ -524,8 +525,9 @@ extern "C" int conv_q_plan_set_config(conv_q_plan_t *p, int i) {
     if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
     if (i < 0 || i >= (int)p->cands.size()) return set_err(CONV_Q_EINVAL, "candidate %d out of range", i);
     p->sel = i;
+    p->user_sel = 1;
     p->tuned_us = -1.f;
-    // allocate a split-K workspace now, so a later run may be graph-captured
+    // allocate a split-K workspace now: conv_q_run never allocates
     if (p->cands[i].split > 1 && ensure_device() == CONV_Q_OK) return ensure_ws(p);
     return CONV_Q_OK;
 }
@@ -706,7 +708,8 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
         return set_err(CONV_Q_EINVAL, "tensor pointers must be 16-byte aligned");
     int rc = ensure_device();
     if (rc) return rc;
-    if ((rc = ensure_ws(p))) return rc;
+    if (p->cands[p->sel].split > 1 && !p->ws)   // allocated by plan creation / set_config / set_epilogue / tune
+        return set_err(CONV_Q_EINVAL, "split-K workspace missing (select the config with conv_q_plan_set_config)");
     if (p->c_x != x || p->c_w != w || p->c_y != y || p->c_sel != p->sel || p->c_mode != p->out_mode) {
         rc = encode_maps(p, x, w, y);
         if (rc) return rc;
@@ -735,6 +738,7 @@ extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, 
     const int saved = p->sel;
     for (int i = 0; i < (int)p->cands.size(); ++i) {
         p->sel = i;
+        if ((rc = ensure_ws(p))) break;   // split-K workspace (grows only), before any timed run
         for (int k = 0; k < warmup; ++k)
             if ((rc = conv_q_run(p, x, w, scale, y))) break;
         if (rc) break;
@@ -769,6 +773,7 @@ extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, 
     cudaError_t e = cudaStreamSynchronize(p->stream);
     if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "tuning run failed: %s", cudaGetErrorString(e));
     p->sel = best;
+    p->user_sel = 1;
     p->tuned_us = best_us;
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
@@ -851,6 +856,40 @@ extern "C" int conv_q_pack_weights(const int8_t *w, int K, int R, int S, int C, 
     else
         pack_weights_kernel<4><<<grid, 256, 0, st>>>(w, static_cast<uint4 *>(wp), n_out_vec);
     CUDA_TRY(cudaGetLastError());
+    return CONV_Q_OK;
+}
+
+// R x R max pooling of packed codes (pack.cuh maxpool_kernel)
+extern "C" int conv_q_maxpool(const void *x, int N, int H, int W, int C, int R, int stride, int pad, int bits,
+                              void *y, void *stream) {
+    if (!x || !y) return set_err(CONV_Q_EINVAL, "NULL tensor pointer");
+    if (N < 1 || H < 1 || W < 1 || C < 1 || R < 1 || stride < 1) return set_err(CONV_Q_EINVAL, "dimensions must be >= 1");
+    if (bits != 4 && bits != 8) return set_err(CONV_Q_EINVAL, "bits must be 4 or 8");
+    if (pad < 0 || pad >= R) return set_err(CONV_Q_EINVAL, "pad must be in [0, R)");
+    if (H + 2 * pad < R || W + 2 * pad < R) return set_err(CONV_Q_EINVAL, "output is empty");
+    if (((int64_t)C * bits) % 128) return set_err(CONV_Q_EUNSUPPORTED, "C*bits must be a multiple of 128");
+    if (!aligned16(x) || !aligned16(y)) return set_err(CONV_Q_EINVAL, "pointers must be 16-byte aligned");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - R) / stride + 1;
+    const int vpp = (int)((int64_t)C * bits / 128);
+    const int64_t total = (int64_t)N * P * Q * vpp;
+    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 1 << 30);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const uint4 *xs = static_cast<const uint4 *>(x);
+    uint4 *ys = static_cast<uint4 *>(y);
+    if (bits == 8)
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, maxpool_kernel<8>, xs, ys, N, H, W, P, Q, vpp, R, stride, pad));
+    else
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, maxpool_kernel<4>, xs, ys, N, H, W, P, Q, vpp, R, stride, pad));
     return CONV_Q_OK;
 }
 

@@ -279,4 +279,59 @@ __global__ void __launch_bounds__(256) s2d_weights_kernel(const int8_t *__restri
     }
 }
 
+// ---------------------------------------------------------------- max pool
+// R x R max pooling of packed NHWC codes (the ResNet stem's 3x3/2 pool between
+// conv1 and layer1): one thread per 16-byte output vector
+// (16 s8 / 32 s4 channels of one output pixel), consecutive threads along the
+// channel vectors of a pixel, then along pixels (coalesced 16-byte loads and
+// stores; the R*R-fold tap re-reads hit L1/L2).  Out-of-range taps are
+// skipped (padding never wins); quantization is monotone, so the max of the
+// codes is the code of the max.  s8: byte-wise signed max (VIMNMX.S8); s4: the
+// even / odd nibbles expanded to 16*v bytes, byte max, repacked.
+__device__ __forceinline__ uint32_t vmax_s8x4(uint32_t a, uint32_t b) { return __vmaxs4(a, b); }
+__device__ __forceinline__ uint32_t vmax_s4x8(uint32_t a, uint32_t b) {
+    const uint32_t ae = (a << 4) & 0xF0F0F0F0u, ao = a & 0xF0F0F0F0u;   // 16 * even / odd nibbles as s8
+    const uint32_t be = (b << 4) & 0xF0F0F0F0u, bo = b & 0xF0F0F0F0u;
+    const uint32_t me = __vmaxs4(ae, be), mo = __vmaxs4(ao, bo);
+    return ((me >> 4) & 0x0F0F0F0Fu) | (mo & 0xF0F0F0F0u);
+}
+template <int BITS>
+__global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ x, uint4 *__restrict__ y, int N,
+                                                     int H, int W, int P, int Q, int vpp, int R, int stride,
+                                                     int pad) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // x is the previous kernel's output
+    const int64_t total = (int64_t)N * P * Q * vpp;
+    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
+         o += (int64_t)gridDim.x * blockDim.x) {
+        const int v = (int)(o % vpp);
+        const int64_t pix = o / vpp;
+        const int q = (int)(pix % Q);
+        const int64_t t = pix / Q;
+        const int p = (int)(t % P);
+        const int n = (int)(t / P);
+        const int h0 = p * stride - pad, w0 = q * stride - pad;
+        uint4 m;
+        bool any = false;
+        for (int r = 0; r < R; ++r) {
+            const int h = h0 + r;
+            if (h < 0 || h >= H) continue;
+            for (int s = 0; s < R; ++s) {
+                const int w = w0 + s;
+                if (w < 0 || w >= W) continue;
+                const uint4 a = __ldg(x + (((int64_t)n * H + h) * W + w) * vpp + v);
+                if (!any) {
+                    m = a;
+                    any = true;
+                } else if constexpr (BITS == 8) {
+                    m = make_uint4(vmax_s8x4(m.x, a.x), vmax_s8x4(m.y, a.y), vmax_s8x4(m.z, a.z), vmax_s8x4(m.w, a.w));
+                } else {
+                    m = make_uint4(vmax_s4x8(m.x, a.x), vmax_s4x8(m.y, a.y), vmax_s4x8(m.z, a.z), vmax_s4x8(m.w, a.w));
+                }
+            }
+        }
+        y[o] = any ? m : make_uint4(0, 0, 0, 0);
+    }
+}
+
 }  // namespace convq

@@ -79,6 +79,7 @@ struct conv_q_plan_s {
     cudaStream_t stream = nullptr;
     std::vector<Cand> cands;
     int sel = 0;
+    int user_sel = 0;  // sel chosen explicitly (conv_q_plan_set_config / conv_q_plan_tune): the cache never overrides it
     float tuned_us = -1.f;
     int rotate = 0;    // CONV_Q_ROTATE=1: rotate each CTA's k-block start (A/B measurement)
     int probe = 0;     // CONV_Q_PROBE (measurement only; results are garbage when != 0)
@@ -152,9 +153,14 @@ template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO = 0>
 inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>;
     auto kern = conv_igemm_kernel<BITS, BN, KCH, OUT, CG, NSUB, HALO>;
+    // One CTA per SM: every CTA allocates up to all 512 TMEM columns, so a second
+    // resident CTA would block in tcgen05.alloc until the first exits.  Configs
+    // whose shared memory would let two CTAs share an SM (228 KB per SM, 1 KB
+    // reserved per CTA) launch with their request padded past half of it.
+    constexpr int SMEM_LAUNCH = Cfg::SMEM > 116 * 1024 ? Cfg::SMEM : 116 * 1024;
     static bool attr_set = false;
     if (!attr_set) {
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LAUNCH));
         attr_set = true;
     }
     ConvParams prm;
@@ -181,7 +187,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
         const size_t need = (size_t)prm.num_tiles * CG * 128 * BN * sizeof(int32_t);
         const size_t regions = (size_t)prm.num_tiles * CG * 4 * Cfg::EPI_PER_BUF;
         if (!p->ws || p->ws_bytes < need || p->cnt_bytes < regions * sizeof(unsigned))
-            return set_err(CONV_Q_EINVAL, "split-K workspace not allocated (select the config outside graph capture)");
+            return set_err(CONV_Q_EINVAL, "split-K workspace not allocated (conv_q_plan_set_config / _tune allocate it)");
     }
     prm.fd_ntiles = make_fastdiv(prm.n_tiles);
     prm.fd_PQ = make_fastdiv(p->P * p->Q);
@@ -212,7 +218,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * CG);
     cfg.blockDim = dim3(Cfg::NUM_THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.dynamicSmemBytes = SMEM_LAUNCH;
     cfg.stream = p->stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;

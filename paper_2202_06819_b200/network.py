@@ -1,0 +1,165 @@
+"""Layer-sequence executor for the quantized conv path (product code).
+
+A ``ConvNet`` is one device's copy of a ResNet-shaped convolution network in
+the packed layout the paper's epilogue produces (section 3.3:
+"the output of one convolution layer is ... the input of the next"):
+
+  input stage   either the stem -- fp16 image -> s2d quantize -> conv1 (stride-2
+                7x7 as a stride-1 window conv, StemPlan) -> 3x3/2 max pool -- or a
+                plain quantize + pack of an fp16 activation tensor (a1)
+  conv layers   one ConvPlan per layer (a3-a6), each reading the packed output of
+                an earlier layer (or the input stage), fused requantize + repack
+                epilogue writing the next layer's packed NHWC input
+
+Weights are packed once (a2), tile configs are picked per unique shape by
+on-device timing (a7), and one ``step`` launches every kernel on one stream,
+so the whole step can be captured as one CUDA graph.  Argument marshalling
+and buffer ownership only: every step of the path runs in libconvq.so's
+kernels; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import (ConvPlan, StemPlan, maxpool, pack_weights, quantize, padded_channels)
+
+
+@dataclass
+class _Conv:
+    name: str
+    layer: object           # has H, W, C, K, R, S, stride, pad, P, Q
+    src: int                # index of the producing conv, -1 = the input stage's output
+    relu: bool
+    plan: ConvPlan
+    w: object               # packed weights (device uint8)
+    ss: object              # [scale | shift] (device float32)
+    y: object               # packed output (device uint8)
+    key: tuple = field(default=())
+
+
+class ConvNet:
+    """Quantized conv network on one device.
+
+    net = ConvNet(batch, bits, device)
+    net.set_stem(conv1, w_codes, ss, inv_scale)      # or net.set_quantize_input(H, W, C, inv_scale)
+    for L, src in layers: net.add_conv(L, src, w_codes, ss, relu=True)
+    net.tune(); net.step(stream)                      # net.x_in is the fp16 input, net.outputs the results
+    """
+
+    def __init__(self, batch: int, bits: int, device, stream=None):
+        import torch
+        self.torch = torch
+        self.B, self.bits, self.device = batch, bits, device
+        self.stream = stream
+        self.convs: list[_Conv] = []
+        self.stem = None
+        self.x_in = None
+        self.input_desc = None
+        self.net_in = None        # packed tensor the first conv reads (quantized input or pooled stem output)
+        self._stages = []         # ("quantize" | "s2d" | "stem" | "pool", callable) in launch order
+
+    # ------------------------------------------------------------- input stage
+    def set_quantize_input(self, H: int, W: int, C: int, inv_scale: float):
+        """a1 only: fp16 [B,H,W,C] -> packed [B,H,W,C'] (conv_q_quantize)."""
+        t = self.torch
+        self.x_in = t.empty((self.B, H, W, C), dtype=t.float16, device=self.device)
+        Cp = padded_channels(C, self.bits)
+        self.net_in = t.empty((self.B, H, W, Cp * self.bits // 8), dtype=t.uint8, device=self.device)
+        self.inv_scale = inv_scale
+        self._stages = [("quantize", lambda s: quantize(self.x_in, inv_scale, self.bits, out=self.net_in, stream=s))]
+        self.input_desc = f"quantize fp16 [{self.B},{H},{W},{C}]"
+
+    def set_stem(self, conv1, w_codes, ss, inv_scale: float, pool=(3, 2, 1), relu: bool = True):
+        """conv1 through the s2d StemPlan (fused quantize + space-to-depth, then a
+        stride-1 window conv) followed by an R x R max pool of its packed output."""
+        t = self.torch
+        L = conv1
+        self.x_in = t.empty((self.B, L.H, L.W, L.C), dtype=t.float16, device=self.device)
+        sp = StemPlan(self.B, L.H, L.W, L.C, L.K, L.R, L.S, L.pad, self.bits, relu=relu)
+        xs = t.empty(sp.x_dims, dtype=t.uint8, device=self.device)
+        wp = sp.pack_weights(w_codes)
+        y1 = t.empty((self.B, sp.P, sp.Q, L.K * self.bits // 8), dtype=t.uint8, device=self.device)
+        pr, pst, ppad = pool
+        Pp, Qp = (sp.P + 2 * ppad - pr) // pst + 1, (sp.Q + 2 * ppad - pr) // pst + 1
+        self.net_in = t.empty((self.B, Pp, Qp, L.K * self.bits // 8), dtype=t.uint8, device=self.device)
+        self.stem = dict(layer=L, plan=sp, xs=xs, w=wp, ss=ss, y=y1, pool=pool, inv_scale=inv_scale, relu=relu)
+        self.inv_scale = inv_scale
+        self._stages = [
+            ("s2d", lambda s: sp.quantize(self.x_in, inv_scale, out=xs, stream=s)),
+            ("stem", lambda s: sp.run(xs, wp, ss, y1, stream=s)),
+            ("pool", lambda s: maxpool(y1, L.K, pr, pst, ppad, self.bits, out=self.net_in, stream=s)),
+        ]
+        self.input_desc = f"stem {L.name} {L.R}x{L.S}/{L.stride} {L.C}->{L.K} (s2d) + maxpool {pr}x{pr}/{pst}"
+
+    # ------------------------------------------------------------- conv layers
+    def add_conv(self, L, src: int, w_codes, ss, relu: bool = True, name: str | None = None) -> int:
+        """One conv layer reading the output of conv `src` (-1: the input stage)."""
+        t = self.torch
+        assert src < len(self.convs)
+        plan = ConvPlan(self.B, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, self.bits, relu=relu)
+        wp = pack_weights(w_codes, self.bits)
+        y = t.empty((self.B, L.P, L.Q, L.K * self.bits // 8), dtype=t.uint8, device=self.device)
+        key = (L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, relu)
+        self.convs.append(_Conv(name or getattr(L, "name", f"conv{len(self.convs)}"), L, src, relu, plan, wp, ss,
+                                y, key))
+        return len(self.convs) - 1
+
+    def src_tensor(self, i: int):
+        s = self.convs[i].src
+        return self.net_in if s < 0 else self.convs[s].y
+
+    @property
+    def outputs(self):
+        return [c.y for c in self.convs]
+
+    def set_stream(self, stream):
+        self.stream = stream
+        for c in self.convs:
+            c.plan.set_stream(stream)
+        if self.stem is not None:
+            self.stem["plan"].set_stream(stream)
+
+    # ------------------------------------------------------------- a7 tuning
+    def tune(self, warmup: int = 2, reps: int = 5) -> dict:
+        """Pick each unique shape's tile config by on-device timing (conv_q_plan_tune),
+        on the network's real buffers (the input stage is run once first)."""
+        self.run_input_stage(self.stream)
+        if self.stem is not None:
+            st = self.stem
+            st["plan"].tune(st["xs"], st["w"], st["ss"], st["y"], warmup=warmup, reps=reps, stream=self.stream)
+            self.run_input_stage(self.stream)
+        picks = {}
+        for i, c in enumerate(self.convs):
+            if c.key in picks:
+                c.plan.set_config(picks[c.key][0])
+            else:
+                idx = c.plan.tune(self.src_tensor(i), c.w, c.ss, c.y, warmup=warmup, reps=reps, stream=self.stream)
+                picks[c.key] = (idx, c.plan.info().config)
+        self.torch.cuda.synchronize(self.device)
+        return {str(k): v[1] for k, v in picks.items()}
+
+    # ------------------------------------------------------------- execution
+    def run_input_stage(self, stream=None, ev=None):
+        s = stream if stream is not None else self.stream
+        for j, (_, f) in enumerate(self._stages):
+            f(s)
+            if ev is not None:
+                ev(("input", j))
+
+    def step(self, stream=None, ev=None):
+        """One pass of the whole hot path over the batch; ev(tag) is called after
+        every launch (per-launch timing events), tag = ("input", j) or ("conv", i)."""
+        s = stream if stream is not None else self.stream
+        self.run_input_stage(s, ev)
+        for i, c in enumerate(self.convs):
+            c.plan.run(self.src_tensor(i), c.w, c.ss, c.y, stream=s)
+            if ev is not None:
+                ev(("conv", i))
+
+    @property
+    def launches_per_step(self) -> int:
+        return len(self._stages) + len(self.convs)
+
+    @property
+    def stage_names(self) -> list[str]:
+        return [n for n, _ in self._stages]

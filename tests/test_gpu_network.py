@@ -1,0 +1,146 @@
+"""Whole-network and launch-configuration parity on the GPU (-m gpu).
+
+* The EXACT bench chains (bench.build_network: s2d stem + max pool + every conv,
+  tuned on the box the way bench.py tunes them, ReLU on) at the bench's batch:
+  every launch checked against the oracle on sampled pixels of the first, a
+  middle and the last image (>= 256 pixels per layer, tile boundaries
+  included), each layer from the device's own input bytes.
+* Every weight-stationary / MT2 / halo / CTA-pair / split candidate forced at
+  N = 32, so each persistent CTA (pair) runs several work units (TMEM buffer
+  rotation and barrier phase wrap), packed ReLU and s32 outputs.
+* The requant FMA on adversarial near-tie (acc, scale, shift) triples.
+* Max pooling over packed codes.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+from oracle import check
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def cq():
+    import paper_2202_06819_b200 as m
+    m.load()
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ----------------------------------------------------------------- the bench chains
+@pytest.mark.parametrize("workload", ["resnet50_int8_b256", "resnet18_int4_b16", "resnet18_int8_b1"])
+def test_bench_chain_parity(cq, workload):
+    import bench
+    spec = bench.workload_spec(workload)
+    B = spec.batch
+    net = bench.build_network(spec, B, torch.device("cuda", 0))
+    g = wl.rng(spec.cfg_id, 1000)
+    net.x_in.copy_(torch.from_numpy(wl.fp16_activations(g, B, *tuple(net.x_in.shape[1:]))))
+    net.tune(warmup=1, reps=2)           # the bench's a7 selection on this box (fewer reps)
+    for _ in range(2):                   # back-to-back steps (PDL overlap between launches)
+        net.step()
+    torch.cuda.synchronize()
+    imgs = sorted({0, B // 2, B - 1})
+    ok, bad = bench.parity_check(net, spec, imgs, n_rand=256, seed=11)
+    assert ok, bad[:5]
+
+
+# ----------------------------------------------------------------- forced candidates, several units per CTA
+FORCED = [("l1.b0.c2", 8), ("l1.b0.c1", 8), ("l1.b1.c1", 8), ("l2.b1.c1", 8), ("l2.b1.c2", 8), ("l3.b1.c3", 8),
+          ("l3.b1.c2", 8), ("l4.b1.c1", 8), ("l4.b0.c3", 8), ("l2.b0.c2", 8), ("l1.b0.c2", 4), ("l3.b1.c3", 4)]
+
+
+@pytest.mark.parametrize("name,bits", FORCED)
+def test_every_candidate_n32(cq, name, bits):
+    """Batch 32: every persistent CTA (pair) runs several work units, so TMEM
+    buffer rotation, MT2 groups and mbarrier phase wrap are all exercised, for
+    EVERY candidate of the shape (ReLU packed output -- the OUT_RELU kernels --
+    and raw s32)."""
+    L = dict((l.name, l) for l, _ in wl.resnet50_layers())[name]
+    N = 32
+    g = wl.rng(4, 300 + len(name))
+    x, w, ss = wl.layer_inputs(g, L, N, bits)
+    plan = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits)
+    M = N * L.P * L.Q
+    pix = check.sample_pixels(N, L.P, L.Q, g, 256)
+    ref32 = oracle.conv_s32(x, w, L.C, L.stride, L.pad, bits, pix=pix)
+    refq = oracle.requant(ref32, ss, True, bits)
+    xd, wd, sd = dev(x), dev(w), dev(ss)
+    y = torch.empty((M, L.K * bits // 8), dtype=torch.uint8, device="cuda")
+    y32 = torch.empty((M, L.K), dtype=torch.int32, device="cuda")
+    names = plan.candidates()
+    assert len(names) >= 4
+    for ci, cname in enumerate(names):
+        plan.set_config(ci)
+        plan.set_epilogue(True, cq.OUT_PACKED)
+        assert plan.info().config == cname             # the explicit pick is never overridden by the cache
+        y.fill_(0xA5)
+        plan.run(xd, wd, sd, y)
+        plan.set_epilogue(True, cq.OUT_S32)
+        y32.fill_(-7777777)
+        plan.run(xd, wd, sd, y32)
+        torch.cuda.synchronize()
+        got = y.cpu().numpy()[pix]
+        assert np.array_equal(got, refq), (cname, check.first_diff(got, refq))
+        got32 = y32.cpu().numpy()[pix]
+        assert np.array_equal(got32, ref32), (cname, check.first_diff(got32, ref32))
+
+
+# ----------------------------------------------------------------- requant FMA, adversarial
+def test_requant_fma_near_ties(cq):
+    """Reading 5 on the device: per-channel scale/shift chosen so that one
+    pixel's exact acc*scale + shift sits within half an ulp of a half-integer
+    (or on it); the kernel's codes equal the oracle's for every output, and the
+    inputs include cases where a two-rounding epilogue would differ."""
+    import exact_fp
+    L = wl.Layer("fma", 8, 8, 256, 256, 1, 1, 1, 0)
+    N = 2
+    g = np.random.default_rng(505)
+    x, w, _ = wl.layer_inputs(g, L, N, 8)
+    acc = oracle.conv_s32(x, w, L.C, 1, 0, 8).reshape(-1, L.K)        # exact accumulators (pinned oracle)
+    plan = cq.ConvPlan(N, L.H, L.W, L.C, L.K, 1, 1, 1, 0, 8)
+    xd, wd = dev(x), dev(w)
+    y = torch.empty((N * 64, L.K), dtype=torch.uint8, device="cuda")
+    differ = 0
+    for rep in range(24):
+        tgt = g.integers(0, acc.shape[0], L.K)                       # one adversarial pixel per channel
+        a = acc[tgt, np.arange(L.K)]
+        _, sc, sh = exact_fp.near_tie_cases(g, L.K, 8)
+        # re-target the shifts at this channel's chosen accumulator
+        sh = np.array([exact_fp.f32_rne(exact_fp.Fraction(int(2 * g.integers(-100, 100) + 1), 2)
+                                        - exact_fp.Fraction(exact_fp.f32_rne(exact_fp.Fraction(int(ai))))
+                                        * exact_fp.Fraction(float(si)))
+                       for ai, si in zip(a, sc)], np.float32)
+        ss = np.concatenate([sc, sh]).astype(np.float32)
+        relu = bool(rep % 2)
+        plan.set_epilogue(relu, cq.OUT_PACKED)
+        plan.run(xd, wd, dev(ss), y)
+        torch.cuda.synchronize()
+        ref = oracle.requant(acc.astype(np.int32), ss, relu, 8)
+        got = y.cpu().numpy()
+        assert np.array_equal(got, ref), (rep, check.first_diff(got, ref))
+        ex = np.array([exact_fp.requant_exact(int(ai), float(s), float(h), relu, 8) for ai, s, h in zip(a, sc, sh)])
+        assert np.array_equal(got[tgt, np.arange(L.K)].view(np.int8).astype(np.int64), ex)
+        differ += int(np.count_nonzero(exact_fp.requant_two_roundings(a, sc, sh, relu, 8) != ex))
+    assert differ >= 100, differ
+
+
+# ----------------------------------------------------------------- max pool
+@pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("N,H,W,C,R,st,pad", [(2, 112, 112, 64, 3, 2, 1), (3, 9, 7, 32, 3, 2, 1),
+                                               (1, 6, 6, 128, 2, 2, 0), (2, 5, 5, 64, 3, 1, 1)])
+def test_maxpool_parity(cq, bits, N, H, W, C, R, st, pad):
+    if (C * bits) % 128:
+        pytest.skip("C*bits")
+    g = np.random.default_rng(900 + H)
+    x = wl.random_bytes(g, (N, H, W, C * bits // 8))
+    got = cq.maxpool(dev(x), C, R, st, pad, bits).cpu().numpy()
+    ref = oracle.maxpool(x, C, R, st, pad, bits)
+    assert np.array_equal(got, ref), check.first_diff(got, ref)

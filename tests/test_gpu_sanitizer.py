@@ -1,0 +1,28 @@
+"""compute-sanitizer over every candidate family at cfg1 and edge sizes (-m gpu;
+skipped when the tool is absent).  memcheck: out-of-bounds / misaligned
+global and shared accesses; synccheck: invalid barrier use.  The async
+pipeline (TMA, mbarriers, tcgen05) is the part a race or a wrong byte count
+would break (round 1 hit a real pipeline race in the dual-MMA variant)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_compute_sanitizer(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    cmd = [SAN, f"--tool={tool}", "--error-exitcode=17", "--print-limit=20", sys.executable,
+           os.path.join(ROOT, "scripts", "sanitize_run.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "sanitize_run:" in out and "ERROR SUMMARY: 0 errors" in out, out[-4000:]

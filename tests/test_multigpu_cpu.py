@@ -66,3 +66,52 @@ def test_gloo_two_ranks_concat_equals_single(N):
     ref = oracle.conv_q(x, w, L.C, L.stride, L.pad, 8, ss, True)
     assert np.array_equal(ret["y"], ref)
     assert ret["tmax"] == 2.0
+
+
+# ---------------------------------------------------------------- bench.py's own rank logic
+def _bench_worker(rank, world, port, ret):
+    """Drives bench.py's rank functions (shard_plan, replicate, max_over_ranks,
+    gather_outputs) under gloo with a stubbed device arm: the oracle computes
+    each rank's shard of a small ResNet-shaped layer on the host."""
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    spec = bench.workload_spec("cfg1")
+    L = wl.Layer("mg", 6, 5, 32, 16, 3, 3, 1, 1)
+    Bg, B, start = bench.shard_plan(6, world, rank, "strong")
+    x, w, ss = wl.layer_inputs(wl.rng(4, 98), L, Bg, 8)
+    # rank-dependent garbage before the broadcast: replicate() must make every rank equal rank 0
+    wt = torch.from_numpy(w.copy() if rank == 0 else np.zeros_like(w))
+    st = torch.from_numpy(ss.copy() if rank == 0 else np.zeros_like(ss))
+    bench.replicate([wt, st], world, dist)
+    y = oracle.conv_q(x[start:start + B], wt.numpy(), L.C, L.stride, L.pad, 8, st.numpy(), True, nthreads=1)
+    out = bench.gather_outputs(torch.from_numpy(y), world, dist)
+    tmax = bench.max_over_ranks(10.0 + rank, world, dist, "cpu")
+    tmin = bench.min_over_ranks(1.0 - rank, world, dist, "cpu")
+    ret[rank] = (Bg, B, start, tmax, tmin)
+    if rank == 0:
+        ret["y"] = out.numpy()
+    dist.destroy_process_group()
+
+
+def test_bench_rank_logic_gloo_two_ranks():
+    world = 2
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_bench_worker, args=(world, _free_port(), ret), nprocs=world, join=True)
+    L = wl.Layer("mg", 6, 5, 32, 16, 3, 3, 1, 1)
+    x, w, ss = wl.layer_inputs(wl.rng(4, 98), L, 6, 8)
+    assert ret[0][:3] == (6, 3, 0) and ret[1][:3] == (6, 3, 3)      # strong: global 6 split 3 + 3
+    assert ret[0][3] == ret[1][3] == 11.0                            # max over ranks
+    assert ret[0][4] == ret[1][4] == 0.0
+    assert np.array_equal(ret["y"], oracle.conv_q(x, w, L.C, L.stride, L.pad, 8, ss, True))
+
+
+def test_bench_shard_plan_rules():
+    import bench
+    assert bench.shard_plan(256, 8, 7, "strong") == (256, 32, 224)
+    assert bench.shard_plan(256, 1, 0, "strong") == (256, 256, 0)
+    assert bench.shard_plan(256, 4, 3, "weak") == (1024, 256, 768)
+    with pytest.raises(SystemExit):
+        bench.shard_plan(255, 2, 0, "strong")                        # uneven shards are rejected
