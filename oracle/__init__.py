@@ -70,6 +70,10 @@ def _load():
         lib.oracle_conv_q.restype = i32
         lib.oracle_conv_q.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, i64, i64, i32,
                                       vp, i32, vp, i64, vp, i32]
+        lib.oracle_requant_res_value.restype = i32
+        lib.oracle_requant_res_value.argtypes = [i32, f32, f32, i32, f32, i32, i32]
+        lib.oracle_requant_res.restype = None
+        lib.oracle_requant_res.argtypes = [vp, i64, i64, vp, vp, f32, i32, i32, vp, i32]
         lib.oracle_maxpool.restype = i32
         lib.oracle_maxpool.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, i32, vp, i32]
         _lib = lib
@@ -104,6 +108,14 @@ def requant_value(acc: int, scale: float, shift: float, relu: bool, bits: int) -
     readings 4 and 5."""
     return int(_load().oracle_requant_value(int(acc), float(np.float32(scale)),
                                             float(np.float32(shift)), int(bool(relu)), bits))
+
+
+def requant_res_value(acc: int, scale: float, shift: float, skip: int, res_scale: float, relu: bool,
+                      bits: int) -> int:
+    """y = clamp(rne(fmaf(skip, res_scale, fmaf((float)acc, scale, shift)))) -- the
+    residual epilogue of DESIGN reading 15."""
+    return int(_load().oracle_requant_res_value(int(acc), float(np.float32(scale)), float(np.float32(shift)),
+                                                int(skip), float(np.float32(res_scale)), int(bool(relu)), bits))
 
 
 def out_dim(H: int, R: int, stride: int, pad: int) -> int:
@@ -201,11 +213,34 @@ def requant(acc: np.ndarray, scale_shift: np.ndarray, relu: bool, bits: int,
     return out.reshape(*acc.shape[:-1], K * bits // 8)
 
 
+def requant_res(acc: np.ndarray, scale_shift: np.ndarray, skip: np.ndarray, res_scale: float, relu: bool,
+                bits: int, nthreads: int | None = None) -> np.ndarray:
+    """requant with the fused residual add (reading 15); skip: packed [..., K*b/8]
+    with the same leading shape as acc."""
+    acc = np.ascontiguousarray(acc, dtype=np.int32)
+    K = acc.shape[-1]
+    ss = np.ascontiguousarray(scale_shift, dtype=np.float32)
+    assert ss.size == 2 * K and K <= 8192
+    M = acc.size // K
+    sk = np.ascontiguousarray(skip, dtype=np.uint8).reshape(M, K * bits // 8)
+    out = np.empty((M, K * bits // 8), dtype=np.uint8)
+    _load().oracle_requant_res(_ptr(acc), M, K, _ptr(ss), _ptr(sk), float(np.float32(res_scale)),
+                               int(bool(relu)), bits, _ptr(out), nthreads or default_threads())
+    return out.reshape(*acc.shape[:-1], K * bits // 8)
+
+
 def conv_q(x: np.ndarray, w: np.ndarray, C: int, stride: int, pad: int, bits: int,
            scale_shift: np.ndarray, relu: bool, pix: np.ndarray | None = None,
-           nthreads: int | None = None) -> np.ndarray:
-    """One whole layer: conv_s32 -> requant -> pack."""
+           nthreads: int | None = None, skip: np.ndarray | None = None, res_scale: float = 0.0) -> np.ndarray:
+    """One whole layer: conv_s32 -> requant -> pack; with
+    `skip` (packed, the output's shape; rows `pix` only when pix is given) the
+    residual epilogue of reading 15."""
     acc = conv_s32(x, w, C, stride, pad, bits, pix=pix, nthreads=nthreads)
+    if skip is not None:
+        sk = skip.reshape(-1, skip.shape[-1])
+        if pix is not None:
+            sk = sk[pix]
+        return requant_res(acc, scale_shift, sk, res_scale, relu, bits, nthreads=nthreads)
     return requant(acc, scale_shift, relu, bits, nthreads=nthreads)
 
 

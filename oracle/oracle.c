@@ -33,6 +33,10 @@
  *                          evaluation (separates fmaf from mul-then-add)
  *   oracle_maxpool         pinned: torch max_pool2d (float64, library) on the
  *                          unpacked codes; all-equal / one-hot windows
+ *   oracle_requant_res_value  pinned: res_scale 0 == oracle_requant_value;
+ *                          unit scales == clamp(acc + skip) (exact integers);
+ *                          exact-rational evaluation with the two single
+ *                          roundings of reading 15 on random / near-tie cases
  */
 #include <math.h>
 #include <stdint.h>
@@ -244,6 +248,29 @@ ORACLE_API int oracle_requant_value(int32_t acc, float scale, float shift, int r
     return (int)c;
 }
 
+/* ------------------------------------------------------------------------
+ * Requantize with a fused residual add (PAPER.md:200
+ * section 3.2.2 names the epilogue's elementwise work -- "relu, batch
+ * normalization, and bias addition" -- and the residual add of a ResNet block,
+ * relu(bn(conv(x)) + identity), is the same class of work).  DESIGN reading 15:
+ *   u = fmaf((float)acc, scale, shift)       the conv's BN / bias, one rounding
+ *   v = fmaf((float)skip, res_scale, u)      + the skip code rescaled, one rounding
+ *   y = clamp(rne(v), lo, hi), lo = 0 with ReLU (ReLU after the add)
+ * skip = the skip tensor's code at the same (pixel, channel), res_scale one
+ * fp32 per layer (the skip tensor's scale relative to the output's).
+ * ---------------------------------------------------------------------- */
+ORACLE_API int oracle_requant_res_value(int32_t acc, float scale, float shift, int skip, float res_scale,
+                                        int relu, int bits)
+{
+    float f = (float)acc;
+    float u = fmaf(f, scale, shift);
+    float v = fmaf((float)skip, res_scale, u);
+    float r = nearbyintf(v);
+    float lo = relu ? 0.0f : lo_of(bits);
+    float c = fminf(fmaxf(r, lo), hi_of(bits));
+    return (int)c;
+}
+
 /* Requantize an [M, K] accumulator matrix and pack each row into K*b/8 bytes.
  * scale_shift = [scale_0..scale_{K-1}, shift_0..shift_{K-1}]. */
 ORACLE_API void oracle_requant(const int32_t *acc, int64_t M, int64_t K,
@@ -257,6 +284,24 @@ ORACLE_API void oracle_requant(const int32_t *acc, int64_t M, int64_t K,
         for (int64_t k = 0; k < K; ++k)
             q[k] = (int8_t)oracle_requant_value(acc[m * K + k], scale_shift[k],
                                                 scale_shift[K + k], relu, bits);
+        oracle_pack(q, K, bits, y + m * row_bytes);
+    }
+}
+
+/* As oracle_requant, with the residual add of reading 15: skip is a packed
+ * [M, K*b/8] tensor (the same layout as y). */
+ORACLE_API void oracle_requant_res(const int32_t *acc, int64_t M, int64_t K,
+                                   const float *scale_shift, const uint8_t *skip, float res_scale,
+                                   int relu, int bits, uint8_t *y, int nthreads)
+{
+    int64_t row_bytes = K * bits / 8;
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        int8_t q[8192], sk[8192];
+        oracle_unpack(skip + m * row_bytes, K, bits, sk);
+        for (int64_t k = 0; k < K; ++k)
+            q[k] = (int8_t)oracle_requant_res_value(acc[m * K + k], scale_shift[k], scale_shift[K + k],
+                                                    sk[k], res_scale, relu, bits);
         oracle_pack(q, K, bits, y + m * row_bytes);
     }
 }

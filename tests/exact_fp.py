@@ -94,3 +94,17 @@ def near_tie_cases(g: np.random.Generator, n: int, bits: int = 8):
         out_scale.append(scale)
         out_shift.append(shift)
     return (np.array(out_acc, np.int64), np.array(out_scale, np.float32), np.array(out_shift, np.float32))
+
+
+def requant_res_exact(acc: int, scale: float, shift: float, skip: int, res_scale: float, relu: bool,
+                      bits: int) -> int:
+    """Reading 15 with exact rationals: u = RN32(acc*scale + shift), v = RN32(skip*res_scale + u),
+    then round half to even and clamp."""
+    f = f32_rne(Fraction(int(acc)))
+    u = f32_rne(Fraction(f) * Fraction(float(scale)) + Fraction(float(shift)))
+    v = f32_rne(Fraction(int(skip)) * Fraction(float(res_scale)) + Fraction(u))
+    lo = 0 if relu else -(1 << (bits - 1))
+    hi = (1 << (bits - 1)) - 1
+    if math.isinf(v):
+        return hi if v > 0 else lo
+    return min(max(round(Fraction(v)), lo), hi)

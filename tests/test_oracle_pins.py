@@ -368,3 +368,49 @@ def test_maxpool_closed_forms():
         for q in range(3):
             assert y[0, p, q, 5] == (100 if (p, q) in hit else 0)
     assert np.all(np.delete(y, 5, axis=3) == 0)
+
+
+
+# ---------------------------------------------------------------- residual epilogue (NEXT-2, reading 15)
+def test_requant_res_zero_scale_is_plain_requant():
+    g = np.random.default_rng(41)
+    for _ in range(2000):
+        acc, sc, sh = int(g.integers(-(1 << 20), 1 << 20)), float(np.float32(g.uniform(1e-4, 1e-2))), \
+            float(np.float32(g.uniform(-3, 3)))
+        sk = int(g.integers(-128, 128))
+        for relu in (False, True):
+            assert oracle.requant_res_value(acc, sc, sh, sk, 0.0, relu, 8) == oracle.requant_value(acc, sc, sh, relu, 8)
+
+
+def test_requant_res_unit_scales_add_integers():
+    """scale = res_scale = 1, shift = 0: y = clamp(acc + skip) (every step exact)."""
+    for acc in range(-150, 151, 7):
+        for sk in range(-128, 128, 5):
+            assert oracle.requant_res_value(acc, 1.0, 0.0, sk, 1.0, False, 8) == min(max(acc + sk, -128), 127)
+            assert oracle.requant_res_value(acc, 1.0, 0.0, sk, 1.0, True, 8) == min(max(acc + sk, 0), 127)
+    for acc in range(-12, 13):
+        for sk in range(-8, 8):
+            assert oracle.requant_res_value(acc, 1.0, 0.0, sk, 1.0, False, 4) == min(max(acc + sk, -8), 7)
+
+
+@pytest.mark.parametrize("relu", [False, True])
+def test_requant_res_exact_two_roundings(relu):
+    """Reading 15's two single-rounded FMAs, against exact rationals: random
+    cases plus near-tie cases (the shift puts u next to a half-integer, the
+    skip term moves it by a non-dyadic amount)."""
+    import exact_fp
+    g = np.random.default_rng(4242 + relu)
+    acc, sc, sh = exact_fp.near_tie_cases(g, 6000, 8)
+    sk = g.integers(-128, 128, acc.size)
+    rs = np.float32(g.uniform(0.05, 1.5))
+    K = acc.size
+    skip = oracle.pack(sk.astype(np.int8).reshape(1, K), 8)
+    got = oracle.unpack(oracle.requant_res(acc.astype(np.int32).reshape(1, K), np.concatenate([sc, sh]), skip,
+                                           float(rs), relu, 8), K, 8)[0]
+    ref = np.array([exact_fp.requant_res_exact(int(a), float(s), float(h), int(k), float(rs), relu, 8)
+                    for a, s, h, k in zip(acc, sc, sh, sk)])
+    assert np.array_equal(got, ref), np.nonzero(got != ref)[0][:5]
+    # scalar entry point == packed entry point
+    for i in range(0, K, 97):
+        assert oracle.requant_res_value(int(acc[i]), float(sc[i]), float(sh[i]), int(sk[i]), float(rs), relu, 8) \
+            == ref[i]
