@@ -57,13 +57,26 @@ class Spec:
     """A bench workload: network layers, per-GPU batch, precision, input stage."""
 
     def __init__(self, name, layers, batch, bits, conv1, desc, cfg_id, metric):
+        # layers: (Layer, src) pairs, or (Layer, src, skip) triples for a network with residual adds
+        layers = [tuple(t) + (None,) * (3 - len(t)) for t in layers]
+        self.residual = any(t[2] is not None for t in layers)
         self.name, self.layers, self.batch, self.bits = name, layers, batch, bits
         self.conv1, self.desc, self.cfg_id, self.metric = conv1, desc, cfg_id, metric
         self.inv_scale = 127 / 4 if bits == 8 else 7 / 3
         self.pool = (3, 2, 1)
 
 
+RES_SUFFIX = "_res"
+
+
 def workload_spec(name: str) -> Spec:
+    if name.endswith(RES_SUFFIX):
+        # the same network with its residual adds fused into the c3 / c2 epilogues (NEXT-2)
+        base = workload_spec(name[:-len(RES_SUFFIX)])
+        blocks = wl.resnet50_blocks() if "resnet50" in name else wl.resnet18_blocks()
+        return Spec(name, blocks, base.batch, base.bits, base.conv1,
+                    base.desc + ", residual adds fused into the block-output epilogues",
+                    base.cfg_id, base.metric.replace("fused requant-repack", "fused requant-repack + residual"))
     if name == "resnet50_int8_b256":
         return Spec(name, wl.resnet50_layers(), 256, 8, wl.resnet18_conv1(),
                     "ResNet-50 v1.5: conv1 (s2d stem) + 3x3/2 max pool + layer1-4 convs, INT8", 4,
@@ -120,6 +133,10 @@ def layer_weights(spec: Spec, i: int):
     return wv, ss
 
 
+def layer_res_scale(spec: Spec, i: int) -> float:
+    return wl.res_scale(wl.rng(spec.cfg_id, 500 + i))
+
+
 def build_network(spec: Spec, B: int, device, world: int = 1, dist=None):
     """The device network of a workload (packed weights broadcast from rank 0)."""
     import torch
@@ -140,9 +157,10 @@ def build_network(spec: Spec, B: int, device, world: int = 1, dist=None):
     else:
         L0 = spec.layers[0][0]
         net.set_quantize_input(L0.H, L0.W, L0.C, spec.inv_scale)
-    for i, (L, src) in enumerate(spec.layers):
+    for i, (L, src, skip) in enumerate(spec.layers):
         wt, st = dev_params(i)
-        net.add_conv(L, src, wt, st, relu=True, name=L.name)
+        net.add_conv(L, src, wt, st, relu=True, name=L.name, skip=skip,
+                     res_scale=layer_res_scale(spec, i) if skip is not None else 0.0)
     return net
 
 
@@ -272,8 +290,10 @@ def parity_check(net, spec: Spec, imgs, n_rand: int = 64, seed: int = 0, nthread
     for i, c in enumerate(net.convs):
         L = c.layer
         pix = check.sample_pixels(len(imgs), L.P, L.Q, g, n_rand)
+        sk = net.skip_tensor(i)
         ok, d = check.check_conv(host(net.src_tensor(i)), c.w.cpu().numpy(), c.ss.cpu().numpy(), L, bits, c.relu,
-                                 host(c.y), pix, nthreads)
+                                 host(c.y), pix, nthreads, skip=None if sk is None else host(sk),
+                                 res_scale=c.res_scale)
         if not ok:
             bad.append((c.name, d))
     return not bad, bad
@@ -610,7 +630,7 @@ def _oracle_layers(spec: Spec):
     """The conv layers the oracle computes for one image (conv1 over its
     channel-padded input, as the oracle's direct convolution runs it)."""
     import oracle
-    layers = [L for L, _ in spec.layers]
+    layers = [t[0] for t in spec.layers]
     if spec.conv1 is not None:
         L1 = spec.conv1
         layers = [wl.Layer(L1.name, L1.H, L1.W, oracle.padded_channels(L1.C, spec.bits), L1.K, L1.R, L1.S,
@@ -654,16 +674,17 @@ def cpu_baseline(spec: Spec, B, budget_s=15.0):
     per_image = _per_image_macs(layers)
 
     def timed(nt, budget):
-        probe = _oracle_sample(layers, spec.bits, 0.01, g)
-        t = time.perf_counter()
-        m = _oracle_step(probe, spec.bits, nt)
-        rate = m / (time.perf_counter() - t)
-        frac = max(0.002, budget * rate / per_image)
-        reps = max(1, int(frac))
-        sample = _oracle_sample(layers, spec.bits, min(frac, 1.0), g)
-        t = time.perf_counter()
-        macs = sum(_oracle_step(sample, spec.bits, nt) for _ in range(reps))
-        dt = time.perf_counter() - t
+        # grow the sample until it takes about `budget` seconds (10-30 s of CPU work by default)
+        frac = 0.01
+        while True:
+            reps = max(1, int(frac))
+            sample = _oracle_sample(layers, spec.bits, min(frac, 1.0), g)
+            t = time.perf_counter()
+            macs = sum(_oracle_step(sample, spec.bits, nt) for _ in range(reps))
+            dt = time.perf_counter() - t
+            if dt >= 0.5 * budget or frac >= 256:
+                break
+            frac *= min(16.0, max(2.0, budget / max(dt, 1e-3)))
         desc = (f"{reps} image(s), every output pixel of every layer" if frac >= 1 else
                 f"{frac * 100:.2f}% of the output pixels of every layer of one image")
         return macs / per_image / dt, f"{desc} ({macs / 1e9:.2f} GMAC in {dt:.1f} s)", dt
@@ -725,7 +746,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="resnet50_int8_b256",
-                    choices=["resnet50_int8_b256", "resnet18_int8_b1", "resnet18_int4_b16", "cfg1"])
+                    choices=[w + r for w in ("resnet50_int8_b256", "resnet18_int8_b1", "resnet18_int4_b16")
+                             for r in ("", RES_SUFFIX)] + ["cfg1"])
     ap.add_argument("--batch", type=int, default=0, help="override the batch (global for strong scaling)")
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="strong (default for N > 1): the global batch is split across GPUs; "

@@ -142,17 +142,34 @@ CONVQ_API int conv_q_s2d_pack_weights(const conv_q_plan_t *plan, const int8_t *w
 /*
  * Run the plan: y = requant(conv(x, w), scale) (or raw s32 accumulators).
  * x, w, scale, y: device pointers in the layouts above, 16-byte aligned.
- * One launch of the implicit-GEMM kernel on the plan's stream.  Allocates
- * only for a split-K config (name suffix "_k<s>": s CTAs share one output
+ * One launch of the implicit-GEMM kernel on the plan's stream.  Never
+ * allocates: a split-K config (name suffix "_k<s>": s CTAs share one output
  * tile's K loop, and meet in a plan-owned s32 workspace of
- * ceil(M/BM)*BM*K*4 bytes + counters, zeroed once and left zero by every run);
- * that allocation happens at conv_q_plan_set_config / conv_q_plan_tune / the
- * first run, never inside CUDA graph capture (EINVAL there).
+ * ceil(M/BM)*BM*K*4 bytes + counters, zeroed once and left zero by every run)
+ * gets its workspace when it is selected (conv_q_plan / _set_config /
+ * _set_epilogue / _set_residual / _tune), so a run may be graph-captured.
  * Errors: EINVAL (NULL / misaligned pointer), ECUDA (no device, launch failure).
  * One run in flight per plan is allowed (the plan caches tensor maps and owns
  * the split-K workspace).
  */
 CONVQ_API int conv_q_run(conv_q_plan_t *plan, const void *x, const void *w, const float *scale, void *y);
+
+/*
+ * Fused residual add (ABI 1.03; SURVEY 8(f) NEXT-2 -- a ResNet block's
+ * relu(bn(conv(x)) + identity); section 3.2.2 puts the elementwise
+ * "relu, batch normalization, and bias addition" in the epilogue).  With a
+ * non-NULL skip every later conv_q_run / conv_q_plan_tune computes, per
+ * output (pixel m, channel k), DESIGN reading 15:
+ *   u = fmaf((float)acc, scale[k], shift[k]);  v = fmaf((float)skip[m,k], res_scale, u)
+ *   y = clamp(rne(v), lo, hi)       (ReLU, if enabled, after the add)
+ * skip: device packed tensor in y's layout [N][P][Q][K*bits/8] (16-byte
+ * aligned, caller-owned, read only; e.g. the block input or the downsample
+ * conv's output); res_scale: one fp32 per layer.  NULL disables.  The pointer
+ * is stored in the plan (a captured CUDA graph keeps the one it was captured
+ * with).  Errors: EINVAL (misaligned skip; S32 output mode at run time),
+ * EUNSUPPORTED (s2d stem plans).
+ */
+CONVQ_API int conv_q_plan_set_residual(conv_q_plan_t *plan, const void *skip, float res_scale);
 
 /* Stream for subsequent runs (a cudaStream_t; NULL = legacy default stream). */
 CONVQ_API int conv_q_plan_set_stream(conv_q_plan_t *plan, void *stream);
@@ -223,7 +240,8 @@ CONVQ_API int conv_q_pack_weights(const int8_t *w_krsc, int K, int R, int S, int
  * Q likewise.  y[n,p,q,c] = max of x[n, p*stride-pad+r, q*stride-pad+s, c] over
  * the in-range taps (padding never wins); max of signed codes, exact.
  * Errors: EINVAL (NULL / misaligned pointer, dims < 1, pad not in [0,R),
- * empty output), EUNSUPPORTED (C*bits not a multiple of 128), ECUDA.
+ * empty output), EUNSUPPORTED (C*bits not a multiple of 128, R not in {2,3},
+ * more than 2^31 output vectors), ECUDA.
  */
 CONVQ_API int conv_q_maxpool(const void *x, int N, int H, int W, int C, int R, int stride, int pad, int bits,
                              void *y, void *stream);

@@ -33,10 +33,13 @@ def first_diff(a: np.ndarray, b: np.ndarray):
 
 
 def check_conv(x: np.ndarray, w: np.ndarray, ss: np.ndarray, L, bits: int, relu: bool, y: np.ndarray,
-               pix: np.ndarray, nthreads: int | None = None):
+               pix: np.ndarray, nthreads: int | None = None, skip: np.ndarray | None = None,
+               res_scale: float = 0.0):
     """y (packed [n,P,Q,K*b/8] from the device) vs the oracle at pixels `pix`
-    of the same n-image batch x.  Returns (ok, diff)."""
-    ref = conv_q(x, w, L.C, L.stride, L.pad, bits, ss, relu, pix=pix, nthreads=nthreads)
+    of the same n-image batch x (with `skip`: the residual epilogue, reading
+    15, adding the device's own skip bytes).  Returns (ok, diff)."""
+    ref = conv_q(x, w, L.C, L.stride, L.pad, bits, ss, relu, pix=pix, nthreads=nthreads, skip=skip,
+                 res_scale=res_scale)
     got = y.reshape(-1, y.shape[-1])[pix]
     d = first_diff(got, ref)
     return d is None, d

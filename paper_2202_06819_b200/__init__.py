@@ -110,6 +110,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.conv_q_last_error.argtypes = []
     lib.conv_q_version.restype = i
     lib.conv_q_version.argtypes = []
+    lib.conv_q_plan_set_residual.restype = i
+    lib.conv_q_plan_set_residual.argtypes = [vp, vp, f]
     lib.conv_q_maxpool.restype = i
     lib.conv_q_maxpool.argtypes = [vp, i, i, i, i, i, i, i, i, vp, vp]
     lib.conv_q_int8_peak.restype = i
@@ -177,6 +179,16 @@ class ConvPlan:
 
     def set_stream(self, stream):
         _check(load().conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
+
+    def set_residual(self, skip, res_scale: float = 0.0):
+        """Fused residual add (conv_q_plan_set_residual, DESIGN reading 15): skip is a
+        packed tensor in y's layout (kept alive by the caller), or None to disable."""
+        if skip is not None and not isinstance(skip, int):
+            if skip.numel() * skip.element_size() < self.N * self.P * self.Q * self.K * self.bits // 8:
+                raise ConvQError(EINVAL, "skip: smaller than the output tensor")
+        self._skip = skip
+        ptr = None if skip is None else _ptr(skip)
+        _check(load().conv_q_plan_set_residual(self._h, ctypes.c_void_p(ptr), float(res_scale)))
 
     def candidates(self) -> list[str]:
         lib = load()

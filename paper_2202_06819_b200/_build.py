@@ -22,7 +22,8 @@ _SFX = ("_instr" if INSTR else "") + (f"_wg{os.environ['CONVQ_EPI_WG8']}" if os.
     ("_dual" if os.environ.get("CONVQ_DUAL_MMA") == "1" else "")
 OBJ = os.path.join(HERE, "build_obj" + _SFX)
 LIB = os.path.join(HERE, f"libconvq{_SFX}.so")
-SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2)] + ["kern_b8_o4.cu", "kern_b8_o6.cu"]
+SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2, 8, 10)] + \
+    ["kern_b8_o4.cu", "kern_b8_o6.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"] + \

@@ -74,15 +74,6 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA
 
-// n / d for 0 <= n < 2^31 by multiply-high + shift (divisors fixed per launch;
-// the single-thread control loops run several per tile, and a runtime integer
-// division is ~20 dependent instructions).  m, s from make_fastdiv (plan.cuh).
-struct FastDiv {
-    uint32_t d, m, s;
-    __device__ __forceinline__ int div(int n) const {
-        return (int)((__umulhi((uint32_t)n, m) + (uint32_t)n) >> s);
-    }
-};
 
 struct ConvParams {
     int N, H, W, C, K, R, S, stride, pad;
@@ -110,6 +101,8 @@ struct ConvParams {
     int m_tiles;         // N * tiles_per_img
     int halo_tx;         // bytes of one halo TMA box
     const float *scale;  // [2K] scale then shift
+    const uint8_t *skip; // OUT_RES: packed skip tensor [M][K*BITS/8] (the output's layout), read by the epilogue
+    float res_scale;     // OUT_RES: the skip code's scale relative to the output's (DESIGN reading 15)
     int32_t *y32;        // s32 output (OUT = OUT_S32)
     uint8_t *y8;         // packed output for direct stores (OUT = OUT_DIRECT)
     int out_row;         // packed output bytes per pixel row = K*BITS/8
@@ -128,8 +121,8 @@ struct ConvParams {
 constexpr int OUT_TMA = 0;     // packed codes staged in smem, written by TMA stores
 constexpr int OUT_S32 = 1;     // raw int32 accumulators, direct global stores (debug / parity)
 constexpr int OUT_DIRECT = 2;
-constexpr int OUT_RELU = 4;    // flag: INT8 ReLU-specialised epilogue (OUT_TMA | OUT_RELU, OUT_DIRECT | OUT_RELU)  // packed codes, 16-byte direct global stores (no staging smem ->
-                               // deeper operand pipeline; L2 merges the row pieces)
+constexpr int OUT_RELU = 4;    // flag: INT8 ReLU-specialised epilogue (OUT_TMA | OUT_RELU, OUT_DIRECT | OUT_RELU)
+constexpr int OUT_RES = 8;     // flag: fused residual add (OUT_TMA | OUT_RES, OUT_DIRECT | OUT_RES; runtime ReLU)
 
 // Epilogue warpgroups (INT8: CONVQ_EPI_WG8, default 4; INT4: 2) and TMEM
 // accumulator buffers (512 columns / BN, at most 4, at most one per warpgroup);
@@ -187,6 +180,7 @@ struct ConvCfg {
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUTP = OUT & 3;                     // output path
     static constexpr bool RELU8 = BITS == 8 && (OUT & OUT_RELU) != 0;
+    static constexpr bool RES = (OUT & OUT_RES) != 0;          // residual add: v = fmaf(skip, res_scale, u)
     static constexpr int OUT_BYTES = OUTP == OUT_TMA ? BM * OUT_ROW : 0;   // staging per TMEM buffer
     static constexpr int NUM_EPI = epi_warpgroups(BITS);            // epilogue warpgroups
     // TMEM accumulator buffers: as many as the 512 columns allow (max 4), so
@@ -231,6 +225,7 @@ struct ConvCfg {
     static constexpr int NUM_THREADS = 32 * (MMA_WARP + kNumMma);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
     static constexpr bool FITS = STAGES >= 2 && (!HB || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
+                                 (!RES || (OUTP != OUT_S32 && !(OUT & OUT_RELU))) &&
                                  (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
                                  (!S2H || (WS && !HA && KCH == 64)) &&
                                  (MT == 1 || (WS && HB) || (WS && BITS == 8 && CG == 1));  // else never instantiated
@@ -990,6 +985,28 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 return ok ? (n * p.P + pp) * p.Q + qq : p.M;
             };
             if constexpr (HA || S2H) m = halo_m(row);
+            // residual (OUT_RES): the skip tensor's 16-byte chunk at (row mm, this chunk's bytes)
+            auto load_skip = [&](int mm, int c) -> uint4 {
+                const int gbyte = n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + c * 16;
+                if (mm < p.M && gbyte < p.out_row)
+                    return __ldcs(reinterpret_cast<const uint4 *>(p.skip + (int64_t)mm * p.out_row + gbyte));
+                return make_uint4(0u, 0u, 0u, 0u);
+            };
+            // OUT_RES: this thread's skip chunks of every m-group, loaded before the
+            // accumulator wait (the skip tensor is an earlier layer's output), so
+            // their latency overlaps the tile's mainloop
+            constexpr int NCH = Cfg::EPI_COLS / Cfg::CW;
+            uint4 skp[Cfg::RES ? Cfg::MT : 1][Cfg::RES ? NCH : 1];
+            if constexpr (Cfg::RES) {
+                if (p.splits == 1) {
+#pragma unroll
+                    for (int g = 0; g < Cfg::MT; ++g) {
+                        const int mg = Cfg::MT == 1 ? m : (HA || S2H) ? halo_m(g * BM + row) : mrow0 + g * BM + row;
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) skp[g][c] = load_skip(mg, c);
+                    }
+                }
+            }
             {
                 const long long t0 = trace ? clock64() : 0;
                 mbar_wait_relaxed(&acc_full[b], j & 1, p.epi_wait, p.epi_wait_ns);
@@ -1013,7 +1030,6 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             // TMEM -> registers, software-pipelined: the load of chunk c+1 is in
             // flight while chunk c is requantized (tcgen05.wait::ld waits for all
             // of this thread's loads, so each wait covers exactly one chunk).
-            constexpr int NCH = Cfg::EPI_COLS / Cfg::CW;
             auto release_acc = [&]() {   // every column of this warp is in registers
                 tc_fence_before();
                 __syncwarp();
@@ -1025,7 +1041,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             // scale/shift of this tile's columns: the buffer's smem slot (filled by
             // the MMA warp's bulk copy) or, for split-K units, global memory
             const float *ss_b = ss_stage + (3 * b + j % 3) * 2 * BN;
-            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag) {
+            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag, const uint4 sk) {
                     constexpr bool SMEM_SS = decltype(smem_tag)::value;
                     const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
                     const int col0 = n_blk * BN + ccol;
@@ -1087,6 +1103,17 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                         sb.x, sb.y, u0, u1);
                                 fma2_rn(__int2float_rn((int)v[4 * q + 2]), __int2float_rn((int)v[4 * q + 3]), sa.z,
                                         sa.w, sb.z, sb.w, u2, u3);
+                                if constexpr (Cfg::RES) {
+                                    // v = fmaf(skip, res_scale, u) (reading 15); skip byte -> exact float as
+                                    // (2^23 + (byte ^ 0x80)) - (2^23 + 128): one PRMT + one FADD per code
+                                    const uint32_t wv = (&sk.x)[q] ^ 0x80808080u;
+                                    float k0 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7650)), 8388736.f);
+                                    float k1 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7651)), 8388736.f);
+                                    float k2 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7652)), 8388736.f);
+                                    float k3 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7653)), 8388736.f);
+                                    fma2_rn(k0, k1, p.res_scale, p.res_scale, u0, u1, u0, u1);
+                                    fma2_rn(k2, k3, p.res_scale, p.res_scale, u2, u3, u2, u3);
+                                }
                                 w4[q] = pack4_f32_s8(u0, u1, u2, u3);
                                 if (relu8 || p.relu) w4[q] = relu_s8x4(w4[q]);
                             }
@@ -1097,10 +1124,25 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             for (int q = 0; q < Cfg::CW / 4; ++q) {
                                 float4 sa, sb;
                                 ss4(q, sa, sb);
-                                r[4 * q] = requant_int((int)v[4 * q] >> 8, sa.x, sb.x, lo);
-                                r[4 * q + 1] = requant_int((int)v[4 * q + 1] >> 8, sa.y, sb.y, lo);
-                                r[4 * q + 2] = requant_int((int)v[4 * q + 2] >> 8, sa.z, sb.z, lo);
-                                r[4 * q + 3] = requant_int((int)v[4 * q + 3] >> 8, sa.w, sb.w, lo);
+                                if constexpr (Cfg::RES) {
+                                    // codes 4q..4q+3 = nibbles 4(q%2).. of skip word q/2; nibble -> exact
+                                    // float as (2^23 + (nib ^ 8)) - (2^23 + 8); ReLU / clamp after the add
+                                    const uint32_t wv = (&sk.x)[q >> 1] ^ 0x88888888u;
+                                    const float sav[4] = {sa.x, sa.y, sa.z, sa.w}, sbv[4] = {sb.x, sb.y, sb.z, sb.w};
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const uint32_t nib = (wv >> (4 * (4 * (q & 1) + e))) & 0xFu;
+                                        const float kf = __fsub_rn(__uint_as_float(0x4B000000u | nib), 8388616.f);
+                                        const float u = __fmaf_rn(__int2float_rn((int)v[4 * q + e] >> 8), sav[e], sbv[e]);
+                                        const float vv = fmaxf(__fmaf_rn(kf, p.res_scale, u), lo);
+                                        asm("cvt.rni.s32.f32 %0, %1;" : "=r"(r[4 * q + e]) : "f"(vv));
+                                    }
+                                } else {
+                                    r[4 * q] = requant_int((int)v[4 * q] >> 8, sa.x, sb.x, lo);
+                                    r[4 * q + 1] = requant_int((int)v[4 * q + 1] >> 8, sa.y, sb.y, lo);
+                                    r[4 * q + 2] = requant_int((int)v[4 * q + 2] >> 8, sa.z, sb.z, lo);
+                                    r[4 * q + 3] = requant_int((int)v[4 * q + 3] >> 8, sa.w, sb.w, lo);
+                                }
                             }
                             pk = make_uint4(pack8_sat_s4(r), pack8_sat_s4(r + 8), pack8_sat_s4(r + 16),
                                             pack8_sat_s4(r + 24));
@@ -1174,7 +1216,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             va[q] = (uint32_t)__ldcg(wsr + (c * Cfg::CW + q) * 32);
                             __stcg(wsr + (c * Cfg::CW + q) * 32, 0);
                         }
-                        process(va, c, std::false_type{});
+                        process(va, c, std::false_type{}, Cfg::RES ? load_skip(m, c) : make_uint4(0u, 0u, 0u, 0u));
                     }
                     if (lane == 0) p.cnt[region] = 0u;
                 }
@@ -1186,6 +1228,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     taddr = taddr0 + g * BN;
                     if constexpr (Cfg::MT > 1) m = (HA || S2H) ? halo_m(g * BM + row) : mrow0 + g * BM + row;
                     const bool last = g == Cfg::MT - 1;
+                    auto skr = [&](int c) -> uint4 { return skp[Cfg::RES ? g : 0][Cfg::RES ? c : 0]; };
                     if constexpr (BITS == 8 && NCH % 2 == 0) {
                         // 32 columns per tcgen05.ld (two 16-byte output pieces): half
                         // the exposed TMEM-load round trips of a 16-column loop
@@ -1195,8 +1238,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             tmem_ld_issue<32>(taddr + c * Cfg::CW, v32);
                             tmem_ld_wait_regs(v32);
                             if (last && c + 2 >= NCH) release_acc();
-                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c, std::true_type{});
-                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[16]), c + 1, std::true_type{});
+                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c, std::true_type{}, skr(c));
+                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[16]), c + 1, std::true_type{},
+                                    skr(c + 1));
                         }
                     } else {
                         tmem_ld_issue<Cfg::CW>(taddr, va);
@@ -1206,13 +1250,13 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             const bool more1 = c + 1 < NCH;
                             if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
                             else if (last) release_acc();   // every column of this warp is in registers
-                            process(va, c, std::true_type{});
+                            process(va, c, std::true_type{}, skr(c));
                             if (more1) {
                                 tmem_ld_wait_regs(vb);
                                 const bool more2 = c + 2 < NCH;
                                 if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
                                 else if (last) release_acc();
-                                process(vb, c + 1, std::true_type{});
+                                process(vb, c + 1, std::true_type{}, skr(c + 1));
                                 if (more2) tmem_ld_wait_regs(va);
                             }
                         }

@@ -48,7 +48,7 @@ int set_err(int code, const char *fmt, ...) {
 
 extern "C" const char *conv_q_last_error(void) { return g_err.c_str(); }
 extern "C" int conv_q_last_status(void) { return g_status; }
-extern "C" int conv_q_version(void) { return 102; }
+extern "C" int conv_q_version(void) { return 103; }
 
 // ============================================================== driver entry points
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -96,6 +96,7 @@ static void init_device() {
     g_encode_im2col = reinterpret_cast<PFN_encodeIm2col_t>(f2);
 }
 static int ensure_ws(conv_q_plan_s *p);
+static bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 static int ensure_device() {
     std::call_once(g_init_once, init_device);
     if (g_init_status != CONV_Q_OK) return set_err(g_init_status, "%s", g_init_msg.c_str());
@@ -122,8 +123,8 @@ static std::string cand_name(const conv_q_plan_s *p, int i) {
 
 static std::string shape_key(const conv_q_plan_s *p) {
     char b[160];
-    snprintf(b, sizeof b, "N%d_H%d_W%d_C%d_K%d_R%d_S%d_st%d_p%d_b%d_sm%d_m%d_r%d", p->N, p->H, p->W, p->C, p->K, p->R,
-             p->S, p->stride, p->pad, p->bits, g_num_sms, p->out_mode, p->relu);
+    snprintf(b, sizeof b, "N%d_H%d_W%d_C%d_K%d_R%d_S%d_st%d_p%d_b%d_sm%d_m%d_r%d%s", p->N, p->H, p->W, p->C, p->K,
+             p->R, p->S, p->stride, p->pad, p->bits, g_num_sms, p->out_mode, p->relu, p->skip ? "_res" : "");
     return p->s2d ? std::string(b) + "_s2d" : std::string(b);
 }
 
@@ -509,6 +510,17 @@ extern "C" int conv_q_plan_set_epilogue(conv_q_plan_t *p, int relu, int out_mode
     return CONV_Q_OK;
 }
 
+extern "C" int conv_q_plan_set_residual(conv_q_plan_t *p, const void *skip, float res_scale) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    if (skip && !aligned16(skip)) return set_err(CONV_Q_EINVAL, "skip must be 16-byte aligned");
+    if (skip && p->s2d) return set_err(CONV_Q_EUNSUPPORTED, "no residual add on the s2d stem plan");
+    p->skip = skip;
+    p->res_scale = skip ? res_scale : 0.f;
+    apply_cache(p);
+    if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK) return ensure_ws(p);
+    return CONV_Q_OK;
+}
+
 extern "C" int conv_q_plan_num_candidates(const conv_q_plan_t *p) {
     if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
     return (int)p->cands.size();
@@ -669,7 +681,6 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
     return CONV_Q_OK;
 }
 
-static bool aligned16(const void *ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
 // Split-K workspace for the selected config: partial sums + region counters,
 // zeroed once here and left zero by every run (the kernel's last arriving warp
@@ -716,6 +727,11 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
     }
     const bool s32 = p->out_mode == CONV_Q_OUT_S32;
     const bool direct = p->cands[p->sel].direct != 0;
+    if (p->skip) {   // fused residual add (reading 15): packed output only, runtime ReLU
+        if (s32) return set_err(CONV_Q_EINVAL, "the residual add needs the packed output mode");
+        if (p->bits == 8) return direct ? dispatch_conv_8_10(p, scale, y) : dispatch_conv_8_8(p, scale, y);
+        return direct ? dispatch_conv_4_10(p, scale, y) : dispatch_conv_4_8(p, scale, y);
+    }
     if (p->bits == 8) {
         if (s32) return dispatch_conv_8_1(p, scale, y);
         if (p->relu) return direct ? dispatch_conv_8_6(p, scale, y) : dispatch_conv_8_4(p, scale, y);
@@ -874,7 +890,10 @@ extern "C" int conv_q_maxpool(const void *x, int N, int H, int W, int C, int R, 
     const int P = (H + 2 * pad - R) / stride + 1, Q = (W + 2 * pad - R) / stride + 1;
     const int vpp = (int)((int64_t)C * bits / 128);
     const int64_t total = (int64_t)N * P * Q * vpp;
-    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 1 << 30);
+    if (total >= ((int64_t)1 << 31) || (int64_t)N * H * W * vpp >= ((int64_t)1 << 40))
+        return set_err(CONV_Q_EUNSUPPORTED, "max pool output exceeds 2^31 16-byte vectors");
+    if (R != 2 && R != 3) return set_err(CONV_Q_EUNSUPPORTED, "max pool window R=%d (2 or 3 supported)", R);
+    const int grid = (int)ceil_div(total, 256);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(256);
@@ -886,10 +905,10 @@ extern "C" int conv_q_maxpool(const void *x, int N, int H, int W, int C, int R, 
     cfg.numAttrs = 1;
     const uint4 *xs = static_cast<const uint4 *>(x);
     uint4 *ys = static_cast<uint4 *>(y);
-    if (bits == 8)
-        CUDA_TRY(cudaLaunchKernelEx(&cfg, maxpool_kernel<8>, xs, ys, N, H, W, P, Q, vpp, R, stride, pad));
-    else
-        CUDA_TRY(cudaLaunchKernelEx(&cfg, maxpool_kernel<4>, xs, ys, N, H, W, P, Q, vpp, R, stride, pad));
+    const FastDiv fv = make_fastdiv(vpp), fq = make_fastdiv(Q), fp = make_fastdiv(P);
+    auto kern = bits == 8 ? (R == 3 ? maxpool_kernel<8, 3> : maxpool_kernel<8, 2>)
+                          : (R == 3 ? maxpool_kernel<4, 3> : maxpool_kernel<4, 2>);
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, xs, ys, N, H, W, P, Q, vpp, stride, pad, fv, fq, fp));
     return CONV_Q_OK;
 }
 
@@ -902,9 +921,10 @@ extern "C" int conv_q_s2d_quantize(const conv_q_plan_t *p, const void *x_fp16, f
     int rc = ensure_device();
     if (rc) return rc;
     const int64_t total = (int64_t)p->N * p->H * p->xs_W;
+    if (total >= ((int64_t)1 << 31)) return set_err(CONV_Q_EUNSUPPORTED, "s2d tensor exceeds 2^31 pixels");
     // one thread per stored s2d pixel (no grid-stride loop: every thread's loads
     // are in flight at once; the kernel is a single HBM pass)
-    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 1 << 30);
+    const int grid = (int)ceil_div(total, 256);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int PL = p->pad;
     // (even W keeps every row's 6*W-byte offset 4-byte aligned)
@@ -912,7 +932,7 @@ extern "C" int conv_q_s2d_quantize(const conv_q_plan_t *p, const void *x_fp16, f
     auto kern = p->bits == 8 ? (c3 ? s2d_quantize_kernel<8, true> : s2d_quantize_kernel<8, false>)
                              : (c3 ? s2d_quantize_kernel<4, true> : s2d_quantize_kernel<4, false>);
     kern<<<grid, 256, 0, st>>>(static_cast<const __half *>(x_fp16), static_cast<uint4 *>(xs), p->N, p->o_H, p->o_W,
-                               p->o_C, p->H, p->xs_W, PL, inv_scale);
+                               p->o_C, p->H, p->xs_W, PL, inv_scale, make_fastdiv(p->xs_W), make_fastdiv(p->H));
     CUDA_TRY(cudaGetLastError());
     return CONV_Q_OK;
 }

@@ -1,0 +1,10 @@
+// kern_b4_o8.cu -- instantiates the implicit-GEMM conv kernels for
+// BITS=4, output path OUT_TMA | OUT_RES: the fused residual-add epilogue
+// (DESIGN reading 15).  Separate translation unit only to compile in parallel.
+#include "plan.cuh"
+
+namespace convq {
+int dispatch_conv_4_8(conv_q_plan_s *p, const float *scale, void *y) {
+    return dispatch_bn_kch<4, 8>(p, scale, y);
+}
+}  // namespace convq

@@ -11,6 +11,8 @@
 #include <cstdint>
 #include <cuda_fp16.h>
 
+#include "ptx.cuh"   // FastDiv
+
 namespace convq {
 
 // q = clamp(rne(fp32(x) * inv_scale), lo, hi); NaN -> lo (max.f32 returns the
@@ -178,16 +180,15 @@ __global__ void __launch_bounds__(256) pack_weights_kernel(const int8_t *__restr
 template <int BITS, bool C3>
 __global__ void __launch_bounds__(256) s2d_quantize_kernel(const __half *__restrict__ x, uint4 *__restrict__ y,
                                                           int N, int H, int W, int C, int H2, int XW, int PL,
-                                                          float inv_scale) {
+                                                          float inv_scale, FastDiv fd_xw, FastDiv fd_h2) {
     constexpr int CP = BITS == 8 ? 4 : 8;      // channels per phase (16 bytes = 4 phases)
     const float lo = -(float)(1 << (BITS - 1)), hi = (float)((1 << (BITS - 1)) - 1);
-    const int64_t total = (int64_t)N * H2 * XW;
-    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
-         o += (int64_t)gridDim.x * blockDim.x) {
-        const int xc = (int)(o % XW);
-        const int64_t t = o / XW;
-        const int h2 = (int)(t % H2);
-        const int n = (int)(t / H2);
+    const int total = N * H2 * XW;              // < 2^31 (checked on the host)
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+        const int t = fd_xw.div(o);
+        const int xc = o - t * XW;
+        const int n = fd_h2.div(t);
+        const int h2 = t - n * H2;
         const int w2 = xc - PL;
         int q[4 * CP];
 #pragma unroll
@@ -295,42 +296,45 @@ __device__ __forceinline__ uint32_t vmax_s4x8(uint32_t a, uint32_t b) {
     const uint32_t me = __vmaxs4(ae, be), mo = __vmaxs4(ao, bo);
     return ((me >> 4) & 0x0F0F0F0Fu) | (mo & 0xF0F0F0F0u);
 }
-template <int BITS>
+template <int BITS, int R>
 __global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ x, uint4 *__restrict__ y, int N,
-                                                     int H, int W, int P, int Q, int vpp, int R, int stride,
-                                                     int pad) {
+                                                     int H, int W, int P, int Q, int vpp, int stride, int pad,
+                                                     FastDiv fd_vpp, FastDiv fd_q, FastDiv fd_p) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");   // x is the previous kernel's output
-    const int64_t total = (int64_t)N * P * Q * vpp;
-    for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < total;
-         o += (int64_t)gridDim.x * blockDim.x) {
-        const int v = (int)(o % vpp);
-        const int64_t pix = o / vpp;
-        const int q = (int)(pix % Q);
-        const int64_t t = pix / Q;
-        const int p = (int)(t % P);
-        const int n = (int)(t / P);
+    // identity of the max: the most negative code in every lane (out-of-range
+    // taps read as it, so the padding never wins: every window has an in-range tap)
+    constexpr uint32_t MINV = BITS == 8 ? 0x80808080u : 0x88888888u;
+    const int total = N * P * Q * vpp;          // < 2^31 (checked on the host)
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+        const int pix = fd_vpp.div(o);
+        const int v = o - pix * vpp;
+        const int t = fd_q.div(pix);
+        const int q = pix - t * Q;
+        const int n = fd_p.div(t);
+        const int p = t - n * P;
         const int h0 = p * stride - pad, w0 = q * stride - pad;
-        uint4 m;
-        bool any = false;
-        for (int r = 0; r < R; ++r) {
-            const int h = h0 + r;
-            if (h < 0 || h >= H) continue;
-            for (int s = 0; s < R; ++s) {
-                const int w = w0 + s;
-                if (w < 0 || w >= W) continue;
-                const uint4 a = __ldg(x + (((int64_t)n * H + h) * W + w) * vpp + v);
-                if (!any) {
-                    m = a;
-                    any = true;
-                } else if constexpr (BITS == 8) {
-                    m = make_uint4(vmax_s8x4(m.x, a.x), vmax_s8x4(m.y, a.y), vmax_s8x4(m.z, a.z), vmax_s8x4(m.w, a.w));
-                } else {
-                    m = make_uint4(vmax_s4x8(m.x, a.x), vmax_s4x8(m.y, a.y), vmax_s4x8(m.z, a.z), vmax_s4x8(m.w, a.w));
-                }
+        const uint4 *base = x + ((int64_t)n * H * W) * vpp + v;
+        uint4 a[R * R];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int s = 0; s < R; ++s) {   // all R*R loads in flight before the first max
+                const int h = h0 + r, w = w0 + s;
+                a[r * R + s] = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(base + ((int64_t)h * W + w) * vpp)
+                                                                    : make_uint4(MINV, MINV, MINV, MINV);
             }
+        uint4 m = a[0];
+#pragma unroll
+        for (int i = 1; i < R * R; ++i) {
+            if constexpr (BITS == 8)
+                m = make_uint4(vmax_s8x4(m.x, a[i].x), vmax_s8x4(m.y, a[i].y), vmax_s8x4(m.z, a[i].z),
+                               vmax_s8x4(m.w, a[i].w));
+            else
+                m = make_uint4(vmax_s4x8(m.x, a[i].x), vmax_s4x8(m.y, a[i].y), vmax_s4x8(m.z, a[i].z),
+                               vmax_s4x8(m.w, a[i].w));
         }
-        y[o] = any ? m : make_uint4(0, 0, 0, 0);
+        y[o] = m;
     }
 }
 

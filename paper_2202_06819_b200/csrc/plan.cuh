@@ -76,6 +76,8 @@ struct conv_q_plan_s {
     int row_bytes;     // C*bits/8
     int out_row;       // K*bits/8
     int relu = 0, out_mode = CONV_Q_OUT_PACKED;
+    const void *skip = nullptr;   // conv_q_plan_set_residual: fused residual add (NULL = none)
+    float res_scale = 0.f;
     cudaStream_t stream = nullptr;
     std::vector<Cand> cands;
     int sel = 0;
@@ -207,6 +209,8 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.trace = p->trace;
     prm.tl = p->tl;
     prm.scale = scale;
+    prm.skip = static_cast<const uint8_t *>(p->skip);
+    prm.res_scale = p->res_scale;
     prm.y32 = static_cast<int32_t *>(y);
     prm.y8 = static_cast<uint8_t *>(y);
     prm.out_row = p->out_row;
@@ -296,5 +300,9 @@ int dispatch_conv_8_6(conv_q_plan_s *p, const float *scale, void *y);   // OUT_D
 int dispatch_conv_4_0(conv_q_plan_s *p, const float *scale, void *y);
 int dispatch_conv_4_1(conv_q_plan_s *p, const float *scale, void *y);
 int dispatch_conv_4_2(conv_q_plan_s *p, const float *scale, void *y);
+int dispatch_conv_8_8(conv_q_plan_s *p, const float *scale, void *y);    // OUT_TMA | OUT_RES
+int dispatch_conv_8_10(conv_q_plan_s *p, const float *scale, void *y);   // OUT_DIRECT | OUT_RES
+int dispatch_conv_4_8(conv_q_plan_s *p, const float *scale, void *y);
+int dispatch_conv_4_10(conv_q_plan_s *p, const float *scale, void *y);
 
 }  // namespace convq

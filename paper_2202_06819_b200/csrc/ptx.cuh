@@ -8,6 +8,17 @@
 
 namespace convq {
 
+// n / d for 0 <= n < 2^31 by multiply-high + shift (divisors fixed per launch;
+// the single-thread control loops run several per tile, and a runtime integer
+// division is ~20 dependent instructions -- a 64-bit one ~70).  m, s from
+// make_fastdiv (plan.cuh).
+struct FastDiv {
+    uint32_t d, m, s;
+    __device__ __forceinline__ int div(int n) const {
+        return (int)((__umulhi((uint32_t)n, m) + (uint32_t)n) >> s);
+    }
+};
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

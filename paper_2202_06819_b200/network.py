@@ -30,6 +30,8 @@ class _Conv:
     layer: object           # has H, W, C, K, R, S, stride, pad, P, Q
     src: int                # index of the producing conv, -1 = the input stage's output
     relu: bool
+    skip: object            # residual: index of the conv whose output is added (-1 = input stage), or None
+    res_scale: float
     plan: ConvPlan
     w: object               # packed weights (device uint8)
     ss: object              # [scale | shift] (device float32)
@@ -92,17 +94,28 @@ class ConvNet:
         self.input_desc = f"stem {L.name} {L.R}x{L.S}/{L.stride} {L.C}->{L.K} (s2d) + maxpool {pr}x{pr}/{pst}"
 
     # ------------------------------------------------------------- conv layers
-    def add_conv(self, L, src: int, w_codes, ss, relu: bool = True, name: str | None = None) -> int:
-        """One conv layer reading the output of conv `src` (-1: the input stage)."""
+    def add_conv(self, L, src: int, w_codes, ss, relu: bool = True, name: str | None = None,
+                 skip: int | None = None, res_scale: float = 0.0) -> int:
+        """One conv layer reading the output of conv `src` (-1: the input stage);
+        with `skip`, the epilogue adds res_scale * (the output of conv `skip`)
+        before ReLU / rounding (a ResNet block's residual, DESIGN reading 15)."""
         t = self.torch
-        assert src < len(self.convs)
+        assert src < len(self.convs) and (skip is None or skip < len(self.convs))
         plan = ConvPlan(self.B, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, self.bits, relu=relu)
         wp = pack_weights(w_codes, self.bits)
         y = t.empty((self.B, L.P, L.Q, L.K * self.bits // 8), dtype=t.uint8, device=self.device)
-        key = (L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, relu)
-        self.convs.append(_Conv(name or getattr(L, "name", f"conv{len(self.convs)}"), L, src, relu, plan, wp, ss,
-                                y, key))
+        if skip is not None:
+            sk = self.net_in if skip < 0 else self.convs[skip].y
+            assert tuple(sk.shape) == tuple(y.shape), (sk.shape, y.shape)
+            plan.set_residual(sk, res_scale)
+        key = (L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, relu, skip is not None)
+        self.convs.append(_Conv(name or getattr(L, "name", f"conv{len(self.convs)}"), L, src, relu, skip, res_scale,
+                                plan, wp, ss, y, key))
         return len(self.convs) - 1
+
+    def skip_tensor(self, i: int):
+        s = self.convs[i].skip
+        return None if s is None else (self.net_in if s < 0 else self.convs[s].y)
 
     def src_tensor(self, i: int):
         s = self.convs[i].src

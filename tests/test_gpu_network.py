@@ -144,3 +144,46 @@ def test_maxpool_parity(cq, bits, N, H, W, C, R, st, pad):
     got = cq.maxpool(dev(x), C, R, st, pad, bits).cpu().numpy()
     ref = oracle.maxpool(x, C, R, st, pad, bits)
     assert np.array_equal(got, ref), check.first_diff(got, ref)
+
+
+# ----------------------------------------------------------------- residual epilogue (NEXT-2, reading 15)
+RES_SHAPES = [(wl.Layer("l1.c3", 56, 56, 64, 256, 1, 1, 1, 0), 8, 8), (wl.Layer("l4.c3", 7, 7, 512, 2048, 1, 1, 1, 0), 8, 32),
+              (wl.Layer("k96", 9, 11, 64, 96, 3, 3, 1, 1), 3, 8), (wl.Layer("l2.c2", 28, 28, 128, 128, 3, 3, 1, 1), 4, 8),
+              (wl.Layer("l1.c3", 56, 56, 64, 256, 1, 1, 1, 0), 4, 4), (wl.Layer("r18", 14, 14, 256, 256, 3, 3, 1, 1), 4, 4)]
+
+
+@pytest.mark.parametrize("L,N,bits", RES_SHAPES)
+def test_residual_every_candidate(cq, L, N, bits):
+    """conv_q_plan_set_residual: every candidate, ReLU on and off, vs the oracle's
+    reading-15 epilogue on sampled pixels (incl. the ragged tail and K edge)."""
+    if (L.K * bits) % 128:
+        pytest.skip("K*bits")
+    g = wl.rng(9, L.K + N)
+    x, w, ss = wl.layer_inputs(g, L, N, bits)
+    skip = wl.random_bytes(g, (N, L.P, L.Q, L.K * bits // 8))
+    rs = wl.res_scale(g)
+    pix = check.sample_pixels(N, L.P, L.Q, g, 256)
+    plan = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits)
+    xd, wd, sd, kd = dev(x), dev(w), dev(ss), dev(skip)
+    plan.set_residual(kd, rs)
+    y = torch.empty((N * L.P * L.Q, L.K * bits // 8), dtype=torch.uint8, device="cuda")
+    for relu in (True, False):
+        ref = oracle.conv_q(x, w, L.C, L.stride, L.pad, bits, ss, relu, pix=pix, skip=skip, res_scale=rs)
+        for ci, name in enumerate(plan.candidates()):
+            plan.set_config(ci)
+            plan.set_epilogue(relu, cq.OUT_PACKED)
+            y.fill_(0x5A)
+            plan.run(xd, wd, sd, y)
+            torch.cuda.synchronize()
+            got = y.cpu().numpy()[pix]
+            assert np.array_equal(got, ref), (name, relu, check.first_diff(got, ref))
+    plan.set_residual(None)
+    plan.set_epilogue(True, cq.OUT_PACKED)
+    plan.run(xd, wd, sd, y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy()[pix], oracle.conv_q(x, w, L.C, L.stride, L.pad, bits, ss, True, pix=pix))
+
+
+@pytest.mark.parametrize("workload", ["resnet50_int8_b256_res", "resnet18_int4_b16_res", "resnet18_int8_b1_res"])
+def test_bench_chain_residual_parity(cq, workload):
+    test_bench_chain_parity(cq, workload)

@@ -119,6 +119,62 @@ def resnet50_layers():
     return out
 
 
+def resnet18_blocks():
+    """ResNet-18 with its residual adds, in execution order: (layer, src, skip)
+    triples -- skip is the index whose output the layer's epilogue adds (-1 =
+    the layer1 input) or None.  Basic block: c1 -> [ds] -> c2 + (ds or block input)."""
+    out = []
+    prev = -1
+    chans = [(64, 56), (128, 28), (256, 14), (512, 7)]
+    cin, hin = 64, 56
+    for li, (c, hw) in enumerate(chans):
+        for b in range(2):
+            stride = 2 if (li > 0 and b == 0) else 1
+            blk_in = prev
+            name = f"l{li+1}.b{b}"
+            out.append((Layer(name + ".c1", hin, hin, cin, c, 3, 3, stride, 1), blk_in, None))
+            c1 = len(out) - 1
+            ident = blk_in
+            if stride == 2:
+                out.append((Layer(name + ".ds", hin, hin, cin, c, 1, 1, 2, 0), blk_in, None))
+                ident = len(out) - 1
+            out.append((Layer(name + ".c2", hw, hw, c, c, 3, 3, 1, 1), c1, ident))
+            prev = len(out) - 1
+            cin, hin = c, hw
+    return out
+
+
+def resnet50_blocks():
+    """ResNet-50 v1.5 with its residual adds, as (layer, src, skip) triples like
+    resnet18_blocks().  Bottleneck: c1 -> c2 -> [ds] -> c3 + (ds or block input)."""
+    out = []
+    prev = -1
+    stages = [(64, 3, 56), (128, 4, 28), (256, 6, 14), (512, 3, 7)]
+    cin, hin = 64, 56
+    for si, (width, nblk, hw) in enumerate(stages):
+        for b in range(nblk):
+            stride = 2 if (si > 0 and b == 0) else 1
+            blk_in = prev
+            name = f"l{si+1}.b{b}"
+            out.append((Layer(name + ".c1", hin, hin, cin, width, 1, 1, 1, 0), blk_in, None))
+            c1 = len(out) - 1
+            out.append((Layer(name + ".c2", hin, hin, width, width, 3, 3, stride, 1), c1, None))
+            c2 = len(out) - 1
+            ident = blk_in
+            if b == 0:
+                out.append((Layer(name + ".ds", hin, hin, cin, 4 * width, 1, 1, stride, 0), blk_in, None))
+                ident = len(out) - 1
+            out.append((Layer(name + ".c3", hw, hw, width, 4 * width, 1, 1, 1, 0), c2, ident))
+            prev = len(out) - 1
+            cin, hin = 4 * width, hw
+    return out
+
+
+def res_scale(g: np.random.Generator) -> float:
+    """The fp32 scale of a residual add's skip codes (uniform in [0.25, 0.75])."""
+    return float(np.float32(g.uniform(0.25, 0.75)))
+
+
 def paper_table1_layers():
     """PAPER.md:319-331 Table 1: the 3x3 s1 p1 convolutions of ResNet-50
     stages 2-5 (K = C), quoted at N = 8."""
