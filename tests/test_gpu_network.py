@@ -147,7 +147,7 @@ def test_maxpool_parity(cq, bits, N, H, W, C, R, st, pad):
 
 
 # ----------------------------------------------------------------- residual epilogue (NEXT-2, reading 15)
-RES_SHAPES = [(wl.Layer("l1.c3", 56, 56, 64, 256, 1, 1, 1, 0), 8, 8), (wl.Layer("l4.c3", 7, 7, 512, 2048, 1, 1, 1, 0), 8, 32),
+RES_SHAPES = [(wl.Layer("l1.c3", 56, 56, 64, 256, 1, 1, 1, 0), 8, 8), (wl.Layer("l4.c3", 7, 7, 512, 2048, 1, 1, 1, 0), 32, 8),
               (wl.Layer("k96", 9, 11, 64, 96, 3, 3, 1, 1), 3, 8), (wl.Layer("l2.c2", 28, 28, 128, 128, 3, 3, 1, 1), 4, 8),
               (wl.Layer("l1.c3", 56, 56, 64, 256, 1, 1, 1, 0), 4, 4), (wl.Layer("r18", 14, 14, 256, 256, 3, 3, 1, 1), 4, 4)]
 
