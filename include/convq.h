@@ -204,6 +204,16 @@ CONVQ_API int conv_q_plan_set_config(conv_q_plan_t *plan, int index);
 CONVQ_API int conv_q_plan_tune(conv_q_plan_t *plan, const void *x, const void *w, const float *scale,
                      void *y, int warmup, int reps);
 
+/*
+ * (ABI 1.04) Time every candidate exactly as conv_q_plan_tune does and write
+ * candidate i's per-launch time in microseconds to us[i] (host array of
+ * conv_q_plan_num_candidates floats; -1 if it did not run), WITHOUT changing
+ * the selection or the cache.  Returns the fastest index or an error code.
+ * Used by the per-shape sweep and the ablation (scripts/ablation.py).
+ */
+CONVQ_API int conv_q_plan_time_candidates(conv_q_plan_t *plan, const void *x, const void *w, const float *scale,
+                                          void *y, int warmup, int reps, float *us);
+
 /* Fill *info (host memory). */
 CONVQ_API int conv_q_plan_info(const conv_q_plan_t *plan, conv_q_info_t *info);
 
@@ -231,6 +241,21 @@ CONVQ_API int conv_q_padded_channels(int C, int bits);
  */
 CONVQ_API int conv_q_pack_weights(const int8_t *w_krsc, int K, int R, int S, int C, int bits,
                         void *w_packed, void *stream);
+
+/*
+ * Unfused epilogue (ABI 1.04): requantize + repack an s32 accumulator matrix
+ * acc [M][K] (device; e.g. conv_q_run's CONV_Q_OUT_S32 output, M = N*P*Q) into
+ * packed y [M][K*bits/8] (device) with exactly the fused epilogue's arithmetic
+ * (section 3.2.2; DESIGN readings 4-5):
+ *   y = clamp(rne(fmaf((float)acc, scale[k], shift[k])), lo, hi), lo = relu ? 0 : -2^(bits-1).
+ * A separate HBM pass (4 + bits/8 bytes per output) -- the design the fused
+ * epilogue replaces; kept for the NEXT-3 ablation (section 4.4)
+ * and for callers that need the s32 accumulators too.  scale: 2*K floats.
+ * Errors: EINVAL (NULL / misaligned pointer, M or K < 1, relu not 0/1, bits),
+ * EUNSUPPORTED (K*bits not a multiple of 128, > 2^31 output vectors), ECUDA.
+ */
+CONVQ_API int conv_q_requant(const int32_t *acc, int64_t M, int K, const float *scale, int relu, int bits, void *y,
+                             void *stream);
 
 /*
  * R x R max pooling of packed codes (ABI 1.02; the pooling glue of a ResNet

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 
 __all__ = [
     "ConvQError", "ConvPlan", "PlanInfo", "load", "quantize", "pack_weights", "padded_channels",
-    "int8_peak", "out_dim", "OUT_PACKED", "OUT_S32", "StemPlan", "maxpool",
+    "int8_peak", "out_dim", "OUT_PACKED", "OUT_S32", "StemPlan", "maxpool", "requant",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -110,6 +110,10 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.conv_q_last_error.argtypes = []
     lib.conv_q_version.restype = i
     lib.conv_q_version.argtypes = []
+    lib.conv_q_plan_time_candidates.restype = i
+    lib.conv_q_plan_time_candidates.argtypes = [vp, vp, vp, vp, vp, i, i, ctypes.POINTER(ctypes.c_float)]
+    lib.conv_q_requant.restype = i
+    lib.conv_q_requant.argtypes = [vp, ctypes.c_int64, i, vp, i, i, vp, vp]
     lib.conv_q_plan_set_residual.restype = i
     lib.conv_q_plan_set_residual.argtypes = [vp, vp, f]
     lib.conv_q_maxpool.restype = i
@@ -257,6 +261,18 @@ class ConvPlan:
                               ctypes.c_void_p(_ptr(scale)), ctypes.c_void_p(_ptr(y))))
         return y
 
+    def time_candidates(self, x, w, scale, y, warmup=3, reps=10, stream=None) -> list[float]:
+        """Per-candidate launch time in us (conv_q_plan_time_candidates); selection unchanged."""
+        self._check_buffers(x, w, scale, y)
+        lib = load()
+        _check(lib.conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
+        n = _check(lib.conv_q_plan_num_candidates(self._h))
+        arr = (ctypes.c_float * n)()
+        _check(lib.conv_q_plan_time_candidates(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)),
+                                               ctypes.c_void_p(_ptr(scale)), ctypes.c_void_p(_ptr(y)),
+                                               warmup, reps, arr))
+        return list(arr)
+
     def tune(self, x, w, scale, y, warmup=3, reps=10, stream=None) -> int:
         self._check_buffers(x, w, scale, y)
         lib = load()
@@ -341,6 +357,22 @@ def pack_weights(w_codes, bits: int, out=None, stream=None):
         out = torch.empty((K, R, S, C * bits // 8), dtype=torch.uint8, device=w_codes.device)
     _check(load().conv_q_pack_weights(ctypes.c_void_p(w_codes.data_ptr()), K, R, S, C, bits,
                                       ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream(stream))))
+    return out
+
+
+def requant(acc, scale, relu: bool, bits: int, out=None, stream=None):
+    """Unfused epilogue (conv_q_requant): int32 [..., K] accumulators -> packed uint8 [..., K*bits/8]."""
+    import torch
+    assert acc.dtype == torch.int32 and acc.is_contiguous()
+    K = acc.shape[-1]
+    M = acc.numel() // K
+    assert scale.dtype == torch.float32 and scale.is_contiguous() and scale.numel() >= 2 * K
+    if out is None:
+        out = torch.empty(tuple(acc.shape[:-1]) + (K * bits // 8,), dtype=torch.uint8, device=acc.device)
+    assert out.dtype == torch.uint8 and out.is_contiguous() and out.numel() >= M * K * bits // 8
+    _check(load().conv_q_requant(ctypes.c_void_p(acc.data_ptr()), M, K, ctypes.c_void_p(scale.data_ptr()),
+                                 int(bool(relu)), bits, ctypes.c_void_p(out.data_ptr()),
+                                 ctypes.c_void_p(_stream(stream))))
     return out
 
 

@@ -331,6 +331,62 @@ __device__ __forceinline__ uint32_t pack8_sat_s4(const int *r) {
     return pack2_s4(r[1], r[0], pack2_s4(r[3], r[2], pack2_s4(r[5], r[4], pack2_s4(r[7], r[6], 0u))));
 }
 
+// ---------------------------------------------------------------- unfused epilogue
+// Standalone requantize + repack of an s32 accumulator matrix [M][K] (the
+// conv kernel's CONV_Q_OUT_S32 output) into packed [M][K*BITS/8] -- the SAME
+// arithmetic as the fused epilogue (readings 4-5), as a separate HBM pass.  It
+// exists for the NEXT-3 ablation (fused vs unfused epilogue, PAPER.md:375-377
+// section 4.4) and as the boundary's explicit re-layout step.  One thread per
+// 16-byte output vector (16 s8 / 32 s4 codes of one row): 4 / 8 x 16-byte
+// accumulator loads, scale/shift through the read-only cache.
+template <int BITS>
+__global__ void __launch_bounds__(256) requant_kernel(const int4 *__restrict__ acc, const float *__restrict__ scale,
+                                                     uint4 *__restrict__ y, int total, int K, int vpr, int relu,
+                                                     FastDiv fd_vpr) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int CW = BITS == 8 ? 16 : 32;     // codes per 16-byte output vector
+    const float lo = relu ? 0.f : -(float)(1 << (BITS - 1));
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+        const int m = fd_vpr.div(o);
+        const int c0 = (o - m * vpr) * CW;
+        int a[CW];
+        const int4 *src = acc + ((int64_t)m * K + c0) / 4;
+#pragma unroll
+        for (int i = 0; i < CW / 4; ++i) {
+            const int4 t = __ldcs(src + i);
+            a[4 * i] = t.x; a[4 * i + 1] = t.y; a[4 * i + 2] = t.z; a[4 * i + 3] = t.w;
+        }
+        const float4 *s4 = reinterpret_cast<const float4 *>(scale + c0);
+        const float4 *h4 = reinterpret_cast<const float4 *>(scale + K + c0);
+        uint32_t w[4];
+        if constexpr (BITS == 8) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 sa = __ldg(s4 + q), sb = __ldg(h4 + q);
+                float u0, u1, u2, u3;
+                fma2_rn(__int2float_rn(a[4 * q]), __int2float_rn(a[4 * q + 1]), sa.x, sa.y, sb.x, sb.y, u0, u1);
+                fma2_rn(__int2float_rn(a[4 * q + 2]), __int2float_rn(a[4 * q + 3]), sa.z, sa.w, sb.z, sb.w, u2, u3);
+                w[q] = pack4_f32_s8(u0, u1, u2, u3);
+                if (relu) w[q] = relu_s8x4(w[q]);
+            }
+        } else {
+            int r[CW];
+#pragma unroll
+            for (int q = 0; q < CW / 4; ++q) {
+                const float4 sa = __ldg(s4 + q), sb = __ldg(h4 + q);
+                r[4 * q] = requant_int(a[4 * q], sa.x, sb.x, lo);
+                r[4 * q + 1] = requant_int(a[4 * q + 1], sa.y, sb.y, lo);
+                r[4 * q + 2] = requant_int(a[4 * q + 2], sa.z, sb.z, lo);
+                r[4 * q + 3] = requant_int(a[4 * q + 3], sa.w, sb.w, lo);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[q] = pack8_sat_s4(r + 8 * q);
+        }
+        __stcs(y + o, make_uint4(w[0], w[1], w[2], w[3]));
+    }
+}
+
 // Work unit -> (tile, k-block range).  splits == 1 (every non-split config)
 // takes the division-free branch: these run once per tile in the single-thread
 // control loops, where a few dozen extra instructions per tile show up on

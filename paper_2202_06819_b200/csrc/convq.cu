@@ -48,7 +48,7 @@ int set_err(int code, const char *fmt, ...) {
 
 extern "C" const char *conv_q_last_error(void) { return g_err.c_str(); }
 extern "C" int conv_q_last_status(void) { return g_status; }
-extern "C" int conv_q_version(void) { return 103; }
+extern "C" int conv_q_version(void) { return 104; }
 
 // ============================================================== driver entry points
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -740,16 +740,17 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
     return s32 ? dispatch_conv_4_1(p, scale, y) : direct ? dispatch_conv_4_2(p, scale, y) : dispatch_conv_4_0(p, scale, y);
 }
 
-extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y,
-                                int warmup, int reps) {
-    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
-    if (warmup < 0 || reps < 1) return set_err(CONV_Q_EINVAL, "warmup >= 0 and reps >= 1 required");
-    int rc = ensure_device();
-    if (rc) return rc;
+// Time every candidate (a7): `warmup` untimed runs, then 3 rounds of `reps`
+// back-to-back launches (PDL overlaps each launch's prologue with the previous
+// kernel, as in a layer sequence), score = the median round's mean.  us[i]
+// receives candidate i's score (or -1 if it failed to run).  Restores the
+// previous selection.  Returns the index of the fastest candidate.
+static int time_candidates(conv_q_plan_s *p, const void *x, const void *w, const float *scale, void *y, int warmup,
+                           int reps, float *us) {
     cudaEvent_t e0, e1;
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
-    int best = -1;
+    int best = -1, rc = CONV_Q_OK;
     float best_us = 0.f;
     const int saved = p->sel;
     for (int i = 0; i < (int)p->cands.size(); ++i) {
@@ -758,9 +759,6 @@ extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, 
         for (int k = 0; k < warmup; ++k)
             if ((rc = conv_q_run(p, x, w, scale, y))) break;
         if (rc) break;
-        // back-to-back launches (as in a step, where PDL overlaps each
-        // launch's prologue with the previous kernel's tail): the mean over
-        // `reps` launches, median of 3 rounds
         float rt[3];
         for (int k = 0; k < 3 && !rc; ++k) {
             cudaEventRecord(e0, p->stream);
@@ -774,27 +772,50 @@ extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, 
         }
         if (rc) break;
         std::sort(rt, rt + 3);
-        float med = rt[1];
-        if (best < 0 || med < best_us) {
+        if (us) us[i] = rt[1];
+        if (best < 0 || rt[1] < best_us) {
             best = i;
-            best_us = med;
+            best_us = rt[1];
         }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    if (rc) {
-        p->sel = saved;
-        return rc;
-    }
+    p->sel = saved;
+    if (rc) return rc;
     cudaError_t e = cudaStreamSynchronize(p->stream);
-    if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "tuning run failed: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "candidate run failed: %s", cudaGetErrorString(e));
+    return best;
+}
+
+extern "C" int conv_q_plan_time_candidates(conv_q_plan_t *p, const void *x, const void *w, const float *scale,
+                                           void *y, int warmup, int reps, float *us) {
+    if (!p || !us) return set_err(CONV_Q_EINVAL, "NULL argument");
+    if (warmup < 0 || reps < 1) return set_err(CONV_Q_EINVAL, "warmup >= 0 and reps >= 1 required");
+    int rc = ensure_device();
+    if (rc) return rc;
+    for (size_t i = 0; i < p->cands.size(); ++i) us[i] = -1.f;
+    rc = time_candidates(p, x, w, scale, y, warmup, reps, us);
+    if (rc >= 0 && p->cands[p->sel].split > 1) ensure_ws(p);
+    return rc;
+}
+
+extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y,
+                                int warmup, int reps) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    if (warmup < 0 || reps < 1) return set_err(CONV_Q_EINVAL, "warmup >= 0 and reps >= 1 required");
+    int rc = ensure_device();
+    if (rc) return rc;
+    std::vector<float> us(p->cands.size(), -1.f);
+    const int best = time_candidates(p, x, w, scale, y, warmup, reps, us.data());
+    if (best < 0) return best;
     p->sel = best;
     p->user_sel = 1;
-    p->tuned_us = best_us;
+    p->tuned_us = us[best];
+    if ((rc = ensure_ws(p))) return rc;
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
         cache_load_locked();
-        g_cache[shape_key(p)] = {cand_name(p, best), best_us};
+        g_cache[shape_key(p)] = {cand_name(p, best), us[best]};
         cache_store_locked();
     }
     return best;
@@ -872,6 +893,38 @@ extern "C" int conv_q_pack_weights(const int8_t *w, int K, int R, int S, int C, 
     else
         pack_weights_kernel<4><<<grid, 256, 0, st>>>(w, static_cast<uint4 *>(wp), n_out_vec);
     CUDA_TRY(cudaGetLastError());
+    return CONV_Q_OK;
+}
+
+// Unfused epilogue: s32 [M][K] -> packed [M][K*bits/8] (conv.cuh requant_kernel)
+extern "C" int conv_q_requant(const int32_t *acc, int64_t M, int K, const float *scale, int relu, int bits, void *y,
+                              void *stream) {
+    if (!acc || !scale || !y) return set_err(CONV_Q_EINVAL, "NULL tensor pointer");
+    if (M < 1 || K < 1) return set_err(CONV_Q_EINVAL, "M and K must be >= 1");
+    if (bits != 4 && bits != 8) return set_err(CONV_Q_EINVAL, "bits must be 4 or 8");
+    if (relu != 0 && relu != 1) return set_err(CONV_Q_EINVAL, "relu must be 0 or 1");
+    if (((int64_t)K * bits) % 128) return set_err(CONV_Q_EUNSUPPORTED, "K*bits must be a multiple of 128");
+    if (!aligned16(acc) || !aligned16(scale) || !aligned16(y)) return set_err(CONV_Q_EINVAL, "pointers must be 16-byte aligned");
+    const int vpr = (int)((int64_t)K * bits / 128);
+    if (M * vpr >= ((int64_t)1 << 31)) return set_err(CONV_Q_EUNSUPPORTED, "more than 2^31 output vectors");
+    int rc = ensure_device();
+    if (rc) return rc;
+    const int total = (int)(M * vpr);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ceil_div(total, 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int4 *a = reinterpret_cast<const int4 *>(acc);
+    uint4 *ys = static_cast<uint4 *>(y);
+    if (bits == 8)
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, requant_kernel<8>, a, scale, ys, total, K, vpr, relu, make_fastdiv(vpr)));
+    else
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, requant_kernel<4>, a, scale, ys, total, K, vpr, relu, make_fastdiv(vpr)));
     return CONV_Q_OK;
 }
 

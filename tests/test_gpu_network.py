@@ -187,3 +187,23 @@ def test_residual_every_candidate(cq, L, N, bits):
 @pytest.mark.parametrize("workload", ["resnet50_int8_b256_res", "resnet18_int4_b16_res", "resnet18_int8_b1_res"])
 def test_bench_chain_residual_parity(cq, workload):
     test_bench_chain_parity(cq, workload)
+
+
+# ----------------------------------------------------------------- unfused epilogue (NEXT-3 baseline)
+@pytest.mark.parametrize("bits", [8, 4])
+@pytest.mark.parametrize("M,K", [(1000, 256), (37, 64), (4096, 2048)])
+def test_requant_kernel_parity(cq, bits, M, K):
+    """conv_q_requant == oracle.requant on random accumulators (incl. near-ties)."""
+    import exact_fp
+    if (K * bits) % 128:
+        pytest.skip("K*bits")
+    g = np.random.default_rng(M + K + bits)
+    acc = g.integers(-(1 << 21), 1 << 21, size=(M, K)).astype(np.int32)
+    ss = wl.scale_shift(g, K, 2304, 74, 74, bits)
+    _, sc, sh = exact_fp.near_tie_cases(g, K, bits)
+    ss2 = np.concatenate([sc, sh]).astype(np.float32)
+    for s_ in (ss, ss2):
+        for relu in (False, True):
+            got = cq.requant(dev(acc), dev(s_), relu, bits).cpu().numpy()
+            ref = oracle.requant(acc, s_, relu, bits)
+            assert np.array_equal(got, ref), check.first_diff(got, ref)
