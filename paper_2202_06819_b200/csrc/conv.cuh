@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         const int nmma = p.splits == 1 && Cfg::NBUF % 2 == 0 ? kNumMma : 1;
         // smem stages per unit (uniform when splits == 1)
         const int s_unit = (WS && (HA || S2H)) ? p.num_cblk
-                         : HA ? p.num_cblk * Cfg::HST : (p.num_kb + NSUB - 1) / NSUB;
+                         : HA ? p.num_cblk * ((p.R * p.S + NSUB - 1) / NSUB) : (p.num_kb + NSUB - 1) / NSUB;
         // Whole warp (converged) waits; one elected lane issues the MMAs and
         // commits.  Descriptors: base + byte offset >> 4 in the start-address
         // field (addresses < 2^18, so the 14-bit field never carries).
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         if (rank == 0 && (!kMma1T || lane == 0) && mw < nmma) {
             const uint64_t a_desc0 = umma_desc_kmajor(smem_u32(a_s8), KCH);
             const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(b_s8), KCH);
-            // HALO (3x3): descriptor start-address delta of tap t's window, (r*Wp + s)*KCH bytes
+            // HALO: descriptor start-address delta of tap t's window, (r*Wp + s)*KCH bytes (3x3 table)
             const uint64_t a_desc_h = umma_desc_kmajor(smem_u32(halo_buf), KCH);
             uint32_t toff[9];
 #pragma unroll
@@ -810,17 +810,34 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             else mma_commit(&empty[stage]);
                         } else if (!S2H && mma_elect()) {
                             const uint64_t ad_s = a_desc0 + (uint64_t)((stage * Cfg::A_S8) >> 4);
+                            if (p.R == 3 && p.S == 3) {   // 3x3: fully unrolled, tap offsets in registers
 #pragma unroll
+                                for (int g = 0; g < Cfg::MT; ++g)   // MT2: m-group g = halo rows from 128 g
 #pragma unroll
-                            for (int g = 0; g < Cfg::MT; ++g)   // MT2: m-group g = halo rows from 128 g
+                                for (int t = 0; t < 9; ++t) {
+                                    const uint64_t ad = ad_s + toff[t] + (uint64_t)((g * BM * KCH) >> 4);
+                                    const uint64_t bd = b_desc_res + (uint64_t)(((t * p.num_cblk + cblk) * Cfg::B_TILE) >> 4);
 #pragma unroll
-                            for (int t = 0; t < 9; ++t) {
-                                const uint64_t ad = ad_s + toff[t] + (uint64_t)((g * BM * KCH) >> 4);
-                                const uint64_t bd = b_desc_res + (uint64_t)(((t * p.num_cblk + cblk) * Cfg::B_TILE) >> 4);
+                                    for (int k = 0; k < KCH / 32; ++k) {
+                                        if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                        else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                    }
+                                }
+                            } else {                       // any R x S: tap (r, s) at row offset r*Wp + s
 #pragma unroll
-                                for (int k = 0; k < KCH / 32; ++k) {
-                                    if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
-                                    else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                for (int g = 0; g < Cfg::MT; ++g) {
+                                    int t = 0;
+                                    for (int r = 0; r < p.R; ++r)
+                                        for (int s_ = 0; s_ < p.S; ++s_, ++t) {
+                                            const uint64_t ad = ad_s + (uint64_t)((uint32_t)((r * p.Wp + s_) * KCH) >> 4) +
+                                                                (uint64_t)((g * BM * KCH) >> 4);
+                                            const uint64_t bd = b_desc_res + (uint64_t)(((t * p.num_cblk + cblk) * Cfg::B_TILE) >> 4);
+#pragma unroll
+                                            for (int k = 0; k < KCH / 32; ++k) {
+                                                if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                                else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                            }
+                                        }
                                 }
                             }
                             if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
@@ -835,13 +852,24 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     // filter tap (r, s) reads the halo rows starting at r*Wp + s:
                     // the duplicate-aware load of PAPER.md Alg. 1, with the
                     // "genuine index" remap done by the UMMA descriptor start
-                    // address (3x3 filters; tap offsets precomputed in toff[])
-                    constexpr int RS = 9;
+                    // address (any R x S; the 3x3 tap offsets are precomputed in toff[])
+                    const int RS = p.R * p.S;
+                    const int hst = (RS + NSUB - 1) / NSUB;   // stages (weight groups of NSUB taps) per halo box
+                    const bool k3x3 = p.R == 3 && p.S == 3;
+                    auto tap_off = [&](int t) -> uint64_t {
+                        if (k3x3) {
+                            uint32_t o = toff[0];
+#pragma unroll
+                            for (int i = 1; i < 9; ++i) o = t == i ? toff[i] : o;   // register select, no local memory
+                            return o;
+                        }
+                        const int r = p.fd_S.div(t);
+                        return (uint64_t)((uint32_t)((r * p.Wp + (t - r * p.S)) * KCH) >> 4);
+                    };
                     for (int cblk = 0; cblk < p.num_cblk; ++cblk, ++hcount) {
                         const int hb = hcount % Cfg::NHALO;
                         const uint64_t ad_h = a_desc_h + (uint64_t)((hb * Cfg::HALO_BYTES) >> 4);
-#pragma unroll
-                        for (int g = 0; g < Cfg::HST; ++g) {
+                        auto halo_stage = [&](const int g, const int hst_) {
                             long long t0 = trace ? clock64() : 0;
                             mma_gate();
                             mbar_wait(&full[stage], phase);
@@ -856,10 +884,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             if (mma_elect()) {
                                 if (probe & 1) {
                                     mbar_arrive(&empty[stage]);
-                                    if (g == Cfg::HST - 1) mbar_arrive(&hempty[hb]);
+                                    if (g == hst_ - 1) mbar_arrive(&hempty[hb]);
                                     if constexpr (CG == 2) {
                                         mbar_arrive_cluster(mapa_shared(smem_u32(&empty[stage]), 1));
-                                        if (g == Cfg::HST - 1) mbar_arrive_cluster(mapa_shared(smem_u32(&hempty[hb]), 1));
+                                        if (g == hst_ - 1) mbar_arrive_cluster(mapa_shared(smem_u32(&hempty[hb]), 1));
                                     }
                                 } else {
                                     const uint64_t bd0 = b_desc0 + (uint64_t)((stage * Cfg::B_S8) >> 4);
@@ -867,7 +895,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                     for (int j = 0; j < NSUB; ++j) {
                                         const int t = g * NSUB + j;
                                         if (t < RS) {
-                                            const uint64_t ad = ad_h + toff[t];
+                                            const uint64_t ad = ad_h + tap_off(t);
                                             const uint64_t bd = bd0 + (uint64_t)((j * Cfg::B_SUB) >> 4);
 #pragma unroll
                                             for (int k = 0; k < KCH / 32; ++k) {
@@ -879,7 +907,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                     }
                                     if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
                                     else mma_commit(&empty[stage]);
-                                    if (g == Cfg::HST - 1) {        // last use of this halo buffer
+                                    if (g == hst_ - 1) {             // last use of this halo buffer
                                         if constexpr (CG == 2) mma_commit_cg2_mc(&hempty[hb], 0x3);
                                         else mma_commit(&hempty[hb]);
                                     }
@@ -888,7 +916,14 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             mma_sync();
                             if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                             ++gsi;
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        };
+                        if (k3x3) {   // 3x3: unrolled, tap offsets resolved at compile time
+#pragma unroll
+                            for (int g = 0; g < Cfg::HST; ++g) halo_stage(g, Cfg::HST);
+                        } else {
+#pragma unroll 1
+                            for (int g = 0; g < hst; ++g) halo_stage(g, hst);
                         }
                     }
                 } else

@@ -204,7 +204,9 @@ static void enumerate_candidates(conv_q_plan_s *p) {
     // duplicate-aware (halo) candidates: stride-1 INT8 R x S convolutions whose
     // halo box (rows covering 128 MMA rows + the largest tap shift) fits 32 KB
     const int Wp = p->W + 2 * p->pad;
-    if (p->bits == 8 && p->stride == 1 && p->R == 3 && p->S == 3 && Wp <= BM && p->C % 64 == 0) {
+    // (any R x S up to 7 x 7: tap (r, s) reads the box at row offset r*Wp + s)
+    const bool halo_ok = p->stride == 1 && p->R * p->S > 1 && p->R <= 7 && p->S <= 7 && Wp <= BM;
+    if (p->bits == 8 && halo_ok && p->C % 64 == 0) {
         const int kch = p->C % 128 == 0 ? 128 : 64;
         const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
         if ((int64_t)halo_rows * Wp * kch <= 32768 && halo_rows <= 256)
@@ -240,7 +242,7 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                             cand.halo = 8;
                             if (cand_fits<8>(cand)) p->cands.push_back(cand);
                         }
-                        if (p->stride == 1 && p->R == 3 && p->S == 3 && Wp <= BM && direct) {
+                        if (halo_ok && direct) {
                             const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
                             if ((int64_t)halo_rows * Wp * kch <= (kch == 64 ? 20480 : 32768) && halo_rows <= 256) {
                                 Cand cand{bn, kch, cg, 1, direct};

@@ -37,6 +37,7 @@ FEATURES = ["fused", "halo", "pair", "ws", "split"]
 
 
 def feats_of(name: str) -> set:
+    import re
     f = set()
     if "_h" in name:
         f.add("halo")
@@ -44,7 +45,7 @@ def feats_of(name: str) -> set:
         f.add("pair")
     if "_w" in name:
         f.add("ws")
-    if "_k" in name:
+    if re.search(r"_k\d", name):      # split-K suffix _k<s> (not the _kc<ch> field)
         f.add("split")
     return f
 
@@ -97,7 +98,13 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default="profiles/r02_ablation.json")
+    ap.add_argument("--from-raw", default="", help="recompute the tables from a saved _raw.json")
     args = ap.parse_args()
+    if args.from_raw:
+        raw = json.load(open(args.from_raw))
+        tabs = {int(b): {tuple(int(v) for v in k.strip("()").split(",")): t for k, t in d.items()}
+                for b, d in raw.items()}
+        return report(args, tabs)
     cq.load()
     layers = [L for L, _ in wl.resnet50_layers()]
     uniq = {}
@@ -109,6 +116,17 @@ def main():
             g = wl.rng(7, hash(k) % 1000)
             tabs[bits][k] = layer_table(L, args.batch, bits, g, args.reps)
             print(f"[ablation] int{bits} {L.name} {k}: {len(tabs[bits][k]['names'])} candidates", file=sys.stderr)
+    os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+    with open(args.out.replace(".json", "_raw.json"), "w") as f:   # raw per-candidate times first
+        json.dump({str(b): {str(k): v for k, v in t.items()} for b, t in tabs.items()}, f)
+    report(args, tabs)
+
+
+def report(args, tabs):
+    layers = [L for L, _ in wl.resnet50_layers()]
+    uniq = {}
+    for L in layers:
+        uniq.setdefault((L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad), L)
 
     def stage_of(L):
         return L.name.split(".")[0]

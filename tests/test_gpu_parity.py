@@ -112,6 +112,9 @@ def test_cfg1_parity_all_configs(cq, bits):
     (wl.Layer("5x5p2", 8, 8, 64, 32, 5, 5, 1, 2), 2),
     (wl.Layer("1px", 1, 1, 128, 64, 1, 1, 1, 0), 5),             # 1x1 images
     (wl.Layer("pad3", 4, 4, 32, 64, 3, 3, 1, 3), 1),             # padding larger than the filter reach
+    (wl.Layer("7x7s1", 12, 10, 64, 64, 7, 7, 1, 3), 2),          # general R x S halo (49 taps)
+    (wl.Layer("1x3", 9, 20, 128, 64, 1, 3, 1, 1), 2),            # R=1 x S=3 halo, pad rows
+    (wl.Layer("5x5c128", 11, 13, 128, 128, 5, 5, 1, 2), 3),      # 25 taps, 2 channel blocks
 ])
 def test_shape_edge_parity(cq, bits, L, N):
     if (L.K * bits) % 128:
