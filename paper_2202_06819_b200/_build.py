@@ -19,7 +19,8 @@ CSRC = os.path.join(HERE, "csrc")
 # scripts/trace.py / probe.py) -> libconvq_instr.so, loaded via CONV_Q_LIB
 INSTR = os.environ.get("CONVQ_INSTRUMENT") == "1"
 _SFX = ("_instr" if INSTR else "") + (f"_wg{os.environ['CONVQ_EPI_WG8']}" if os.environ.get("CONVQ_EPI_WG8") else "") + \
-    ("_dual" if os.environ.get("CONVQ_DUAL_MMA") == "1" else "")
+    ("_dual" if os.environ.get("CONVQ_DUAL_MMA") == "1" else "") + \
+    ("_allw0" if os.environ.get("CONVQ_EPI_ALLW") == "0" else "")
 OBJ = os.path.join(HERE, "build_obj" + _SFX)
 LIB = os.path.join(HERE, f"libconvq{_SFX}.so")
 SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2, 8, 10)] + \
@@ -29,7 +30,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"] + \
     (["-DCONVQ_INSTRUMENT"] if INSTR else []) + \
     ([f"-DCONVQ_EPI_WG8={os.environ['CONVQ_EPI_WG8']}"] if os.environ.get("CONVQ_EPI_WG8") else []) + \
-    (["-DCONVQ_DUAL_MMA=1"] if os.environ.get("CONVQ_DUAL_MMA") == "1" else [])
+    (["-DCONVQ_DUAL_MMA=1"] if os.environ.get("CONVQ_DUAL_MMA") == "1" else []) + \
+    (["-DCONVQ_EPI_ALLW=0"] if os.environ.get("CONVQ_EPI_ALLW") == "0" else [])
 
 
 def _deps():

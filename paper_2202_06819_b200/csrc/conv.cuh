@@ -135,6 +135,19 @@ constexpr int tmem_buffers(int bits, int bn) {
     return (512 / bn) < epi_warpgroups(bits) ? ((512 / bn) < 4 ? 512 / bn : 4)
                                               : (epi_warpgroups(bits) < 4 ? epi_warpgroups(bits) : 4);
 }
+// All-warps epilogue (CONVQ_EPI_ALLW, default on): with only two TMEM buffers
+// (256-column accumulators) every INT8 epilogue warpgroup drains EVERY tile
+// (BN/4 columns each) instead of half of them draining every other tile.  The
+// buffer is then drained ~2x sooner and released to the MMA warp earlier --
+// measured (profiles/r01_timeline_cta0.txt) the two-buffer 1x1 layers were
+// paced by the epilogue's per-buffer drain time, not by its instruction rate.
+#ifndef CONVQ_EPI_ALLW
+#define CONVQ_EPI_ALLW 1
+#endif
+constexpr bool epi_all_warps(int bits, int nbuf) { return CONVQ_EPI_ALLW && bits == 8 && nbuf == 2; }
+constexpr int epi_per_buf(int bits, int nbuf) {
+    return epi_all_warps(bits, nbuf) ? epi_warpgroups(bits) : epi_warpgroups(bits) / nbuf;
+}
 
 template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO = 0>
 struct ConvCfg {
@@ -170,13 +183,16 @@ struct ConvCfg {
     static constexpr int AMT = HB ? 1 : MT;                 // A sub-tiles per k-block (generic MT2: one per m-group)
     static constexpr int A_S8 = NSUB * AMT * A_SUB;         // per stage
     static constexpr int B_S8 = NSUB * B_SUB;
-    static constexpr int A_PK_SUB = BITS == 4 ? BM * LOAD_ROW : 0;
+    static constexpr int A_PK_SUB = BITS == 4 && !HB ? BM * LOAD_ROW : 0;   // (halo modes: A lives in the halo buffers)
     static constexpr int B_PK_SUB = BITS == 4 ? BNL * LOAD_ROW : 0;
     static constexpr int A_PK = NSUB * A_PK_SUB;
     static constexpr int B_PK = NSUB * B_PK_SUB;
     static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
     static constexpr int SUB_TX = ((HB ? 0 : AMT * BM) + (WS ? 0 : BNL)) * LOAD_ROW;  // TMA bytes per k-block per CTA
     static constexpr int HALO_BYTES = HA && !WS ? 32768 : 0;  // one halo buffer (budget; checked at plan time)
+    // INT4 halo: the TMA lands the packed s4 box here; the transform warps expand
+    // it once per (tile, channel block) into the s8 halo buffer (not once per tap)
+    static constexpr int HALO_PK = BITS == 4 ? HALO_BYTES / 2 : 0;
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUTP = OUT & 3;                     // output path
     static constexpr bool RELU8 = BITS == 8 && (OUT & OUT_RELU) != 0;
@@ -186,7 +202,8 @@ struct ConvCfg {
     // TMEM accumulator buffers: as many as the 512 columns allow (max 4), so
     // up to NBUF tiles are in the epilogue while the MMA fills the next one
     static constexpr int NBUF = tmem_buffers(BITS, TBW);
-    static constexpr int EPI_PER_BUF = NUM_EPI / NBUF;              // warpgroups per TMEM buffer
+    static constexpr bool ALLW = epi_all_warps(BITS, NBUF);         // every warpgroup drains every buffer
+    static constexpr int EPI_PER_BUF = epi_per_buf(BITS, NBUF);     // warpgroups per TMEM buffer
     static constexpr int EPI_COLS = BN / EPI_PER_BUF;               // columns one warp drains (of its 32 rows)
     static constexpr int EPI_ROW = EPI_COLS * BITS / 8;             // packed bytes of one row of a warp's slab
     static constexpr int EPI_SUBW = EPI_ROW < 128 ? EPI_ROW : 128;  // TMA store box width (= swizzle span)
@@ -203,7 +220,8 @@ struct ConvCfg {
     static constexpr int SS_BYTES = OUTP == OUT_S32 ? 0 : 3 * 8 * BN;
     static constexpr int BAR_BYTES = 1024;
     static constexpr int stages_with(int nhalo) {
-        return (SMEM_LIMIT - 1024 - BAR_BYTES - WSB - NBUF * (OUT_BYTES + SS_BYTES) - nhalo * HALO_BYTES) / STAGE_BYTES;
+        return (SMEM_LIMIT - 1024 - BAR_BYTES - WSB - NBUF * (OUT_BYTES + SS_BYTES) - nhalo * (HALO_BYTES + HALO_PK)) /
+               STAGE_BYTES;
     }
     // halo buffers in flight: the halo load of tile t+NHALO-1 overlaps tiles
     // t..t+NHALO-2, so more buffers hide more TMA latency; keep >= 2 tiles of
@@ -212,7 +230,8 @@ struct ConvCfg {
     static constexpr int NHALO = !HA || WS ? 0 : stages_with(4) >= 2 * HST ? 4 : stages_with(3) >= 2 * HST ? 3 : 2;
     static constexpr int STAGES_FIT = stages_with(NHALO);
     static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
-    static constexpr int SMEM = 1024 + WSB + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * HALO_BYTES + BAR_BYTES;
+    static constexpr int SMEM = 1024 + WSB + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) +
+                                NHALO * (HALO_BYTES + HALO_PK) + BAR_BYTES;
     static constexpr int TMEM_COLS = NBUF * TBW < 32 ? 32 : NBUF * TBW;
     // Warp layout: epilogue warpgroups first, then (INT4) the transform
     // warpgroup, then the TMA producer and the MMA issuer as the two highest
@@ -224,7 +243,8 @@ struct ConvCfg {
     static constexpr int MMA_WARP = PROD_WARP + 1;
     static constexpr int NUM_THREADS = 32 * (MMA_WARP + kNumMma);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
-    static constexpr bool FITS = STAGES >= 2 && (!HB || (BITS == 8 && OUTP != OUT_TMA)) && (BITS == 8 || !(OUT & OUT_RELU)) &&
+    static constexpr bool FITS = STAGES >= 2 && (!HB || (OUTP != OUT_TMA && (BITS == 8 || (HA && !WS)))) &&
+                                 (BITS == 8 || !(OUT & OUT_RELU)) &&
                                  (!RES || (OUTP != OUT_S32 && !(OUT & OUT_RELU))) &&
                                  (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
                                  (!S2H || (WS && !HA && KCH == 64)) &&
@@ -476,7 +496,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [NBUF][EPB][4 quads] slabs [EPI_NSUB][32][EPI_SUBW]
     float *ss_stage = reinterpret_cast<float *>(out_stage + Cfg::NBUF * Cfg::OUT_BYTES);  // [NBUF][3 slots][2][BN]
     uint8_t *halo_buf = out_stage + Cfg::NBUF * (Cfg::OUT_BYTES + Cfg::SS_BYTES);   // HALO: [NHALO][HALO_BYTES]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(halo_buf + Cfg::NHALO * Cfg::HALO_BYTES);
+    uint8_t *halo_pk = halo_buf + Cfg::NHALO * Cfg::HALO_BYTES;  // INT4 halo: [NHALO][HALO_PK] packed boxes
+    uint64_t *bars = reinterpret_cast<uint64_t *>(halo_pk + Cfg::NHALO * Cfg::HALO_PK);
     uint64_t *full = bars;                  // TMA -> (transform | MMA)
     uint64_t *empty = bars + STAGES;        // MMA -> TMA
     uint64_t *ready = bars + 2 * STAGES;    // transform -> MMA (INT4)
@@ -628,10 +649,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 {
                                     mbar_arrive_expect_tx(&full[stage], tx);
                                     if (tap == 0)
-                                        tma_load_4d(halo_buf + hb * Cfg::HALO_BYTES, &tm_a, &full[stage],
-                                                    cblk * Cfg::LOAD_ROW, -p.pad, p0 - p.pad, n, pol_a);
+                                        tma_load_4d(BITS == 4 ? halo_pk + hb * Cfg::HALO_PK : halo_buf + hb * Cfg::HALO_BYTES,
+                                                    &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, -p.pad, p0 - p.pad, n, pol_a);
                                     for (int j = 0; j < nsub; ++j)
-                                        tma_load_2d(b_s8 + stage * Cfg::B_S8 + j * Cfg::B_SUB, &tm_b, &full[stage],
+                                        tma_load_2d(b_dst + stage * B_LD + j * B_LD_SUB, &tm_b, &full[stage],
                                                     (tap + j) * p.row_bytes + cblk * Cfg::LOAD_ROW, brow, pol_b);
                                 }
                             }
@@ -872,7 +893,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                         auto halo_stage = [&](const int g, const int hst_) {
                             long long t0 = trace ? clock64() : 0;
                             mma_gate();
-                            mbar_wait(&full[stage], phase);
+                            mbar_wait(BITS == 4 ? &ready[stage] : &full[stage], phase);   // INT4: expanded
                             if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's half of the stage
                             mma_mark();
                             if (trace && lane == 0) {
@@ -1029,13 +1050,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         // anywhere in the epilogue.  In a CTA pair each CTA drains its own 128
         // rows (its TMEM half) and releases the leader's buffer.
         constexpr int EPB = Cfg::EPI_PER_BUF;
+        constexpr bool ALLW = Cfg::ALLW;
         const int e = (warp - Cfg::EPI_WARP0) >> 2;
-        const int b = e / EPB;                     // TMEM buffer
-        const int half = e % EPB;                  // column part
+        const int b0 = ALLW ? 0 : e / EPB;         // first TMEM buffer (ALLW: every buffer in turn)
+        const int half = ALLW ? e : e % EPB;       // column part
         const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
         const int row = quad * 32 + lane;          // tile row = output pixel
+        int b = b0;                                // this unit's TMEM buffer
         uint8_t *slab = out_stage + b * Cfg::OUT_BYTES + (half * 4 + quad) * Cfg::SLAB;
-        const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(&acc_empty[b]), 0) : 0;
+        uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(&acc_empty[b]), 0) : 0;
         const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
         const uint64_t out_pol = p.out_policy == 1 ? policy_evict_last() : p.out_policy == 2 ? policy_evict_first() : 0;
         constexpr bool relu8 = Cfg::RELU8;   // ReLU specialisation (p.relu == 1 guaranteed by the dispatch)
@@ -1043,23 +1066,33 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         // buffer's first warp one tile ahead (see SS_BYTES)
         const bool ss_smem = Cfg::OUTP != OUT_S32 && p.splits == 1;
         const bool ss_issuer = ss_smem && half == 0 && quad == 0;
-        auto ss_issue = [&](int u, int jj) {
+        auto ss_issue = [&](int u, int bb, int jj) {
             if (u < p.num_units && elect_one()) {
                 const int n0 = (u - p.fd_ntiles.div(u) * p.n_tiles) * BN;
                 const uint32_t bytes = 4u * (uint32_t)min(BN, p.K - n0);
-                uint64_t *barp = &ss_full[3 * b + jj % 3];
+                uint64_t *barp = &ss_full[3 * bb + jj % 3];
                 const uint32_t bar = smem_u32(barp);
-                const uint32_t dst = smem_u32(ss_stage + (3 * b + jj % 3) * 2 * BN);
+                const uint32_t dst = smem_u32(ss_stage + (3 * bb + jj % 3) * 2 * BN);
                 mbar_arrive_expect_tx(barp, 2 * bytes);
                 bulk_load_g2s(dst, p.scale + n0, bytes, bar);
                 bulk_load_g2s(dst + 4 * BN, p.scale + p.K + n0, bytes, bar);
             }
             __syncwarp();
         };
-        if (ss_issuer && !(probe & 4)) ss_issue(tile0 + b * tstep, 0);   // constants: before the PDL wait
+        if (ss_issuer && !(probe & 4))   // constants: before the PDL wait
+            for (int bb = ALLW ? 0 : b0; bb < (ALLW ? Cfg::NBUF : b0 + 1); ++bb) ss_issue(tile0 + bb * tstep, bb, 0);
         pdl_wait();   // outputs are written only after the previous kernel completed
-        int j = 0;
-        for (int unit = tile0 + b * tstep; unit < p.num_units; unit += Cfg::NBUF * tstep, ++j) {
+        int j = 0;    // this unit's index among the units of its buffer
+        for (int unit = tile0 + b0 * tstep, lu = 0; unit < p.num_units;
+             unit += (ALLW ? 1 : Cfg::NBUF) * tstep, ++lu) {
+            if constexpr (ALLW) {
+                b = lu % Cfg::NBUF;
+                j = lu / Cfg::NBUF;
+                slab = out_stage + b * Cfg::OUT_BYTES + (half * 4 + quad) * Cfg::SLAB;
+                if constexpr (CG == 2) acc_empty_leader = mapa_shared(smem_u32(&acc_empty[b]), 0);
+            } else {
+                j = lu;
+            }
             const int tile = p.splits == 1 ? unit : p.fd_splits.div(unit);
             const int m_blk = p.fd_ntiles.div(tile), n_blk = tile - m_blk * p.n_tiles;
             const int mrow0 = m_blk * (BM * CG * Cfg::AMT) + (int)rank * BM;
@@ -1116,7 +1149,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
                 continue;
             }
-            if (ss_issuer) ss_issue(unit + Cfg::NBUF * tstep, j + 1);
+            if (ss_issuer) ss_issue(unit + Cfg::NBUF * tstep, b, j + 1);
             const uint32_t taddr0 = tmem_base + ((uint32_t)(quad * 32) << 16) + b * Cfg::TBW + half * Cfg::EPI_COLS;
             // TMEM -> registers, software-pipelined: the load of chunk c+1 is in
             // flight while chunk c is requantized (tcgen05.wait::ld waits for all
@@ -1362,7 +1395,39 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 #undef CONVQ_TL
     } else if (warp < Cfg::PROD_WARP) {
         // =========================== INT4 transform =========================
-        if constexpr (BITS == 4) {
+        if constexpr (BITS == 4 && HA) {
+            // halo mode: per (tile, channel block) the first stage carries the packed
+            // halo box -> expanded ONCE into the s8 halo buffer the filter taps'
+            // shifted descriptors read; every stage carries NSUB taps' weights
+            const int tid = threadIdx.x - 32 * Cfg::XF_WARP0;  // 0..127
+            const uint32_t ready0 = CG == 2 ? mapa_shared(smem_u32(&ready[0]), 0) : 0;
+            const int RS = p.R * p.S;
+            const int halo_pix = p.halo_tx / Cfg::LOAD_ROW;  // box rows x Wp pixels
+            int stage = 0, hcount = 0;
+            uint32_t phase = 0;
+            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+                for (int cblk = 0; cblk < p.num_cblk; ++cblk, ++hcount) {
+                    const int hb = hcount % Cfg::NHALO;
+                    for (int tap = 0; tap < RS; tap += NSUB) {
+                        const int nsub = min(NSUB, RS - tap);
+                        mbar_wait(&full[stage], phase);
+                        if (tap == 0)
+                            expand_tile<KCH>(halo_pk + hb * Cfg::HALO_PK, halo_buf + hb * Cfg::HALO_BYTES, halo_pix,
+                                             tid, 128);
+                        for (int j = 0; j < nsub; ++j)
+                            expand_kblock<KCH, 0, Cfg::BNL, 128>(nullptr, nullptr, b_pk + stage * Cfg::B_PK + j * Cfg::B_PK_SUB,
+                                                                b_s8 + stage * Cfg::B_S8 + j * Cfg::B_SUB, tid);
+                        fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.mma
+                        __syncwarp();
+                        if (lane == 0) {
+                            if constexpr (CG == 2) mbar_arrive_cluster(ready0 + 8u * stage);
+                            else mbar_arrive(&ready[stage]);
+                        }
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        } else if constexpr (BITS == 4) {
             const int tid = threadIdx.x - 32 * Cfg::XF_WARP0;  // 0..127
             const uint32_t ready0 = CG == 2 ? mapa_shared(smem_u32(&ready[0]), 0) : 0;
             int stage = 0;

@@ -182,22 +182,43 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                     const Cand cand{bn, kch, cg, nsub, direct};
                     if (!(p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand))) continue;
                     p->cands.push_back(cand);
-                    // split-K variants when the tiles fill fewer than two waves:
-                    // ~1 and ~2 work units per SM, each unit >= 2 stages of K
+                    // split-K variants (K among the tiled loops), each unit >= 2
+                    // stages of K: when the tiles fill fewer than two waves, ~1 and ~2 work
+                    // units per SM; up to six waves, the (at most two) splits that cut the
+                    // wave-quantisation loss of the last partial wave the most
                     const int64_t tiles = ceil_div(p->M, 128 * cg) * ceil_div(p->K, bn);
                     const int64_t num_kb = (int64_t)p->R * p->S * (p->C / kch);
                     const int sms = g_num_sms > 0 ? g_num_sms : 148;
+                    const int64_t slots = sms / cg;
                     const int64_t ws = tiles * cg * 128 * bn * 4;
-                    if (tiles >= 2 * sms / cg || ws > ((int64_t)64 << 20) || 16 * num_kb >= ((int64_t)1 << 31)) continue;
-                    int last = 1;
-                    for (int waves : {1, 2}) {
-                        int sp = (int)std::min<int64_t>(ceil_div((int64_t)waves * sms / cg, tiles), 16);
-                        sp = (int)std::min<int64_t>(sp, num_kb / (2 * nsub));
-                        if (sp <= last) continue;
-                        Cand sc = cand;
-                        sc.split = sp;
-                        p->cands.push_back(sc);
-                        last = sp;
+                    if (tiles >= 6 * slots || ws > ((int64_t)64 << 20) || 16 * num_kb >= ((int64_t)1 << 31)) continue;
+                    const int max_sp = (int)std::min<int64_t>(16, num_kb / (2 * nsub));
+                    if (tiles < 2 * slots) {
+                        int last = 1;
+                        for (int waves : {1, 2}) {
+                            int sp = (int)std::min<int64_t>(ceil_div((int64_t)waves * slots, tiles), max_sp);
+                            if (sp <= last) continue;
+                            Cand sc = cand;
+                            sc.split = sp;
+                            p->cands.push_back(sc);
+                            last = sp;
+                        }
+                    } else {
+                        auto eff = [&](int64_t units) {   // busy fraction of the last (partial) wave's slots
+                            const double w = (double)units / (double)slots;
+                            return w / std::ceil(w);
+                        };
+                        const double e1 = eff(tiles);
+                        std::vector<std::pair<double, int>> opts;
+                        for (int sp : {2, 3, 4, 6, 8})
+                            if (sp <= max_sp && tiles * sp <= 12 * slots && eff(tiles * sp) > e1 + 0.12)
+                                opts.push_back({-eff(tiles * sp) + 0.01 * sp, sp});
+                        std::sort(opts.begin(), opts.end());
+                        for (size_t i = 0; i < opts.size() && i < 2; ++i) {
+                            Cand sc = cand;
+                            sc.split = opts[i].second;
+                            p->cands.push_back(sc);
+                        }
                     }
                 }
             }
@@ -206,7 +227,8 @@ static void enumerate_candidates(conv_q_plan_s *p) {
     const int Wp = p->W + 2 * p->pad;
     // (any R x S up to 7 x 7: tap (r, s) reads the box at row offset r*Wp + s)
     const bool halo_ok = p->stride == 1 && p->R * p->S > 1 && p->R <= 7 && p->S <= 7 && Wp <= BM;
-    if (p->bits == 8 && halo_ok && p->C % 64 == 0) {
+    // (INT4: the packed box is expanded once per (tile, channel block) by the transform warps)
+    if (halo_ok && p->C % 64 == 0) {
         const int kch = p->C % 128 == 0 ? 128 : 64;
         const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
         if ((int64_t)halo_rows * Wp * kch <= 32768 && halo_rows <= 256)
@@ -216,7 +238,7 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                         if (bn > 64 && bn / 2 >= p->K) continue;
                         Cand cand{bn, kch, cg, nsub, 1};
                         cand.halo = 1;
-                        if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                        if (p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand)) p->cands.push_back(cand);
                     }
     }
     // weight-stationary candidates (INT8): the CTA's whole (BN/CG) x R*S*C
@@ -665,7 +687,8 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
         // one box = one epilogue warp's 32-row slab (or a 128-byte column block of it)
         const int num_epi = epi_warpgroups(p->bits);
         const int nbuf = tmem_buffers(p->bits, ((c.halo & 8) ? 2 : 1) * c.bn);   // the kernel's rule (MT2: 2*BN TMEM columns per buffer)
-        const int epb = num_epi / nbuf;
+        const int epb = epi_per_buf(p->bits, nbuf);   // the kernel's rule (all-warps epilogue for 2 buffers)
+        (void)num_epi;
         const int epi_row = c.bn / epb * p->bits / 8;
         const int subw = epi_row < 128 ? epi_row : 128;
         cuuint64_t dims[2] = {(cuuint64_t)p->out_row, (cuuint64_t)p->M};
