@@ -226,7 +226,9 @@ static void enumerate_candidates(conv_q_plan_s *p) {
     // halo box (rows covering 128 MMA rows + the largest tap shift) fits 32 KB
     const int Wp = p->W + 2 * p->pad;
     // (any R x S up to 7 x 7: tap (r, s) reads the box at row offset r*Wp + s)
-    const bool halo_ok = p->stride == 1 && p->R * p->S > 1 && p->R <= 7 && p->S <= 7 && Wp <= BM;
+    // (not for the s2d stem plans: their stored tensor has its own window geometry, handled by
+    // enumerate_s2d_halo; a regular halo box over it would not match the kernel's byte count)
+    const bool halo_ok = !p->s2d && p->stride == 1 && p->R * p->S > 1 && p->R <= 7 && p->S <= 7 && Wp <= BM;
     // (INT4: the packed box is expanded once per (tile, channel block) by the transform warps)
     if (halo_ok && p->C % 64 == 0) {
         const int kch = p->C % 128 == 0 ? 128 : 64;

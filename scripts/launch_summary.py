@@ -1,8 +1,13 @@
-"""Summarise an ncu launch list (--metrics gpu__time_duration.sum,dram__bytes_read.sum,
-dram__bytes_write.sum --csv) of bench.py: the last complete step (quantize + the
-conv launches), each launch's cold-cache time, share of the step and DRAM bytes.
+"""Summarise an ncu launch list of bench.py (--csv, metrics below): the last
+complete step -- the input stage (s2d quantize + stem conv + max pool, or
+quantize) and every conv launch -- with each launch's cold-cache time, its
+share of the step, DRAM bytes, tensor-pipe utilisation and issue activity.
 
-python scripts/launch_summary.py gpurun_out/r01_launches.csv resnet50_int8_b256 > profiles/...txt
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,\
+sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,\
+smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none --csv ...
+  python scripts/launch_summary.py launches.csv resnet50_int8_b256 > profiles/r02_launches_....txt
+
 Also writes profiles/traffic_<workload>.json (conv DRAM bytes per step), which
 bench.py reports as roofline.traffic."""
 import csv
@@ -13,7 +18,10 @@ from collections import OrderedDict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import workloads as wl  # noqa: E402
+import bench  # noqa: E402
+
+TENSOR = "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"
+ISSUE = "smsp__issue_active.avg.pct_of_peak_sustained_active"
 
 
 def main(path, workload):
@@ -23,42 +31,44 @@ def main(path, workload):
     for r in rows[1:]:
         d = dict(zip(h, r))
         e = ks.setdefault(d["ID"], {"name": d["Kernel Name"], "grid": d["Grid Size"], "block": d["Block Size"]})
-        e[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
-    ks = list(ks.values())
-    layers = {"resnet50_int8_b256": wl.resnet50_layers, "resnet18_int8_b1": wl.resnet18_layers,
-              "resnet18_int4_b16": wl.resnet18_layers}[workload]()
-    n = len(layers)
-    # last quantize launch followed by n conv launches
+        try:
+            e[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+        except ValueError:
+            pass
+    ks = [k for k in ks.values() if any(t in k["name"] for t in ("conv_igemm", "quantize", "maxpool"))]
+    spec = bench.workload_spec(workload)
+    convs = [t[0] for t in spec.layers]
+    n = len(convs)
+    head = ["s2d_quantize", "conv_igemm", "maxpool"] if spec.conv1 is not None else ["quantize"]
+    pattern = head + ["conv_igemm"] * n
     start = None
-    for i in range(len(ks) - n - 1, -1, -1):
-        if "quantize" in ks[i]["name"] and all("conv_igemm" in ks[i + 1 + j]["name"] for j in range(n)):
+    for i in range(len(ks) - len(pattern), -1, -1):
+        if all(pattern[j] in ks[i + j]["name"] for j in range(len(pattern))):
             start = i
             break
     assert start is not None, "no complete step in the launch list"
-    step = ks[start:start + n + 1]
-    unit = 1e-3  # gpu__time_duration.sum is in ns -> us
-    tot = sum(k["gpu__time_duration.sum"] for k in step) * unit
-    conv = step[1:]
-    conv_t = sum(k["gpu__time_duration.sum"] for k in conv) * unit
-    conv_b = sum(k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for k in conv)
-    print(f"# ncu launch list, {workload}: last complete step = launches {start}..{start + n} of {len(ks)}")
-    print("# cold-cache, serialised kernel times (ncu --clock-control none); the bench's timed step is warm and")
-    print("# PDL-overlapped, so compare SHARES, not absolutes")
-    print(f"{'#':>3} {'layer':10s} {'kernel (template args)':58s} {'grid':>12s} {'us':>9s} {'share':>6s} {'DRAM MB':>9s}")
-    names = ["quantize"] + [L.name for L, _ in layers]
-    for i, k in enumerate(step):
-        nm = k["name"].replace("void convq::", "")
-        nm = nm[:nm.find("(")] if "(" in nm else nm
-        t = k["gpu__time_duration.sum"] * unit
-        b = (k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]) / 1e6
-        print(f"{i:3d} {names[i]:10s} {nm[:58]:58s} {k['grid']:>12s} {t:9.1f} {t / tot:6.1%} {b:9.1f}")
-    print(f"step total {tot:.1f} us; conv_igemm_kernel {conv_t:.1f} us ({conv_t / tot:.1%} of the step), "
-          f"DRAM {conv_b / 1e9:.3f} GB per step")
+    step = ks[start:start + len(pattern)]
+    names = (["s2d quantize", "conv1 (stem)", "maxpool"] if spec.conv1 is not None else ["quantize"]) + \
+        [L.name for L in convs]
+    us = [k["gpu__time_duration.sum"] * 1e-3 for k in step]
+    tot = sum(us)
+    conv_idx = [i for i, k in enumerate(step) if "conv_igemm" in k["name"]]
+    conv_us = sum(us[i] for i in conv_idx)
+    dram = [k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0) for k in step]
+    conv_dram = sum(dram[i] for i in conv_idx)
+    print(f"# ncu launch list ({os.path.basename(path)}), last complete step of {workload}: "
+          f"{len(step)} launches, {tot:.1f} us summed (cold-cache, serialised)")
+    print(f"# conv_igemm_kernel share of the step: {100 * conv_us / tot:.1f} % ({conv_us:.1f} us); "
+          f"conv DRAM bytes/step {conv_dram / 1e9:.3f} GB")
+    print(f"{'launch':14s} {'us':>8s} {'share%':>7s} {'DRAM MB':>9s} {'tensor%':>8s} {'issue%':>7s}  kernel")
+    for nm, k, t, d in zip(names, step, us, dram):
+        print(f"{nm:14s} {t:8.2f} {100 * t / tot:7.2f} {d / 1e6:9.1f} {k.get(TENSOR, float('nan')):8.1f} "
+              f"{k.get(ISSUE, float('nan')):7.1f}  {k['name'][:70]}")
     out = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
-    json.dump({"source": os.path.basename(path), "workload": workload,
-               "dram_bytes_per_step": int(conv_b), "conv_launches": n,
-               "conv_kernel_us_cold": round(conv_t, 1), "step_kernel_us_cold": round(tot, 1),
-               "conv_share_cold": round(conv_t / tot, 4)}, open(out, "w"), indent=1)
+    with open(out, "w") as f:
+        json.dump({"source": os.path.basename(path), "dram_bytes_per_step": int(conv_dram),
+                   "conv_us_per_step_cold": round(conv_us, 2), "launches": len(step),
+                   "conv_share_of_step": round(conv_us / tot, 4)}, f, indent=1)
 
 
 if __name__ == "__main__":

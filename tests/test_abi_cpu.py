@@ -110,6 +110,11 @@ def test_stem_s2d_plan_geometry(lib):
         assert ei.value.code == code, args
     i0 = cq.ConvPlan(1, 8, 8, 64, 64, 3, 3, 1, 1, 8).info()
     assert i0.s2d == 0 and i0.x_dims == (1, 8, 8, 64) and i0.w_dims == (64, 3, 3, 64)
+    # the only duplicate-aware candidates of an s2d plan are its window-halo ones
+    # (a regular halo box over the stored s2d tensor would not match the kernel's
+    # TMA byte count -- a round-2 regression that hung a GPU test)
+    for plan in (p, q, r):
+        assert all("_h_w" in n for n in plan.candidates() if "_h" in n), plan.candidates()
 
 
 def test_candidates_and_selection(lib):
