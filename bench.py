@@ -355,8 +355,25 @@ def run_ours(args):
             e[k[0]].record(stream)
         net.step(stream, cb)
 
+    # conv-chain window: events only at the step start, after the input stage and
+    # at the step end, so the conv launches between them keep their PDL overlap
+    # exactly as in the plain graph (the roofline's kernel time)
+    n_in_st = len(net.stage_names)
+    evc = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)] for _ in range(n_ev)]
+
+    def chain_step(e):
+        k = [0]
+        e[0].record(stream)
+
+        def cb(tag):
+            k[0] += 1
+            if k[0] == n_in_st:
+                e[1].record(stream)
+        net.step(stream, cb)
+        e[2].record(stream)
+
     use_graph = not args.no_graph
-    graph, graphs_ev = None, None
+    graph, graphs_ev, graphs_ch = None, None, None
     if use_graph:
         try:
             graph = torch.cuda.CUDAGraph()
@@ -368,13 +385,20 @@ def run_ours(args):
                 with torch.cuda.graph(ge, stream=stream):
                     ev_step(e)
                 graphs_ev.append(ge)
+            graphs_ch = []
+            for e in evc:
+                gc = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gc, stream=stream):
+                    chain_step(e)
+                graphs_ch.append(gc)
             for _ in range(args.warmup):
                 graph.replay()
             torch.cuda.synchronize()
         except Exception as ex:  # fall back to eager launches
             print(f"[bench] CUDA graph capture failed ({ex}); eager launches", file=sys.stderr)
-            use_graph, graph, graphs_ev = False, None, None
+            use_graph, graph, graphs_ev, graphs_ch = False, None, None, None
             evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nl + 1)] for _ in range(n_ev)]
+            evc = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n_ev)]
 
     # ---- timed region: exactly K plain steps, barrier + sync on both sides
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -402,7 +426,13 @@ def run_ours(args):
             graphs_ev[j].replay()
         else:
             ev_step(evs[j])
+    for j in range(n_ev):
+        if use_graph:
+            graphs_ch[j].replay()
+        else:
+            chain_step(evc[j])
     torch.cuda.synchronize()
+    chain_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evc)
     per_launch_ms = [statistics.mean(e[k].elapsed_time(e[k + 1]) for e in evs) for k in range(nl)]
     ev_step_ms = statistics.mean(e[0].elapsed_time(e[nl]) for e in evs)
     n_in = len(net.stage_names)
@@ -423,7 +453,9 @@ def run_ours(args):
     hbm_peak = peaks["hbm_gbs"]
     bits = spec.bits
     conv_layers = [c.layer for c in net.convs]
-    conv_ms = sum(per_layer_ms) + in_ms.get("stem", 0.0)
+    # the conv launches of a step: the layer chain timed as one PDL-overlapped
+    # segment (conv-chain window) + conv1 from the per-launch window
+    conv_ms = chain_ms + in_ms.get("stem", 0.0)
     ops_step = sum(layer_ops(L, B) for L in conv_layers) + (layer_ops(spec.conv1, B) if net.stem else 0)
     bytes_step = sum(layer_bytes(L, B, bits) for L in conv_layers)
     achieved_tops = ops_step / (conv_ms * 1e-3) / 1e12
@@ -502,7 +534,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2: per-step working set %.2f GB >> 126 MB L2" % (
                            (bytes_step + net.x_in.numel() * 2) / 1e9),
                        "launch": "CUDA graph per step (PDL between kernels)" if use_graph else "eager launches",
-                       "timed_window": "plain graph replays only; per-launch events in a separate window"},
+                       "timed_window": "plain graph replays only; conv-chain and per-launch events in separate windows"},
             "conv_tops": round(achieved_tops, 1),
             "conv_frac_int8_peak": round(achieved_tops / int8_peak_tops, 3),
             "int8_peak_k7_tops": k7,
@@ -511,7 +543,11 @@ def run_ours(args):
                          "unit": "TOPS", "frac": round(achieved_tops / int8_peak_tops, 4),
                          "traffic": traffic, "kernel": "conv_igemm_kernel (all conv launches of one step, conv1 incl.)",
                          "algorithmic_ops_per_step": ops_step, "algorithmic_bytes_per_step": bytes_step,
-                         "kernel_ms_per_step": round(conv_ms, 4), "event_window_ms_per_step": round(ev_step_ms, 4),
+                         "kernel_ms_per_step": round(conv_ms, 4),
+                         "kernel_ms_source": f"conv chain ({len(net.convs)} launches, PDL intact) between two CUDA events on the "
+                                             "launch stream + conv1's per-launch event time",
+                         "per_launch_sum_ms": round(sum(per_layer_ms) + in_ms.get("stem", 0.0), 4),
+                         "event_window_ms_per_step": round(ev_step_ms, 4),
                          "peak_source": f"2 x bf16_tflops of MEASURED_PEAKS.json ({peak_src}, burst)"},
             "quantize": {"ms": round(quant_ms, 4), "kernel": net.stage_names[0]},
             "gpu_launches": args.steps * nl,
