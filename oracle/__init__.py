@@ -74,6 +74,21 @@ def _load():
         lib.oracle_requant_res_value.argtypes = [i32, f32, f32, i32, f32, i32, i32]
         lib.oracle_requant_res.restype = None
         lib.oracle_requant_res.argtypes = [vp, i64, i64, vp, vp, f32, i32, i32, vp, i32]
+        lib.oracle_unpack_fmt.restype = None
+        lib.oracle_unpack_fmt.argtypes = [vp, i64, i32, i32, vp]
+        lib.oracle_pack_fmt.restype = None
+        lib.oracle_pack_fmt.argtypes = [vp, i64, i32, vp]
+        lib.oracle_conv_s32_fmt.restype = i32
+        lib.oracle_conv_s32_fmt.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, i64, i64, i32, i32,
+                                            vp, i64, vp, i32]
+        lib.oracle_requant_value_fmt.restype = i32
+        lib.oracle_requant_value_fmt.argtypes = [i32, f32, f32, i32, i32, i32]
+        lib.oracle_requant_res_value_fmt.restype = i32
+        lib.oracle_requant_res_value_fmt.argtypes = [i32, f32, f32, i32, f32, i32, i32, i32]
+        lib.oracle_requant_fmt.restype = None
+        lib.oracle_requant_fmt.argtypes = [vp, i64, i64, vp, vp, i32, f32, i32, i32, i32, vp, i32]
+        lib.oracle_maxpool_fmt.restype = i32
+        lib.oracle_maxpool_fmt.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, i32, i32, vp, i32]
         lib.oracle_maxpool.restype = i32
         lib.oracle_maxpool.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, i32, vp, i32]
         _lib = lib
@@ -118,6 +133,21 @@ def requant_res_value(acc: int, scale: float, shift: float, skip: int, res_scale
                                                 int(skip), float(np.float32(res_scale)), int(bool(relu)), bits))
 
 
+def requant_value_fmt(acc: int, scale: float, shift: float, relu: bool, bits: int, y_uns: bool) -> int:
+    """requant_value into output format y_uns (reading 16: unsigned codes clamp to
+    [0, 2^b - 1])."""
+    return int(_load().oracle_requant_value_fmt(int(acc), float(np.float32(scale)), float(np.float32(shift)),
+                                                int(bool(relu)), bits, int(bool(y_uns))))
+
+
+def requant_res_value_fmt(acc: int, scale: float, shift: float, skip: int, res_scale: float, relu: bool,
+                          bits: int, y_uns: bool) -> int:
+    """requant_res_value into output format y_uns (readings 15, 16)."""
+    return int(_load().oracle_requant_res_value_fmt(int(acc), float(np.float32(scale)), float(np.float32(shift)),
+                                                    int(skip), float(np.float32(res_scale)), int(bool(relu)), bits,
+                                                    int(bool(y_uns))))
+
+
 def out_dim(H: int, R: int, stride: int, pad: int) -> int:
     """P = floor((H + 2 pad - R) / stride) + 1 (reading 6)."""
     return int(_load().oracle_out_dim(H, R, stride, pad))
@@ -159,6 +189,34 @@ def unpack(p: np.ndarray, C: int, bits: int) -> np.ndarray:
     return out.reshape(*p.shape[:-1], C)
 
 
+def unpack_fmt(p: np.ndarray, C: int, bits: int, uns: bool) -> np.ndarray:
+    """Unpack codes of format uns (reading 16) -> int16 [..., C]."""
+    p = np.ascontiguousarray(p, dtype=np.uint8)
+    nb = C * bits // 8
+    rows = p.reshape(-1, nb)
+    out = np.empty((rows.shape[0], C), dtype=np.int16)
+    lib = _load()
+    for i in range(rows.shape[0]):
+        r = np.ascontiguousarray(rows[i])
+        o = out[i]
+        lib.oracle_unpack_fmt(_ptr(r), C, bits, int(bool(uns)), o.ctypes.data_as(ctypes.c_void_p))
+    return out.reshape(*p.shape[:-1], C)
+
+
+def pack_fmt(q: np.ndarray, bits: int) -> np.ndarray:
+    """Pack int16 codes of either format (their low b bits, reading 2)."""
+    q = np.ascontiguousarray(q, dtype=np.int16)
+    C = q.shape[-1]
+    rows = q.reshape(-1, C)
+    out = np.empty((rows.shape[0], C * bits // 8), dtype=np.uint8)
+    lib = _load()
+    for i in range(rows.shape[0]):
+        r = np.ascontiguousarray(rows[i])
+        o = out[i]
+        lib.oracle_pack_fmt(_ptr(r), C, bits, o.ctypes.data_as(ctypes.c_void_p))
+    return out.reshape(*q.shape[:-1], C * bits // 8)
+
+
 def quantize(x_fp16: np.ndarray, inv_scale: float, bits: int, nthreads: int | None = None) -> np.ndarray:
     """fp16 NHWC -> packed NHWC with C' channels (section 1)."""
     x = np.ascontiguousarray(x_fp16, dtype=np.float16)
@@ -171,12 +229,12 @@ def quantize(x_fp16: np.ndarray, inv_scale: float, bits: int, nthreads: int | No
 
 
 def conv_s32(x: np.ndarray, w: np.ndarray, C: int, stride: int, pad: int, bits: int,
-             pix: np.ndarray | None = None, nthreads: int | None = None) -> np.ndarray:
+             pix: np.ndarray | None = None, nthreads: int | None = None, x_uns: bool = False) -> np.ndarray:
     """Exact integer direct convolution (section 2.1).
 
     x: packed NHWC uint8 [N,H,W,C*b/8]; w: packed KRSC uint8 [K,R,S,C*b/8].
     Returns int32 [N,P,Q,K], or [len(pix),K] for a list of linear output
-    pixel indices m = (n*P+p)*Q+q.
+    pixel indices m = (n*P+p)*Q+q.  x_uns: x holds unsigned codes (reading 16).
     """
     x = np.ascontiguousarray(x, dtype=np.uint8)
     w = np.ascontiguousarray(w, dtype=np.uint8)
@@ -191,8 +249,8 @@ def conv_s32(x: np.ndarray, w: np.ndarray, C: int, stride: int, pad: int, bits: 
         pix = np.ascontiguousarray(pix, dtype=np.int64)
         acc = np.empty((pix.size, K), dtype=np.int32)
         pl, npix = _ptr(pix), pix.size
-    rc = _load().oracle_conv_s32(_ptr(x), _ptr(w), N, H, W, C, K, R, S, stride, pad, bits,
-                                 pl, npix, _ptr(acc), nthreads or default_threads())
+    rc = _load().oracle_conv_s32_fmt(_ptr(x), _ptr(w), N, H, W, C, K, R, S, stride, pad, bits, int(bool(x_uns)),
+                                     pl, npix, _ptr(acc), nthreads or default_threads())
     if rc != 0:
         raise OverflowError(f"oracle_conv_s32 rc={rc} (accumulator left int32 or OOM)")
     return acc
@@ -229,13 +287,41 @@ def requant_res(acc: np.ndarray, scale_shift: np.ndarray, skip: np.ndarray, res_
     return out.reshape(*acc.shape[:-1], K * bits // 8)
 
 
+def requant_fmt(acc: np.ndarray, scale_shift: np.ndarray, relu: bool, bits: int, y_uns: bool,
+                skip: np.ndarray | None = None, skip_uns: bool = False, res_scale: float = 0.0,
+                nthreads: int | None = None) -> np.ndarray:
+    """Requantize s32 [..., K] into packed codes of format y_uns, optionally with
+    the residual add of reading 15 (skip codes of format skip_uns) -- reading 16."""
+    acc = np.ascontiguousarray(acc, dtype=np.int32)
+    K = acc.shape[-1]
+    ss = np.ascontiguousarray(scale_shift, dtype=np.float32)
+    assert ss.size == 2 * K and K <= 8192
+    M = acc.size // K
+    sk = None if skip is None else np.ascontiguousarray(skip, dtype=np.uint8).reshape(M, K * bits // 8)
+    out = np.empty((M, K * bits // 8), dtype=np.uint8)
+    _load().oracle_requant_fmt(_ptr(acc), M, K, _ptr(ss), None if sk is None else _ptr(sk), int(bool(skip_uns)),
+                               float(np.float32(res_scale)), int(bool(relu)), bits, int(bool(y_uns)), _ptr(out),
+                               nthreads or default_threads())
+    return out.reshape(*acc.shape[:-1], K * bits // 8)
+
+
 def conv_q(x: np.ndarray, w: np.ndarray, C: int, stride: int, pad: int, bits: int,
            scale_shift: np.ndarray, relu: bool, pix: np.ndarray | None = None,
-           nthreads: int | None = None, skip: np.ndarray | None = None, res_scale: float = 0.0) -> np.ndarray:
+           nthreads: int | None = None, skip: np.ndarray | None = None, res_scale: float = 0.0,
+           x_uns: bool = False, y_uns: bool = False, skip_uns: bool = False) -> np.ndarray:
     """One whole layer: conv_s32 -> requant -> pack; with
     `skip` (packed, the output's shape; rows `pix` only when pix is given) the
-    residual epilogue of reading 15."""
-    acc = conv_s32(x, w, C, stride, pad, bits, pix=pix, nthreads=nthreads)
+    residual epilogue of reading 15; x_uns / y_uns / skip_uns: unsigned code
+    formats of the input, output and skip tensors (reading 16)."""
+    acc = conv_s32(x, w, C, stride, pad, bits, pix=pix, nthreads=nthreads, x_uns=x_uns)
+    if x_uns or y_uns or skip_uns:
+        sk = None
+        if skip is not None:
+            sk = skip.reshape(-1, skip.shape[-1])
+            if pix is not None:
+                sk = sk[pix]
+        return requant_fmt(acc, scale_shift, relu, bits, y_uns, skip=sk, skip_uns=skip_uns, res_scale=res_scale,
+                           nthreads=nthreads)
     if skip is not None:
         sk = skip.reshape(-1, skip.shape[-1])
         if pix is not None:
@@ -245,16 +331,17 @@ def conv_q(x: np.ndarray, w: np.ndarray, C: int, stride: int, pad: int, bits: in
 
 
 def maxpool(x: np.ndarray, C: int, R: int, stride: int, pad: int, bits: int,
-            nthreads: int | None = None) -> np.ndarray:
+            nthreads: int | None = None, uns: bool = False) -> np.ndarray:
     """R x R max pooling of packed NHWC codes, padding never wins (the ResNet
-    stem's 3x3/2 pool; section 1)."""
+    stem's 3x3/2 pool; section 1); uns: the codes
+    are unsigned (reading 16)."""
     x = np.ascontiguousarray(x, dtype=np.uint8)
     N, H, W, nb = x.shape
     assert nb == C * bits // 8 and C <= 4096
     P, Q = out_dim(H, R, stride, pad), out_dim(W, R, stride, pad)
     y = np.empty((N, P, Q, nb), dtype=np.uint8)
-    rc = _load().oracle_maxpool(_ptr(x), N, H, W, C, R, stride, pad, bits, _ptr(y),
-                                nthreads or default_threads())
+    rc = _load().oracle_maxpool_fmt(_ptr(x), N, H, W, C, R, stride, pad, bits, int(bool(uns)), _ptr(y),
+                                    nthreads or default_threads())
     if rc != 0:
         raise ValueError("oracle_maxpool: a window has no in-range tap")
     return y

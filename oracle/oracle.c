@@ -37,6 +37,14 @@
  *                          unit scales == clamp(acc + skip) (exact integers);
  *                          exact-rational evaluation with the two single
  *                          roundings of reading 15 on random / near-tie cases
+ *   *_fmt variants (unsigned post-ReLU codes, reading 16): unpack_fmt pinned by
+ *                          all 256 bytes / the SPEC.md:226 word read unsigned;
+ *                          conv_s32_fmt by torch float64 conv2d on the unsigned
+ *                          values and by the identity u = s + 2^b [s < 0]
+ *                          (acc_u = acc_s + 2^b conv(neg-mask, w)); requant_fmt
+ *                          by closed forms (scale 1 -> clamp(acc, 0, 2^b - 1))
+ *                          and exact rationals; maxpool_fmt by torch max_pool2d
+ *                          on the unsigned values
  */
 #include <math.h>
 #include <stdint.h>
@@ -128,6 +136,49 @@ ORACLE_API void oracle_unpack(const uint8_t *p, int64_t count, int bits, int8_t 
 }
 
 /* ------------------------------------------------------------------------
+ * Code formats (reading 16, SURVEY 8(f) NEXT-2 "unsigned u8/u4 post-ReLU
+ * activations"): a packed tensor holds either signed two's-complement codes
+ * (reading 3) or unsigned codes [0, 2^b - 1] -- the same b bits per value, the
+ * same little-nibble-first layout (reading 2); only their meaning differs.
+ * Weights are always signed.
+ * ---------------------------------------------------------------------- */
+static int code_lo(int bits, int uns) { return uns ? 0 : -(1 << (bits - 1)); }
+static int code_hi(int bits, int uns) { return uns ? (1 << bits) - 1 : (1 << (bits - 1)) - 1; }
+
+/* Unpack count codes of format uns (0 signed, 1 unsigned) into int16 values. */
+ORACLE_API void oracle_unpack_fmt(const uint8_t *p, int64_t count, int bits, int uns, int16_t *q)
+{
+    for (int64_t c = 0; c < count; ++c) {
+        int v;
+        if (bits == 8) {
+            v = p[c];                                   /* the byte as 0..255 */
+        } else {
+            uint32_t word_shift = 4u * (uint32_t)(c % 8);
+            int64_t byte = 4 * (c / 8) + word_shift / 8;
+            v = (p[byte] >> (word_shift % 8)) & 0xF;    /* the nibble as 0..15 */
+        }
+        if (!uns && v >= (1 << (bits - 1))) v -= 1 << bits;   /* two's complement */
+        q[c] = (int16_t)v;
+    }
+}
+
+/* Pack int16 codes (each within its format's range): the low b bits of each
+ * value at the position oracle_pack uses (reading 2). */
+ORACLE_API void oracle_pack_fmt(const int16_t *q, int64_t count, int bits, uint8_t *out)
+{
+    if (bits == 8) {
+        for (int64_t c = 0; c < count; ++c) out[c] = (uint8_t)(q[c] & 0xFF);
+        return;
+    }
+    memset(out, 0, (size_t)(count / 2));
+    for (int64_t c = 0; c < count; ++c) {
+        uint32_t word_shift = 4u * (uint32_t)(c % 8);
+        int64_t byte = 4 * (c / 8) + word_shift / 8;
+        out[byte] |= (uint8_t)((uint32_t)(q[c] & 0xF) << (word_shift % 8));
+    }
+}
+
+/* ------------------------------------------------------------------------
  * Quantize + pack an fp16 NHWC tensor into packed NHWC with C' channels,
  * C' = ceil(C/32)*32 (reading 14: whole 32-channel granules, i.e. >= 16-byte
  * pixel rows for both widths); channels [C, C') are 0.
@@ -178,12 +229,12 @@ ORACLE_API int64_t oracle_out_dim(int64_t H, int64_t R, int64_t stride, int64_t 
  * pix_list: NULL for all N*P*Q output pixels, else npix linear output pixel
  * indices m = (n*P + p)*Q + q, and acc has npix*K entries in that order.
  * ---------------------------------------------------------------------- */
-ORACLE_API int oracle_conv_s32(const uint8_t *x, const uint8_t *w,
-                               int64_t N, int64_t H, int64_t W, int64_t C,
-                               int64_t K, int64_t R, int64_t S,
-                               int64_t stride, int64_t pad, int bits,
-                               const int64_t *pix_list, int64_t npix,
-                               int32_t *acc, int nthreads)
+ORACLE_API int oracle_conv_s32_fmt(const uint8_t *x, const uint8_t *w,
+                                   int64_t N, int64_t H, int64_t W, int64_t C,
+                                   int64_t K, int64_t R, int64_t S,
+                                   int64_t stride, int64_t pad, int bits, int x_uns,
+                                   const int64_t *pix_list, int64_t npix,
+                                   int32_t *acc, int nthreads)
 {
     int64_t P = oracle_out_dim(H, R, stride, pad);
     int64_t Q = oracle_out_dim(W, S, stride, pad);
@@ -191,14 +242,15 @@ ORACLE_API int oracle_conv_s32(const uint8_t *x, const uint8_t *w,
     int64_t n_out = pix_list ? npix : N * P * Q;
     int overflow = 0;
 
-    /* unpack both operands to one int8 per channel */
-    int8_t *xs = (int8_t *)malloc((size_t)(N * H * W * C));
-    int8_t *ws = (int8_t *)malloc((size_t)(K * R * S * C));
+    /* unpack both operands to one int16 per channel: x in its format (reading
+     * 16), w signed */
+    int16_t *xs = (int16_t *)malloc((size_t)(N * H * W * C) * sizeof(int16_t));
+    int16_t *ws = (int16_t *)malloc((size_t)(K * R * S * C) * sizeof(int16_t));
     if (!xs || !ws) { free(xs); free(ws); return -2; }
     for (int64_t pix = 0; pix < N * H * W; ++pix)
-        oracle_unpack(x + pix * row_bytes, C, bits, xs + pix * C);
+        oracle_unpack_fmt(x + pix * row_bytes, C, bits, x_uns, xs + pix * C);
     for (int64_t t = 0; t < K * R * S; ++t)
-        oracle_unpack(w + t * row_bytes, C, bits, ws + t * C);
+        oracle_unpack_fmt(w + t * row_bytes, C, bits, 0, ws + t * C);
 
 #pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1) reduction(| : overflow)
     for (int64_t i = 0; i < n_out; ++i) {
@@ -214,8 +266,8 @@ ORACLE_API int oracle_conv_s32(const uint8_t *x, const uint8_t *w,
                 for (int64_t s = 0; s < S; ++s) {
                     int64_t ww = q * stride - pad + s;
                     if (ww < 0 || ww >= W) continue;
-                    const int8_t *xp = xs + ((n * H + h) * W + ww) * C;
-                    const int8_t *wp = ws + ((k * R + r) * S + s) * C;
+                    const int16_t *xp = xs + ((n * H + h) * W + ww) * C;
+                    const int16_t *wp = ws + ((k * R + r) * S + s) * C;
                     for (int64_t c = 0; c < C; ++c)
                         sum += (int64_t)xp[c] * (int64_t)wp[c];
                 }
@@ -227,6 +279,17 @@ ORACLE_API int oracle_conv_s32(const uint8_t *x, const uint8_t *w,
     free(xs);
     free(ws);
     return overflow ? -1 : 0;
+}
+
+/* Signed activations (reading 3): the format-0 case of oracle_conv_s32_fmt. */
+ORACLE_API int oracle_conv_s32(const uint8_t *x, const uint8_t *w,
+                               int64_t N, int64_t H, int64_t W, int64_t C,
+                               int64_t K, int64_t R, int64_t S,
+                               int64_t stride, int64_t pad, int bits,
+                               const int64_t *pix_list, int64_t npix,
+                               int32_t *acc, int nthreads)
+{
+    return oracle_conv_s32_fmt(x, w, N, H, W, C, K, R, S, stride, pad, bits, 0, pix_list, npix, acc, nthreads);
 }
 
 /* ------------------------------------------------------------------------
@@ -306,6 +369,54 @@ ORACLE_API void oracle_requant_res(const int32_t *acc, int64_t M, int64_t K,
     }
 }
 
+/* ------------------------------------------------------------------------
+ * Requantize into a code format (reading 16): as oracle_requant_value /
+ * oracle_requant_res_value with the clamp bounds of the output format --
+ * unsigned output codes: y = clamp(rne(v), 0, 2^b - 1) (the lower bound 0 is
+ * the ReLU); signed: reading 4's bounds.
+ * ---------------------------------------------------------------------- */
+ORACLE_API int oracle_requant_value_fmt(int32_t acc, float scale, float shift, int relu, int bits, int y_uns)
+{
+    float f = (float)acc;
+    float v = fmaf(f, scale, shift);
+    float r = nearbyintf(v);
+    float lo = (relu || y_uns) ? 0.0f : (float)code_lo(bits, 0);
+    float c = fminf(fmaxf(r, lo), (float)code_hi(bits, y_uns));
+    return (int)c;
+}
+
+ORACLE_API int oracle_requant_res_value_fmt(int32_t acc, float scale, float shift, int skip, float res_scale,
+                                            int relu, int bits, int y_uns)
+{
+    float f = (float)acc;
+    float u = fmaf(f, scale, shift);
+    float v = fmaf((float)skip, res_scale, u);
+    float r = nearbyintf(v);
+    float lo = (relu || y_uns) ? 0.0f : (float)code_lo(bits, 0);
+    float c = fminf(fmaxf(r, lo), (float)code_hi(bits, y_uns));
+    return (int)c;
+}
+
+/* [M, K] accumulators -> packed rows of format y_uns; with skip != NULL the
+ * residual add of reading 15, the skip codes read in format skip_uns. */
+ORACLE_API void oracle_requant_fmt(const int32_t *acc, int64_t M, int64_t K, const float *scale_shift,
+                                   const uint8_t *skip, int skip_uns, float res_scale,
+                                   int relu, int bits, int y_uns, uint8_t *y, int nthreads)
+{
+    int64_t row_bytes = K * bits / 8;
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        int16_t q[8192], sk[8192];
+        if (skip) oracle_unpack_fmt(skip + m * row_bytes, K, bits, skip_uns, sk);
+        for (int64_t k = 0; k < K; ++k)
+            q[k] = (int16_t)(skip ? oracle_requant_res_value_fmt(acc[m * K + k], scale_shift[k], scale_shift[K + k],
+                                                                 sk[k], res_scale, relu, bits, y_uns)
+                                  : oracle_requant_value_fmt(acc[m * K + k], scale_shift[k], scale_shift[K + k],
+                                                             relu, bits, y_uns));
+        oracle_pack_fmt(q, K, bits, y + m * row_bytes);
+    }
+}
+
 /* The whole per-layer path: conv_s32 then requant+pack. */
 ORACLE_API int oracle_conv_q(const uint8_t *x, const uint8_t *w,
                              int64_t N, int64_t H, int64_t W, int64_t C,
@@ -337,9 +448,9 @@ ORACLE_API int oracle_conv_q(const uint8_t *x, const uint8_t *w,
  * Output spatial size: floor form (reading 6).  Returns -1 if some window has
  * no in-range tap (not possible for pad < R), else 0.
  * ---------------------------------------------------------------------- */
-ORACLE_API int oracle_maxpool(const uint8_t *x, int64_t N, int64_t H, int64_t W, int64_t C,
-                              int64_t R, int64_t stride, int64_t pad, int bits,
-                              uint8_t *y, int nthreads)
+ORACLE_API int oracle_maxpool_fmt(const uint8_t *x, int64_t N, int64_t H, int64_t W, int64_t C,
+                                  int64_t R, int64_t stride, int64_t pad, int bits, int uns,
+                                  uint8_t *y, int nthreads)
 {
     int64_t P = oracle_out_dim(H, R, stride, pad);
     int64_t Q = oracle_out_dim(W, R, stride, pad);
@@ -348,7 +459,7 @@ ORACLE_API int oracle_maxpool(const uint8_t *x, int64_t N, int64_t H, int64_t W,
 #pragma omp parallel for num_threads(nthreads) schedule(static) reduction(| : empty)
     for (int64_t m = 0; m < N * P * Q; ++m) {
         int64_t n = m / (P * Q), p = (m / Q) % P, q = m % Q;
-        int8_t best[4096], v[4096];
+        int16_t best[4096], v[4096];   /* codes compared in their format (reading 16) */
         int any = 0;
         for (int64_t r = 0; r < R; ++r) {
             int64_t h = p * stride - pad + r;
@@ -356,14 +467,21 @@ ORACLE_API int oracle_maxpool(const uint8_t *x, int64_t N, int64_t H, int64_t W,
             for (int64_t s = 0; s < R; ++s) {
                 int64_t w = q * stride - pad + s;
                 if (w < 0 || w >= W) continue;
-                oracle_unpack(x + ((n * H + h) * W + w) * row_bytes, C, bits, v);
+                oracle_unpack_fmt(x + ((n * H + h) * W + w) * row_bytes, C, bits, uns, v);
                 for (int64_t c = 0; c < C; ++c)
                     if (!any || v[c] > best[c]) best[c] = v[c];
                 any = 1;
             }
         }
-        if (!any) { empty |= 1; memset(best, 0, (size_t)C); }
-        oracle_pack(best, C, bits, y + m * row_bytes);
+        if (!any) { empty |= 1; memset(best, 0, (size_t)C * sizeof(int16_t)); }
+        oracle_pack_fmt(best, C, bits, y + m * row_bytes);
     }
     return empty ? -1 : 0;
+}
+
+ORACLE_API int oracle_maxpool(const uint8_t *x, int64_t N, int64_t H, int64_t W, int64_t C,
+                              int64_t R, int64_t stride, int64_t pad, int bits,
+                              uint8_t *y, int nthreads)
+{
+    return oracle_maxpool_fmt(x, N, H, W, C, R, stride, pad, bits, 0, y, nthreads);
 }

@@ -40,13 +40,14 @@ def f32_rne(v: Fraction) -> float:
     return sign * math.ldexp(n, q)
 
 
-def requant_exact(acc: int, scale: float, shift: float, relu: bool, bits: int) -> int:
+def requant_exact(acc: int, scale: float, shift: float, relu: bool, bits: int, uns: bool = False) -> int:
     """clamp(rne(RN32((float)acc * scale + shift))) with one rounding of the
-    multiply-add (readings 4-5); (float)acc is itself RN to binary32."""
+    multiply-add (readings 4-5); (float)acc is itself RN to binary32.  uns:
+    unsigned output codes, clamp to [0, 2^b - 1] (reading 16)."""
     f = f32_rne(Fraction(int(acc)))
     v = f32_rne(Fraction(f) * Fraction(float(scale)) + Fraction(float(shift)))
-    lo = 0 if relu else -(1 << (bits - 1))
-    hi = (1 << (bits - 1)) - 1
+    lo = 0 if (relu or uns) else -(1 << (bits - 1))
+    hi = (1 << bits) - 1 if uns else (1 << (bits - 1)) - 1
     if math.isnan(v):
         return lo
     if math.isinf(v):
@@ -66,7 +67,7 @@ def requant_two_roundings(acc, scale, shift, relu: bool, bits: int) -> np.ndarra
     return np.clip(r, lo, hi).astype(np.int64)
 
 
-def near_tie_cases(g: np.random.Generator, n: int, bits: int = 8):
+def near_tie_cases(g: np.random.Generator, n: int, bits: int = 8, k_lo: int | None = None, k_hi: int | None = None):
     """n (acc, scale, shift) triples whose exact (float)acc*scale + shift lies
     within half a binary32 ulp of shift from a half-integer inside the code
     range: the rounding of a separate product decides the code there.
@@ -76,7 +77,7 @@ def near_tie_cases(g: np.random.Generator, n: int, bits: int = 8):
     accs = g.integers(-(1 << 22), 1 << 22, size=n)
     exps = g.integers(-22, -6, size=n)
     mants = g.integers(1 << 23, 1 << 24, size=n)
-    ks = g.integers(-hi, hi, size=n)
+    ks = g.integers(-hi if k_lo is None else k_lo, hi if k_hi is None else k_hi, size=n)
     out_acc, out_scale, out_shift = [], [], []
     for i in range(n):
         acc = int(accs[i])
@@ -97,14 +98,14 @@ def near_tie_cases(g: np.random.Generator, n: int, bits: int = 8):
 
 
 def requant_res_exact(acc: int, scale: float, shift: float, skip: int, res_scale: float, relu: bool,
-                      bits: int) -> int:
+                      bits: int, uns: bool = False) -> int:
     """Reading 15 with exact rationals: u = RN32(acc*scale + shift), v = RN32(skip*res_scale + u),
-    then round half to even and clamp."""
+    then round half to even and clamp (uns: to [0, 2^b - 1], reading 16)."""
     f = f32_rne(Fraction(int(acc)))
     u = f32_rne(Fraction(f) * Fraction(float(scale)) + Fraction(float(shift)))
     v = f32_rne(Fraction(int(skip)) * Fraction(float(res_scale)) + Fraction(u))
-    lo = 0 if relu else -(1 << (bits - 1))
-    hi = (1 << (bits - 1)) - 1
+    lo = 0 if (relu or uns) else -(1 << (bits - 1))
+    hi = (1 << bits) - 1 if uns else (1 << (bits - 1)) - 1
     if math.isinf(v):
         return hi if v > 0 else lo
     return min(max(round(Fraction(v)), lo), hi)
