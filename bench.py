@@ -64,12 +64,21 @@ class Spec:
         self.conv1, self.desc, self.cfg_id, self.metric = conv1, desc, cfg_id, metric
         self.inv_scale = 127 / 4 if bits == 8 else 7 / 3
         self.pool = (3, 2, 1)
+        self.unsigned = False     # unsigned post-ReLU codes (workload suffix _uns)
 
 
 RES_SUFFIX = "_res"
+UNS_SUFFIX = "_uns"
 
 
 def workload_spec(name: str) -> Spec:
+    if name.endswith(UNS_SUFFIX):
+        # the same network with unsigned post-ReLU activation codes (NEXT-2, DESIGN reading 16)
+        base = workload_spec(name[:-len(UNS_SUFFIX)])
+        base.name, base.unsigned = name, True
+        base.desc += ", unsigned post-ReLU codes (u%d activations)" % base.bits
+        base.metric = base.metric.replace("fused requant-repack", "fused requant-repack, u%d activations" % base.bits)
+        return base
     if name.endswith(RES_SUFFIX):
         # the same network with its residual adds fused into the c3 / c2 epilogues (NEXT-2)
         base = workload_spec(name[:-len(RES_SUFFIX)])
@@ -143,7 +152,7 @@ def build_network(spec: Spec, B: int, device, world: int = 1, dist=None):
 
     from paper_2202_06819_b200.network import ConvNet
 
-    net = ConvNet(B, spec.bits, device)
+    net = ConvNet(B, spec.bits, device, unsigned=spec.unsigned)
 
     def dev_params(i):
         wv, ss = layer_weights(spec, i)
@@ -281,10 +290,11 @@ def parity_check(net, spec: Spec, imgs, n_rand: int = 64, seed: int = 0, nthread
         wv, ss = layer_weights(spec, -1)
         y1 = host(st["y"])
         pix = check.sample_pixels(len(imgs), st["plan"].P, st["plan"].Q, g, n_rand)
-        ok, d = check.check_stem(host(net.x_in), wv, ss, L1, bits, spec.inv_scale, st["relu"], y1, pix, nthreads)
+        ok, d = check.check_stem(host(net.x_in), wv, ss, L1, bits, spec.inv_scale, st["relu"], y1, pix, nthreads,
+                                 y_uns=net.in_uns)
         if not ok:
             bad.append(("conv1", d))
-        ok, d = check.check_pool(y1, L1.K, st["pool"], bits, host(net.net_in), nthreads)
+        ok, d = check.check_pool(y1, L1.K, st["pool"], bits, host(net.net_in), nthreads, uns=net.in_uns)
         if not ok:
             bad.append(("maxpool", d))
     for i, c in enumerate(net.convs):
@@ -293,7 +303,8 @@ def parity_check(net, spec: Spec, imgs, n_rand: int = 64, seed: int = 0, nthread
         sk = net.skip_tensor(i)
         ok, d = check.check_conv(host(net.src_tensor(i)), c.w.cpu().numpy(), c.ss.cpu().numpy(), L, bits, c.relu,
                                  host(c.y), pix, nthreads, skip=None if sk is None else host(sk),
-                                 res_scale=c.res_scale)
+                                 res_scale=c.res_scale, x_uns=c.plan.x_uns, y_uns=c.plan.y_uns,
+                                 skip_uns=c.plan.skip_uns)
         if not ok:
             bad.append((c.name, d))
     return not bad, bad
@@ -782,8 +793,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="resnet50_int8_b256",
-                    choices=[w + r for w in ("resnet50_int8_b256", "resnet18_int8_b1", "resnet18_int4_b16")
-                             for r in ("", RES_SUFFIX)] + ["cfg1"])
+                    choices=[w + r + u for w in ("resnet50_int8_b256", "resnet18_int8_b1", "resnet18_int4_b16")
+                             for r in ("", RES_SUFFIX) for u in ("", UNS_SUFFIX)] + ["cfg1"])
     ap.add_argument("--batch", type=int, default=0, help="override the batch (global for strong scaling)")
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="strong (default for N > 1): the global batch is split across GPUs; "

@@ -271,6 +271,35 @@ CONVQ_API int conv_q_requant(const int32_t *acc, int64_t M, int K, const float *
 CONVQ_API int conv_q_maxpool(const void *x, int N, int H, int W, int C, int R, int stride, int pad, int bits,
                              void *y, void *stream);
 
+/*
+ * As conv_q_maxpool over codes of format uns (ABI 1.05; DESIGN reading 16):
+ * uns = 1 compares unsigned codes [0, 2^bits - 1] (post-ReLU activations),
+ * uns = 0 signed codes (== conv_q_maxpool).  Errors: as conv_q_maxpool, plus
+ * EINVAL for uns not 0/1.
+ */
+CONVQ_API int conv_q_maxpool_fmt(const void *x, int N, int H, int W, int C, int R, int stride, int pad, int bits,
+                                 int uns, void *y, void *stream);
+
+/*
+ * Code formats of a plan (ABI 1.05; SURVEY 8(f) NEXT-2 "unsigned u8/u4
+ * post-ReLU activations"; DESIGN reading 16 -- the paper's codes are signed,
+ * SPEC.md:274, and a ReLU epilogue (section 3.2.2) leaves the
+ * sign bit unused).  Each flag 0 = signed two's-complement codes (the
+ * default), 1 = unsigned codes [0, 2^bits - 1]; same packed layout either way:
+ *   x_unsigned     the activations x are read as unsigned (tcgen05 A format u8;
+ *                  INT4 nibbles expand to 16*v as before)
+ *   y_unsigned     the packed output is written as unsigned codes:
+ *                  y = clamp(rne(v), 0, 2^bits - 1) -- the lower bound is the
+ *                  ReLU, so it applies whatever conv_q_plan_set_epilogue's relu
+ *   skip_unsigned  the residual skip tensor (conv_q_plan_set_residual) holds
+ *                  unsigned codes
+ * Weights stay signed.  Ownership: none.  The plan re-applies the tuning cache
+ * (its key includes the formats).  Errors: EINVAL (NULL plan, flag not 0/1),
+ * EOVERFLOW (x_unsigned with R*S*C*255*128 > 2^31 - 1: the accumulator guard
+ * of PAPER.md:166 section 3.2.1 for unsigned activations).
+ */
+CONVQ_API int conv_q_plan_set_formats(conv_q_plan_t *plan, int x_unsigned, int y_unsigned, int skip_unsigned);
+
 /* Thread-local status code of the last failed call on this thread (0 if none). */
 CONVQ_API int conv_q_last_status(void);
 

@@ -34,19 +34,20 @@ def first_diff(a: np.ndarray, b: np.ndarray):
 
 def check_conv(x: np.ndarray, w: np.ndarray, ss: np.ndarray, L, bits: int, relu: bool, y: np.ndarray,
                pix: np.ndarray, nthreads: int | None = None, skip: np.ndarray | None = None,
-               res_scale: float = 0.0):
+               res_scale: float = 0.0, x_uns: bool = False, y_uns: bool = False, skip_uns: bool = False):
     """y (packed [n,P,Q,K*b/8] from the device) vs the oracle at pixels `pix`
     of the same n-image batch x (with `skip`: the residual epilogue, reading
-    15, adding the device's own skip bytes).  Returns (ok, diff)."""
+    15, adding the device's own skip bytes; *_uns: unsigned code formats,
+    reading 16).  Returns (ok, diff)."""
     ref = conv_q(x, w, L.C, L.stride, L.pad, bits, ss, relu, pix=pix, nthreads=nthreads, skip=skip,
-                 res_scale=res_scale)
+                 res_scale=res_scale, x_uns=x_uns, y_uns=y_uns, skip_uns=skip_uns)
     got = y.reshape(-1, y.shape[-1])[pix]
     d = first_diff(got, ref)
     return d is None, d
 
 
 def check_stem(x_fp16: np.ndarray, w_codes: np.ndarray, ss: np.ndarray, conv1, bits: int, inv_scale: float,
-               relu: bool, y: np.ndarray, pix: np.ndarray, nthreads: int | None = None):
+               relu: bool, y: np.ndarray, pix: np.ndarray, nthreads: int | None = None, y_uns: bool = False):
     """The stem conv (any implementation of conv1) vs the oracle's quantize +
     direct stride-2 conv over the channel-padded image, at pixels `pix`."""
     L = conv1
@@ -54,14 +55,16 @@ def check_stem(x_fp16: np.ndarray, w_codes: np.ndarray, ss: np.ndarray, conv1, b
     wpad = np.zeros((L.K, L.R, L.S, Cp), np.int8)
     wpad[..., :L.C] = w_codes
     xq = quantize(x_fp16, inv_scale, bits, nthreads=nthreads)
-    ref = conv_q(xq, pack(wpad, bits), Cp, L.stride, L.pad, bits, ss, relu, pix=pix, nthreads=nthreads)
+    ref = conv_q(xq, pack(wpad, bits), Cp, L.stride, L.pad, bits, ss, relu, pix=pix, nthreads=nthreads,
+                 y_uns=y_uns)
     got = y.reshape(-1, y.shape[-1])[pix]
     d = first_diff(got, ref)
     return d is None, d
 
 
-def check_pool(x: np.ndarray, C: int, pool, bits: int, y: np.ndarray, nthreads: int | None = None):
+def check_pool(x: np.ndarray, C: int, pool, bits: int, y: np.ndarray, nthreads: int | None = None,
+               uns: bool = False):
     R, st, pad = pool
-    ref = maxpool(x, C, R, st, pad, bits, nthreads=nthreads)
+    ref = maxpool(x, C, R, st, pad, bits, nthreads=nthreads, uns=uns)
     d = first_diff(y, ref)
     return d is None, d

@@ -118,6 +118,10 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.conv_q_plan_set_residual.argtypes = [vp, vp, f]
     lib.conv_q_maxpool.restype = i
     lib.conv_q_maxpool.argtypes = [vp, i, i, i, i, i, i, i, i, vp, vp]
+    lib.conv_q_maxpool_fmt.restype = i
+    lib.conv_q_maxpool_fmt.argtypes = [vp, i, i, i, i, i, i, i, i, i, vp, vp]
+    lib.conv_q_plan_set_formats.restype = i
+    lib.conv_q_plan_set_formats.argtypes = [vp, i, i, i]
     lib.conv_q_int8_peak.restype = i
     lib.conv_q_int8_peak.argtypes = [i, ctypes.POINTER(ctypes.c_double)]
     _lib = lib
@@ -157,7 +161,8 @@ def padded_channels(C: int, bits: int) -> int:
 class ConvPlan:
     """conv_q_plan(N,H,W,C,K,R,S,stride,pad,bits) + conv_q_run(plan,x,w,scale,y)."""
 
-    def __init__(self, N, H, W, C, K, R, S, stride, pad, bits, relu=False, out_mode=OUT_PACKED):
+    def __init__(self, N, H, W, C, K, R, S, stride, pad, bits, relu=False, out_mode=OUT_PACKED,
+                 x_uns=False, y_uns=False):
         lib = load()
         h = lib.conv_q_plan(N, H, W, C, K, R, S, stride, pad, bits)
         if not h:
@@ -167,6 +172,9 @@ class ConvPlan:
         self.R, self.S, self.stride, self.pad, self.bits = R, S, stride, pad, bits
         self.P, self.Q = out_dim(H, R, stride, pad), out_dim(W, S, stride, pad)
         self._need = None
+        self.x_uns = self.y_uns = self.skip_uns = False
+        if x_uns or y_uns:
+            self.set_formats(x_uns, y_uns)
         self.set_epilogue(relu, out_mode)
 
     def __del__(self):
@@ -183,6 +191,12 @@ class ConvPlan:
 
     def set_stream(self, stream):
         _check(load().conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
+
+    def set_formats(self, x_uns: bool = False, y_uns: bool = False, skip_uns: bool = False):
+        """Unsigned code formats of x / y / the residual skip (conv_q_plan_set_formats,
+        DESIGN reading 16)."""
+        _check(load().conv_q_plan_set_formats(self._h, int(bool(x_uns)), int(bool(y_uns)), int(bool(skip_uns))))
+        self.x_uns, self.y_uns, self.skip_uns = bool(x_uns), bool(y_uns), bool(skip_uns)
 
     def set_residual(self, skip, res_scale: float = 0.0):
         """Fused residual add (conv_q_plan_set_residual, DESIGN reading 15): skip is a
@@ -288,7 +302,7 @@ class StemPlan(ConvPlan):
     Same output as ConvPlan(N,H,W,C',K,R,S,2,pad,bits) on the channel-padded
     input; inputs come from quantize() / pack_weights() of this class."""
 
-    def __init__(self, N, H, W, C, K, R, S, pad, bits, relu=False, out_mode=OUT_PACKED):
+    def __init__(self, N, H, W, C, K, R, S, pad, bits, relu=False, out_mode=OUT_PACKED, y_uns=False):
         lib = load()
         h = lib.conv_q_plan_s2d(N, H, W, C, K, R, S, pad, bits)
         if not h:
@@ -298,6 +312,9 @@ class StemPlan(ConvPlan):
         self.R, self.S, self.stride, self.pad, self.bits = R, S, 2, pad, bits
         self.P, self.Q = out_dim(H, R, 2, pad), out_dim(W, S, 2, pad)
         self._need = None
+        self.x_uns = self.y_uns = self.skip_uns = False
+        if y_uns:
+            self.set_formats(False, True)
         self.set_epilogue(relu, out_mode)
         inf = self.info()
         self.x_dims, self.w_dims = inf.x_dims, inf.w_dims
@@ -376,8 +393,9 @@ def requant(acc, scale, relu: bool, bits: int, out=None, stream=None):
     return out
 
 
-def maxpool(x, C: int, R: int, stride: int, pad: int, bits: int, out=None, stream=None):
-    """R x R max pooling of packed NHWC codes (conv_q_maxpool): uint8 [N,H,W,C*bits/8]."""
+def maxpool(x, C: int, R: int, stride: int, pad: int, bits: int, out=None, stream=None, uns: bool = False):
+    """R x R max pooling of packed NHWC codes (conv_q_maxpool_fmt): uint8 [N,H,W,C*bits/8];
+    uns: the codes are unsigned (DESIGN reading 16)."""
     import torch
     N, H, W, nb = x.shape
     assert x.dtype == torch.uint8 and x.is_contiguous() and nb == C * bits // 8
@@ -385,8 +403,8 @@ def maxpool(x, C: int, R: int, stride: int, pad: int, bits: int, out=None, strea
     if out is None:
         out = torch.empty((N, P, Q, nb), dtype=torch.uint8, device=x.device)
     assert out.dtype == torch.uint8 and out.is_contiguous() and tuple(out.shape) == (N, P, Q, nb)
-    _check(load().conv_q_maxpool(ctypes.c_void_p(x.data_ptr()), N, H, W, C, R, stride, pad, bits,
-                                 ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream(stream))))
+    _check(load().conv_q_maxpool_fmt(ctypes.c_void_p(x.data_ptr()), N, H, W, C, R, stride, pad, bits, int(bool(uns)),
+                                     ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream(stream))))
     return out
 
 

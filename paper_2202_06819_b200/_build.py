@@ -1,7 +1,8 @@
 """Build libconvq.so in-tree with nvcc for sm_100a (no torch extension, no JIT).
 
-The kernel instantiations live in eight translation units (kern_b{8,4}_o{0,1,2}.cu and
-the INT8 ReLU-specialised kern_b8_o{4,6}.cu)
+The kernel instantiations live in sixteen translation units kern_b{8,4}_o{OUT}.cu,
+one per (bits, output path) -- packed TMA / s32 / direct stores, ReLU, residual,
+unsigned u8 codes --
 compiled in parallel, plus the host library convq.cu; objects are linked into
 one shared library with the CUDA runtime linked statically."""
 from __future__ import annotations
@@ -23,8 +24,8 @@ _SFX = ("_instr" if INSTR else "") + (f"_wg{os.environ['CONVQ_EPI_WG8']}" if os.
     ("_allw0" if os.environ.get("CONVQ_EPI_ALLW") == "0" else "")
 OBJ = os.path.join(HERE, "build_obj" + _SFX)
 LIB = os.path.join(HERE, f"libconvq{_SFX}.so")
-SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2, 8, 10)] + \
-    ["kern_b8_o4.cu", "kern_b8_o6.cu"]
+SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2, 4, 6, 8, 10)] + \
+    ["kern_b8_o20.cu", "kern_b8_o22.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"] + \

@@ -103,6 +103,12 @@ struct ConvParams {
     const float *scale;  // [2K] scale then shift
     const uint8_t *skip; // OUT_RES: packed skip tensor [M][K*BITS/8] (the output's layout), read by the epilogue
     float res_scale;     // OUT_RES: the skip code's scale relative to the output's (DESIGN reading 15)
+    // code formats (DESIGN reading 16, unsigned post-ReLU codes)
+    int x_uns;           // activations are unsigned codes: A format u8 in the instruction descriptor
+    int y_uns;           // output codes are unsigned: clamp to [0, 2^b - 1]
+    int code_hi;         // INT4 ReLU epilogue: the largest output code (7 signed, 15 unsigned)
+    uint32_t skip_xor;   // OUT_RES: code -> biased unsigned (0x80 / 0x8 per code for signed skips, 0 unsigned)
+    float skip_off;      // OUT_RES: 2^23 + that bias (the skip code as an exact float, see the epilogue)
     int32_t *y32;        // s32 output (OUT = OUT_S32)
     uint8_t *y8;         // packed output for direct stores (OUT = OUT_DIRECT)
     int out_row;         // packed output bytes per pixel row = K*BITS/8
@@ -112,6 +118,11 @@ struct ConvParams {
     // warp of each 32-row region requantizes.  splits = 1: plain tiles.
     int splits;
     int num_units;       // num_tiles * splits
+    // shared-memory carve-up chosen on the host (plan.cuh launch_conv): the
+    // weight-stationary region is sized to THIS layer's weight block (not the
+    // 64 KB budget), and every byte left over goes to pipeline stages
+    int stages;          // smem ring depth, 2 <= stages <= MAX_STAGES
+    int wsb;             // bytes of the resident weight region (WS; multiple of 1024)
     int32_t *ws;         // [num_tiles*CG][4*EPB regions][EPI_COLS][32] partial sums (kept zero between runs)
     unsigned *cnt;       // per-region arrival counters (kept zero between runs)
     FastDiv fd_ntiles, fd_PQ, fd_Q, fd_cblk, fd_S, fd_tpi, fd_splits, fd_Wp;
@@ -123,6 +134,9 @@ constexpr int OUT_S32 = 1;     // raw int32 accumulators, direct global stores (
 constexpr int OUT_DIRECT = 2;
 constexpr int OUT_RELU = 4;    // flag: INT8 ReLU-specialised epilogue (OUT_TMA | OUT_RELU, OUT_DIRECT | OUT_RELU)
 constexpr int OUT_RES = 8;     // flag: fused residual add (OUT_TMA | OUT_RES, OUT_DIRECT | OUT_RES; runtime ReLU)
+// flag with OUT_RELU, INT8: unsigned output codes (reading 16) -- F2IP.U8 saturates to
+// [0, 255], which IS the ReLU + upper clamp (no sign masking)
+constexpr int OUT_U = 16;
 
 // Epilogue warpgroups (INT8: CONVQ_EPI_WG8, default 4; INT4: 2) and TMEM
 // accumulator buffers (512 columns / BN, at most 4, at most one per warpgroup);
@@ -196,6 +210,8 @@ struct ConvCfg {
     static constexpr int OUT_ROW = BN * BITS / 8;            // packed output bytes per pixel row
     static constexpr int OUTP = OUT & 3;                     // output path
     static constexpr bool RELU8 = BITS == 8 && (OUT & OUT_RELU) != 0;
+    static constexpr bool U8 = RELU8 && (OUT & OUT_U) != 0;          // unsigned u8 output codes
+    static constexpr bool RELU4 = BITS == 4 && (OUT & OUT_RELU) != 0;  // INT4 ReLU epilogue (runtime top code)
     static constexpr bool RES = (OUT & OUT_RES) != 0;          // residual add: v = fmaf(skip, res_scale, u)
     static constexpr int OUT_BYTES = OUTP == OUT_TMA ? BM * OUT_ROW : 0;   // staging per TMEM buffer
     static constexpr int NUM_EPI = epi_warpgroups(BITS);            // epilogue warpgroups
@@ -229,9 +245,17 @@ struct ConvCfg {
     static constexpr int HST = NSUB >= 9 ? 1 : (9 + NSUB - 1) / NSUB;
     static constexpr int NHALO = !HA || WS ? 0 : stages_with(4) >= 2 * HST ? 4 : stages_with(3) >= 2 * HST ? 3 : 2;
     static constexpr int STAGES_FIT = stages_with(NHALO);
-    static constexpr int STAGES = STAGES_FIT > 12 ? 12 : STAGES_FIT;
-    static constexpr int SMEM = 1024 + WSB + STAGES * STAGE_BYTES + NBUF * (OUT_BYTES + SS_BYTES) +
-                                NHALO * (HALO_BYTES + HALO_PK) + BAR_BYTES;
+    static constexpr int MAX_STAGES = 12;
+    // stages with the full weight-stationary budget (the minimum the config
+    // guarantees; the launch uses stages_for(wsb) >= STAGES for the real block)
+    static constexpr int STAGES = STAGES_FIT > MAX_STAGES ? MAX_STAGES : STAGES_FIT;
+    static constexpr int FIXED_BYTES = 1024 + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * (HALO_BYTES + HALO_PK) + BAR_BYTES;
+    static constexpr int SMEM = FIXED_BYTES + WSB + STAGES * STAGE_BYTES;
+    static int stages_for(int wsb) {
+        const int st = (SMEM_LIMIT - FIXED_BYTES - wsb) / STAGE_BYTES;
+        return st > MAX_STAGES ? MAX_STAGES : st;
+    }
+    static int smem_for(int wsb, int stages) { return FIXED_BYTES + wsb + stages * STAGE_BYTES; }
     static constexpr int TMEM_COLS = NBUF * TBW < 32 ? 32 : NBUF * TBW;
     // Warp layout: epilogue warpgroups first, then (INT4) the transform
     // warpgroup, then the TMA producer and the MMA issuer as the two highest
@@ -244,7 +268,7 @@ struct ConvCfg {
     static constexpr int NUM_THREADS = 32 * (MMA_WARP + kNumMma);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
     static constexpr bool FITS = STAGES >= 2 && (!HB || (OUTP != OUT_TMA && (BITS == 8 || (HA && !WS)))) &&
-                                 (BITS == 8 || !(OUT & OUT_RELU)) &&
+                                 (!(OUT & OUT_U) || (BITS == 8 && (OUT & OUT_RELU))) &&
                                  (!RES || (OUTP != OUT_S32 && !(OUT & OUT_RELU))) &&
                                  (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
                                  (!S2H || (WS && !HA && KCH == 64)) &&
@@ -332,6 +356,33 @@ __device__ __forceinline__ void fma2_rn(float a0, float a1, float b0, float b1, 
 // four float values -> one packed s8 word (value 0 in byte 0)
 __device__ __forceinline__ uint32_t pack4_f32_s8(float u0, float u1, float u2, float u3) {
     return pack2_f32_s8(u1, u0, pack2_f32_s8(u3, u2, 0u));
+}
+// Unsigned codes (reading 16): "cvt.rni.s32.f32 x2 ; cvt.pack.sat.u8.s32.b32" -> one
+// F2IP.U8 per two codes: round to nearest even, saturate to [0, 255] (the
+// ReLU and the upper clamp at once), pack.
+__device__ __forceinline__ uint32_t pack2_f32_u8(float a, float b, uint32_t c) {
+    uint32_t d;
+    asm("{\n .reg .s32 ia, ib;\n cvt.rni.s32.f32 ia, %1;\n cvt.rni.s32.f32 ib, %2;\n"
+        " cvt.pack.sat.u8.s32.b32 %0, ia, ib, %3;\n}" : "=r"(d) : "f"(a), "f"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t pack4_f32_u8(float u0, float u1, float u2, float u3) {
+    return pack2_f32_u8(u1, u0, pack2_f32_u8(u3, u2, 0u));
+}
+// clamp(rne(u), 0, 255) in one F2I.U8 (64 lanes/clk/SM; the s32 F2I runs at 16)
+__device__ __forceinline__ int f2u8_rn(float u) {
+    int r;
+    asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(u));
+    return r;
+}
+// cvt.pack.sat.u4.s32.b32 d, a, b, c:  d = c << 8 | sat_u4(a) << 4 | sat_u4(b)
+__device__ __forceinline__ uint32_t pack2_u4(int a, int b, uint32_t c) {
+    uint32_t d;
+    asm("cvt.pack.sat.u4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t pack8_sat_u4(const int *r) {
+    return pack2_u4(r[1], r[0], pack2_u4(r[3], r[2], pack2_u4(r[5], r[4], pack2_u4(r[7], r[6], 0u))));
 }
 // ReLU on four packed s8 codes: PRMT with sign-replicating selectors gives
 // 0xFF for every negative byte; clear those bytes.  Two instructions per word.
@@ -479,7 +530,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     do { if (tl && lane == 0) tl[(region) * 256 + ((idx) & 255)] = (unsigned long long)clock64(); } while (0)
     const int probe = kInstrument ? p.probe : 0;
     static_assert(Cfg::FITS, "tile does not fit shared memory");
-    constexpr int STAGES = Cfg::STAGES;
+    const int STAGES = p.stages;      // runtime ring depth (host: all smem left after the fixed regions)
+    constexpr int MAXST = Cfg::MAX_STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment by offset (pointer arithmetic on the shared array keeps
     // the compiler's shared-space inference: LDS/STS instead of generic LD/ST)
@@ -489,7 +541,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     // in both CTAs of a pair, as cta_group::2 descriptors require)
     constexpr bool HA = Cfg::HA, WS = Cfg::WS, S2H = Cfg::S2H;
     uint8_t *b_res = smem;                              // WS: [num_kb][BN rows][KCH] resident weights
-    uint8_t *a_s8 = smem + Cfg::WSB;                    // [STAGES][NSUB][BM*KCH] (WS halo: [STAGES][HBOX])
+    uint8_t *a_s8 = smem + (WS ? p.wsb : 0);            // [STAGES][NSUB][BM*KCH] (WS halo: [STAGES][HBOX])
     uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][NSUB][BNL*KCH]
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][NSUB][BM*KCH/2]
     uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][NSUB][BNL*KCH/2]
@@ -499,9 +551,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint8_t *halo_pk = halo_buf + Cfg::NHALO * Cfg::HALO_BYTES;  // INT4 halo: [NHALO][HALO_PK] packed boxes
     uint64_t *bars = reinterpret_cast<uint64_t *>(halo_pk + Cfg::NHALO * Cfg::HALO_PK);
     uint64_t *full = bars;                  // TMA -> (transform | MMA)
-    uint64_t *empty = bars + STAGES;        // MMA -> TMA
-    uint64_t *ready = bars + 2 * STAGES;    // transform -> MMA (INT4)
-    uint64_t *acc_full = bars + 3 * STAGES; // MMA -> epilogue [NBUF]
+    uint64_t *empty = bars + MAXST;         // MMA -> TMA
+    uint64_t *ready = bars + 2 * MAXST;     // transform -> MMA (INT4)
+    uint64_t *acc_full = bars + 3 * MAXST;  // MMA -> epilogue [NBUF]
     uint64_t *acc_empty = acc_full + 4;     // epilogue -> MMA [NBUF]
     uint64_t *hempty = acc_empty + 4;       // HALO: MMA -> TMA, halo buffer free [NHALO <= 4]
     uint64_t *bfull = hempty;               // WS (no separate halo buffers): resident weights loaded
@@ -743,6 +795,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         auto mma_elect = [&]() { return kMma1T ? true : elect_one(); };
         auto mma_sync = [&]() { if (!kMma1T) __syncwarp(); };
         if (rank == 0 && (!kMma1T || lane == 0) && mw < nmma) {
+            // A format: s8 (bit 7 set) or, for unsigned activation codes (reading 16), u8
+            const uint32_t idesc = p.x_uns ? (Cfg::IDESC & ~(1u << 7)) : Cfg::IDESC;
             const uint64_t a_desc0 = umma_desc_kmajor(smem_u32(a_s8), KCH);
             const uint64_t b_desc0 = umma_desc_kmajor(smem_u32(b_s8), KCH);
             // HALO: descriptor start-address delta of tap t's window, (r*Wp + s)*KCH bytes (3x3 table)
@@ -823,8 +877,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 #pragma unroll
                                 for (int kk = 0; kk < 2; ++kk) {
                                     const uint64_t ad = ad_s + (uint64_t)(g * BM + jr * p.Wp + 2 * kk);
-                                    if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad, bd + 2 * kk, Cfg::IDESC, (jr | kk) != 0);
-                                    else mma_i8(d_tmem + g * BN, ad, bd + 2 * kk, Cfg::IDESC, (jr | kk) != 0);
+                                    if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad, bd + 2 * kk, idesc, (jr | kk) != 0);
+                                    else mma_i8(d_tmem + g * BN, ad, bd + 2 * kk, idesc, (jr | kk) != 0);
                                 }
                             }
                             if constexpr (CG == 2) mma_commit_cg2_mc(&empty[stage], 0x3);
@@ -840,8 +894,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                     const uint64_t bd = b_desc_res + (uint64_t)(((t * p.num_cblk + cblk) * Cfg::B_TILE) >> 4);
 #pragma unroll
                                     for (int k = 0; k < KCH / 32; ++k) {
-                                        if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
-                                        else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                        if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, idesc, (cblk | t | k) != 0);
+                                        else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, idesc, (cblk | t | k) != 0);
                                     }
                                 }
                             } else {                       // any R x S: tap (r, s) at row offset r*Wp + s
@@ -855,8 +909,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                             const uint64_t bd = b_desc_res + (uint64_t)(((t * p.num_cblk + cblk) * Cfg::B_TILE) >> 4);
 #pragma unroll
                                             for (int k = 0; k < KCH / 32; ++k) {
-                                                if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
-                                                else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (cblk | t | k) != 0);
+                                                if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, idesc, (cblk | t | k) != 0);
+                                                else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, idesc, (cblk | t | k) != 0);
                                             }
                                         }
                                 }
@@ -921,8 +975,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 #pragma unroll
                                             for (int k = 0; k < KCH / 32; ++k) {
                                                 const uint32_t acc = (cblk | t | k) != 0;
-                                                if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
-                                                else mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
+                                                if constexpr (CG == 2) mma_i8_cg2(d_tmem, ad + 2 * k, bd + 2 * k, idesc, acc);
+                                                else mma_i8(d_tmem, ad + 2 * k, bd + 2 * k, idesc, acc);
                                             }
                                         }
                                     }
@@ -985,8 +1039,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 #pragma unroll
                                         for (int k = 0; k < KCH / 32; ++k) {
                                             const uint32_t acc = (kb - kb_lo + j + k) != 0;
-                                            if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
-                                            else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, Cfg::IDESC, acc);
+                                            if constexpr (CG == 2) mma_i8_cg2(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, idesc, acc);
+                                            else mma_i8(d_tmem + g * BN, ad + 2 * k, bd + 2 * k, idesc, acc);
                                         }
                                     }
                                 }
@@ -1059,7 +1113,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         int b = b0;                                // this unit's TMEM buffer
         uint8_t *slab = out_stage + b * Cfg::OUT_BYTES + (half * 4 + quad) * Cfg::SLAB;
         uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(&acc_empty[b]), 0) : 0;
-        const float lo = p.relu ? 0.f : -(float)(1 << (BITS - 1));
+        const float lo = (p.relu || p.y_uns) ? 0.f : -(float)(1 << (BITS - 1));
         const uint64_t out_pol = p.out_policy == 1 ? policy_evict_last() : p.out_policy == 2 ? policy_evict_first() : 0;
         constexpr bool relu8 = Cfg::RELU8;   // ReLU specialisation (p.relu == 1 guaranteed by the dispatch)
         // scale/shift of the j-th tile of this buffer -> slot j % 3, issued by the
@@ -1229,17 +1283,24 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                         sa.w, sb.z, sb.w, u2, u3);
                                 if constexpr (Cfg::RES) {
                                     // v = fmaf(skip, res_scale, u) (reading 15); skip byte -> exact float as
-                                    // (2^23 + (byte ^ 0x80)) - (2^23 + 128): one PRMT + one FADD per code
-                                    const uint32_t wv = (&sk.x)[q] ^ 0x80808080u;
-                                    float k0 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7650)), 8388736.f);
-                                    float k1 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7651)), 8388736.f);
-                                    float k2 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7652)), 8388736.f);
-                                    float k3 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7653)), 8388736.f);
+                                    // (2^23 + (byte ^ bias)) - (2^23 + bias), bias 0x80 for a signed skip,
+                                    // 0 for an unsigned one (reading 16): one PRMT + one FADD per code
+                                    const uint32_t wv = (&sk.x)[q] ^ p.skip_xor;
+                                    float k0 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7650)), p.skip_off);
+                                    float k1 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7651)), p.skip_off);
+                                    float k2 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7652)), p.skip_off);
+                                    float k3 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7653)), p.skip_off);
                                     fma2_rn(k0, k1, p.res_scale, p.res_scale, u0, u1, u0, u1);
                                     fma2_rn(k2, k3, p.res_scale, p.res_scale, u2, u3, u2, u3);
                                 }
-                                w4[q] = pack4_f32_s8(u0, u1, u2, u3);
-                                if (relu8 || p.relu) w4[q] = relu_s8x4(w4[q]);
+                                if constexpr (Cfg::U8) {
+                                    w4[q] = pack4_f32_u8(u0, u1, u2, u3);       // unsigned codes: clamp [0, 255]
+                                } else if (Cfg::RES && p.y_uns) {
+                                    w4[q] = pack4_f32_u8(u0, u1, u2, u3);
+                                } else {
+                                    w4[q] = pack4_f32_s8(u0, u1, u2, u3);
+                                    if (relu8 || p.relu) w4[q] = relu_s8x4(w4[q]);
+                                }
                             }
                             pk = make_uint4(w4[0], w4[1], w4[2], w4[3]);
                         } else {
@@ -1248,15 +1309,28 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             for (int q = 0; q < Cfg::CW / 4; ++q) {
                                 float4 sa, sb;
                                 ss4(q, sa, sb);
-                                if constexpr (Cfg::RES) {
+                                if constexpr (Cfg::RELU4) {
+                                    // ReLU epilogue: clamp(rne(u), 0, 255) in one F2I.U8 (4x the s32 F2I
+                                    // rate), then min with the top code (7 signed / 15 unsigned, reading 16)
+                                    float u0, u1, u2, u3;
+                                    fma2_rn(__int2float_rn((int)v[4 * q] >> 8), __int2float_rn((int)v[4 * q + 1] >> 8),
+                                            sa.x, sa.y, sb.x, sb.y, u0, u1);
+                                    fma2_rn(__int2float_rn((int)v[4 * q + 2] >> 8), __int2float_rn((int)v[4 * q + 3] >> 8),
+                                            sa.z, sa.w, sb.z, sb.w, u2, u3);
+                                    r[4 * q] = min(f2u8_rn(u0), p.code_hi);
+                                    r[4 * q + 1] = min(f2u8_rn(u1), p.code_hi);
+                                    r[4 * q + 2] = min(f2u8_rn(u2), p.code_hi);
+                                    r[4 * q + 3] = min(f2u8_rn(u3), p.code_hi);
+                                } else if constexpr (Cfg::RES) {
                                     // codes 4q..4q+3 = nibbles 4(q%2).. of skip word q/2; nibble -> exact
-                                    // float as (2^23 + (nib ^ 8)) - (2^23 + 8); ReLU / clamp after the add
-                                    const uint32_t wv = (&sk.x)[q >> 1] ^ 0x88888888u;
+                                    // float as (2^23 + (nib ^ bias)) - (2^23 + bias), bias 8 for a signed
+                                    // skip, 0 unsigned (reading 16); ReLU / clamp after the add
+                                    const uint32_t wv = (&sk.x)[q >> 1] ^ p.skip_xor;
                                     const float sav[4] = {sa.x, sa.y, sa.z, sa.w}, sbv[4] = {sb.x, sb.y, sb.z, sb.w};
 #pragma unroll
                                     for (int e = 0; e < 4; ++e) {
                                         const uint32_t nib = (wv >> (4 * (4 * (q & 1) + e))) & 0xFu;
-                                        const float kf = __fsub_rn(__uint_as_float(0x4B000000u | nib), 8388616.f);
+                                        const float kf = __fsub_rn(__uint_as_float(0x4B000000u | nib), p.skip_off);
                                         const float u = __fmaf_rn(__int2float_rn((int)v[4 * q + e] >> 8), sav[e], sbv[e]);
                                         const float vv = fmaxf(__fmaf_rn(kf, p.res_scale, u), lo);
                                         asm("cvt.rni.s32.f32 %0, %1;" : "=r"(r[4 * q + e]) : "f"(vv));
@@ -1268,8 +1342,12 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                     r[4 * q + 3] = requant_int((int)v[4 * q + 3] >> 8, sa.w, sb.w, lo);
                                 }
                             }
-                            pk = make_uint4(pack8_sat_s4(r), pack8_sat_s4(r + 8), pack8_sat_s4(r + 16),
-                                            pack8_sat_s4(r + 24));
+                            if (Cfg::RELU4 || (Cfg::RES && p.y_uns))   // codes in [0, hi]: unsigned packing
+                                pk = make_uint4(pack8_sat_u4(r), pack8_sat_u4(r + 8), pack8_sat_u4(r + 16),
+                                                pack8_sat_u4(r + 24));
+                            else
+                                pk = make_uint4(pack8_sat_s4(r), pack8_sat_s4(r + 8), pack8_sat_s4(r + 16),
+                                                pack8_sat_s4(r + 24));
                         }
                         const int sbyte = c * 16;                 // byte within this warp's slab row
                         if constexpr (Cfg::OUTP == OUT_TMA) {

@@ -48,7 +48,7 @@ int set_err(int code, const char *fmt, ...) {
 
 extern "C" const char *conv_q_last_error(void) { return g_err.c_str(); }
 extern "C" int conv_q_last_status(void) { return g_status; }
-extern "C" int conv_q_version(void) { return 104; }
+extern "C" int conv_q_version(void) { return 105; }
 
 // ============================================================== driver entry points
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -123,8 +123,11 @@ static std::string cand_name(const conv_q_plan_s *p, int i) {
 
 static std::string shape_key(const conv_q_plan_s *p) {
     char b[160];
-    snprintf(b, sizeof b, "N%d_H%d_W%d_C%d_K%d_R%d_S%d_st%d_p%d_b%d_sm%d_m%d_r%d%s", p->N, p->H, p->W, p->C, p->K,
-             p->R, p->S, p->stride, p->pad, p->bits, g_num_sms, p->out_mode, p->relu, p->skip ? "_res" : "");
+    snprintf(b, sizeof b, "N%d_H%d_W%d_C%d_K%d_R%d_S%d_st%d_p%d_b%d_sm%d_m%d_r%d%s%s", p->N, p->H, p->W, p->C, p->K,
+             p->R, p->S, p->stride, p->pad, p->bits, g_num_sms, p->out_mode, p->relu, p->skip ? "_res" : "",
+             (p->x_uns || p->y_uns || (p->skip && p->skip_uns))
+                 ? (std::string("_u") + char('0' + p->x_uns) + char('0' + p->y_uns) + char('0' + p->skip_uns)).c_str()
+                 : "");
     return p->s2d ? std::string(b) + "_s2d" : std::string(b);
 }
 
@@ -547,6 +550,22 @@ extern "C" int conv_q_plan_set_residual(conv_q_plan_t *p, const void *skip, floa
     return CONV_Q_OK;
 }
 
+extern "C" int conv_q_plan_set_formats(conv_q_plan_t *p, int x_unsigned, int y_unsigned, int skip_unsigned) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    if ((x_unsigned | y_unsigned | skip_unsigned) & ~1) return set_err(CONV_Q_EINVAL, "formats must be 0/1");
+    // accumulator guard for unsigned activations (reading 16): |acc| <= R*S*C*(2^b - 1)*2^(b-1);
+    // INT4's MMA accumulator holds 256*acc -> bound R*S*C*255*128 for both widths
+    if (x_unsigned && p->Kg * (int64_t)(255 * 128) > 2147483647LL)
+        return set_err(CONV_Q_EOVERFLOW, "R*S*C = %lld: unsigned-activation accumulator bound exceeds int32",
+                       (long long)p->Kg);
+    p->x_uns = x_unsigned;
+    p->y_uns = y_unsigned;
+    p->skip_uns = skip_unsigned;
+    apply_cache(p);
+    if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK) return ensure_ws(p);
+    return CONV_Q_OK;
+}
+
 extern "C" int conv_q_plan_num_candidates(const conv_q_plan_t *p) {
     if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
     return (int)p->cands.size();
@@ -759,12 +778,17 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
         if (p->bits == 8) return direct ? dispatch_conv_8_10(p, scale, y) : dispatch_conv_8_8(p, scale, y);
         return direct ? dispatch_conv_4_10(p, scale, y) : dispatch_conv_4_8(p, scale, y);
     }
+    // ReLU epilogues (unsigned output codes clamp at 0: the ReLU, reading 16)
+    const bool relu = p->relu || p->y_uns;
     if (p->bits == 8) {
         if (s32) return dispatch_conv_8_1(p, scale, y);
-        if (p->relu) return direct ? dispatch_conv_8_6(p, scale, y) : dispatch_conv_8_4(p, scale, y);
+        if (relu && p->y_uns) return direct ? dispatch_conv_8_22(p, scale, y) : dispatch_conv_8_20(p, scale, y);
+        if (relu) return direct ? dispatch_conv_8_6(p, scale, y) : dispatch_conv_8_4(p, scale, y);
         return direct ? dispatch_conv_8_2(p, scale, y) : dispatch_conv_8_0(p, scale, y);
     }
-    return s32 ? dispatch_conv_4_1(p, scale, y) : direct ? dispatch_conv_4_2(p, scale, y) : dispatch_conv_4_0(p, scale, y);
+    if (s32) return dispatch_conv_4_1(p, scale, y);
+    if (relu) return direct ? dispatch_conv_4_6(p, scale, y) : dispatch_conv_4_4(p, scale, y);
+    return direct ? dispatch_conv_4_2(p, scale, y) : dispatch_conv_4_0(p, scale, y);
 }
 
 // Time every candidate (a7): `warmup` untimed runs, then 3 rounds of `reps`
@@ -958,6 +982,12 @@ extern "C" int conv_q_requant(const int32_t *acc, int64_t M, int K, const float 
 // R x R max pooling of packed codes (pack.cuh maxpool_kernel)
 extern "C" int conv_q_maxpool(const void *x, int N, int H, int W, int C, int R, int stride, int pad, int bits,
                               void *y, void *stream) {
+    return conv_q_maxpool_fmt(x, N, H, W, C, R, stride, pad, bits, 0, y, stream);
+}
+
+extern "C" int conv_q_maxpool_fmt(const void *x, int N, int H, int W, int C, int R, int stride, int pad, int bits,
+                                  int uns, void *y, void *stream) {
+    if (uns != 0 && uns != 1) return set_err(CONV_Q_EINVAL, "uns must be 0 or 1");
     if (!x || !y) return set_err(CONV_Q_EINVAL, "NULL tensor pointer");
     if (N < 1 || H < 1 || W < 1 || C < 1 || R < 1 || stride < 1) return set_err(CONV_Q_EINVAL, "dimensions must be >= 1");
     if (bits != 4 && bits != 8) return set_err(CONV_Q_EINVAL, "bits must be 4 or 8");
@@ -986,8 +1016,10 @@ extern "C" int conv_q_maxpool(const void *x, int N, int H, int W, int C, int R, 
     const uint4 *xs = static_cast<const uint4 *>(x);
     uint4 *ys = static_cast<uint4 *>(y);
     const FastDiv fv = make_fastdiv(vpp), fq = make_fastdiv(Q), fp = make_fastdiv(P);
-    auto kern = bits == 8 ? (R == 3 ? maxpool_kernel<8, 3> : maxpool_kernel<8, 2>)
-                          : (R == 3 ? maxpool_kernel<4, 3> : maxpool_kernel<4, 2>);
+    auto kern = uns ? (bits == 8 ? (R == 3 ? maxpool_kernel<8, 3, true> : maxpool_kernel<8, 2, true>)
+                                 : (R == 3 ? maxpool_kernel<4, 3, true> : maxpool_kernel<4, 2, true>))
+                    : (bits == 8 ? (R == 3 ? maxpool_kernel<8, 3> : maxpool_kernel<8, 2>)
+                                 : (R == 3 ? maxpool_kernel<4, 3> : maxpool_kernel<4, 2>));
     CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, xs, ys, N, H, W, P, Q, vpp, stride, pad, fv, fq, fp));
     return CONV_Q_OK;
 }

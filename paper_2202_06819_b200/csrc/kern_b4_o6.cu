@@ -1,0 +1,11 @@
+// kern_b4_o6.cu -- instantiates the implicit-GEMM conv kernels for
+// BITS=4, output path OUT_DIRECT | OUT_RELU (direct stores): the INT4 ReLU
+// epilogue (F2I.U8 conversion, runtime top code 7 / 15 for signed / unsigned
+// codes, DESIGN reading 16).  Separate translation unit only to compile in parallel.
+#include "plan.cuh"
+
+namespace convq {
+int dispatch_conv_4_6(conv_q_plan_s *p, const float *scale, void *y) {
+    return dispatch_bn_kch<4, 6>(p, scale, y);
+}
+}  // namespace convq

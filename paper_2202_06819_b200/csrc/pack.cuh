@@ -290,13 +290,21 @@ __global__ void __launch_bounds__(256) s2d_weights_kernel(const int8_t *__restri
 // codes is the code of the max.  s8: byte-wise signed max (VIMNMX.S8); s4: the
 // even / odd nibbles expanded to 16*v bytes, byte max, repacked.
 __device__ __forceinline__ uint32_t vmax_s8x4(uint32_t a, uint32_t b) { return __vmaxs4(a, b); }
+// unsigned codes (DESIGN reading 16): byte-wise unsigned max; u4 nibbles as 16*v bytes
+__device__ __forceinline__ uint32_t vmax_u8x4(uint32_t a, uint32_t b) { return __vmaxu4(a, b); }
+__device__ __forceinline__ uint32_t vmax_u4x8(uint32_t a, uint32_t b) {
+    const uint32_t ae = (a << 4) & 0xF0F0F0F0u, ao = a & 0xF0F0F0F0u;
+    const uint32_t be = (b << 4) & 0xF0F0F0F0u, bo = b & 0xF0F0F0F0u;
+    const uint32_t me = __vmaxu4(ae, be), mo = __vmaxu4(ao, bo);
+    return ((me >> 4) & 0x0F0F0F0Fu) | (mo & 0xF0F0F0F0u);
+}
 __device__ __forceinline__ uint32_t vmax_s4x8(uint32_t a, uint32_t b) {
     const uint32_t ae = (a << 4) & 0xF0F0F0F0u, ao = a & 0xF0F0F0F0u;   // 16 * even / odd nibbles as s8
     const uint32_t be = (b << 4) & 0xF0F0F0F0u, bo = b & 0xF0F0F0F0u;
     const uint32_t me = __vmaxs4(ae, be), mo = __vmaxs4(ao, bo);
     return ((me >> 4) & 0x0F0F0F0Fu) | (mo & 0xF0F0F0F0u);
 }
-template <int BITS, int R>
+template <int BITS, int R, bool UNS = false>
 __global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ x, uint4 *__restrict__ y, int N,
                                                      int H, int W, int P, int Q, int vpp, int stride, int pad,
                                                      FastDiv fd_vpp, FastDiv fd_q, FastDiv fd_p) {
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ 
     asm volatile("griddepcontrol.wait;" ::: "memory");   // x is the previous kernel's output
     // identity of the max: the most negative code in every lane (out-of-range
     // taps read as it, so the padding never wins: every window has an in-range tap)
-    constexpr uint32_t MINV = BITS == 8 ? 0x80808080u : 0x88888888u;
+    constexpr uint32_t MINV = UNS ? 0u : BITS == 8 ? 0x80808080u : 0x88888888u;
     const int total = N * P * Q * vpp;          // < 2^31 (checked on the host)
     for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
         const int pix = fd_vpp.div(o);
@@ -327,7 +335,13 @@ __global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ 
         uint4 m = a[0];
 #pragma unroll
         for (int i = 1; i < R * R; ++i) {
-            if constexpr (BITS == 8)
+            if constexpr (BITS == 8 && UNS)
+                m = make_uint4(vmax_u8x4(m.x, a[i].x), vmax_u8x4(m.y, a[i].y), vmax_u8x4(m.z, a[i].z),
+                               vmax_u8x4(m.w, a[i].w));
+            else if constexpr (UNS)
+                m = make_uint4(vmax_u4x8(m.x, a[i].x), vmax_u4x8(m.y, a[i].y), vmax_u4x8(m.z, a[i].z),
+                               vmax_u4x8(m.w, a[i].w));
+            else if constexpr (BITS == 8)
                 m = make_uint4(vmax_s8x4(m.x, a[i].x), vmax_s8x4(m.y, a[i].y), vmax_s8x4(m.z, a[i].z),
                                vmax_s8x4(m.w, a[i].w));
             else

@@ -78,6 +78,7 @@ struct conv_q_plan_s {
     int relu = 0, out_mode = CONV_Q_OUT_PACKED;
     const void *skip = nullptr;   // conv_q_plan_set_residual: fused residual add (NULL = none)
     float res_scale = 0.f;
+    int x_uns = 0, y_uns = 0, skip_uns = 0;   // conv_q_plan_set_formats: unsigned codes (DESIGN reading 16)
     cudaStream_t stream = nullptr;
     std::vector<Cand> cands;
     int sel = 0;
@@ -159,13 +160,22 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     // resident CTA would block in tcgen05.alloc until the first exits.  Configs
     // whose shared memory would let two CTAs share an SM (228 KB per SM, 1 KB
     // reserved per CTA) launch with their request padded past half of it.
-    constexpr int SMEM_LAUNCH = Cfg::SMEM > 116 * 1024 ? Cfg::SMEM : 116 * 1024;
+    // Shared memory: the weight-stationary region holds exactly this layer's
+    // BN/CG x R*S*C block (rounded to 1 KB; the 64 KB budget is the plan-time
+    // bound), and the ring gets as many stages as the rest of the 227 KB allows.
+    const int wsb = (HALO & 2) ? (int)ceil_div((int64_t)p->R * p->S * (p->C / KCH) * Cfg::B_TILE, 1024) * 1024 : 0;
+    if (wsb > Cfg::WSB) return set_err(CONV_Q_EUNSUPPORTED, "weight block %d B exceeds the resident region", wsb);
+    const int stages = Cfg::stages_for(wsb);
+    const int smem = Cfg::smem_for(wsb, stages);
+    const int SMEM_LAUNCH = smem > 116 * 1024 ? smem : 116 * 1024;
     static bool attr_set = false;
     if (!attr_set) {
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LAUNCH));
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
         attr_set = true;
     }
     ConvParams prm;
+    prm.stages = stages;
+    prm.wsb = wsb;
     prm.N = p->N; prm.H = p->H; prm.W = p->W; prm.C = p->C; prm.K = p->K; prm.R = p->R; prm.S = p->S;
     prm.stride = p->stride; prm.pad = p->pad; prm.pad_w = p->s2d ? 0 : p->pad; prm.P = p->P; prm.Q = p->Q; prm.M = (int)p->M;
     prm.row_bytes = p->row_bytes;
@@ -211,6 +221,11 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.scale = scale;
     prm.skip = static_cast<const uint8_t *>(p->skip);
     prm.res_scale = p->res_scale;
+    prm.x_uns = p->x_uns;
+    prm.y_uns = p->y_uns;
+    prm.code_hi = p->y_uns ? (1 << BITS) - 1 : (1 << (BITS - 1)) - 1;
+    prm.skip_xor = p->skip_uns ? 0u : (BITS == 8 ? 0x80808080u : 0x88888888u);
+    prm.skip_off = 8388608.f + (p->skip_uns ? 0.f : (BITS == 8 ? 128.f : 8.f));
     prm.y32 = static_cast<int32_t *>(y);
     prm.y8 = static_cast<uint8_t *>(y);
     prm.out_row = p->out_row;
@@ -302,6 +317,10 @@ int dispatch_conv_4_1(conv_q_plan_s *p, const float *scale, void *y);
 int dispatch_conv_4_2(conv_q_plan_s *p, const float *scale, void *y);
 int dispatch_conv_8_8(conv_q_plan_s *p, const float *scale, void *y);    // OUT_TMA | OUT_RES
 int dispatch_conv_8_10(conv_q_plan_s *p, const float *scale, void *y);   // OUT_DIRECT | OUT_RES
+int dispatch_conv_8_20(conv_q_plan_s *p, const float *scale, void *y);   // OUT_TMA | OUT_RELU | OUT_U
+int dispatch_conv_8_22(conv_q_plan_s *p, const float *scale, void *y);   // OUT_DIRECT | OUT_RELU | OUT_U
+int dispatch_conv_4_4(conv_q_plan_s *p, const float *scale, void *y);    // OUT_TMA | OUT_RELU
+int dispatch_conv_4_6(conv_q_plan_s *p, const float *scale, void *y);    // OUT_DIRECT | OUT_RELU
 int dispatch_conv_4_8(conv_q_plan_s *p, const float *scale, void *y);
 int dispatch_conv_4_10(conv_q_plan_s *p, const float *scale, void *y);
 

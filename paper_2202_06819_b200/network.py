@@ -48,10 +48,13 @@ class ConvNet:
     net.tune(); net.step(stream)                      # net.x_in is the fp16 input, net.outputs the results
     """
 
-    def __init__(self, batch: int, bits: int, device, stream=None):
+    def __init__(self, batch: int, bits: int, device, stream=None, unsigned: bool = False):
+        """unsigned: every ReLU output is written as unsigned codes [0, 2^b - 1] and
+        read as unsigned activations by its consumers (DESIGN reading 16)."""
         import torch
         self.torch = torch
         self.B, self.bits, self.device = batch, bits, device
+        self.unsigned = unsigned
         self.stream = stream
         self.convs: list[_Conv] = []
         self.stem = None
@@ -68,6 +71,7 @@ class ConvNet:
         Cp = padded_channels(C, self.bits)
         self.net_in = t.empty((self.B, H, W, Cp * self.bits // 8), dtype=t.uint8, device=self.device)
         self.inv_scale = inv_scale
+        self.in_uns = False                           # quantized fp16 input: signed codes
         self._stages = [("quantize", lambda s: quantize(self.x_in, inv_scale, self.bits, out=self.net_in, stream=s))]
         self.input_desc = f"quantize fp16 [{self.B},{H},{W},{C}]"
 
@@ -77,7 +81,9 @@ class ConvNet:
         t = self.torch
         L = conv1
         self.x_in = t.empty((self.B, L.H, L.W, L.C), dtype=t.float16, device=self.device)
-        sp = StemPlan(self.B, L.H, L.W, L.C, L.K, L.R, L.S, L.pad, self.bits, relu=relu)
+        sp = StemPlan(self.B, L.H, L.W, L.C, L.K, L.R, L.S, L.pad, self.bits, relu=relu,
+                      y_uns=self.unsigned and relu)
+        self.in_uns = self.unsigned and relu          # format of the pooled stem output
         xs = t.empty(sp.x_dims, dtype=t.uint8, device=self.device)
         wp = sp.pack_weights(w_codes)
         y1 = t.empty((self.B, sp.P, sp.Q, L.K * self.bits // 8), dtype=t.uint8, device=self.device)
@@ -89,7 +95,8 @@ class ConvNet:
         self._stages = [
             ("s2d", lambda s: sp.quantize(self.x_in, inv_scale, out=xs, stream=s)),
             ("stem", lambda s: sp.run(xs, wp, ss, y1, stream=s)),
-            ("pool", lambda s: maxpool(y1, L.K, pr, pst, ppad, self.bits, out=self.net_in, stream=s)),
+            ("pool", lambda s: maxpool(y1, L.K, pr, pst, ppad, self.bits, out=self.net_in, stream=s,
+                                       uns=self.in_uns)),
         ]
         self.input_desc = f"stem {L.name} {L.R}x{L.S}/{L.stride} {L.C}->{L.K} (s2d) + maxpool {pr}x{pr}/{pst}"
 
@@ -101,14 +108,21 @@ class ConvNet:
         before ReLU / rounding (a ResNet block's residual, DESIGN reading 15)."""
         t = self.torch
         assert src < len(self.convs) and (skip is None or skip < len(self.convs))
-        plan = ConvPlan(self.B, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, self.bits, relu=relu)
+        x_uns = self.in_uns if src < 0 else self.convs[src].plan.y_uns
+        y_uns = self.unsigned and relu
+        plan = ConvPlan(self.B, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, self.bits, relu=relu,
+                        x_uns=x_uns, y_uns=y_uns)
         wp = pack_weights(w_codes, self.bits)
         y = t.empty((self.B, L.P, L.Q, L.K * self.bits // 8), dtype=t.uint8, device=self.device)
+        skip_uns = False
         if skip is not None:
             sk = self.net_in if skip < 0 else self.convs[skip].y
             assert tuple(sk.shape) == tuple(y.shape), (sk.shape, y.shape)
+            skip_uns = self.in_uns if skip < 0 else self.convs[skip].plan.y_uns
+            if skip_uns:
+                plan.set_formats(x_uns, y_uns, True)
             plan.set_residual(sk, res_scale)
-        key = (L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, relu, skip is not None)
+        key = (L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, relu, skip is not None, x_uns, y_uns, skip_uns)
         self.convs.append(_Conv(name or getattr(L, "name", f"conv{len(self.convs)}"), L, src, relu, skip, res_scale,
                                 plan, wp, ss, y, key))
         return len(self.convs) - 1
