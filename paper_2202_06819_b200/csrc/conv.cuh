@@ -213,6 +213,13 @@ struct ConvCfg {
     static constexpr bool U8 = RELU8 && (OUT & OUT_U) != 0;          // unsigned u8 output codes
     static constexpr bool RELU4 = BITS == 4 && (OUT & OUT_RELU) != 0;  // INT4 ReLU epilogue (runtime top code)
     static constexpr bool RES = (OUT & OUT_RES) != 0;          // residual add: v = fmaf(skip, res_scale, u)
+    // residual with TMA-store output and one m-group per unit: each epilogue warp
+    // TMA-loads its 32-row skip slab into its output staging slab (same box, same
+    // swizzle as the store), reads each 16-byte skip chunk from the address its
+    // packed output chunk then overwrites, and stores the slab as usual -- the
+    // skip tensor moves as coalesced bulk copies issued before the accumulator
+    // wait, not as one 16-byte load per thread and row
+    static constexpr bool SKIP_TMA = RES && (OUT & 3) == OUT_TMA && MT == 1;
     static constexpr int OUT_BYTES = OUTP == OUT_TMA ? BM * OUT_ROW : 0;   // staging per TMEM buffer
     static constexpr int NUM_EPI = epi_warpgroups(BITS);            // epilogue warpgroups
     // TMEM accumulator buffers: as many as the 512 columns allow (max 4), so
@@ -249,7 +256,8 @@ struct ConvCfg {
     // stages with the full weight-stationary budget (the minimum the config
     // guarantees; the launch uses stages_for(wsb) >= STAGES for the real block)
     static constexpr int STAGES = STAGES_FIT > MAX_STAGES ? MAX_STAGES : STAGES_FIT;
-    static constexpr int FIXED_BYTES = 1024 + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * (HALO_BYTES + HALO_PK) + BAR_BYTES;
+    // (1024: base alignment of the dynamic smem; + 1024: the ring end rounded up to 1 KB)
+    static constexpr int FIXED_BYTES = 2048 + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * (HALO_BYTES + HALO_PK) + BAR_BYTES;
     static constexpr int SMEM = FIXED_BYTES + WSB + STAGES * STAGE_BYTES;
     static int stages_for(int wsb) {
         const int st = (SMEM_LIMIT - FIXED_BYTES - wsb) / STAGE_BYTES;
@@ -517,7 +525,8 @@ __device__ __forceinline__ void expand_kblock(const uint8_t *a_src, uint8_t *a_d
 template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO>
 __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::NUM_THREADS, 1)
     conv_igemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                      const __grid_constant__ CUtensorMap tm_y, const ConvParams p) {
+                      const __grid_constant__ CUtensorMap tm_y, const __grid_constant__ CUtensorMap tm_s,
+                      const ConvParams p) {
     using Cfg = ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>;
     // measurement hooks (wait-cycle trace, probe modes) exist only in the
     // CONVQ_INSTRUMENT build (libconvq_instr.so); compiled out otherwise
@@ -545,7 +554,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][NSUB][BNL*KCH]
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][NSUB][BM*KCH/2]
     uint8_t *b_pk = a_pk + STAGES * Cfg::A_PK;          // INT4: [STAGES][NSUB][BNL*KCH/2]
-    uint8_t *out_stage = b_pk + STAGES * Cfg::B_PK;     // [NBUF][EPB][4 quads] slabs [EPI_NSUB][32][EPI_SUBW]
+    // [NBUF][EPB][4 quads] slabs [EPI_NSUB][32][EPI_SUBW]: 1024-byte aligned (swizzled TMA boxes)
+    // whatever the runtime ring depth (INT4 stage sizes need not be multiples of 1 KB)
+    uint8_t *out_stage = smem + ((b_pk + STAGES * Cfg::B_PK - smem + 1023) & ~1023);
     float *ss_stage = reinterpret_cast<float *>(out_stage + Cfg::NBUF * Cfg::OUT_BYTES);  // [NBUF][3 slots][2][BN]
     uint8_t *halo_buf = out_stage + Cfg::NBUF * (Cfg::OUT_BYTES + Cfg::SS_BYTES);   // HALO: [NHALO][HALO_BYTES]
     uint8_t *halo_pk = halo_buf + Cfg::NHALO * Cfg::HALO_BYTES;  // INT4 halo: [NHALO][HALO_PK] packed boxes
@@ -558,7 +569,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     uint64_t *hempty = acc_empty + 4;       // HALO: MMA -> TMA, halo buffer free [NHALO <= 4]
     uint64_t *bfull = hempty;               // WS (no separate halo buffers): resident weights loaded
     uint64_t *ss_full = hempty + 4;         // scale/shift bulk copy -> epilogue [NBUF][3 slots]
-    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(ss_full + 12);
+    uint64_t *skbar = ss_full + 12;         // SKIP_TMA: per epilogue warp, its skip slab landed [16]
+    uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(skbar + 16);
     // dual MMA warps: per smem stage, the last global stage index whose fill an
     // MMA warp has waited for.  A parity wait on a stage is only valid once the
     // stage's PREVIOUS fill has completed -- and TMA fills of different stages
@@ -583,6 +595,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         tma_prefetch_desc(&tm_a);
         tma_prefetch_desc(&tm_b);
         if (Cfg::OUTP == OUT_TMA) tma_prefetch_desc(&tm_y);
+        if (Cfg::SKIP_TMA) tma_prefetch_desc(&tm_s);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -597,6 +610,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             for (int k = 0; k < 3; ++k) mbar_init(&ss_full[3 * b + k], 1);
         }
         for (int i = 0; i < STAGES; ++i) stage_done[i] = -1;
+        if (Cfg::SKIP_TMA)
+            for (int w = 0; w < 4 * Cfg::NUM_EPI; ++w) mbar_init(&skbar[w], 1);
         fence_mbar_init();
     }
     if (warp == Cfg::MMA_WARP) {
@@ -1174,8 +1189,24 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             // accumulator wait (the skip tensor is an earlier layer's output), so
             // their latency overlaps the tile's mainloop
             constexpr int NCH = Cfg::EPI_COLS / Cfg::CW;
-            uint4 skp[Cfg::RES ? Cfg::MT : 1][Cfg::RES ? NCH : 1];
-            if constexpr (Cfg::RES) {
+            constexpr bool SKT = Cfg::SKIP_TMA;
+            uint4 skp[Cfg::RES && !SKT ? Cfg::MT : 1][Cfg::RES && !SKT ? NCH : 1];
+            if constexpr (SKT) {
+                // the warp's skip slab -> its (free) output staging slab, one bulk copy per
+                // 128-byte column block, completing on the warp's own barrier
+                if (p.splits == 1) {
+                    if (lane == 0) {
+                        tma_store_wait_read0();   // the slab's previous store has read it out
+                        mbar_arrive_expect_tx(&skbar[warp], (uint32_t)Cfg::SLAB);
+#pragma unroll
+                        for (int s = 0; s < Cfg::EPI_NSUB; ++s)
+                            tma_load_2d(slab + s * (32 * Cfg::EPI_SUBW), &tm_s, &skbar[warp],
+                                        n_blk * Cfg::OUT_ROW + half * Cfg::EPI_ROW + s * Cfg::EPI_SUBW, mrow0 + quad * 32,
+                                        policy_evict_first());
+                    }
+                    __syncwarp();
+                }
+            } else if constexpr (Cfg::RES) {
                 if (p.splits == 1) {
 #pragma unroll
                     for (int g = 0; g < Cfg::MT; ++g) {
@@ -1219,7 +1250,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             // scale/shift of this tile's columns: the buffer's smem slot (filled by
             // the MMA warp's bulk copy) or, for split-K units, global memory
             const float *ss_b = ss_stage + (3 * b + j % 3) * 2 * BN;
-            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag, const uint4 sk) {
+            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag, const uint4 sk_in) {
                     constexpr bool SMEM_SS = decltype(smem_tag)::value;
                     const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
                     const int col0 = n_blk * BN + ccol;
@@ -1242,6 +1273,17 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             }
                         }
                     } else {
+                        // SKIP_TMA: this chunk's skip codes sit in the staging slab at the very
+                        // address the packed output chunk is written to below
+                        uint4 sk = sk_in;
+                        if constexpr (Cfg::SKIP_TMA) {
+                            if (SMEM_SS) {
+                                const int sb = c * 16;
+                                sk = *reinterpret_cast<const uint4 *>(
+                                    slab + (sb / Cfg::EPI_SUBW) * (32 * Cfg::EPI_SUBW) +
+                                    swz<Cfg::EPI_SUBW>(lane * Cfg::EPI_SUBW + sb % Cfg::EPI_SUBW));
+                            }
+                        }
                         // (smem slot: columns past K hold stale values; their codes are never stored)
                         const bool full = SMEM_SS || col0 + Cfg::CW <= p.K;
                         const float4 *s4 = reinterpret_cast<const float4 *>(SMEM_SS ? ss_b + ccol : p.scale + col0);
@@ -1425,12 +1467,15 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             } else {
                 // the MMA warp's copy of this tile's scale/shift (long done by now)
                 if (Cfg::OUTP != OUT_S32) mbar_wait(&ss_full[3 * b + j % 3], (j / 3) & 1);
+                if constexpr (SKT) {   // this warp's skip slab (issued before the accumulator wait)
+                    mbar_wait(&skbar[warp], (uint32_t)(lu & 1));
+                }
                 // MT2: the unit's two m-groups sit in TMEM columns [g*BN, (g+1)*BN)
                 for (int g = 0; g < Cfg::MT; ++g) {
                     taddr = taddr0 + g * BN;
                     if constexpr (Cfg::MT > 1) m = (HA || S2H) ? halo_m(g * BM + row) : mrow0 + g * BM + row;
                     const bool last = g == Cfg::MT - 1;
-                    auto skr = [&](int c) -> uint4 { return skp[Cfg::RES ? g : 0][Cfg::RES ? c : 0]; };
+                    auto skr = [&](int c) -> uint4 { return skp[Cfg::RES && !SKT ? g : 0][Cfg::RES && !SKT ? c : 0]; };
                     if constexpr (BITS == 8 && NCH % 2 == 0) {
                         // 32 columns per tcgen05.ld (two 16-byte output pieces): half
                         // the exposed TMEM-load round trips of a 16-column loop

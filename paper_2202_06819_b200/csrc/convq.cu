@@ -720,10 +720,20 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(subw), CU_TENSOR_MAP_L2_PROMOTION_NONE,
                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(y) failed: %d", (int)r);
+        // the residual skip tensor has y's layout: the same box and swizzle, so the
+        // epilogue can TMA-load a warp's skip slab into its output staging slab
+        memset(&p->tm_s, 0, sizeof p->tm_s);
+        if (p->skip) {
+            r = g_encode_tiled(&p->tm_s, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(p->skip), dims, strides,
+                               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(subw),
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(skip) failed: %d", (int)r);
+        }
     } else {
         memset(&p->tm_y, 0, sizeof p->tm_y);
+        memset(&p->tm_s, 0, sizeof p->tm_s);
     }
-    p->c_x = x; p->c_w = w; p->c_y = y; p->c_sel = p->sel; p->c_mode = p->out_mode;
+    p->c_x = x; p->c_w = w; p->c_y = y; p->c_sel = p->sel; p->c_mode = p->out_mode; p->c_skip = p->skip;
     return CONV_Q_OK;
 }
 
@@ -767,7 +777,8 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
     if (rc) return rc;
     if (p->cands[p->sel].split > 1 && !p->ws)   // allocated by plan creation / set_config / set_epilogue / tune
         return set_err(CONV_Q_EINVAL, "split-K workspace missing (select the config with conv_q_plan_set_config)");
-    if (p->c_x != x || p->c_w != w || p->c_y != y || p->c_sel != p->sel || p->c_mode != p->out_mode) {
+    if (p->c_x != x || p->c_w != w || p->c_y != y || p->c_sel != p->sel || p->c_mode != p->out_mode ||
+        p->c_skip != p->skip) {
         rc = encode_maps(p, x, w, y);
         if (rc) return rc;
     }

@@ -92,8 +92,8 @@ struct conv_q_plan_s {
     unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
     unsigned long long *tl = nullptr;     // conv_q_plan_set_timeline (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
-    CUtensorMap tm_a, tm_b, tm_y;
-    const void *c_x = nullptr, *c_w = nullptr, *c_y = nullptr;
+    CUtensorMap tm_a, tm_b, tm_y, tm_s;   // tm_s: the residual skip tensor (y's box / swizzle)
+    const void *c_x = nullptr, *c_w = nullptr, *c_y = nullptr, *c_skip = nullptr;
     int c_sel = -1, c_mode = -1;
     // split-K workspace (zero between runs; owned by the plan)
     int32_t *ws = nullptr;
@@ -248,7 +248,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p->tm_a, p->tm_b, p->tm_y, prm));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p->tm_a, p->tm_b, p->tm_y, p->tm_s, prm));
     return CONV_Q_OK;
 }
 
