@@ -146,13 +146,17 @@ def layer_res_scale(spec: Spec, i: int) -> float:
     return wl.res_scale(wl.rng(spec.cfg_id, 500 + i))
 
 
-def build_network(spec: Spec, B: int, device, world: int = 1, dist=None):
-    """The device network of a workload (packed weights broadcast from rank 0)."""
+def build_network(spec: Spec, B: int, device, world: int = 1, dist=None, dataflow=None):
+    """The device network of a workload (packed weights broadcast from rank 0);
+    dataflow None = auto (row flags for per-GPU batch <= 8)."""
     import torch
 
     from paper_2202_06819_b200.network import ConvNet
 
-    net = ConvNet(B, spec.bits, device, unsigned=spec.unsigned)
+    if dataflow is None:
+        dataflow = B <= 8
+
+    net = ConvNet(B, spec.bits, device, unsigned=spec.unsigned, dataflow=dataflow)
 
     def dev_params(i):
         wv, ss = layer_weights(spec, i)
@@ -336,7 +340,11 @@ def run_ours(args):
     B_global, B, img0 = shard_plan(B_arg, world, rank, scaling)
 
     # ---- setup (off the timed path): weights, scales, plans, buffers, tuning
-    net = build_network(spec, B, dev, world, dist)
+    # row-flag dataflow between conv launches: measured faster only for the
+    # latency-bound tiny batches (ResNet-18 b1: 0.095 vs 0.101 ms); at b16 / b256
+    # whole-grid dependencies are faster (DESIGN 6), so it is on for B <= 8
+    dataflow = (B <= 8) if args.dataflow == "auto" else args.dataflow == "on"
+    net = build_network(spec, B, dev, world, dist, dataflow=dataflow)
     stream = torch.cuda.Stream(dev)          # all work (and graph capture) on one side stream
     torch.cuda.set_stream(stream)
     net.set_stream(stream)
@@ -544,7 +552,9 @@ def run_ours(args):
                        "kernels_per_step": nl, "input": net.input_desc, "parallelism": f"batch-shard dp{world}",
                        "l2": "inputs larger than L2: per-step working set %.2f GB >> 126 MB L2" % (
                            (bytes_step + net.x_in.numel() * 2) / 1e9),
-                       "launch": "CUDA graph per step (PDL between kernels)" if use_graph else "eager launches",
+                       "launch": ("CUDA graph per step (PDL between kernels" +
+                                  (", per-row dataflow flags between conv launches)" if net.dataflow else ")"))
+                                 if use_graph else "eager launches",
                        "timed_window": "plain graph replays only; conv-chain and per-launch events in separate windows"},
             "conv_tops": round(achieved_tops, 1),
             "conv_frac_int8_peak": round(achieved_tops / int8_peak_tops, 3),
@@ -803,6 +813,9 @@ def main():
                     help="process-group backend (gloo: several ranks may share one GPU, for testing)")
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
+    ap.add_argument("--dataflow", default="auto", choices=["auto", "on", "off"],
+                    help="per-row flags between conv launches instead of whole-grid dependencies "
+                         "(auto: on for per-GPU batch <= 8)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--parity-pixels", type=int, default=64)

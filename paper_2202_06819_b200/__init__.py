@@ -122,6 +122,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.conv_q_maxpool_fmt.argtypes = [vp, i, i, i, i, i, i, i, i, i, vp, vp]
     lib.conv_q_plan_set_formats.restype = i
     lib.conv_q_plan_set_formats.argtypes = [vp, i, i, i]
+    lib.conv_q_plan_set_deps.restype = i
+    lib.conv_q_plan_set_deps.argtypes = [vp, vp, vp, vp]
     lib.conv_q_int8_peak.restype = i
     lib.conv_q_int8_peak.argtypes = [i, ctypes.POINTER(ctypes.c_double)]
     _lib = lib
@@ -207,6 +209,13 @@ class ConvPlan:
         self._skip = skip
         ptr = None if skip is None else _ptr(skip)
         _check(load().conv_q_plan_set_residual(self._h, ctypes.c_void_p(ptr), float(res_scale)))
+
+    def set_deps(self, in_rows=None, skip_rows=None, out_rows=None):
+        """Cross-launch row flags (conv_q_plan_set_deps): int32/uint32 device tensors
+        [N*H] / [N*P] / [N*P] (zeroed before each chain run), or None."""
+        ptr = lambda t: ctypes.c_void_p(None if t is None else _ptr(t))  # noqa: E731
+        _check(load().conv_q_plan_set_deps(self._h, ptr(in_rows), ptr(skip_rows), ptr(out_rows)))
+        self._deps = (in_rows, skip_rows, out_rows)
 
     def candidates(self) -> list[str]:
         lib = load()

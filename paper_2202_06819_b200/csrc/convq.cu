@@ -550,6 +550,19 @@ extern "C" int conv_q_plan_set_residual(conv_q_plan_t *p, const void *skip, floa
     return CONV_Q_OK;
 }
 
+extern "C" int conv_q_plan_set_deps(conv_q_plan_t *p, const unsigned *in_rows, const unsigned *skip_rows,
+                                    unsigned *out_rows) {
+    if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
+    if (p->s2d && in_rows) return set_err(CONV_Q_EUNSUPPORTED, "the s2d stem plan reads the s2d quantize output");
+    if ((in_rows && (reinterpret_cast<uintptr_t>(in_rows) & 3)) || (skip_rows && (reinterpret_cast<uintptr_t>(skip_rows) & 3)) ||
+        (out_rows && (reinterpret_cast<uintptr_t>(out_rows) & 3)))
+        return set_err(CONV_Q_EINVAL, "row flag arrays must be 4-byte aligned");
+    p->dep_in = in_rows;
+    p->dep_skip = skip_rows;
+    p->dep_out = out_rows;
+    return CONV_Q_OK;
+}
+
 extern "C" int conv_q_plan_set_formats(conv_q_plan_t *p, int x_unsigned, int y_unsigned, int skip_unsigned) {
     if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
     if ((x_unsigned | y_unsigned | skip_unsigned) & ~1) return set_err(CONV_Q_EINVAL, "formats must be 0/1");
@@ -807,31 +820,63 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
 // kernel, as in a layer sequence), score = the median round's mean.  us[i]
 // receives candidate i's score (or -1 if it failed to run).  Restores the
 // previous selection.  Returns the index of the fastest candidate.
+// The `reps` back-to-back launches of a round are captured into a CUDA graph
+// and the graph is replayed: the device time of the launch sequence (PDL
+// between them, as in a layer chain) without the host's per-launch cost --
+// measured ~4 us per conv_q_run and ~13 us through the Python binding, which
+// exceeds the device time of small-batch layers and would make eager timing
+// pick configs by host overhead.
 static int time_candidates(conv_q_plan_s *p, const void *x, const void *w, const float *scale, void *y, int warmup,
                            int reps, float *us) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(p->stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return set_err(CONV_Q_EINVAL, "tuning cannot run inside a graph capture");
+    // capture needs a non-legacy stream: use a private one when the plan's is the NULL stream
+    cudaStream_t user_stream = p->stream, ts = p->stream;
+    if (ts == nullptr || ts == cudaStreamLegacy || ts == cudaStreamPerThread) {
+        CUDA_TRY(cudaStreamSynchronize(ts));
+        CUDA_TRY(cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking));
+    }
+    p->stream = ts;
     cudaEvent_t e0, e1;
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
     int best = -1, rc = CONV_Q_OK;
     float best_us = 0.f;
     const int saved = p->sel;
-    for (int i = 0; i < (int)p->cands.size(); ++i) {
+    for (int i = 0; i < (int)p->cands.size() && !rc; ++i) {
         p->sel = i;
         if ((rc = ensure_ws(p))) break;   // split-K workspace (grows only), before any timed run
-        for (int k = 0; k < warmup; ++k)
-            if ((rc = conv_q_run(p, x, w, scale, y))) break;
+        for (int k = 0; k < warmup + 1 && !rc; ++k) rc = conv_q_run(p, x, w, scale, y);   // + tensor maps encoded
         if (rc) break;
-        float rt[3];
-        for (int k = 0; k < 3 && !rc; ++k) {
-            cudaEventRecord(e0, p->stream);
-            for (int j = 0; j < reps && !rc; ++j) rc = conv_q_run(p, x, w, scale, y);
-            cudaEventRecord(e1, p->stream);
-            if (rc) break;
-            cudaEventSynchronize(e1);
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, e0, e1);
-            rt[k] = ms * 1000.f / reps;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaError_t ce = cudaStreamBeginCapture(ts, cudaStreamCaptureModeThreadLocal);
+        if (ce != cudaSuccess) { rc = set_err(CONV_Q_ECUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(ce)); break; }
+        for (int j = 0; j < reps && !rc; ++j) rc = conv_q_run(p, x, w, scale, y);
+        ce = cudaStreamEndCapture(ts, &graph);
+        if (!rc && ce != cudaSuccess) rc = set_err(CONV_Q_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(ce));
+        if (!rc) {
+            ce = cudaGraphInstantiate(&exec, graph, 0);
+            if (ce != cudaSuccess) rc = set_err(CONV_Q_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ce));
         }
+        float rt[3] = {0.f, 0.f, 0.f};
+        if (!rc) {
+            cudaGraphLaunch(exec, ts);   // upload / first-replay costs outside the timed rounds
+            for (int k = 0; k < 3; ++k) {
+                cudaEventRecord(e0, ts);
+                cudaGraphLaunch(exec, ts);
+                cudaEventRecord(e1, ts);
+                cudaEventSynchronize(e1);
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                rt[k] = ms * 1000.f / reps;
+            }
+            ce = cudaGetLastError();
+            if (ce != cudaSuccess) rc = set_err(CONV_Q_ECUDA, "candidate graph replay: %s", cudaGetErrorString(ce));
+        }
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
         if (rc) break;
         std::sort(rt, rt + 3);
         if (us) us[i] = rt[1];
@@ -843,8 +888,10 @@ static int time_candidates(conv_q_plan_s *p, const void *x, const void *w, const
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     p->sel = saved;
+    cudaError_t e = cudaStreamSynchronize(ts);
+    if (ts != user_stream) cudaStreamDestroy(ts);
+    p->stream = user_stream;
     if (rc) return rc;
-    cudaError_t e = cudaStreamSynchronize(p->stream);
     if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "candidate run failed: %s", cudaGetErrorString(e));
     return best;
 }

@@ -79,6 +79,9 @@ struct conv_q_plan_s {
     const void *skip = nullptr;   // conv_q_plan_set_residual: fused residual add (NULL = none)
     float res_scale = 0.f;
     int x_uns = 0, y_uns = 0, skip_uns = 0;   // conv_q_plan_set_formats: unsigned codes (DESIGN reading 16)
+    // conv_q_plan_set_deps: cross-launch row flags (NULL in = griddepcontrol.wait)
+    const unsigned *dep_in = nullptr, *dep_skip = nullptr;
+    unsigned *dep_out = nullptr;
     cudaStream_t stream = nullptr;
     std::vector<Cand> cands;
     int sel = 0;
@@ -221,6 +224,12 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.scale = scale;
     prm.skip = static_cast<const uint8_t *>(p->skip);
     prm.res_scale = p->res_scale;
+    prm.dep_in = p->dep_in;
+    prm.dep_skip = p->skip ? p->dep_skip : nullptr;
+    prm.dep_out = p->dep_out;
+    prm.dep_in_target = (unsigned)(p->W * p->C);      // pixels x channels of one input row
+    prm.dep_out_target = (unsigned)(p->Q * p->K);     // of one output (and skip) row
+    prm.halo_rows = halo_rows;
     prm.x_uns = p->x_uns;
     prm.y_uns = p->y_uns;
     prm.code_hi = p->y_uns ? (1 << BITS) - 1 : (1 << (BITS - 1)) - 1;

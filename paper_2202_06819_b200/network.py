@@ -48,13 +48,19 @@ class ConvNet:
     net.tune(); net.step(stream)                      # net.x_in is the fp16 input, net.outputs the results
     """
 
-    def __init__(self, batch: int, bits: int, device, stream=None, unsigned: bool = False):
+    def __init__(self, batch: int, bits: int, device, stream=None, unsigned: bool = False,
+                 dataflow: bool = True):
         """unsigned: every ReLU output is written as unsigned codes [0, 2^b - 1] and
-        read as unsigned activations by its consumers (DESIGN reading 16)."""
+        read as unsigned activations by its consumers (DESIGN reading 16).
+        dataflow: consecutive conv launches synchronise through per-row flags
+        (conv_q_plan_set_deps) instead of whole-grid completion; the flags are
+        zeroed at the start of every step."""
         import torch
         self.torch = torch
         self.B, self.bits, self.device = batch, bits, device
         self.unsigned = unsigned
+        self.dataflow = dataflow
+        self.flags = None         # int32 row counters of every conv output, one buffer (zeroed per step)
         self.stream = stream
         self.convs: list[_Conv] = []
         self.stem = None
@@ -147,9 +153,32 @@ class ConvNet:
             self.stem["plan"].set_stream(stream)
 
     # ------------------------------------------------------------- a7 tuning
+    # ------------------------------------------------------------- dataflow flags
+    def _apply_deps(self, on: bool):
+        """Row flags of every conv (conv_q_plan_set_deps): conv i counts its output rows
+        in its slice of self.flags; it waits on its source's rows (not for the input
+        stage: that one is waited for as a whole grid) and on its skip's rows."""
+        t = self.torch
+        if on and self.flags is None:
+            sizes = [self.B * c.layer.P + 1 for c in self.convs]     # + the layer's total counter
+            self.flags = t.zeros(sum(sizes), dtype=t.int32, device=self.device)
+            offs, o = [], 0
+            for n in sizes:
+                offs.append(o)
+                o += n
+            self._flag_rows = [self.flags[a:a + n] for a, n in zip(offs, sizes)]
+        for i, c in enumerate(self.convs):
+            if not on:
+                c.plan.set_deps(None, None, None)
+                continue
+            rows = self._flag_rows
+            c.plan.set_deps(rows[c.src] if c.src >= 0 else None,
+                            rows[c.skip] if (c.skip is not None and c.skip >= 0) else None, rows[i])
+
     def tune(self, warmup: int = 2, reps: int = 5) -> dict:
         """Pick each unique shape's tile config by on-device timing (conv_q_plan_tune),
         on the network's real buffers (the input stage is run once first)."""
+        self._apply_deps(False)          # layers timed standalone: no flags
         self.run_input_stage(self.stream)
         if self.stem is not None:
             st = self.stem
@@ -163,6 +192,8 @@ class ConvNet:
                 idx = c.plan.tune(self.src_tensor(i), c.w, c.ss, c.y, warmup=warmup, reps=reps, stream=self.stream)
                 picks[c.key] = (idx, c.plan.info().config)
         self.torch.cuda.synchronize(self.device)
+        if self.dataflow:
+            self._apply_deps(True)
         return {str(k): v[1] for k, v in picks.items()}
 
     # ------------------------------------------------------------- execution
@@ -177,6 +208,14 @@ class ConvNet:
         """One pass of the whole hot path over the batch; ev(tag) is called after
         every launch (per-launch timing events), tag = ("input", j) or ("conv", i)."""
         s = stream if stream is not None else self.stream
+        if self.dataflow:
+            if self.flags is None:
+                self._apply_deps(True)
+            if hasattr(s, "cuda_stream"):
+                with self.torch.cuda.stream(s):
+                    self.flags.zero_()   # row counters start at zero every step
+            else:
+                self.flags.zero_()
         self.run_input_stage(s, ev)
         for i, c in enumerate(self.convs):
             c.plan.run(self.src_tensor(i), c.w, c.ss, c.y, stream=s)

@@ -33,9 +33,15 @@ for i, cname in enumerate(p.candidates()):
         continue
     p.set_config(i)
     for _ in range(3): p.run(xd, wd, sd, y)
+    torch.cuda.synchronize()
+    # 20 launches captured as one CUDA graph: device time, not the binding's ~13 us per call
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        for _ in range(20): p.run(xd, wd, sd, y)
+    gr.replay(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    for _ in range(20): p.run(xd, wd, sd, y)
+    gr.replay()
     e1.record(); torch.cuda.synchronize()
     res[cname] = round(e0.elapsed_time(e1) / 20 * 1000, 1)
 print(json.dumps(res))
