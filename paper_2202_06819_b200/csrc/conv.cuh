@@ -122,7 +122,8 @@ struct ConvParams {
     // weight-stationary region is sized to THIS layer's weight block (not the
     // 64 KB budget), and every byte left over goes to pipeline stages
     int stages;          // smem ring depth, 2 <= stages <= MAX_STAGES
-    int wsb;             // bytes of the resident weight region (WS; multiple of 1024)
+    int wsb;             // bytes of the resident weight regions (WS; s8 block + INT4 packed block)
+    int wsb_s8;          // bytes of the s8 resident block (the INT4 packed block follows it)
     // Cross-launch row flags (conv_q_plan_set_deps; NULL dep_in = wait for the whole
     // previous grid with griddepcontrol.wait).  dep_in[n*H + h]: pixels x channels of
     // input row (n, h) in memory, complete at W*C; dep_skip[n*P + p]: the residual
@@ -198,6 +199,9 @@ struct ConvCfg {
     static constexpr int MT = (HALO & 8) ? 2 : 1;
     static constexpr int TBW = MT * BN;                      // TMEM columns of one accumulator buffer
     static constexpr int WSB = WS ? 65536 : 0;               // resident weight region (budget; plan-time check)
+    // INT4 weight-stationary: the packed block lands here once and the transform
+    // warps expand it ONCE into the s8 resident region (not once per k-block stage)
+    static constexpr int WSB_PK = WS && BITS == 4 ? WSB / 2 : 0;
     static constexpr int HBOX = WS && HB ? (KCH == 64 && MT == 1 ? 20480 : 32768) : 0;   // WS halo stage (budget)
     static constexpr int B_TILE = BN / CG * KCH;             // one resident k-block of this CTA's weight rows
     static constexpr int BNL = BN / CG;                     // B rows staged per CTA
@@ -208,8 +212,8 @@ struct ConvCfg {
     static constexpr int A_S8 = NSUB * AMT * A_SUB;         // per stage
     static constexpr int B_S8 = NSUB * B_SUB;
     static constexpr int A_PK_SUB = BITS == 4 && !HB ? BM * LOAD_ROW : 0;   // (halo modes: A lives in the halo buffers)
-    static constexpr int B_PK_SUB = BITS == 4 ? BNL * LOAD_ROW : 0;
-    static constexpr int A_PK = NSUB * A_PK_SUB;
+    static constexpr int B_PK_SUB = BITS == 4 && !WS ? BNL * LOAD_ROW : 0;
+    static constexpr int A_PK = NSUB * AMT * A_PK_SUB;        // (generic MT2: one packed A tile per m-group)
     static constexpr int B_PK = NSUB * B_PK_SUB;
     static constexpr int STAGE_BYTES = A_S8 + B_S8 + A_PK + B_PK;
     static constexpr int SUB_TX = ((HB ? 0 : AMT * BM) + (WS ? 0 : BNL)) * LOAD_ROW;  // TMA bytes per k-block per CTA
@@ -253,7 +257,7 @@ struct ConvCfg {
     static constexpr int SS_BYTES = OUTP == OUT_S32 ? 0 : 3 * 8 * BN;
     static constexpr int BAR_BYTES = 1024;
     static constexpr int stages_with(int nhalo) {
-        return (SMEM_LIMIT - 1024 - BAR_BYTES - WSB - NBUF * (OUT_BYTES + SS_BYTES) - nhalo * (HALO_BYTES + HALO_PK)) /
+        return (SMEM_LIMIT - 1024 - BAR_BYTES - WSB - WSB_PK - NBUF * (OUT_BYTES + SS_BYTES) - nhalo * (HALO_BYTES + HALO_PK)) /
                STAGE_BYTES;
     }
     // halo buffers in flight: the halo load of tile t+NHALO-1 overlaps tiles
@@ -268,7 +272,7 @@ struct ConvCfg {
     static constexpr int STAGES = STAGES_FIT > MAX_STAGES ? MAX_STAGES : STAGES_FIT;
     // (1024: base alignment of the dynamic smem; + 1024: the ring end rounded up to 1 KB)
     static constexpr int FIXED_BYTES = 2048 + NBUF * (OUT_BYTES + SS_BYTES) + NHALO * (HALO_BYTES + HALO_PK) + BAR_BYTES;
-    static constexpr int SMEM = FIXED_BYTES + WSB + STAGES * STAGE_BYTES;
+    static constexpr int SMEM = FIXED_BYTES + WSB + WSB_PK + STAGES * STAGE_BYTES;
     static int stages_for(int wsb) {
         const int st = (SMEM_LIMIT - FIXED_BYTES - wsb) / STAGE_BYTES;
         return st > MAX_STAGES ? MAX_STAGES : st;
@@ -288,9 +292,9 @@ struct ConvCfg {
     static constexpr bool FITS = STAGES >= 2 && (!HB || (OUTP != OUT_TMA && (BITS == 8 || (HA && !WS)))) &&
                                  (!(OUT & OUT_U) || (BITS == 8 && (OUT & OUT_RELU))) &&
                                  (!RES || (OUTP != OUT_S32 && !(OUT & OUT_RELU))) &&
-                                 (!WS || (BITS == 8 && (!HB || NSUB == 1))) &&
+                                 (!WS || ((BITS == 8 || !HB) && (!HB || NSUB == 1))) &&   // INT4 WS: generic only
                                  (!S2H || (WS && !HA && KCH == 64)) &&
-                                 (MT == 1 || (WS && HB) || (WS && BITS == 8 && CG == 1));  // else never instantiated
+                                 (MT == 1 || (WS && HB) || (WS && CG == 1 && !HB));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
     static_assert(NSUB >= 1 && NSUB <= 4, "NSUB");
     static_assert(BN % (32 * CG) == 0 && BN >= 32 * CG && BN <= 256, "BN");
@@ -601,6 +605,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
     // in both CTAs of a pair, as cta_group::2 descriptors require)
     constexpr bool HA = Cfg::HA, WS = Cfg::WS, S2H = Cfg::S2H;
     uint8_t *b_res = smem;                              // WS: [num_kb][BN rows][KCH] resident weights
+    uint8_t *b_res_pk = smem + (WS ? p.wsb_s8 : 0);     // INT4 WS: [num_kb][BN rows][KCH/2] packed, expanded once
     uint8_t *a_s8 = smem + (WS ? p.wsb : 0);            // [STAGES][NSUB][BM*KCH] (WS halo: [STAGES][HBOX])
     uint8_t *b_s8 = a_s8 + STAGES * Cfg::A_S8;          // [STAGES][NSUB][BNL*KCH]
     uint8_t *a_pk = b_s8 + STAGES * Cfg::B_S8;          // INT4: [STAGES][NSUB][BM*KCH/2]
@@ -654,6 +659,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         }
         for (int h = 0; h < Cfg::NHALO; ++h) mbar_init(&hempty[h], 1);
         if (WS) mbar_init(bfull, 1);
+        if (WS && BITS == 4) mbar_init(&hempty[2], 4 * CG);   // bready: the expanded s8 weight blocks (both CTAs)
         if (WS && CG == 2) mbar_init(&hempty[1], 1);   // leader: the follower's weight block is loaded
         for (int b = 0; b < Cfg::NBUF; ++b) {
             mbar_init(&acc_full[b], 1);
@@ -706,8 +712,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 mbar_arrive_expect_tx(bfull, (uint32_t)(p.num_kb * Cfg::BNL * Cfg::LOAD_ROW));
                 for (int kb = 0; kb < p.num_kb; ++kb) {
                     const int tap = p.fd_cblk.div(kb), cb = kb - tap * p.num_cblk;
-                    tma_load_2d(b_res + kb * Cfg::B_TILE, &tm_b, bfull, tap * p.row_bytes + cb * Cfg::LOAD_ROW, brow,
-                                pol_b);
+                    uint8_t *dst = BITS == 4 ? b_res_pk + kb * (Cfg::BNL * Cfg::LOAD_ROW) : b_res + kb * Cfg::B_TILE;
+                    tma_load_2d(dst, &tm_b, bfull, tap * p.row_bytes + cb * Cfg::LOAD_ROW, brow, pol_b);
                 }
             }
             __syncwarp();
@@ -888,8 +894,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 #pragma unroll
             for (int t = 0; t < 9; ++t) toff[t] = (uint32_t)(((t / 3) * p.Wp + (t % 3)) * KCH) >> 4;
             const uint64_t b_desc_res = umma_desc_kmajor(smem_u32(b_res), KCH);   // WS: resident k-block 0
-            if (WS) mbar_wait(bfull, 0);
-            if (WS && CG == 2) mbar_wait(&hempty[1], 0);   // the follower's weight rows
+            if (WS && BITS == 8) mbar_wait(bfull, 0);
+            if (WS && BITS == 8 && CG == 2) mbar_wait(&hempty[1], 0);   // the follower's weight rows
+            if (WS && BITS == 4) mbar_wait(&hempty[2], 0);   // INT4: both CTAs' blocks expanded to s8
             int stage = 0;
             uint32_t phase = 0;
             int hcount = 0;
@@ -1719,6 +1726,22 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         } else if constexpr (BITS == 4) {
             const int tid = threadIdx.x - 32 * Cfg::XF_WARP0;  // 0..127
             const uint32_t ready0 = CG == 2 ? mapa_shared(smem_u32(&ready[0]), 0) : 0;
+            if constexpr (WS) {
+                // the CTA's packed weight block -> s8 resident block, once; then tell the
+                // (leader's) MMA warp
+                if (tile0 < p.num_tiles) {
+                    mbar_wait(bfull, 0);
+                    for (int kb = 0; kb < p.num_kb; ++kb)
+                        expand_tile<KCH>(b_res_pk + kb * (Cfg::BNL * Cfg::LOAD_ROW), b_res + kb * Cfg::B_TILE, Cfg::BNL,
+                                         tid, 128);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&hempty[2]), 0));
+                        else mbar_arrive(&hempty[2]);
+                    }
+                }
+            }
             int stage = 0;
             uint32_t phase = 0;
             for (int unit = tile0; unit < p.num_units; unit += tstep) {
@@ -1727,9 +1750,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 for (int kb = kb_lo; kb < kb_hi; kb += NSUB) {
                     const int nsub = min(NSUB, kb_hi - kb);
                     mbar_wait(&full[stage], phase);
+                    // (WS: stages carry A only; MT2: the k-block's AMT A tiles are contiguous)
                     for (int j = 0; j < nsub; ++j)
-                        expand_kblock<KCH, BM, Cfg::BNL, 128>(
-                            a_pk + stage * Cfg::A_PK + j * Cfg::A_PK_SUB, a_s8 + stage * Cfg::A_S8 + j * Cfg::A_SUB,
+                        expand_kblock<KCH, Cfg::AMT * BM, WS ? 0 : Cfg::BNL, 128>(
+                            a_pk + stage * Cfg::A_PK + j * Cfg::AMT * Cfg::A_PK_SUB,
+                            a_s8 + stage * Cfg::A_S8 + j * Cfg::AMT * Cfg::A_SUB,
                             b_pk + stage * Cfg::B_PK + j * Cfg::B_PK_SUB, b_s8 + stage * Cfg::B_S8 + j * Cfg::B_SUB, tid);
                     fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.mma
                     __syncwarp();

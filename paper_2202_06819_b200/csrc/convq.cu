@@ -246,10 +246,11 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                         if (p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand)) p->cands.push_back(cand);
                     }
     }
-    // weight-stationary candidates (INT8): the CTA's whole (BN/CG) x R*S*C
-    // weight block stays resident in 64 KB of shared memory, stages carry only
-    // activations (halo boxes for stride-1 3x3, im2col / tiled rows otherwise)
-    if (p->bits == 8) {
+    // weight-stationary candidates: the CTA's whole (BN/CG) x R*S*C weight block
+    // stays resident in 64 KB of shared memory (as s8; INT4: loaded packed and
+    // expanded once by the transform warps), stages carry only activations
+    // (halo boxes for stride-1 3x3 -- INT8 only --, im2col / tiled rows otherwise)
+    {
         const int kch = p->C % 128 == 0 ? 128 : p->C % 64 == 0 ? 64 : 0;
         const int sms = g_num_sms > 0 ? g_num_sms : 148;
         if (kch)
@@ -261,15 +262,15 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                         for (int nsub : {1, 2}) {
                             Cand cand{bn, kch, cg, nsub, direct};
                             cand.ws = 1;
-                            if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                            if (p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand)) p->cands.push_back(cand);
                         }
                         if (cg == 1 && bn <= 128) {   // MT2: two 128-row m-groups per unit
                             Cand cand{bn, kch, 1, 1, direct};
                             cand.ws = 1;
                             cand.halo = 8;
-                            if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                            if (p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand)) p->cands.push_back(cand);
                         }
-                        if (halo_ok && direct) {
+                        if (halo_ok && direct && p->bits == 8) {
                             const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
                             if ((int64_t)halo_rows * Wp * kch <= (kch == 64 ? 20480 : 32768) && halo_rows <= 256) {
                                 Cand cand{bn, kch, cg, 1, direct};

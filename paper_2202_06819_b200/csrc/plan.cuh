@@ -115,7 +115,6 @@ namespace convq {
 template <int BITS>
 inline bool cand_fits(const Cand &c) {
     if (c.ws) {
-        if (BITS != 8) return false;
 #define CONVQ_WFIT(BN_, KC_, NS_, H_, CG_)                                                             \
         if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.halo == H_ && c.cg == CG_)               \
             return (c.direct ? ConvCfg<BITS, BN_, KC_, OUT_DIRECT, CG_, NS_, 2 + H_>::FITS              \
@@ -166,8 +165,9 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     // Shared memory: the weight-stationary region holds exactly this layer's
     // BN/CG x R*S*C block (rounded to 1 KB; the 64 KB budget is the plan-time
     // bound), and the ring gets as many stages as the rest of the 227 KB allows.
-    const int wsb = (HALO & 2) ? (int)ceil_div((int64_t)p->R * p->S * (p->C / KCH) * Cfg::B_TILE, 1024) * 1024 : 0;
-    if (wsb > Cfg::WSB) return set_err(CONV_Q_EUNSUPPORTED, "weight block %d B exceeds the resident region", wsb);
+    const int wsb_s8 = (HALO & 2) ? (int)ceil_div((int64_t)p->R * p->S * (p->C / KCH) * Cfg::B_TILE, 1024) * 1024 : 0;
+    if (wsb_s8 > Cfg::WSB) return set_err(CONV_Q_EUNSUPPORTED, "weight block %d B exceeds the resident region", wsb_s8);
+    const int wsb = wsb_s8 + (BITS == 4 ? (int)ceil_div(wsb_s8 / 2, 1024) * 1024 : 0);   // + INT4 packed block
     const int stages = Cfg::stages_for(wsb);
     const int smem = Cfg::smem_for(wsb, stages);
     const int SMEM_LAUNCH = smem > 116 * 1024 ? smem : 116 * 1024;
@@ -179,6 +179,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     ConvParams prm;
     prm.stages = stages;
     prm.wsb = wsb;
+    prm.wsb_s8 = wsb_s8;
     prm.N = p->N; prm.H = p->H; prm.W = p->W; prm.C = p->C; prm.K = p->K; prm.R = p->R; prm.S = p->S;
     prm.stride = p->stride; prm.pad = p->pad; prm.pad_w = p->s2d ? 0 : p->pad; prm.P = p->P; prm.Q = p->Q; prm.M = (int)p->M;
     prm.row_bytes = p->row_bytes;
@@ -265,7 +266,7 @@ template <int BITS, int OUT>
 inline int dispatch_bn_kch(conv_q_plan_s *p, const float *scale, void *y) {
     const Cand c = p->cands[p->sel];
     if (c.ws) {
-        if constexpr (BITS == 8) {
+        {
 #define CONVQ_WCASE(BN_, KC_, NS_, H_, CG_)                                                        \
             if (c.bn == BN_ && c.kch == KC_ && c.nsub == NS_ && c.halo == H_ && c.cg == CG_) {     \
                 if constexpr (ConvCfg<BITS, BN_, KC_, OUT, CG_, NS_, 2 + H_>::FITS)                \
