@@ -1075,6 +1075,17 @@ extern "C" int conv_q_maxpool_fmt(const void *x, int N, int H, int W, int C, int
     const uint4 *xs = static_cast<const uint4 *>(x);
     uint4 *ys = static_cast<uint4 *>(y);
     const FastDiv fv = make_fastdiv(vpp), fq = make_fastdiv(Q), fp = make_fastdiv(P);
+    if (R == 3 && stride == 2) {
+        // the ResNet stem pool: 4 output rows per thread, shared horizontal maxima
+        constexpr int T = 4;
+        const int groups = (int)ceil_div(P, T);
+        const int64_t total4 = (int64_t)N * groups * Q * vpp;
+        cfg.gridDim = dim3((unsigned)ceil_div(total4, 256));
+        auto k4 = uns ? (bits == 8 ? maxpool3s2_rows_kernel<8, true, T> : maxpool3s2_rows_kernel<4, true, T>)
+                      : (bits == 8 ? maxpool3s2_rows_kernel<8, false, T> : maxpool3s2_rows_kernel<4, false, T>);
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, k4, xs, ys, N, H, W, P, Q, vpp, pad, groups, fv, fq, make_fastdiv(groups)));
+        return CONV_Q_OK;
+    }
     auto kern = uns ? (bits == 8 ? (R == 3 ? maxpool_kernel<8, 3, true> : maxpool_kernel<8, 2, true>)
                                  : (R == 3 ? maxpool_kernel<4, 3, true> : maxpool_kernel<4, 2, true>))
                     : (bits == 8 ? (R == 3 ? maxpool_kernel<8, 3> : maxpool_kernel<8, 2>)

@@ -352,4 +352,61 @@ __global__ void __launch_bounds__(256) maxpool_kernel(const uint4 *__restrict__ 
     }
 }
 
+
+// 3x3 / stride-2 max pool (the ResNet stem's), T output rows per thread: the
+// horizontal 3-tap max of each input row is computed once and shared by the two
+// output rows it belongs to (input row 2p+1 is row 2p+1 of output p and row -1 of
+// output p+1): 3(2T+1) loads per T outputs instead of 9T.  One thread per
+// (image, T-row group, output column, 16-byte channel vector); consecutive
+// threads walk the channel vectors, then the columns (coalesced).
+template <int BITS, bool UNS, int T>
+__global__ void __launch_bounds__(256) maxpool3s2_rows_kernel(const uint4 *__restrict__ x, uint4 *__restrict__ y,
+                                                              int N, int H, int W, int P, int Q, int vpp, int pad,
+                                                              int groups, FastDiv fd_vpp, FastDiv fd_q,
+                                                              FastDiv fd_g) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr uint32_t MINV = UNS ? 0u : BITS == 8 ? 0x80808080u : 0x88888888u;
+    auto vmax = [](uint32_t a, uint32_t b) -> uint32_t {
+        if constexpr (BITS == 8 && UNS) return vmax_u8x4(a, b);
+        else if constexpr (BITS == 8) return vmax_s8x4(a, b);
+        else if constexpr (UNS) return vmax_u4x8(a, b);
+        else return vmax_s4x8(a, b);
+    };
+    auto vmax4 = [&](uint4 a, uint4 b) { return make_uint4(vmax(a.x, b.x), vmax(a.y, b.y), vmax(a.z, b.z), vmax(a.w, b.w)); };
+    const int total = N * groups * Q * vpp;     // < 2^31 (checked on the host)
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+        const int pix = fd_vpp.div(o);
+        const int v = o - pix * vpp;
+        const int t = fd_q.div(pix);
+        const int q = pix - t * Q;
+        const int n = fd_g.div(t);
+        const int p0 = (t - n * groups) * T;
+        const int w0 = 2 * q - pad;
+        const uint4 *base = x + (int64_t)n * H * W * vpp + v;
+        // horizontal maxima of input rows 2 p0 - pad .. 2 (p0 + T - 1) - pad + 2, all loads first
+        constexpr int NR = 2 * T + 1;
+        uint4 a[NR][3];
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+            const int h = 2 * p0 - pad + i;
+#pragma unroll
+            for (int s = 0; s < 3; ++s) {
+                const int w = w0 + s;
+                a[i][s] = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(base + ((int64_t)h * W + w) * vpp)
+                                                                : make_uint4(MINV, MINV, MINV, MINV);
+            }
+        }
+        uint4 hm[NR];
+#pragma unroll
+        for (int i = 0; i < NR; ++i) hm[i] = vmax4(vmax4(a[i][0], a[i][1]), a[i][2]);
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+            const int p = p0 + k;
+            if (p < P)
+                y[(((int64_t)n * P + p) * Q + q) * vpp + v] = vmax4(vmax4(hm[2 * k], hm[2 * k + 1]), hm[2 * k + 2]);
+        }
+    }
+}
+
 }  // namespace convq
