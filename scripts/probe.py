@@ -21,7 +21,7 @@ if name == "stem":
     sd = torch.cat([torch.full((64,), 0.01), torch.zeros(64)]).cuda()
     y = torch.empty((N, 112, 112, 64 * bits // 8), dtype=torch.uint8, device="cuda")
 else:
-    L = {l.name: l for l, _ in wl.resnet50_layers()}[name]
+    L = {l.name: l for l, _ in getattr(wl, os.environ.get("PROBE_NET", "resnet50") + "_layers")()}[name]
     x, w, ss = wl.layer_inputs(g, L, N, bits)
     p = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
     xd, wd, sd = (torch.from_numpy(t).cuda() for t in (x, w, ss))
@@ -51,7 +51,8 @@ for name in sys.argv[1:]:
     MODES = [int(m) for m in os.environ.get('PROBE_MODES', '0,1,2,3,4,7').split(',')]
     for mode in MODES:
         env = dict(os.environ, CONV_Q_PROBE=str(mode))
-        r = subprocess.run([sys.executable, "-c", CODE, name, "256", "8"], env=env, capture_output=True, text=True)
+        r = subprocess.run([sys.executable, "-c", CODE, name, os.environ.get("PROBE_N", "256"),
+                            os.environ.get("PROBE_BITS", "8")], env=env, capture_output=True, text=True)
         out[mode] = r.stdout.strip() or r.stderr[-400:]
     print(name)
     import json
