@@ -211,7 +211,9 @@ struct ConvCfg {
     static constexpr int AMT = HB ? 1 : MT;                 // A sub-tiles per k-block (generic MT2: one per m-group)
     static constexpr int A_S8 = NSUB * AMT * A_SUB;         // per stage
     static constexpr int B_S8 = NSUB * B_SUB;
-    static constexpr int A_PK_SUB = BITS == 4 && !HB ? BM * LOAD_ROW : 0;   // (halo modes: A lives in the halo buffers)
+    // packed INT4 A staging per k-block (halo modes: the box lives in the halo buffers --
+    // or, weight-stationary, the packed box of the stage, expanded into the stage's s8 box)
+    static constexpr int A_PK_SUB = BITS != 4 ? 0 : !HB ? BM * LOAD_ROW : (WS && HA ? HBOX / 2 : 0);
     static constexpr int B_PK_SUB = BITS == 4 && !WS ? BNL * LOAD_ROW : 0;
     static constexpr int A_PK = NSUB * AMT * A_PK_SUB;        // (generic MT2: one packed A tile per m-group)
     static constexpr int B_PK = NSUB * B_PK_SUB;
@@ -289,10 +291,10 @@ struct ConvCfg {
     static constexpr int MMA_WARP = PROD_WARP + 1;
     static constexpr int NUM_THREADS = 32 * (MMA_WARP + kNumMma);
     static constexpr uint32_t IDESC = idesc_i8(BM * CG, BN);
-    static constexpr bool FITS = STAGES >= 2 && (!HB || (OUTP != OUT_TMA && (BITS == 8 || (HA && !WS)))) &&
+    static constexpr bool FITS = STAGES >= 2 && (!HB || (OUTP != OUT_TMA && (BITS == 8 || HA))) &&
                                  (!(OUT & OUT_U) || (BITS == 8 && (OUT & OUT_RELU))) &&
                                  (!RES || (OUTP != OUT_S32 && !(OUT & OUT_RELU))) &&
-                                 (!WS || ((BITS == 8 || !HB) && (!HB || NSUB == 1))) &&   // INT4 WS: generic only
+                                 (!WS || ((BITS == 8 || !S2H) && (!HB || NSUB == 1))) &&   // INT4 WS: generic / halo
                                  (!S2H || (WS && !HA && KCH == 64)) &&
                                  (MT == 1 || (WS && HB) || (WS && CG == 1 && !HB));  // else never instantiated
     static_assert(KCH == 32 || KCH == 64 || KCH == 128, "KCH");
@@ -748,8 +750,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     CONVQ_TL(0, tl_n++);
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&full[stage], p.halo_tx);
-                        tma_load_4d(a_s8 + stage * Cfg::A_S8, &tm_a, &full[stage], cblk * Cfg::LOAD_ROW, -p.pad_w,
-                                    p0 - p.pad, n, pol_a);
+                        // (INT4: the packed box; the transform warps expand it into the stage's s8 box)
+                        tma_load_4d(BITS == 4 ? a_pk + stage * Cfg::A_PK : a_s8 + stage * Cfg::A_S8, &tm_a, &full[stage],
+                                    cblk * Cfg::LOAD_ROW, -p.pad_w, p0 - p.pad, n, pol_a);
                     }
                     __syncwarp();
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -941,7 +944,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     for (int cblk = 0; cblk < p.num_cblk; ++cblk) {
                         long long t0 = trace ? clock64() : 0;
                         mma_gate();
-                        mbar_wait(&full[stage], phase);
+                        mbar_wait(BITS == 4 ? &ready[stage] : &full[stage], phase);   // INT4: expanded box(es)
                         if (PAIR8) mbar_wait(&ready[stage], phase);   // the follower's halo box
                         mma_mark();
                         if (cblk == 0) CONVQ_TL(2, local);
@@ -1691,7 +1694,40 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
 #undef CONVQ_TL
     } else if (warp < Cfg::PROD_WARP) {
         // =========================== INT4 transform =========================
-        if constexpr (BITS == 4 && HA) {
+        if constexpr (BITS == 4 && WS && HA) {
+            // weight-stationary halo: the packed weight block is expanded once; every stage
+            // is one packed halo box (tile, channel block), expanded into the stage's s8 box
+            const int tid = threadIdx.x - 32 * Cfg::XF_WARP0;  // 0..127
+            const uint32_t ready0 = CG == 2 ? mapa_shared(smem_u32(&ready[0]), 0) : 0;
+            if (tile0 < p.num_tiles) {
+                mbar_wait(bfull, 0);
+                for (int kb = 0; kb < p.num_kb; ++kb)
+                    expand_tile<KCH>(b_res_pk + kb * (Cfg::BNL * Cfg::LOAD_ROW), b_res + kb * Cfg::B_TILE, Cfg::BNL,
+                                     tid, 128);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&hempty[2]), 0));
+                    else mbar_arrive(&hempty[2]);
+                }
+            }
+            const int halo_pix = p.halo_tx / Cfg::LOAD_ROW;  // box rows x Wp pixels
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
+                for (int cblk = 0; cblk < p.num_cblk; ++cblk) {
+                    mbar_wait(&full[stage], phase);
+                    expand_tile<KCH>(a_pk + stage * Cfg::A_PK, a_s8 + stage * Cfg::A_S8, halo_pix, tid, 128);
+                    fence_proxy_async_smem();  // generic-proxy writes -> visible to tcgen05.mma
+                    __syncwarp();
+                    if (lane == 0) {
+                        if constexpr (CG == 2) mbar_arrive_cluster(ready0 + 8u * stage);
+                        else mbar_arrive(&ready[stage]);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        } else if constexpr (BITS == 4 && HA) {
             // halo mode: per (tile, channel block) the first stage carries the packed
             // halo box -> expanded ONCE into the s8 halo buffer the filter taps'
             // shifted descriptors read; every stage carries NSUB taps' weights

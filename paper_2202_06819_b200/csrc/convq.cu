@@ -270,13 +270,13 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                             cand.halo = 8;
                             if (p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand)) p->cands.push_back(cand);
                         }
-                        if (halo_ok && direct && p->bits == 8) {
+                        if (halo_ok && direct) {   // (INT4: packed box per stage, expanded once per stage)
                             const int halo_rows = (int)ceil_div(BM + (p->R - 1) * Wp + p->S - 1, Wp);
                             if ((int64_t)halo_rows * Wp * kch <= (kch == 64 ? 20480 : 32768) && halo_rows <= 256) {
                                 Cand cand{bn, kch, cg, 1, direct};
                                 cand.ws = 1;
                                 cand.halo = 1;
-                                if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                                if (p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand)) p->cands.push_back(cand);
                             }
                             // MT2 (one CTA, two m-groups per accumulator round trip)
                             const int rows2 = (int)ceil_div(2 * BM + (p->R - 1) * Wp + p->S - 1, Wp);
@@ -284,7 +284,7 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                                 Cand cand{bn, kch, cg, 1, direct};
                                 cand.ws = 1;
                                 cand.halo = 1 | 8;
-                                if (cand_fits<8>(cand)) p->cands.push_back(cand);
+                                if (p->bits == 8 ? cand_fits<8>(cand) : cand_fits<4>(cand)) p->cands.push_back(cand);
                             }
                         }
                     }
