@@ -148,13 +148,13 @@ def layer_res_scale(spec: Spec, i: int) -> float:
 
 def build_network(spec: Spec, B: int, device, world: int = 1, dist=None, dataflow=None):
     """The device network of a workload (packed weights broadcast from rank 0);
-    dataflow None = auto (row flags for per-GPU batch <= 8)."""
+    dataflow None = auto (completion counters for per-GPU batch <= 4)."""
     import torch
 
     from paper_2202_06819_b200.network import ConvNet
 
     if dataflow is None:
-        dataflow = B <= 8
+        dataflow = B <= 4
 
     net = ConvNet(B, spec.bits, device, unsigned=spec.unsigned, dataflow=dataflow)
 
@@ -340,10 +340,10 @@ def run_ours(args):
     B_global, B, img0 = shard_plan(B_arg, world, rank, scaling)
 
     # ---- setup (off the timed path): weights, scales, plans, buffers, tuning
-    # row-flag dataflow between conv launches: measured faster only for the
-    # latency-bound tiny batches (ResNet-18 b1: 0.095 vs 0.101 ms); at b16 / b256
-    # whole-grid dependencies are faster (DESIGN 6), so it is on for B <= 8
-    dataflow = (B <= 8) if args.dataflow == "auto" else args.dataflow == "on"
+    # completion-counter dataflow between conv launches: measured faster only for
+    # the latency-bound tiny batches (ResNet-18 b1 0.095 vs 0.101 ms, ResNet-50 b1
+    # 0.214 vs 0.220); equal at b256, slower at b32 (DESIGN 6) -> on for B <= 4
+    dataflow = (B <= 4) if args.dataflow == "auto" else args.dataflow == "on"
     net = build_network(spec, B, dev, world, dist, dataflow=dataflow)
     stream = torch.cuda.Stream(dev)          # all work (and graph capture) on one side stream
     torch.cuda.set_stream(stream)
@@ -814,8 +814,8 @@ def main():
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     ap.add_argument("--dataflow", default="auto", choices=["auto", "on", "off"],
-                    help="per-row flags between conv launches instead of whole-grid dependencies "
-                         "(auto: on for per-GPU batch <= 8)")
+                    help="completion counters between conv launches instead of whole-grid dependencies "
+                         "(auto: on for per-GPU batch <= 4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--parity-pixels", type=int, default=64)

@@ -301,36 +301,29 @@ CONVQ_API int conv_q_maxpool_fmt(const void *x, int N, int H, int W, int C, int 
 CONVQ_API int conv_q_plan_set_formats(conv_q_plan_t *plan, int x_unsigned, int y_unsigned, int skip_unsigned);
 
 /*
- * Cross-launch row flags (ABI 1.05): dataflow between the consecutive conv
- * launches of a layer chain (the packed output of one layer IS the next
+ * Cross-launch completion counters (ABI 1.05): dataflow between consecutive
+ * conv launches of a layer chain (the packed output of one layer IS the next
  * layer's input, section 3.3).  Instead of waiting for the whole
- * previous grid to finish (griddepcontrol.wait), each work unit waits only
- * for the input rows it reads, so a layer's tiles start while the previous
- * layer's last tiles are still running (wave tails and batch-1 latency chains
- * overlap).  All three are device arrays of uint32 counters, caller-owned,
- * 4-byte aligned, ZERO at the start of every run of the chain (e.g. one
- * memset per step):
- *   in_rows   [N*H+1] counter of input row (n, h) of x: the kernel waits until it
- *                    reaches W*C (pixels x channels of the row) before loading
- *                    any A tile that reads the row; element N*H is the whole
- *                    tensor's count (complete at N*H*W*C), after which the
- *                    kernel stops reading row counters.  NULL: wait for the
- *                    whole preceding kernel instead (griddepcontrol.wait).
- *   skip_rows [N*P+1] the same for the residual skip tensor's rows (target Q*K;
- *                    element N*P: the whole tensor, N*P*Q*K);
- *                    NULL: none (the skip is complete before the launch).
- *   out_rows  [N*P+1] incremented by pixels x channels as this launch's output
- *                    rows reach global memory (after a fence), element N*P by
- *                    the whole count; the next layer's in_rows.  NULL: not
- *                    counted.
- * With in_rows set, every buffer the launch writes must not be read by a
+ * previous grid to complete and flush (griddepcontrol.wait), the launch waits
+ * for a counter of the codes its input holds; every producer warp adds the
+ * codes it wrote once its stores are complete.  Each argument is ONE device
+ * uint32 counter, caller-owned, 4-byte aligned, ZERO at the start of every run
+ * of the chain (e.g. one memset per step):
+ *   in_done    the input x is complete when it reaches N*H*W*C (the count its
+ *              producer adds); NULL: wait for the whole preceding kernel
+ *              instead (griddepcontrol.wait).
+ *   skip_done  the residual skip is complete at N*P*Q*K; NULL: the skip is
+ *              complete before the launch.
+ *   out_done   incremented by N*P*Q*K in total as this launch's codes reach
+ *              global memory; the next layer's in_done.  NULL: not counted.
+ * With in_done set, every buffer the launch writes must not be read by a
  * kernel still running (true in a chain of distinct per-layer outputs).
- * Tuning (conv_q_plan_tune / _time_candidates) needs the flags cleared.
- * Errors: EINVAL (NULL plan, misaligned arrays), EUNSUPPORTED (in_rows on an
- * s2d stem plan).
+ * Tuning (conv_q_plan_tune / _time_candidates) needs the counters cleared.
+ * Errors: EINVAL (NULL plan, misaligned counters), EUNSUPPORTED (in_done on an
+ * s2d stem plan, tensors with more than 2^32 - 1 codes).
  */
-CONVQ_API int conv_q_plan_set_deps(conv_q_plan_t *plan, const unsigned *in_rows, const unsigned *skip_rows,
-                                   unsigned *out_rows);
+CONVQ_API int conv_q_plan_set_deps(conv_q_plan_t *plan, const unsigned *in_done, const unsigned *skip_done,
+                                   unsigned *out_done);
 
 /* Thread-local status code of the last failed call on this thread (0 if none). */
 CONVQ_API int conv_q_last_status(void);

@@ -210,12 +210,12 @@ class ConvPlan:
         ptr = None if skip is None else _ptr(skip)
         _check(load().conv_q_plan_set_residual(self._h, ctypes.c_void_p(ptr), float(res_scale)))
 
-    def set_deps(self, in_rows=None, skip_rows=None, out_rows=None):
-        """Cross-launch row flags (conv_q_plan_set_deps): int32/uint32 device tensors
-        [N*H] / [N*P] / [N*P] (zeroed before each chain run), or None."""
+    def set_deps(self, in_done=None, skip_done=None, out_done=None):
+        """Cross-launch completion counters (conv_q_plan_set_deps): one-element int32
+        device tensors (zeroed before each chain run), or None."""
         ptr = lambda t: ctypes.c_void_p(None if t is None else _ptr(t))  # noqa: E731
-        _check(load().conv_q_plan_set_deps(self._h, ptr(in_rows), ptr(skip_rows), ptr(out_rows)))
-        self._deps = (in_rows, skip_rows, out_rows)
+        _check(load().conv_q_plan_set_deps(self._h, ptr(in_done), ptr(skip_done), ptr(out_done)))
+        self._deps = (in_done, skip_done, out_done)
 
     def candidates(self) -> list[str]:
         lib = load()

@@ -124,15 +124,15 @@ struct ConvParams {
     int stages;          // smem ring depth, 2 <= stages <= MAX_STAGES
     int wsb;             // bytes of the resident weight regions (WS; s8 block + INT4 packed block)
     int wsb_s8;          // bytes of the s8 resident block (the INT4 packed block follows it)
-    // Cross-launch row flags (conv_q_plan_set_deps; NULL dep_in = wait for the whole
-    // previous grid with griddepcontrol.wait).  dep_in[n*H + h]: pixels x channels of
-    // input row (n, h) in memory, complete at W*C; dep_skip[n*P + p]: the residual
-    // skip's rows, complete at Q*K; dep_out[n*P + p]: this layer's rows, incremented
-    // by every epilogue warp once its codes are in global memory.
+    // Cross-launch completion counters (conv_q_plan_set_deps; NULL dep_in = wait for
+    // the whole previous grid with griddepcontrol.wait): dep_in counts the input
+    // tensor's codes in memory (complete at dep_in_total = N*H*W*C), dep_skip the
+    // residual skip's (dep_skip_total = N*P*Q*K); every epilogue warp adds the codes
+    // it wrote to dep_out once its stores are complete.
     const unsigned *dep_in;
     const unsigned *dep_skip;
     unsigned *dep_out;
-    unsigned dep_in_target, dep_out_target;
+    unsigned dep_in_total, dep_skip_total;
     int halo_rows;       // input rows of one halo box (halo modes)
     int32_t *ws;         // [num_tiles*CG][4*EPB regions][EPI_COLS][32] partial sums (kept zero between runs)
     unsigned *cnt;       // per-region arrival counters (kept zero between runs)
@@ -538,45 +538,21 @@ __device__ __forceinline__ void expand_kblock(const uint8_t *a_src, uint8_t *a_d
     }
 }
 
-// Whole warp: spin until rows [r_lo, r_hi] (flat n*rows + r indices) of a flag array
-// reach `target` (lane i polls rows r_lo + i, r_lo + i + 32, ...), then order the
-// warp's later TMA (async-proxy) reads after the acquire.
-__device__ __forceinline__ void wait_rows(const unsigned *cnt, int r_lo, int r_hi, unsigned target) {
-    for (int r = r_lo + (int)(threadIdx.x & 31); r <= r_hi; r += 32) {
-        // bounded: a flag that never completes (flags not zeroed, a mismatched
-        // producer) traps after ~10 s instead of hanging the device
+// Spin (lane 0, the warp waits at the shuffle) until a completion counter reaches
+// `target`.  Bounded: a counter that never completes (not zeroed, a mismatched
+// producer) traps after ~10 s instead of hanging the device.  No acquire / fence
+// after it: an acquire load or a full / proxy fence would also wait for this
+// warp's TMA loads in flight; the producer's codes reached L2 (store completion +
+// fence) before its add, and the TMA loads issued after this loop read L2.
+__device__ __forceinline__ void wait_counter(const unsigned *c, unsigned target) {
+    if ((threadIdx.x & 31) == 0) {
         long long spins = 0;
-        while (ld_relaxed_gpu(cnt + r) < target) {
+        while (ld_relaxed_gpu(c) < target) {
             if (++spins > (1ll << 24)) __trap();
             __nanosleep(64);
         }
     }
-    // No acquire / fence here: an acquire load or a full / proxy fence also waits
-    // for this warp's TMA loads still in flight (measured: it drains the load
-    // pipeline every unit, 1.3-1.7x slower layers).  The producer's rows reached
-    // L2 (store completion + fence) before its relaxed add raised the count; the
-    // TMA loads issued after this loop exits (control dependency) read L2.
     __syncwarp();
-}
-// Input rows the output pixels [m_lo, m_hi] read (im2col / 1x1: every image the
-// range touches, rows p*stride - pad .. p*stride - pad + R - 1 clipped to [0, H)).
-// The whole input layer is in memory once its total counter (element N*H of the
-// flag array, raised by every producer warp at exit) reaches N*H*W*C: from then
-// on no per-unit flag loads (each costs an L2 round trip in the producer's loop).
-__device__ __forceinline__ bool input_layer_done(const ConvParams &p) {
-    return ld_relaxed_gpu(p.dep_in + p.N * p.H) >= (unsigned)p.N * (unsigned)p.H * p.dep_in_target;
-}
-__device__ __forceinline__ void wait_input_for_pixels(const ConvParams &p, int m_lo, int m_hi) {
-    if (m_hi >= p.M) m_hi = p.M - 1;
-    if (m_lo > m_hi) return;
-    const int PQ = p.P * p.Q;
-    const int n_lo = p.fd_PQ.div(m_lo), n_hi = p.fd_PQ.div(m_hi);
-    const int pl = p.fd_Q.div(m_lo - n_lo * PQ), ph = p.fd_Q.div(m_hi - n_hi * PQ);
-    for (int n = n_lo; n <= n_hi; ++n) {
-        const int a = n == n_lo ? pl : 0, b = n == n_hi ? ph : p.P - 1;
-        const int h_lo = max(0, a * p.stride - p.pad), h_hi = min(p.H - 1, b * p.stride - p.pad + p.R - 1);
-        if (h_lo <= h_hi) wait_rows(p.dep_in, n * p.H + h_lo, n * p.H + h_hi, p.dep_in_target);
-    }
 }
 
 template <int BITS, int BN, int KCH, int OUT, int CG, int NSUB, int HALO>
@@ -721,18 +697,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             __syncwarp();
         }
         // activations (the previous layer's output) only after the previous grid
-        // completed -- or, with row flags, after the rows each unit reads are in memory
-        if (!p.dep_in) pdl_wait();
+        // completed -- or, with completion counters, after its last codes are in memory
+        if (p.dep_in) wait_counter(p.dep_in, p.dep_in_total);
+        else pdl_wait();
         if (trace && lane == 0) trace[blockIdx.x * TR_SLOTS + TR_TPDL] = globaltimer_ns();
-        bool in_done = !p.dep_in;    // the whole input layer known complete (no more flag loads)
-        // halo modes: the box of tile (n, p0) covers input rows p0 - pad .. + halo_rows - 1
-        auto wait_halo_rows = [&](int n, int p0) {
-            if (!in_done) in_done = input_layer_done(p);
-            if (!in_done && n < p.N) {
-                const int h_lo = max(0, p0 - p.pad), h_hi = min(p.H - 1, p0 - p.pad + p.halo_rows - 1);
-                if (h_lo <= h_hi) wait_rows(p.dep_in, n * p.H + h_lo, n * p.H + h_hi, p.dep_in_target);
-            }
-        };
         if constexpr (WS && (HA || S2H)) {
             // one stage = one halo box per (tile, channel block); no weights
             for (int tile = tile0; tile < p.num_tiles; tile += tstep) {
@@ -740,7 +708,6 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 const int rt = m_blk * CG + (int)rank;            // this CTA's row tile
                 const int n = p.fd_tpi.div(rt);                   // (>= N: all-OOB box, rows masked)
                 const int p0 = (rt - n * p.tiles_per_img) * p.rpt;
-                if constexpr (!S2H) wait_halo_rows(n, p0);
                 for (int cblk = 0; cblk < p.num_cblk; ++cblk) {
                     {
                         const long long t0 = trace ? clock64() : 0;
@@ -769,7 +736,6 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 const int n = p.fd_tpi.div(rt);                   // (>= N: all-OOB box, rows masked)
                 const int p0 = (rt - n * p.tiles_per_img) * p.rpt;
                 const int brow = n_blk * BN + (int)rank * Cfg::BNL;
-                wait_halo_rows(n, p0);
                 for (int cblk = 0; cblk < p.num_cblk; ++cblk, ++hcount) {
                     const int hb = hcount % Cfg::NHALO;
                     const uint32_t hph = (hcount / Cfg::NHALO) & 1;
@@ -822,10 +788,6 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             }
             const int brow = n_blk * BN + (int)rank * Cfg::BNL;  // this CTA's B rows
             const int nk = kb_hi - kb_lo;
-            if (!in_done) {
-                in_done = input_layer_done(p);
-                if (!in_done) wait_input_for_pixels(p, m0, m0 + Cfg::AMT * BM - 1);
-            }
             // optional rotated k-block order (CTA c starts at k-block 7c mod nk; any
             // order is bit-exact for integer accumulation)
             const int rot = (p.rotate && !WS) ? (int)(((unsigned)(blockIdx.x / CG) * 7u) % (unsigned)nk) : 0;
@@ -1233,30 +1195,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
         if (!p.dep_in) pdl_wait();
         // count, per output image row n*P + p = m / Q, the pixels x columns this warp
         // wrote (lanes grouped by row with ballots; <= a few rows per 32 pixels)
-        unsigned warp_total = 0;   // pixels x columns this warp counted (lane 0)
-        auto signal_total = [&]() {
-            if (lane == 0 && warp_total) atomicAdd(p.dep_out + p.N * p.P, warp_total);
-            warp_total = 0;
-        };
-        auto signal_rows = [&](const int (&ms)[Cfg::MT], int cols) {
-            if (cols <= 0) return;
-#pragma unroll
-            for (int g = 0; g < Cfg::MT; ++g) {
-                const bool valid = ms[g] < p.M;
-                const int r = valid ? p.fd_Q.div(ms[g]) : -1;
-                unsigned todo = __ballot_sync(0xffffffffu, valid);
-                while (todo) {
-                    const int rr = __shfl_sync(0xffffffffu, r, __ffs(todo) - 1);
-                    const unsigned mask = __ballot_sync(0xffffffffu, valid && r == rr) & todo;
-                    if (lane == 0) {
-                        atomicAdd(p.dep_out + rr, (unsigned)(__popc(mask) * cols));   // after the fence
-                        warp_total += (unsigned)(__popc(mask) * cols);
-                    }
-                    todo &= ~mask;
-                }
-            }
-        };
-        bool skip_done = false;   // the whole skip layer known complete
+        unsigned warp_total = 0;   // codes this warp wrote (counted per unit, added at exit)
+        if constexpr (Cfg::RES) {   // the residual skip (an earlier layer's output) is in memory
+            if (p.dep_skip) wait_counter(p.dep_skip, p.dep_skip_total);
+        }
         int j = 0;    // this unit's index among the units of its buffer
         for (int unit = tile0 + b0 * tstep, lu = 0; unit < p.num_units;
              unit += (ALLW ? 1 : Cfg::NBUF) * tstep, ++lu) {
@@ -1297,27 +1239,6 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             constexpr int NCH = Cfg::EPI_COLS / Cfg::CW;
             constexpr bool SKT = Cfg::SKIP_TMA;
             uint4 skp[Cfg::RES && !SKT ? Cfg::MT : 1][Cfg::RES && !SKT ? NCH : 1];
-            if constexpr (Cfg::RES) {
-                // row flags: the skip rows of this unit's output pixels are in memory
-                if (p.dep_skip && !skip_done) skip_done = ld_relaxed_gpu(p.dep_skip + p.N * p.P) >=
-                                                          (unsigned)p.N * (unsigned)p.P * p.dep_out_target;
-                if (p.dep_skip && !skip_done) {
-                    int r_lo, r_hi;
-                    if constexpr (HA || S2H) {
-                        const int rt = m_blk * CG + (int)rank;
-                        const int n = p.fd_tpi.div(rt);
-                        const int p0 = (rt - n * p.tiles_per_img) * p.rpt;
-                        r_lo = n * p.P + p0;
-                        r_hi = n * p.P + min(p.P - 1, p0 + p.rpt - 1);
-                        if (rt >= p.m_tiles) r_hi = r_lo - 1;
-                    } else {
-                        r_lo = p.fd_Q.div(min(mrow0, p.M - 1));
-                        r_hi = p.fd_Q.div(min(mrow0 + Cfg::MT * BM - 1, p.M - 1));
-                        if (mrow0 >= p.M) r_hi = r_lo - 1;
-                    }
-                    wait_rows(p.dep_skip, r_lo, r_hi, p.dep_out_target);
-                }
-            }
             if constexpr (SKT) {
                 // the warp's skip slab -> its (free) output staging slab, one bulk copy per
                 // 128-byte column block, completing on the warp's own barrier
@@ -1639,57 +1560,29 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 }
             }
             if constexpr (Cfg::MT == 1) store_slab(0);
-            if (p.dep_out && p.splits > 1 && emit) {
-                // split-K: the warp that completed a region wrote it -- signal it now
-                if (Cfg::OUTP == OUT_TMA && lane == 0) {
-                    tma_store_wait0();
-                    fence_proxy_async_global();
-                }
-                __threadfence();
-                __syncwarp();
+            if (p.dep_out && emit) {   // this unit's codes written by this warp (valid pixels x columns)
                 const int cols = min(Cfg::EPI_COLS, p.K - (n_blk * BN + half * Cfg::EPI_COLS));
-                int ms[Cfg::MT];
 #pragma unroll
-                for (int g = 0; g < Cfg::MT; ++g) ms[g] = Cfg::MT == 1 ? m : mrow0 + g * BM + row;
-                signal_rows(ms, cols);
-                signal_total();
+                for (int g = 0; g < Cfg::MT; ++g) {
+                    const int mg = Cfg::MT == 1 ? m : (HA || S2H) ? halo_m(g * BM + row) : mrow0 + g * BM + row;
+                    const unsigned valid = __ballot_sync(0xffffffffu, mg < p.M);
+                    if (cols > 0) warp_total += (unsigned)(__popc(valid) * cols);
+                }
             }
             CONVQ_TL(24 + warp, j);
         }
         if (Cfg::OUTP == OUT_TMA && lane == 0) tma_store_wait0();
-        if (p.dep_out && p.splits == 1) {
-            // Row flags, once per warp at its exit: every store of this warp is complete
-            // (TMA: wait_group 0 above; direct: the fence), then one release fence and
-            // relaxed adds for the rows of every unit the warp wrote.  (Per-unit signals
-            // -- a store-completion wait or a fence per unit -- measured 1.4x slower at
-            // b256.)  The next layer's tiles whose rows came from early-finishing CTAs
-            // start during this layer's tail.
-            if (Cfg::OUTP == OUT_TMA && lane == 0) fence_proxy_async_global();
-            __threadfence();
-            __syncwarp();
-            for (int unit = tile0 + b0 * tstep; unit < p.num_units; unit += (ALLW ? 1 : Cfg::NBUF) * tstep) {
-                const int tile = p.splits == 1 ? unit : p.fd_splits.div(unit);
-                const int m_blk = p.fd_ntiles.div(tile), n_blk = tile - m_blk * p.n_tiles;
-                const int mrow0 = m_blk * (BM * CG * Cfg::AMT) + (int)rank * BM;
-                int ms[Cfg::MT];
-#pragma unroll
-                for (int g = 0; g < Cfg::MT; ++g) {
-                    if constexpr (HA || S2H) {
-                        const int rr = g * BM + row;
-                        const int rt = m_blk * CG + (int)rank;
-                        const int n = p.fd_tpi.div(rt);
-                        const int pl = p.fd_Wp.div(rr), qq = rr - pl * p.Wp;
-                        const int pp = (rt - n * p.tiles_per_img) * p.rpt + pl;
-                        const bool ok = rt < p.m_tiles && pl < p.rpt && pp < p.P && qq < p.Q;
-                        ms[g] = ok ? (n * p.P + pp) * p.Q + qq : p.M;
-                    } else {
-                        ms[g] = mrow0 + g * BM + row;
-                    }
-                }
-                const int cols = min(Cfg::EPI_COLS, p.K - (n_blk * BN + half * Cfg::EPI_COLS));
-                signal_rows(ms, cols);
+        if (p.dep_out) {
+            // once per warp at its exit: every store of this warp is complete (TMA:
+            // lane 0's wait_group 0 above + a proxy fence; direct stores: every lane's
+            // membar), then one relaxed add of the codes it wrote
+            if constexpr (Cfg::OUTP == OUT_TMA) {
+                if (lane == 0) fence_proxy_async_global();
+            } else {
+                __threadfence();
             }
-            signal_total();
+            __syncwarp();
+            if (lane == 0 && warp_total) atomicAdd(p.dep_out, warp_total);
         }
 #undef CONVQ_TL
     } else if (warp < Cfg::PROD_WARP) {

@@ -551,16 +551,18 @@ extern "C" int conv_q_plan_set_residual(conv_q_plan_t *p, const void *skip, floa
     return CONV_Q_OK;
 }
 
-extern "C" int conv_q_plan_set_deps(conv_q_plan_t *p, const unsigned *in_rows, const unsigned *skip_rows,
-                                    unsigned *out_rows) {
+extern "C" int conv_q_plan_set_deps(conv_q_plan_t *p, const unsigned *in_done, const unsigned *skip_done,
+                                    unsigned *out_done) {
     if (!p) return set_err(CONV_Q_EINVAL, "NULL plan");
-    if (p->s2d && in_rows) return set_err(CONV_Q_EUNSUPPORTED, "the s2d stem plan reads the s2d quantize output");
-    if ((in_rows && (reinterpret_cast<uintptr_t>(in_rows) & 3)) || (skip_rows && (reinterpret_cast<uintptr_t>(skip_rows) & 3)) ||
-        (out_rows && (reinterpret_cast<uintptr_t>(out_rows) & 3)))
-        return set_err(CONV_Q_EINVAL, "row flag arrays must be 4-byte aligned");
-    p->dep_in = in_rows;
-    p->dep_skip = skip_rows;
-    p->dep_out = out_rows;
+    if (p->s2d && in_done) return set_err(CONV_Q_EUNSUPPORTED, "the s2d stem plan reads the s2d quantize output");
+    if ((in_done && (reinterpret_cast<uintptr_t>(in_done) & 3)) || (skip_done && (reinterpret_cast<uintptr_t>(skip_done) & 3)) ||
+        (out_done && (reinterpret_cast<uintptr_t>(out_done) & 3)))
+        return set_err(CONV_Q_EINVAL, "completion counters must be 4-byte aligned");
+    if ((int64_t)p->N * p->H * p->W * p->C > 0xFFFFFFFFLL || (int64_t)p->M * p->K > 0xFFFFFFFFLL)
+        return set_err(CONV_Q_EUNSUPPORTED, "tensor too large for a 32-bit completion counter");
+    p->dep_in = in_done;
+    p->dep_skip = skip_done;
+    p->dep_out = out_done;
     return CONV_Q_OK;
 }
 

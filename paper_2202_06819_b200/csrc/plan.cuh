@@ -79,7 +79,7 @@ struct conv_q_plan_s {
     const void *skip = nullptr;   // conv_q_plan_set_residual: fused residual add (NULL = none)
     float res_scale = 0.f;
     int x_uns = 0, y_uns = 0, skip_uns = 0;   // conv_q_plan_set_formats: unsigned codes (DESIGN reading 16)
-    // conv_q_plan_set_deps: cross-launch row flags (NULL in = griddepcontrol.wait)
+    // conv_q_plan_set_deps: cross-launch completion counters (NULL in = griddepcontrol.wait)
     const unsigned *dep_in = nullptr, *dep_skip = nullptr;
     unsigned *dep_out = nullptr;
     cudaStream_t stream = nullptr;
@@ -228,8 +228,8 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.dep_in = p->dep_in;
     prm.dep_skip = p->skip ? p->dep_skip : nullptr;
     prm.dep_out = p->dep_out;
-    prm.dep_in_target = (unsigned)(p->W * p->C);      // pixels x channels of one input row
-    prm.dep_out_target = (unsigned)(p->Q * p->K);     // of one output (and skip) row
+    prm.dep_in_total = (unsigned)((int64_t)p->N * p->H * p->W * p->C);       // codes of x
+    prm.dep_skip_total = (unsigned)((int64_t)p->N * p->P * p->Q * p->K);     // codes of the skip (= y's shape)
     prm.halo_rows = halo_rows;
     prm.x_uns = p->x_uns;
     prm.y_uns = p->y_uns;

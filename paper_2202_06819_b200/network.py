@@ -52,15 +52,15 @@ class ConvNet:
                  dataflow: bool = True):
         """unsigned: every ReLU output is written as unsigned codes [0, 2^b - 1] and
         read as unsigned activations by its consumers (DESIGN reading 16).
-        dataflow: consecutive conv launches synchronise through per-row flags
-        (conv_q_plan_set_deps) instead of whole-grid completion; the flags are
-        zeroed at the start of every step."""
+        dataflow: consecutive conv launches synchronise through completion
+        counters (conv_q_plan_set_deps) instead of whole-grid completion; the
+        counters are zeroed at the start of every step."""
         import torch
         self.torch = torch
         self.B, self.bits, self.device = batch, bits, device
         self.unsigned = unsigned
         self.dataflow = dataflow
-        self.flags = None         # int32 row counters of every conv output, one buffer (zeroed per step)
+        self.flags = None         # int32 completion counter of every conv output (zeroed per step)
         self.stream = stream
         self.convs: list[_Conv] = []
         self.stem = None
@@ -153,27 +153,21 @@ class ConvNet:
             self.stem["plan"].set_stream(stream)
 
     # ------------------------------------------------------------- a7 tuning
-    # ------------------------------------------------------------- dataflow flags
+    # ------------------------------------------------------------- dataflow counters
     def _apply_deps(self, on: bool):
-        """Row flags of every conv (conv_q_plan_set_deps): conv i counts its output rows
-        in its slice of self.flags; it waits on its source's rows (not for the input
-        stage: that one is waited for as a whole grid) and on its skip's rows."""
+        """Completion counters of every conv (conv_q_plan_set_deps): conv i adds the
+        codes it wrote to self.flags[i]; it waits for its source's count (not for the
+        input stage's: that one is waited for as a whole grid) and its skip's."""
         t = self.torch
         if on and self.flags is None:
-            sizes = [self.B * c.layer.P + 1 for c in self.convs]     # + the layer's total counter
-            self.flags = t.zeros(sum(sizes), dtype=t.int32, device=self.device)
-            offs, o = [], 0
-            for n in sizes:
-                offs.append(o)
-                o += n
-            self._flag_rows = [self.flags[a:a + n] for a, n in zip(offs, sizes)]
+            self.flags = t.zeros(len(self.convs), dtype=t.int32, device=self.device)
         for i, c in enumerate(self.convs):
             if not on:
                 c.plan.set_deps(None, None, None)
                 continue
-            rows = self._flag_rows
-            c.plan.set_deps(rows[c.src] if c.src >= 0 else None,
-                            rows[c.skip] if (c.skip is not None and c.skip >= 0) else None, rows[i])
+            f = self.flags
+            c.plan.set_deps(f[c.src:c.src + 1] if c.src >= 0 else None,
+                            f[c.skip:c.skip + 1] if (c.skip is not None and c.skip >= 0) else None, f[i:i + 1])
 
     def tune(self, warmup: int = 2, reps: int = 5) -> dict:
         """Pick each unique shape's tile config by on-device timing (conv_q_plan_tune),
@@ -213,7 +207,7 @@ class ConvNet:
                 self._apply_deps(True)
             if hasattr(s, "cuda_stream"):
                 with self.torch.cuda.stream(s):
-                    self.flags.zero_()   # row counters start at zero every step
+                    self.flags.zero_()   # counters start at zero every step
             else:
                 self.flags.zero_()
         self.run_input_stage(s, ev)

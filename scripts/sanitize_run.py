@@ -65,7 +65,7 @@ def main():
             plan.run(xd, wd, sd, y)
             torch.cuda.synchronize()
             n += 1
-    # two-layer chain with cross-launch row flags (conv_q_plan_set_deps)
+    # two-layer chain with cross-launch completion counters (conv_q_plan_set_deps)
     L1, L2 = wl.Layer("d1", 14, 14, 128, 128, 3, 3, 1, 1), wl.Layer("d2", 14, 14, 128, 128, 1, 1, 1, 0)
     N = 2
     x, w1, s1 = wl.layer_inputs(g, L1, N, 8)
@@ -74,8 +74,8 @@ def main():
     w1d, s1d, w2d, s2d = (torch.from_numpy(a).cuda() for a in (w1, s1, w2, s2))
     y1 = torch.empty((N, 14, 14, 128), dtype=torch.uint8, device="cuda")
     y2 = torch.empty((N, 14, 14, 128), dtype=torch.uint8, device="cuda")
-    f1 = torch.zeros(N * 14 + 1, dtype=torch.int32, device="cuda")
-    f2 = torch.zeros(N * 14 + 1, dtype=torch.int32, device="cuda")
+    f1 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    f2 = torch.zeros(1, dtype=torch.int32, device="cuda")
     p1 = cq.ConvPlan(N, 14, 14, 128, 128, 3, 3, 1, 1, 8, relu=True)
     p2 = cq.ConvPlan(N, 14, 14, 128, 128, 1, 1, 1, 0, 8, relu=True)
     p1.set_deps(None, None, f1)

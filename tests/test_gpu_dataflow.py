@@ -1,8 +1,8 @@
-"""Cross-launch row flags (conv_q_plan_set_deps) on the GPU (-m gpu): the bench
-chains with dataflow between conv launches, every launch checked against the
-oracle on sampled pixels (tile boundaries included), several steps in a row
-(the flags are re-zeroed every step), and dataflow == whole-grid dependencies
-byte for byte on every output."""
+"""Cross-launch completion counters (conv_q_plan_set_deps) on the GPU (-m gpu):
+the bench chains with dataflow between conv launches, every launch checked
+against the oracle on sampled pixels (tile boundaries included), several steps
+in a row (the counters are re-zeroed every step), and dataflow == whole-grid
+dependencies byte for byte on every output."""
 import numpy as np
 import pytest
 
@@ -43,7 +43,7 @@ def test_dataflow_chain_parity(cq, workload, B):
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
         net.step(stream)
-    for _ in range(3):                   # replays: the flags are re-zeroed inside every step
+    for _ in range(3):                   # replays: the counters are re-zeroed inside every step
         graph.replay()
     torch.cuda.synchronize()
     imgs = sorted({0, B // 2, B - 1})

@@ -1,6 +1,6 @@
 """compute-sanitizer over every candidate family at cfg1 and edge sizes, the
 residual epilogue with unsigned codes, and a two-layer chain with cross-launch
-row flags (-m gpu;
+completion counters (-m gpu;
 skipped when the tool is absent).  memcheck: out-of-bounds / misaligned
 global and shared accesses; synccheck: invalid barrier use.  The async
 pipeline (TMA, mbarriers, tcgen05) is the part a race or a wrong byte count
