@@ -1571,7 +1571,14 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             }
             CONVQ_TL(24 + warp, j);
         }
-        if (Cfg::OUTP == OUT_TMA && lane == 0) tma_store_wait0();
+        // before exit the staging smem must have been read out by the TMA (.read); the
+        // writes themselves need not be complete (grid completion flushes them) unless a
+        // completion counter is raised below -- waiting only for the reads lets the CTA
+        // leave (and the next layer's CTA take the SM) a global-write latency earlier
+        if (Cfg::OUTP == OUT_TMA && lane == 0) {
+            if (p.dep_out) tma_store_wait0();
+            else tma_store_wait_read0();
+        }
         if (p.dep_out) {
             // once per warp at its exit: every store of this warp is complete (TMA:
             // lane 0's wait_group 0 above + a proxy fence; direct stores: every lane's
