@@ -214,6 +214,82 @@ CONVQ_API int conv_q_plan_tune(conv_q_plan_t *plan, const void *x, const void *w
 CONVQ_API int conv_q_plan_time_candidates(conv_q_plan_t *plan, const void *x, const void *w, const float *scale,
                                           void *y, int warmup, int reps, float *us);
 
+/*
+ * (ABI 1.06) Learned, diversity-aware schedule search:
+ * the exploration module of PAPER.md:282-298 (section 3.4, Figs. 12-13) with
+ * the settings of PAPER.md:309-314 (section 4.1).  Host-only; no device work.
+ *
+ * A space is n_knobs categorical knobs, knob i taking values 0..knob_sizes[i]-1
+ * (1 <= n_knobs <= CONV_Q_SEARCH_MAX_KNOBS; the product of the sizes < 2^60).
+ *   valid(ctx, knobs): nonzero when the point exists (NULL: every point);
+ *   cost(ctx, knobs):  the measured cost of the point, > 0, lower is better
+ *                      (e.g. microseconds); <= 0 marks a failed point.
+ * Every batch measures `batch` never-measured points: the first batch random,
+ * then the (batch - 1) best points of simulated annealing over a cost model
+ * (pairwise ranking loss on the measurements so far) plus one random point;
+ * diversity != 0: each annealing chain makes two mutants and half of all
+ * mutants are kept by configuration diversity before competing with their
+ * parents (the paper's proposal); 0: one mutant per chain (AutoTVM).
+ * Stops after `trials` measurements or when the space is exhausted.
+ * best_knobs (host, n_knobs ints) receives the fastest measured point;
+ * history_cost (host, trials doubles) / history_knobs (host, trials*n_knobs
+ * ints), if not NULL, receive every measurement in order.
+ * Returns the number of measurements (>= 1) or an error code (EINVAL: bad
+ * arguments; ECUDA: no point measured successfully).  Deterministic for a seed.
+ */
+#define CONV_Q_SEARCH_MAX_KNOBS 16
+typedef struct conv_q_search_opts {
+    int trials;          /* hardware measurements in total (default 128) */
+    int batch;           /* measurements per model round (default 32 = 31 picks + 1 random) */
+    int sa_iters;        /* annealing iterations (500) */
+    int sa_early_stop;   /* stop when the optimal set is unchanged this long (50) */
+    int sa_points;       /* parallel annealing chains (128) */
+    int diversity;       /* 1: diversity-aware selection (default), 0: plain mutation */
+    float sa_temp0;      /* start temperature (1.0) */
+    float sa_cool;       /* temperature decrease per iteration (0.002) */
+    unsigned long long seed;
+} conv_q_search_opts_t;
+typedef int (*conv_q_valid_fn)(void *ctx, const int *knobs);
+typedef double (*conv_q_cost_fn)(void *ctx, const int *knobs);
+CONVQ_API void conv_q_search_opts_default(conv_q_search_opts_t *opts);
+CONVQ_API int conv_q_search(int n_knobs, const int *knob_sizes, conv_q_valid_fn valid, conv_q_cost_fn cost,
+                            void *ctx, const conv_q_search_opts_t *opts, int *best_knobs, double *history_cost,
+                            int *history_knobs);
+
+/*
+ * (ABI 1.06) The plan's enlarged schedule space (NEXT-4): the TileConfig
+ * knobs of the candidate list -- BN, k-block (channels x k-blocks per stage),
+ * CTAs per tile, operand mode (im2col/tiled, halo, weight-stationary, WS halo,
+ * WS MT2, WS halo MT2), output path (TMA store / direct) -- crossed with
+ * runtime knobs: split-K {1,2,3,4,6,8} (im2col/tiled configs), epilogue
+ * accumulator wait {spin, suspend hint, nanosleep}, output L2 policy {none,
+ * evict_last, evict_first}, k-block start rotation {off, on}, persistent
+ * grid {100, 75, 50 % of the SMs}.  *n_knobs (<= CONV_Q_SEARCH_MAX_KNOBS) and
+ * knob_sizes[] describe it; *n_valid receives the number of valid points.
+ */
+CONVQ_API int conv_q_plan_space(const conv_q_plan_t *plan, int *n_knobs, int *knob_sizes, long long *n_valid);
+
+/* (ABI 1.06) Select one point of conv_q_plan_space (knobs: host, n_knobs ints):
+ * its TileConfig (a split-K variant is appended to the candidate list when
+ * needed; its workspace is allocated here) and runtime knobs.  EINVAL: a knob
+ * out of range; EUNSUPPORTED: not a valid point. */
+CONVQ_API int conv_q_plan_set_point(conv_q_plan_t *plan, const int *knobs);
+
+/*
+ * (ABI 1.06) conv_q_search over conv_q_plan_space, each point timed on the
+ * device exactly as conv_q_plan_tune times a candidate (`warmup` runs, 3
+ * rounds of `reps` graph-captured launches, median round).  Selects the
+ * fastest point (TileConfig -- a split-K variant is appended to the candidate
+ * list when needed -- and its runtime knobs), records it in the tuning cache
+ * under the plan's shape key (name = candidate name + "+e<wait>p<policy>r<rot>g<grid %>"),
+ * writes its time to *best_us and every measured time (-1 = failed) to
+ * history_us (host, opts->trials doubles; may be NULL).  y is overwritten.
+ * Synchronises the stream.  Returns the number of measurements or an error code.
+ */
+CONVQ_API int conv_q_plan_search(conv_q_plan_t *plan, const void *x, const void *w, const float *scale, void *y,
+                                 const conv_q_search_opts_t *opts, int warmup, int reps, float *best_us,
+                                 double *history_us);
+
 /* Fill *info (host memory). */
 CONVQ_API int conv_q_plan_info(const conv_q_plan_t *plan, conv_q_info_t *info);
 

@@ -20,6 +20,7 @@ from dataclasses import dataclass
 __all__ = [
     "ConvQError", "ConvPlan", "PlanInfo", "load", "quantize", "pack_weights", "padded_channels",
     "int8_peak", "out_dim", "OUT_PACKED", "OUT_S32", "StemPlan", "maxpool", "requant",
+    "SearchOpts", "search",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -44,6 +45,27 @@ class _Info(ctypes.Structure):
         ("out_mode", ctypes.c_int), ("num_candidates", ctypes.c_int), ("config_index", ctypes.c_int),
         ("config", ctypes.c_char * 64), ("tuned_us", ctypes.c_float), ("macs", ctypes.c_int64),
         ("s2d", ctypes.c_int), ("x_dims", ctypes.c_int * 4), ("w_dims", ctypes.c_int * 4)]
+
+
+class SearchOpts(ctypes.Structure):
+    """conv_q_search_opts_t (include/convq.h, NEXT-4: PAPER.md:309-314 defaults)."""
+    _fields_ = [("trials", ctypes.c_int), ("batch", ctypes.c_int), ("sa_iters", ctypes.c_int),
+                ("sa_early_stop", ctypes.c_int), ("sa_points", ctypes.c_int), ("diversity", ctypes.c_int),
+                ("sa_temp0", ctypes.c_float), ("sa_cool", ctypes.c_float), ("seed", ctypes.c_ulonglong)]
+
+    @classmethod
+    def make(cls, **kw) -> "SearchOpts":
+        o = cls()
+        load().conv_q_search_opts_default(ctypes.byref(o))
+        for k, v in kw.items():
+            if not hasattr(o, k):
+                raise ConvQError(EINVAL, f"unknown search option {k}")
+            setattr(o, k, v)
+        return o
+
+
+_VALID_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int))
+_COST_FN = ctypes.CFUNCTYPE(ctypes.c_double, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int))
 
 
 @dataclass
@@ -126,6 +148,20 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.conv_q_plan_set_deps.argtypes = [vp, vp, vp, vp]
     lib.conv_q_int8_peak.restype = i
     lib.conv_q_int8_peak.argtypes = [i, ctypes.POINTER(ctypes.c_double)]
+    lib.conv_q_search_opts_default.restype = None
+    lib.conv_q_search_opts_default.argtypes = [ctypes.POINTER(SearchOpts)]
+    lib.conv_q_search.restype = i
+    lib.conv_q_search.argtypes = [i, ctypes.POINTER(ctypes.c_int), _VALID_FN, _COST_FN, vp, ctypes.POINTER(SearchOpts),
+                                  ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_int)]
+    lib.conv_q_plan_space.restype = i
+    lib.conv_q_plan_space.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                      ctypes.POINTER(ctypes.c_longlong)]
+    lib.conv_q_plan_set_point.restype = i
+    lib.conv_q_plan_set_point.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
+    lib.conv_q_plan_search.restype = i
+    lib.conv_q_plan_search.argtypes = [vp, vp, vp, vp, vp, ctypes.POINTER(SearchOpts), i, i,
+                                       ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double)]
     _lib = lib
     return lib
 
@@ -296,6 +332,32 @@ class ConvPlan:
                                                warmup, reps, arr))
         return list(arr)
 
+    def space(self) -> tuple[list[int], int]:
+        """(knob sizes, number of valid points) of the plan's enlarged schedule space (NEXT-4)."""
+        n = ctypes.c_int(0)
+        sizes = (ctypes.c_int * 16)()
+        nv = ctypes.c_longlong(0)
+        _check(load().conv_q_plan_space(self._h, ctypes.byref(n), sizes, ctypes.byref(nv)))
+        return list(sizes[:n.value]), nv.value
+
+    def set_point(self, knobs):
+        """Select one point of space() (conv_q_plan_set_point)."""
+        _check(load().conv_q_plan_set_point(self._h, (ctypes.c_int * len(knobs))(*knobs)))
+
+    def search(self, x, w, scale, y, warmup=2, reps=10, stream=None, **opts) -> dict:
+        """Learned, diversity-aware search over space() on the device (conv_q_plan_search):
+        selects the fastest measured point; returns {best_us, history_us, config}."""
+        self._check_buffers(x, w, scale, y)
+        lib = load()
+        _check(lib.conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
+        o = SearchOpts.make(**opts)
+        hist = (ctypes.c_double * max(o.trials, 1))()
+        best = ctypes.c_float(0)
+        n = _check(lib.conv_q_plan_search(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)),
+                                          ctypes.c_void_p(_ptr(scale)), ctypes.c_void_p(_ptr(y)), ctypes.byref(o),
+                                          warmup, reps, ctypes.byref(best), hist))
+        return {"best_us": best.value, "history_us": list(hist[:n]), "config": self.info().config}
+
     def tune(self, x, w, scale, y, warmup=3, reps=10, stream=None) -> int:
         self._check_buffers(x, w, scale, y)
         lib = load()
@@ -422,3 +484,35 @@ def int8_peak(iters: int = 200000) -> float:
     v = ctypes.c_double(0.0)
     _check(load().conv_q_int8_peak(iters, ctypes.byref(v)))
     return v.value
+
+
+def search(knob_sizes, cost, valid=None, **opts) -> dict:
+    """conv_q_search over a generic knob space (host only; NEXT-4 engine):
+    cost(knobs) -> float > 0 (lower is better; <= 0 = failed), valid(knobs) -> bool.
+    Returns {best, n, history_cost, history_knobs}."""
+    lib = load()
+    nk = len(knob_sizes)
+    sizes = (ctypes.c_int * nk)(*knob_sizes)
+    o = SearchOpts.make(**opts)
+    err = []
+
+    def _c(_ctx, k):
+        try:
+            return float(cost([k[i] for i in range(nk)]))
+        except Exception as e:   # noqa: BLE001 -- surfaced after the call
+            err.append(e)
+            return -1.0
+
+    def _v(_ctx, k):
+        return 1 if valid([k[i] for i in range(nk)]) else 0
+
+    cf = _COST_FN(_c)
+    vf = _VALID_FN(_v) if valid is not None else _VALID_FN()
+    best = (ctypes.c_int * nk)()
+    hc = (ctypes.c_double * max(o.trials, 1))()
+    hk = (ctypes.c_int * (max(o.trials, 1) * nk))()
+    n = _check(lib.conv_q_search(nk, sizes, vf, cf, None, ctypes.byref(o), best, hc, hk))
+    if err:
+        raise err[0]
+    return {"best": list(best), "n": n, "history_cost": list(hc[:n]),
+            "history_knobs": [list(hk[i * nk:(i + 1) * nk]) for i in range(n)]}

@@ -3,7 +3,8 @@
 The kernel instantiations live in sixteen translation units kern_b{8,4}_o{OUT}.cu,
 one per (bits, output path) -- packed TMA / s32 / direct stores, ReLU, residual,
 unsigned u8 codes --
-compiled in parallel, plus the host library convq.cu; objects are linked into
+compiled in parallel, plus the host library convq.cu and the host-only schedule
+search search.cpp (NEXT-4); objects are linked into
 one shared library with the CUDA runtime linked statically."""
 from __future__ import annotations
 
@@ -24,7 +25,7 @@ _SFX = ("_instr" if INSTR else "") + (f"_wg{os.environ['CONVQ_EPI_WG8']}" if os.
     ("_allw0" if os.environ.get("CONVQ_EPI_ALLW") == "0" else "")
 OBJ = os.path.join(HERE, "build_obj" + _SFX)
 LIB = os.path.join(HERE, f"libconvq{_SFX}.so")
-SOURCES = ["convq.cu"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2, 4, 6, 8, 10)] + \
+SOURCES = ["convq.cu", "search.cpp"] + [f"kern_b{b}_o{o}.cu" for b in (8, 4) for o in (0, 1, 2, 4, 6, 8, 10)] + \
     ["kern_b8_o20.cu", "kern_b8_o22.cu"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -49,7 +50,7 @@ def _stale(target, deps) -> bool:
 
 def _compile(src, verbose):
     nvcc = os.environ.get("NVCC", "nvcc")
-    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+    obj = os.path.join(OBJ, os.path.splitext(os.path.basename(src))[0] + ".o")
     cmd = [nvcc, *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-I", os.path.join(ROOT, "include"),
            "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)

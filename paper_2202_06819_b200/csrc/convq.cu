@@ -48,7 +48,7 @@ int set_err(int code, const char *fmt, ...) {
 
 extern "C" const char *conv_q_last_error(void) { return g_err.c_str(); }
 extern "C" int conv_q_last_status(void) { return g_status; }
-extern "C" int conv_q_version(void) { return 105; }
+extern "C" int conv_q_version(void) { return 106; }
 
 // ============================================================== driver entry points
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -118,6 +118,14 @@ static std::string cand_name(const conv_q_plan_s *p, int i) {
     snprintf(b, sizeof b, "bm%d_bn%d_kc%dx%d_c%d%s%s%s", 128 * p->cands[i].cg, p->cands[i].bn, p->cands[i].kch,
              p->cands[i].nsub, p->cands[i].cg, p->cands[i].direct ? "_st" : "", (p->cands[i].halo & 5) ? "_h" : "", k);
     if (p->cands[i].ws) return std::string(b) + "_w" + ((p->cands[i].halo & 8) ? "_m2" : "");
+    return b;
+}
+
+// runtime-knob suffix of a searched selection ("" = the defaults)
+static std::string runtime_suffix(const conv_q_plan_s *p) {
+    if (p->epi_wait == 0 && p->out_policy == 1 && p->rotate == 0 && p->grid_pct == 100) return "";
+    char b[48];
+    snprintf(b, sizeof b, "+e%dp%dr%dg%d", p->epi_wait, p->out_policy, p->rotate, p->grid_pct);
     return b;
 }
 
@@ -340,11 +348,35 @@ static void apply_cache(conv_q_plan_s *p) {
     cache_load_locked();
     auto it = g_cache.find(shape_key(p));
     if (it == g_cache.end()) return;
-    for (size_t i = 0; i < p->cands.size(); ++i)
-        if (cand_name(p, (int)i) == it->second.first) {
-            p->sel = (int)i;
-            p->tuned_us = it->second.second;
+    // a searched entry (conv_q_plan_search) carries its runtime knobs after '+'
+    std::string name = it->second.first;
+    int ew = 0, pol = 1, rot = 0, grid = 100;
+    const size_t plus = name.find('+');
+    if (plus != std::string::npos) {
+        if (sscanf(name.c_str() + plus, "+e%dp%dr%dg%d", &ew, &pol, &rot, &grid) != 4) return;
+        name.resize(plus);
+    }
+    int found = -1;
+    for (size_t i = 0; i < p->cands.size() && found < 0; ++i)
+        if (cand_name(p, (int)i) == name) found = (int)i;
+    // a split-K variant outside the enumerated list (the search's split knob)
+    for (size_t i = 0, n = p->cands.size(); i < n && found < 0; ++i) {
+        if (p->cands[i].split != 1 || p->cands[i].ws || p->cands[i].halo) continue;
+        for (int sp = 2; sp <= 16 && found < 0; ++sp) {
+            p->cands.push_back(p->cands[i]);
+            p->cands.back().split = sp;
+            if (cand_name(p, (int)p->cands.size() - 1) == name) found = (int)p->cands.size() - 1;
+            else p->cands.pop_back();
         }
+    }
+    if (found < 0) return;
+    p->sel = found;
+    p->tuned_us = it->second.second;
+    p->epi_wait = ew;
+    p->epi_wait_ns = ew == 1 ? 20000u : ew == 2 ? 64u : 0u;
+    p->out_policy = pol;
+    p->rotate = rot;
+    p->grid_pct = grid;
 }
 
 static conv_q_plan_t *finish_plan(conv_q_plan_s *p);
@@ -623,7 +655,7 @@ extern "C" int conv_q_plan_info(const conv_q_plan_t *p, conv_q_info_t *info) {
     info->out_mode = p->out_mode;
     info->num_candidates = (int)p->cands.size();
     info->config_index = p->sel;
-    snprintf(info->config, sizeof info->config, "%s", p->cands.empty() ? "" : cand_name(p, p->sel).c_str());
+    snprintf(info->config, sizeof info->config, "%s", p->cands.empty() ? "" : (cand_name(p, p->sel) + runtime_suffix(p)).c_str());
     info->tuned_us = p->tuned_us;
     info->macs = p->M * p->K * p->Kg;
     return CONV_Q_OK;
@@ -829,42 +861,50 @@ extern "C" int conv_q_run(conv_q_plan_t *p, const void *x, const void *w, const 
 // measured ~4 us per conv_q_run and ~13 us through the Python binding, which
 // exceeds the device time of small-batch layers and would make eager timing
 // pick configs by host overhead.
-static int time_candidates(conv_q_plan_s *p, const void *x, const void *w, const float *scale, void *y, int warmup,
-                           int reps, float *us) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    CUDA_TRY(cudaStreamIsCapturing(p->stream, &cs));
-    if (cs != cudaStreamCaptureStatusNone) return set_err(CONV_Q_EINVAL, "tuning cannot run inside a graph capture");
-    // capture needs a non-legacy stream: use a private one when the plan's is the NULL stream
-    cudaStream_t user_stream = p->stream, ts = p->stream;
-    if (ts == nullptr || ts == cudaStreamLegacy || ts == cudaStreamPerThread) {
-        CUDA_TRY(cudaStreamSynchronize(ts));
-        CUDA_TRY(cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking));
+// A timing session: the plan's stream (or a private non-blocking one when the
+// plan uses the legacy / per-thread stream -- graph capture needs one) and two
+// events; time_sel() scores the plan's current selection + runtime knobs.
+struct TimingSession {
+    conv_q_plan_s *p;
+    cudaStream_t user_stream, ts;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int rc = CONV_Q_OK;
+    explicit TimingSession(conv_q_plan_s *plan) : p(plan), user_stream(plan->stream), ts(plan->stream) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaError_t e = cudaStreamIsCapturing(p->stream, &cs);
+        if (e != cudaSuccess) { rc = set_err(CONV_Q_ECUDA, "cudaStreamIsCapturing: %s", cudaGetErrorString(e)); return; }
+        if (cs != cudaStreamCaptureStatusNone) { rc = set_err(CONV_Q_EINVAL, "tuning cannot run inside a graph capture"); return; }
+        if (ts == nullptr || ts == cudaStreamLegacy || ts == cudaStreamPerThread) {
+            if ((e = cudaStreamSynchronize(ts)) != cudaSuccess ||
+                (e = cudaStreamCreateWithFlags(&ts, cudaStreamNonBlocking)) != cudaSuccess) {
+                rc = set_err(CONV_Q_ECUDA, "timing stream: %s", cudaGetErrorString(e));
+                ts = user_stream;
+                return;
+            }
+        }
+        p->stream = ts;
+        if ((e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess)
+            rc = set_err(CONV_Q_ECUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
     }
-    p->stream = ts;
-    cudaEvent_t e0, e1;
-    CUDA_TRY(cudaEventCreate(&e0));
-    CUDA_TRY(cudaEventCreate(&e1));
-    int best = -1, rc = CONV_Q_OK;
-    float best_us = 0.f;
-    const int saved = p->sel;
-    for (int i = 0; i < (int)p->cands.size() && !rc; ++i) {
-        p->sel = i;
-        if ((rc = ensure_ws(p))) break;   // split-K workspace (grows only), before any timed run
-        for (int k = 0; k < warmup + 1 && !rc; ++k) rc = conv_q_run(p, x, w, scale, y);   // + tensor maps encoded
-        if (rc) break;
+    // `warmup` runs (+ tensor maps encoded), then 3 rounds of one CUDA-graph
+    // replay of `reps` captured launches; *us = the median round's mean
+    int time_sel(const void *x, const void *w, const float *scale, void *y, int warmup, int reps, float *us) {
+        int r = ensure_ws(p);   // split-K workspace (grows only), before any timed run
+        for (int k = 0; k < warmup + 1 && !r; ++k) r = conv_q_run(p, x, w, scale, y);
+        if (r) return r;
         cudaGraph_t graph = nullptr;
         cudaGraphExec_t exec = nullptr;
         cudaError_t ce = cudaStreamBeginCapture(ts, cudaStreamCaptureModeThreadLocal);
-        if (ce != cudaSuccess) { rc = set_err(CONV_Q_ECUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(ce)); break; }
-        for (int j = 0; j < reps && !rc; ++j) rc = conv_q_run(p, x, w, scale, y);
+        if (ce != cudaSuccess) return set_err(CONV_Q_ECUDA, "cudaStreamBeginCapture: %s", cudaGetErrorString(ce));
+        for (int j = 0; j < reps && !r; ++j) r = conv_q_run(p, x, w, scale, y);
         ce = cudaStreamEndCapture(ts, &graph);
-        if (!rc && ce != cudaSuccess) rc = set_err(CONV_Q_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(ce));
-        if (!rc) {
+        if (!r && ce != cudaSuccess) r = set_err(CONV_Q_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(ce));
+        if (!r) {
             ce = cudaGraphInstantiate(&exec, graph, 0);
-            if (ce != cudaSuccess) rc = set_err(CONV_Q_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ce));
+            if (ce != cudaSuccess) r = set_err(CONV_Q_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ce));
         }
         float rt[3] = {0.f, 0.f, 0.f};
-        if (!rc) {
+        if (!r) {
             cudaGraphLaunch(exec, ts);   // upload / first-replay costs outside the timed rounds
             for (int k = 0; k < 3; ++k) {
                 cudaEventRecord(e0, ts);
@@ -876,27 +916,48 @@ static int time_candidates(conv_q_plan_s *p, const void *x, const void *w, const
                 rt[k] = ms * 1000.f / reps;
             }
             ce = cudaGetLastError();
-            if (ce != cudaSuccess) rc = set_err(CONV_Q_ECUDA, "candidate graph replay: %s", cudaGetErrorString(ce));
+            if (ce != cudaSuccess) r = set_err(CONV_Q_ECUDA, "candidate graph replay: %s", cudaGetErrorString(ce));
         }
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
-        if (rc) break;
+        if (r) return r;
         std::sort(rt, rt + 3);
-        if (us) us[i] = rt[1];
-        if (best < 0 || rt[1] < best_us) {
+        *us = rt[1];
+        return CONV_Q_OK;
+    }
+    // synchronise, restore the plan's stream; the first error wins
+    int finish(int r) {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        cudaError_t e = cudaStreamSynchronize(ts);
+        if (ts != user_stream) cudaStreamDestroy(ts);
+        p->stream = user_stream;
+        if (r) return r;
+        if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "candidate run failed: %s", cudaGetErrorString(e));
+        return CONV_Q_OK;
+    }
+};
+
+static int time_candidates(conv_q_plan_s *p, const void *x, const void *w, const float *scale, void *y, int warmup,
+                           int reps, float *us) {
+    TimingSession t(p);
+    if (t.rc) return t.finish(t.rc);
+    int best = -1, rc = CONV_Q_OK;
+    float best_us = 0.f;
+    const int saved = p->sel;
+    for (int i = 0; i < (int)p->cands.size() && !rc; ++i) {
+        p->sel = i;
+        float u = 0.f;
+        if ((rc = t.time_sel(x, w, scale, y, warmup, reps, &u))) break;
+        if (us) us[i] = u;
+        if (best < 0 || u < best_us) {
             best = i;
-            best_us = rt[1];
+            best_us = u;
         }
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     p->sel = saved;
-    cudaError_t e = cudaStreamSynchronize(ts);
-    if (ts != user_stream) cudaStreamDestroy(ts);
-    p->stream = user_stream;
-    if (rc) return rc;
-    if (e != cudaSuccess) return set_err(CONV_Q_ECUDA, "candidate run failed: %s", cudaGetErrorString(e));
-    return best;
+    rc = t.finish(rc);
+    return rc ? rc : best;
 }
 
 extern "C" int conv_q_plan_time_candidates(conv_q_plan_t *p, const void *x, const void *w, const float *scale,
@@ -931,6 +992,217 @@ extern "C" int conv_q_plan_tune(conv_q_plan_t *p, const void *x, const void *w, 
         cache_store_locked();
     }
     return best;
+}
+
+// ============================================================== learned search (NEXT-4)
+// The plan's enlarged schedule space (include/convq.h conv_q_plan_space):
+// TileConfig knobs taken from the candidate list (only values that occur, so
+// the space stays dense) x runtime knobs.  A point is valid when its
+// TileConfig knobs name a candidate of the list and its runtime knobs apply.
+namespace {
+enum { KB_BN, KB_KBLK, KB_CG, KB_MODE, KB_DIRECT, KB_SPLIT, KB_EPI, KB_POL, KB_ROT, KB_GRID, KB_COUNT };
+const int kSplits[] = {1, 2, 3, 4, 6, 8};
+const int kGrids[] = {100, 75, 50};
+const int kEpiWait[] = {0, 1, 2};
+const unsigned kEpiWaitNs[] = {0, 20000, 64};
+
+struct PlanSpace {
+    conv_q_plan_s *p;
+    std::vector<int> bns, cgs;
+    std::vector<std::pair<int, int>> kblks, modes;   // (kch, nsub), (ws, halo)
+    std::map<std::vector<int>, int> base;            // (bn, kblk, cg, mode, direct) -> candidate index (split 1)
+    int sizes[KB_COUNT];
+    explicit PlanSpace(conv_q_plan_s *plan) : p(plan) {
+        for (const Cand &c : p->cands) {
+            if (c.split != 1) continue;
+            if (std::find(bns.begin(), bns.end(), c.bn) == bns.end()) bns.push_back(c.bn);
+            if (std::find(cgs.begin(), cgs.end(), c.cg) == cgs.end()) cgs.push_back(c.cg);
+            const std::pair<int, int> kb{c.kch, c.nsub}, md{c.ws, c.halo};
+            if (std::find(kblks.begin(), kblks.end(), kb) == kblks.end()) kblks.push_back(kb);
+            if (std::find(modes.begin(), modes.end(), md) == modes.end()) modes.push_back(md);
+        }
+        std::sort(bns.begin(), bns.end());
+        std::sort(cgs.begin(), cgs.end());
+        std::sort(kblks.begin(), kblks.end());
+        std::sort(modes.begin(), modes.end());
+        for (size_t i = 0; i < p->cands.size(); ++i) {
+            const Cand &c = p->cands[i];
+            if (c.split != 1) continue;
+            std::vector<int> k = {idx(bns, c.bn), idx(kblks, std::make_pair(c.kch, c.nsub)), idx(cgs, c.cg),
+                                  idx(modes, std::make_pair(c.ws, c.halo)), c.direct};
+            if (!base.count(k)) base[k] = (int)i;
+        }
+        sizes[KB_BN] = (int)bns.size();
+        sizes[KB_KBLK] = (int)kblks.size();
+        sizes[KB_CG] = (int)cgs.size();
+        sizes[KB_MODE] = (int)modes.size();
+        sizes[KB_DIRECT] = 2;
+        sizes[KB_SPLIT] = 6;
+        sizes[KB_EPI] = 3;
+        sizes[KB_POL] = 3;
+        sizes[KB_ROT] = 2;
+        sizes[KB_GRID] = 3;
+    }
+    template <class T>
+    static int idx(const std::vector<T> &v, const T &x) {
+        return (int)(std::find(v.begin(), v.end(), x) - v.begin());
+    }
+    // candidate index of the point's TileConfig (split 1), or -1
+    int base_of(const int *k) const {
+        auto it = base.find(std::vector<int>{k[KB_BN], k[KB_KBLK], k[KB_CG], k[KB_MODE], k[KB_DIRECT]});
+        return it == base.end() ? -1 : it->second;
+    }
+    bool valid(const int *k) const {
+        const int b = base_of(k);
+        if (b < 0) return false;
+        const Cand &c = p->cands[b];
+        const int sms = g_num_sms > 0 ? g_num_sms : 148;
+        const int split = kSplits[k[KB_SPLIT]];
+        if (split > 1) {   // split-K: im2col / tiled configs, the enumeration's limits
+            if (c.ws || c.halo) return false;
+            const int64_t tiles = ceil_div(p->M, 128 * c.cg) * ceil_div(p->K, c.bn);
+            const int64_t num_kb = (int64_t)p->R * p->S * (p->C / c.kch);
+            if (split > std::min<int64_t>(16, num_kb / (2 * c.nsub))) return false;
+            if (tiles * c.cg * 128 * c.bn * 4 > ((int64_t)64 << 20) || 16 * num_kb >= ((int64_t)1 << 31)) return false;
+        }
+        if (k[KB_ROT] && c.ws) return false;   // the kernel ignores rotation for resident weights
+        if (c.ws) {   // a weight-stationary grid stays a multiple of the N-tile count
+            const int64_t n_tiles = ceil_div(p->K, c.bn);
+            if ((sms / c.cg) * kGrids[k[KB_GRID]] / 100 < n_tiles) return false;
+        }
+        return true;
+    }
+    // select the point on the plan: TileConfig (+ a split-K variant appended to
+    // the candidate list when missing) and the runtime knobs
+    void apply(const int *k) {
+        Cand c = p->cands[base_of(k)];
+        c.split = kSplits[k[KB_SPLIT]];
+        int sel = -1;
+        for (size_t i = 0; i < p->cands.size(); ++i) {
+            const Cand &d = p->cands[i];
+            if (d.bn == c.bn && d.kch == c.kch && d.cg == c.cg && d.nsub == c.nsub && d.direct == c.direct &&
+                d.halo == c.halo && d.ws == c.ws && d.split == c.split) { sel = (int)i; break; }
+        }
+        if (sel < 0) {
+            p->cands.push_back(c);
+            sel = (int)p->cands.size() - 1;
+        }
+        p->sel = sel;
+        p->epi_wait = kEpiWait[k[KB_EPI]];
+        p->epi_wait_ns = kEpiWaitNs[k[KB_EPI]];
+        p->out_policy = k[KB_POL];
+        p->rotate = k[KB_ROT];
+        p->grid_pct = kGrids[k[KB_GRID]];
+    }
+};
+
+struct SearchCtx {
+    PlanSpace *sp;
+    TimingSession *ts;
+    const void *x, *w;
+    const float *scale;
+    void *y;
+    int warmup, reps;
+    int fatal = CONV_Q_OK;
+};
+
+int search_valid(void *ctx, const int *k) { return static_cast<SearchCtx *>(ctx)->sp->valid(k) ? 1 : 0; }
+
+double search_cost(void *ctx, const int *k) {
+    SearchCtx *s = static_cast<SearchCtx *>(ctx);
+    if (s->fatal) return -1.0;
+    s->sp->apply(k);
+    float us = 0.f;
+    const int rc = s->ts->time_sel(s->x, s->w, s->scale, s->y, s->warmup, s->reps, &us);
+    if (rc) {
+        // a launch error leaves the context usable (EUNSUPPORTED / EINVAL are host-side);
+        // a device fault is sticky: stop measuring
+        if (cudaPeekAtLastError() != cudaSuccess || rc == CONV_Q_ECUDA) s->fatal = rc;
+        return -1.0;
+    }
+    return us;
+}
+}  // namespace
+
+extern "C" int conv_q_plan_space(const conv_q_plan_t *p, int *n_knobs, int *knob_sizes, long long *n_valid) {
+    if (!p || !n_knobs || !knob_sizes) return set_err(CONV_Q_EINVAL, "NULL argument");
+    PlanSpace sp(const_cast<conv_q_plan_t *>(p));
+    *n_knobs = KB_COUNT;
+    long long total = 1;
+    for (int i = 0; i < KB_COUNT; ++i) {
+        knob_sizes[i] = sp.sizes[i];
+        total *= sp.sizes[i];
+    }
+    if (n_valid) {
+        long long nv = 0;
+        int k[KB_COUNT];
+        for (long long v = 0; v < total; ++v) {
+            long long r = v;
+            for (int i = KB_COUNT - 1; i >= 0; --i) { k[i] = (int)(r % sp.sizes[i]); r /= sp.sizes[i]; }
+            nv += sp.valid(k);
+        }
+        *n_valid = nv;
+    }
+    return CONV_Q_OK;
+}
+
+extern "C" int conv_q_plan_set_point(conv_q_plan_t *p, const int *knobs) {
+    if (!p || !knobs) return set_err(CONV_Q_EINVAL, "NULL argument");
+    PlanSpace sp(p);
+    for (int i = 0; i < KB_COUNT; ++i)
+        if (knobs[i] < 0 || knobs[i] >= sp.sizes[i]) return set_err(CONV_Q_EINVAL, "knob %d out of range", i);
+    if (!sp.valid(knobs)) return set_err(CONV_Q_EUNSUPPORTED, "not a valid point of the plan's space");
+    sp.apply(knobs);
+    p->user_sel = 1;
+    p->tuned_us = -1.f;
+    if (p->cands[p->sel].split > 1) {
+        const int rc = ensure_device();
+        if (rc) return rc;
+        return ensure_ws(p);
+    }
+    return CONV_Q_OK;
+}
+
+extern "C" int conv_q_plan_search(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y,
+                                  const conv_q_search_opts_t *opts, int warmup, int reps, float *best_us,
+                                  double *history_us) {
+    if (!p || !x || !w || !scale || !y) return set_err(CONV_Q_EINVAL, "NULL argument");
+    if (warmup < 0 || reps < 1) return set_err(CONV_Q_EINVAL, "warmup >= 0 and reps >= 1 required");
+    int rc = ensure_device();
+    if (rc) return rc;
+    PlanSpace sp(p);
+    TimingSession ts(p);
+    if (ts.rc) return ts.finish(ts.rc);
+    // saved selection + runtime knobs (restored if the search fails)
+    const int s_sel = p->sel, s_ew = p->epi_wait, s_pol = p->out_policy, s_rot = p->rotate, s_grid = p->grid_pct;
+    const unsigned s_ns = p->epi_wait_ns;
+    SearchCtx ctx{&sp, &ts, x, w, scale, y, warmup, reps};
+    int best[KB_COUNT];
+    std::vector<double> hist(opts ? std::max(opts->trials, 1) : 128);
+    const int n = conv_q_search(KB_COUNT, sp.sizes, search_valid, search_cost, &ctx, opts, best, hist.data(), nullptr);
+    rc = ts.finish(ctx.fatal ? ctx.fatal : (n < 0 ? n : CONV_Q_OK));
+    if (rc) {
+        p->sel = s_sel; p->epi_wait = s_ew; p->epi_wait_ns = s_ns; p->out_policy = s_pol; p->rotate = s_rot;
+        p->grid_pct = s_grid;
+        return rc;
+    }
+    if (history_us)
+        for (int i = 0; i < n; ++i) history_us[i] = hist[i] > 0 ? hist[i] : -1.0;
+    double bu = -1;
+    for (int i = 0; i < n; ++i)
+        if (hist[i] > 0 && (bu < 0 || hist[i] < bu)) bu = hist[i];
+    sp.apply(best);
+    p->user_sel = 1;
+    p->tuned_us = (float)bu;
+    if (best_us) *best_us = (float)bu;
+    if ((rc = ensure_ws(p))) return rc;
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        cache_load_locked();
+        g_cache[shape_key(p)] = {cand_name(p, p->sel) + runtime_suffix(p), (float)bu};
+        cache_store_locked();
+    }
+    return n;
 }
 
 // ============================================================== quantize / pack

@@ -92,6 +92,7 @@ struct conv_q_plan_s {
     int epi_wait = 0;  // CONV_Q_EPI_WAIT / _NS: how epilogue warps wait for accumulators (A/B)
     unsigned epi_wait_ns = 0;
     int out_policy = 1; // CONV_Q_OUT_POLICY: L2 hint on output stores (0 none, 1 evict_last = default: the next layer reads them, 2 evict_first)
+    int grid_pct = 100; // persistent grid as a percentage of the SMs (conv_q_plan_search's grid knob)
     unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
     unsigned long long *tl = nullptr;     // conv_q_plan_set_timeline (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
@@ -240,6 +241,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.y8 = static_cast<uint8_t *>(y);
     prm.out_row = p->out_row;
     int clusters = std::min(prm.num_units, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
+    if (p->grid_pct < 100) clusters = std::max(1, clusters * p->grid_pct / 100);   // searched grid knob
     if (HALO & 2) {   // weight-stationary: every CTA keeps one N block -> a multiple of the N-tile count
         clusters = clusters / prm.n_tiles * prm.n_tiles;
         if (clusters < 1) return set_err(CONV_Q_EUNSUPPORTED, "weight-stationary config needs n_tiles <= SMs");

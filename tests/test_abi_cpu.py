@@ -38,7 +38,7 @@ def test_library_exports_every_header_symbol(lib):
     out = os.popen(f"nm -D --defined-only {cq.LIB_PATH}").read()
     exported = set(re.findall(r" T (conv_q_\w+)", out))
     assert set(header_symbols()) <= exported
-    assert lib.conv_q_version() == 105
+    assert lib.conv_q_version() == 106
 
 
 @pytest.mark.parametrize("args,code", [
