@@ -351,7 +351,7 @@ def run_ours(args):
     g = wl.rng(spec.cfg_id, 1000)
     x_all = wl.fp16_activations(g, B_global, *tuple(net.x_in.shape[1:]))   # the global batch, this rank's shard
     net.x_in.copy_(torch.from_numpy(x_all[img0:img0 + B]))
-    tuned = {} if args.no_tune else net.tune(warmup=2, reps=5)
+    tuned = {} if args.no_tune else net.tune(warmup=2, reps=5, search_trials=args.search)
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
@@ -574,7 +574,7 @@ def run_ours(args):
             "gpu_launches": args.steps * nl,
             "clocks": clocks, "e2e": e2e, "stem": stem, "gather": gather, "parity": parity,
             "parity_ok": None if parity is None else parity["parity_ok"],
-            "tuned": len(tuned), "cpu_baseline": cpu,
+            "tuned": len(tuned), "tuning": f"search({args.search})" if args.search else "exhaustive", "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
         if args.layers_out:
@@ -812,6 +812,9 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo: several ranks may share one GPU, for testing)")
     ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--search", type=int, default=0,
+                    help="tune the conv layers by the learned search over the enlarged space (NEXT-4) with this "
+                         "many measurements per unique shape instead of timing every TileConfig")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     ap.add_argument("--dataflow", default="auto", choices=["auto", "on", "off"],
                     help="completion counters between conv launches instead of whole-grid dependencies "

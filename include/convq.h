@@ -274,6 +274,11 @@ CONVQ_API int conv_q_plan_space(const conv_q_plan_t *plan, int *n_knobs, int *kn
  * needed; its workspace is allocated here) and runtime knobs.  EINVAL: a knob
  * out of range; EUNSUPPORTED: not a valid point. */
 CONVQ_API int conv_q_plan_set_point(conv_q_plan_t *plan, const int *knobs);
+/* (ABI 1.06) The current selection as a point of conv_q_plan_space (knobs: host,
+ * n_knobs ints) -- e.g. to copy a searched pick to another plan of the same
+ * shape.  EUNSUPPORTED when the selection is not a point of the space (a
+ * split-K count outside {1,2,3,4,6,8}, a runtime knob set by environment). */
+CONVQ_API int conv_q_plan_get_point(const conv_q_plan_t *plan, int *knobs);
 
 /*
  * (ABI 1.06) conv_q_search over conv_q_plan_space, each point timed on the

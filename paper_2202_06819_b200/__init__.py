@@ -158,6 +158,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.conv_q_plan_space.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_longlong)]
     lib.conv_q_plan_set_point.restype = i
+    lib.conv_q_plan_get_point.restype = i
+    lib.conv_q_plan_get_point.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
     lib.conv_q_plan_set_point.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
     lib.conv_q_plan_search.restype = i
     lib.conv_q_plan_search.argtypes = [vp, vp, vp, vp, vp, ctypes.POINTER(SearchOpts), i, i,
@@ -343,6 +345,12 @@ class ConvPlan:
     def set_point(self, knobs):
         """Select one point of space() (conv_q_plan_set_point)."""
         _check(load().conv_q_plan_set_point(self._h, (ctypes.c_int * len(knobs))(*knobs)))
+
+    def get_point(self) -> list[int]:
+        """The current selection as a point of space() (conv_q_plan_get_point)."""
+        k = (ctypes.c_int * 16)()
+        _check(load().conv_q_plan_get_point(self._h, k))
+        return list(k[:len(self.space()[0])])
 
     def search(self, x, w, scale, y, warmup=2, reps=10, stream=None, **opts) -> dict:
         """Learned, diversity-aware search over space() on the device (conv_q_plan_search):

@@ -1056,7 +1056,6 @@ struct PlanSpace {
         const int b = base_of(k);
         if (b < 0) return false;
         const Cand &c = p->cands[b];
-        const int sms = g_num_sms > 0 ? g_num_sms : 148;
         const int split = kSplits[k[KB_SPLIT]];
         if (split > 1) {   // split-K: im2col / tiled configs, the enumeration's limits
             if (c.ws || c.halo) return false;
@@ -1065,12 +1064,8 @@ struct PlanSpace {
             if (split > std::min<int64_t>(16, num_kb / (2 * c.nsub))) return false;
             if (tiles * c.cg * 128 * c.bn * 4 > ((int64_t)64 << 20) || 16 * num_kb >= ((int64_t)1 << 31)) return false;
         }
-        if (k[KB_ROT] && c.ws) return false;   // the kernel ignores rotation for resident weights
-        if (c.ws) {   // a weight-stationary grid stays a multiple of the N-tile count
-            const int64_t n_tiles = ceil_div(p->K, c.bn);
-            if ((sms / c.cg) * kGrids[k[KB_GRID]] / 100 < n_tiles) return false;
-        }
-        return true;
+        // (a reduced weight-stationary grid keeps >= one CTA per N block: plan.cuh)
+        return !(k[KB_ROT] && c.ws);   // the kernel ignores rotation for resident weights
     }
     // select the point on the plan: TileConfig (+ a split-K variant appended to
     // the candidate list when missing) and the runtime knobs
@@ -1161,6 +1156,26 @@ extern "C" int conv_q_plan_set_point(conv_q_plan_t *p, const int *knobs) {
         return ensure_ws(p);
     }
     return CONV_Q_OK;
+}
+
+extern "C" int conv_q_plan_get_point(const conv_q_plan_t *p, int *knobs) {
+    if (!p || !knobs) return set_err(CONV_Q_EINVAL, "NULL argument");
+    PlanSpace sp(const_cast<conv_q_plan_t *>(p));
+    const Cand &c = p->cands[p->sel];
+    knobs[KB_BN] = PlanSpace::idx(sp.bns, c.bn);
+    knobs[KB_KBLK] = PlanSpace::idx(sp.kblks, std::make_pair(c.kch, c.nsub));
+    knobs[KB_CG] = PlanSpace::idx(sp.cgs, c.cg);
+    knobs[KB_MODE] = PlanSpace::idx(sp.modes, std::make_pair(c.ws, c.halo));
+    knobs[KB_DIRECT] = c.direct;
+    knobs[KB_SPLIT] = (int)(std::find(std::begin(kSplits), std::end(kSplits), c.split) - std::begin(kSplits));
+    knobs[KB_EPI] = p->epi_wait;
+    knobs[KB_POL] = p->out_policy;
+    knobs[KB_ROT] = p->rotate;
+    knobs[KB_GRID] = (int)(std::find(std::begin(kGrids), std::end(kGrids), p->grid_pct) - std::begin(kGrids));
+    for (int i = 0; i < KB_COUNT; ++i)
+        if (knobs[i] < 0 || knobs[i] >= sp.sizes[i] || (i == KB_EPI && p->epi_wait_ns != kEpiWaitNs[p->epi_wait]))
+            return set_err(CONV_Q_EUNSUPPORTED, "the current selection is not a point of the plan's space (knob %d)", i);
+    return sp.valid(knobs) ? CONV_Q_OK : set_err(CONV_Q_EUNSUPPORTED, "the current selection is not a valid point");
 }
 
 extern "C" int conv_q_plan_search(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y,

@@ -240,10 +240,11 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.y32 = static_cast<int32_t *>(y);
     prm.y8 = static_cast<uint8_t *>(y);
     prm.out_row = p->out_row;
-    int clusters = std::min(prm.num_units, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
-    if (p->grid_pct < 100) clusters = std::max(1, clusters * p->grid_pct / 100);   // searched grid knob
+    const int full = std::min(prm.num_units, g_num_sms / CG);  // persistent: one CTA (pair) per SM (pair)
+    int clusters = p->grid_pct < 100 ? std::max(1, full * p->grid_pct / 100) : full;   // searched grid knob
     if (HALO & 2) {   // weight-stationary: every CTA keeps one N block -> a multiple of the N-tile count
         clusters = clusters / prm.n_tiles * prm.n_tiles;
+        if (clusters < prm.n_tiles && full >= prm.n_tiles) clusters = prm.n_tiles;   // (a reduced grid: >= one per N block)
         if (clusters < 1) return set_err(CONV_Q_EUNSUPPORTED, "weight-stationary config needs n_tiles <= SMs");
     }
     cudaLaunchConfig_t cfg = {};

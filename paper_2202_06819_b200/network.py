@@ -169,9 +169,11 @@ class ConvNet:
             c.plan.set_deps(f[c.src:c.src + 1] if c.src >= 0 else None,
                             f[c.skip:c.skip + 1] if (c.skip is not None and c.skip >= 0) else None, f[i:i + 1])
 
-    def tune(self, warmup: int = 2, reps: int = 5) -> dict:
+    def tune(self, warmup: int = 2, reps: int = 5, search_trials: int = 0) -> dict:
         """Pick each unique shape's tile config by on-device timing (conv_q_plan_tune),
-        on the network's real buffers (the input stage is run once first)."""
+        on the network's real buffers (the input stage is run once first).
+        search_trials > 0: the conv layers use the learned search over the enlarged
+        space instead (conv_q_plan_search, NEXT-4) with that many measurements."""
         self._apply_deps(False)          # layers timed standalone: no flags
         self.run_input_stage(self.stream)
         if self.stem is not None:
@@ -181,10 +183,18 @@ class ConvNet:
         picks = {}
         for i, c in enumerate(self.convs):
             if c.key in picks:
-                c.plan.set_config(picks[c.key][0])
+                if search_trials > 0:
+                    c.plan.set_point(picks[c.key][2])   # TileConfig + runtime knobs of the searched pick
+                else:
+                    c.plan.set_config(picks[c.key][0])
             else:
-                idx = c.plan.tune(self.src_tensor(i), c.w, c.ss, c.y, warmup=warmup, reps=reps, stream=self.stream)
-                picks[c.key] = (idx, c.plan.info().config)
+                if search_trials > 0:
+                    c.plan.search(self.src_tensor(i), c.w, c.ss, c.y, warmup=warmup, reps=reps, stream=self.stream,
+                                  trials=search_trials)
+                    idx = c.plan.info().config_index
+                else:
+                    idx = c.plan.tune(self.src_tensor(i), c.w, c.ss, c.y, warmup=warmup, reps=reps, stream=self.stream)
+                picks[c.key] = (idx, c.plan.info().config, c.plan.get_point() if search_trials > 0 else None)
         self.torch.cuda.synchronize(self.device)
         if self.dataflow:
             self._apply_deps(True)

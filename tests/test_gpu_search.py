@@ -95,3 +95,11 @@ def test_search_selects_correct_point(cq, bits):
     plan.run(xd, wd, sd, y)
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy(), ref), r["config"]
+    # the pick copies to another plan of the shape (what the network does for repeated layers)
+    other = cq.ConvPlan(N, L.H, L.W, L.C, L.K, L.R, L.S, L.stride, L.pad, bits, relu=True)
+    other.set_point(plan.get_point())
+    assert other.info().config == r["config"]
+    y.fill_(0xA5)
+    other.run(xd, wd, sd, y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), ref), r["config"]

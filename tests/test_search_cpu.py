@@ -165,3 +165,29 @@ def test_plan_space_host_only(shape):
     sizes, nvalid = p.space()
     assert len(sizes) == 10 and sizes[5:] == [6, 3, 3, 2, 3]
     assert nvalid >= 10 * len(p.candidates()) and nvalid > 200
+
+
+def test_plan_point_roundtrip_host_only():
+    """get_point / set_point (no GPU for split-1 points): every valid split-1
+    point of a shape's space round-trips, and the info() name carries the
+    runtime-knob suffix when a knob is off its default."""
+    p = cq.ConvPlan(8, 28, 28, 128, 128, 3, 3, 1, 1, 8)
+    sizes, _ = p.space()
+    pt0 = p.get_point()
+    assert pt0[5:] == [0, 0, 1, 0, 0]          # split 1, spin wait, evict_last, no rotation, full grid
+    n = 0
+    for pt in itertools.product(*[range(s) for s in sizes[:5]]):
+        for rt in ([0, 0, 1, 0, 0], [0, 1, 2, 0, 1], [0, 2, 0, 1, 2]):
+            k = list(pt) + rt
+            try:
+                p.set_point(k)
+            except cq.ConvQError as e:
+                assert e.code == cq.EUNSUPPORTED
+                continue
+            assert p.get_point() == k
+            name = p.info().config
+            assert ("+" in name) == (rt != [0, 0, 1, 0, 0]), name
+            n += 1
+    assert n >= len([c for c in p.candidates() if "_k" not in c])
+    with pytest.raises(cq.ConvQError):
+        p.set_point([99] * len(sizes))
