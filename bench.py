@@ -458,6 +458,10 @@ def run_ours(args):
     in_ms = dict(zip(net.stage_names, per_launch_ms[:n_in]))
     per_layer_ms = per_launch_ms[n_in:]
 
+    # ---- graph-timed per-layer times (each conv alone: `reps` back-to-back launches in
+    # one CUDA graph, PDL between them as in the chain -- no event between launches)
+    graph_layer_us = net.time_layers(warmup=2, reps=20)
+
     # ---- e2e through the public API with host buffers (pinned), H2D + D2H inside
     e2e = None if args.no_e2e else run_e2e(args, net, stream, graph, use_graph, x_all[img0:img0 + B], world,
                                            dist, dev, B_global)
@@ -493,8 +497,12 @@ def run_ours(args):
         ideal = max(ops / (int8_peak_tops * 1e12), by / (hbm_peak * 1e9)) * 1e3
         ideal_sum += ideal
         t = per_layer_ms[i]
+        tg = graph_layer_us[i] * 1e-3
         layer_rows.append({"layer": L.name, "shape": f"{L.H}x{L.W} {L.C}->{L.K} {L.R}x{L.S} s{L.stride}",
-                           "config": c.plan.info().config, "us": round(t * 1e3, 2),
+                           "config": c.plan.info().config,
+                           "graph_us": round(graph_layer_us[i], 2), "graph_roofline_frac": round(ideal / tg, 3),
+                           "graph_tops": round(ops / (tg * 1e-3) / 1e12, 1),
+                           "us": round(t * 1e3, 2),
                            "tops": round(ops / (t * 1e-3) / 1e12, 1),
                            "frac_int8_peak": round(ops / (t * 1e-3) / 1e12 / int8_peak_tops, 3),
                            "gbs": round(by / (t * 1e-3) / 1e9, 1),
@@ -560,6 +568,8 @@ def run_ours(args):
             "conv_frac_int8_peak": round(achieved_tops / int8_peak_tops, 3),
             "int8_peak_k7_tops": k7,
             "step_roofline_frac": round(ideal_sum / sum(per_layer_ms), 3),
+            "graph_layers_sum_ms": round(sum(graph_layer_us) * 1e-3, 4),
+            "graph_step_roofline_frac": round(ideal_sum / (sum(graph_layer_us) * 1e-3), 3),
             "roofline": {"bound": "tensor", "achieved": round(achieved_tops, 1), "peak": round(int8_peak_tops, 1),
                          "unit": "TOPS", "frac": round(achieved_tops / int8_peak_tops, 4),
                          "traffic": traffic, "kernel": "conv_igemm_kernel (all conv launches of one step, conv1 incl.)",
@@ -582,9 +592,10 @@ def run_ours(args):
                 json.dump({"workload": args.workload, "layers": layer_rows, "input_stage_ms": in_ms,
                            "clocks": clocks, "tuned": tuned}, f, indent=1)
         for r in layer_rows:
-            print("  %-10s %-22s %-26s %8.1fus %7.1f TOPS %5.1f%% peak %7.1f GB/s %-6s rf=%.2f" % (
-                r["layer"], r["shape"], r["config"], r["us"], r["tops"], 100 * r["frac_int8_peak"], r["gbs"],
-                r["bound"], r["roofline_frac"]), file=sys.stderr)
+            print("  %-10s %-22s %-34s %8.1fus (graph %7.1fus) %7.1f TOPS %5.1f%% peak %7.1f GB/s %-6s rf=%.2f "
+                  "graph rf=%.2f" % (
+                      r["layer"], r["shape"], r["config"], r["us"], r["graph_us"], r["tops"], 100 * r["frac_int8_peak"],
+                      r["gbs"], r["bound"], r["roofline_frac"], r["graph_roofline_frac"]), file=sys.stderr)
     if world > 1:
         dist.destroy_process_group()
 

@@ -295,6 +295,13 @@ CONVQ_API int conv_q_plan_search(conv_q_plan_t *plan, const void *x, const void 
                                  const conv_q_search_opts_t *opts, int warmup, int reps, float *best_us,
                                  double *history_us);
 
+/* (ABI 1.06) Time the current selection exactly as conv_q_plan_tune times a
+ * candidate (graph-captured `reps` launches, 3 rounds, median) and write its
+ * per-launch microseconds to *us (host).  The per-layer table of bench.py.
+ * Synchronises the stream.  y is overwritten. */
+CONVQ_API int conv_q_plan_time(conv_q_plan_t *plan, const void *x, const void *w, const float *scale, void *y,
+                               int warmup, int reps, float *us);
+
 /* Fill *info (host memory). */
 CONVQ_API int conv_q_plan_info(const conv_q_plan_t *plan, conv_q_info_t *info);
 

@@ -157,6 +157,8 @@ def load(build_if_missing: bool = False) -> ctypes.CDLL:
     lib.conv_q_plan_space.restype = i
     lib.conv_q_plan_space.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_longlong)]
+    lib.conv_q_plan_time.restype = i
+    lib.conv_q_plan_time.argtypes = [vp, vp, vp, vp, vp, i, i, ctypes.POINTER(ctypes.c_float)]
     lib.conv_q_plan_set_point.restype = i
     lib.conv_q_plan_get_point.restype = i
     lib.conv_q_plan_get_point.argtypes = [vp, ctypes.POINTER(ctypes.c_int)]
@@ -333,6 +335,17 @@ class ConvPlan:
                                                ctypes.c_void_p(_ptr(scale)), ctypes.c_void_p(_ptr(y)),
                                                warmup, reps, arr))
         return list(arr)
+
+    def time(self, x, w, scale, y, warmup=2, reps=20, stream=None) -> float:
+        """Graph-timed microseconds per launch of the current selection (conv_q_plan_time)."""
+        self._check_buffers(x, w, scale, y)
+        lib = load()
+        _check(lib.conv_q_plan_set_stream(self._h, ctypes.c_void_p(_stream(stream))))
+        us = ctypes.c_float(0)
+        _check(lib.conv_q_plan_time(self._h, ctypes.c_void_p(_ptr(x)), ctypes.c_void_p(_ptr(w)),
+                                    ctypes.c_void_p(_ptr(scale)), ctypes.c_void_p(_ptr(y)), warmup, reps,
+                                    ctypes.byref(us)))
+        return us.value
 
     def space(self) -> tuple[list[int], int]:
         """(knob sizes, number of valid points) of the plan's enlarged schedule space (NEXT-4)."""

@@ -960,6 +960,18 @@ static int time_candidates(conv_q_plan_s *p, const void *x, const void *w, const
     return rc ? rc : best;
 }
 
+extern "C" int conv_q_plan_time(conv_q_plan_t *p, const void *x, const void *w, const float *scale, void *y,
+                                int warmup, int reps, float *us) {
+    if (!p || !us) return set_err(CONV_Q_EINVAL, "NULL argument");
+    if (warmup < 0 || reps < 1) return set_err(CONV_Q_EINVAL, "warmup >= 0 and reps >= 1 required");
+    int rc = ensure_device();
+    if (rc) return rc;
+    TimingSession t(p);
+    if (t.rc) return t.finish(t.rc);
+    rc = t.time_sel(x, w, scale, y, warmup, reps, us);
+    return t.finish(rc);
+}
+
 extern "C" int conv_q_plan_time_candidates(conv_q_plan_t *p, const void *x, const void *w, const float *scale,
                                            void *y, int warmup, int reps, float *us) {
     if (!p || !us) return set_err(CONV_Q_EINVAL, "NULL argument");

@@ -200,6 +200,19 @@ class ConvNet:
             self._apply_deps(True)
         return {str(k): v[1] for k, v in picks.items()}
 
+    def time_layers(self, warmup: int = 2, reps: int = 20) -> list[float]:
+        """Graph-timed microseconds per launch of every conv on the network's real
+        buffers (conv_q_plan_time: `reps` back-to-back launches captured in a CUDA
+        graph, PDL between them as in the chain; median of 3 replays).  Outputs are
+        rewritten with identical bytes."""
+        self._apply_deps(False)
+        us = [c.plan.time(self.src_tensor(i), c.w, c.ss, c.y, warmup=warmup, reps=reps, stream=self.stream)
+              for i, c in enumerate(self.convs)]
+        self.torch.cuda.synchronize(self.device)
+        if self.dataflow:
+            self._apply_deps(True)
+        return us
+
     # ------------------------------------------------------------- execution
     def run_input_stage(self, stream=None, ev=None):
         s = stream if stream is not None else self.stream
