@@ -603,9 +603,10 @@ def run_ours(args):
 def run_e2e(args, net, stream, graph, use_graph, x_host_np, world, dist, dev, B_global):
     """End to end through the public API with host buffers: every step copies its
     fp16 images H2D from pinned memory and its last output D2H, inside the timed
-    region.  The copies run on a copy stream, double-buffered, so step i+1's
-    upload and step i's download overlap the compute of step i (the compute is
-    the same CUDA graph as the device-only number, one per buffer pair)."""
+    region.  The copies run on two copy streams (uploads, downloads),
+    double-buffered, so step i+1's upload and step i's download overlap each
+    other and the compute of step i (the compute is the same CUDA graph as the
+    device-only number, one per buffer pair)."""
     import torch
     h_in = torch.from_numpy(x_host_np).pin_memory()
     y_last = net.outputs[-1]
@@ -622,9 +623,13 @@ def run_e2e(args, net, stream, graph, use_graph, x_host_np, world, dist, dev, B_
             net.step(stream)
         net.x_in, net.convs[-1].y = saved_x, saved_o
         graphs = [graph, g2]
-    cs = torch.cuda.Stream(dev)
+    # uploads and downloads on two copy streams (separate copy engines: the H2D of
+    # step i+1 and the D2H of step i move in opposite directions over the host link
+    # at the same time, both overlapped with step i's compute)
+    cs_in, cs_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ev_in = [torch.cuda.Event(), torch.cuda.Event()]
     ev_done = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_dl = [torch.cuda.Event(), torch.cuda.Event()]
 
     def steps(k):
         if not pipelined:                       # serial fallback (eager launches)
@@ -633,25 +638,30 @@ def run_e2e(args, net, stream, graph, use_graph, x_host_np, world, dist, dev, B_
                 net.step(stream)
                 h_out[0].copy_(y_last, non_blocking=True)
             return
-        cs.wait_stream(stream)
-        with torch.cuda.stream(cs):
+        cs_in.wait_stream(stream)
+        cs_out.wait_stream(stream)
+        with torch.cuda.stream(cs_in):
             x_bufs[0].copy_(h_in, non_blocking=True)
-        ev_in[0].record(cs)
+        ev_in[0].record(cs_in)
         for i in range(k):
             b = i % 2
             if i + 1 < k:                       # upload step i+1's input now
-                with torch.cuda.stream(cs):
+                with torch.cuda.stream(cs_in):
                     if i >= 1:
-                        cs.wait_event(ev_done[1 - b])   # step i-1 released buffer pair 1-b
+                        cs_in.wait_event(ev_done[1 - b])   # step i-1 released input buffer 1-b
                     x_bufs[1 - b].copy_(h_in, non_blocking=True)
-                ev_in[1 - b].record(cs)
+                ev_in[1 - b].record(cs_in)
             stream.wait_event(ev_in[b])
+            if i >= 2:
+                stream.wait_event(ev_dl[b])     # step i-2's result left output buffer b
             graphs[b].replay()
             ev_done[b].record(stream)
-            with torch.cuda.stream(cs):         # download step i's result
-                cs.wait_event(ev_done[b])
+            with torch.cuda.stream(cs_out):     # download step i's result
+                cs_out.wait_event(ev_done[b])
                 h_out[b].copy_(o_bufs[b], non_blocking=True)
-        stream.wait_stream(cs)
+            ev_dl[b].record(cs_out)
+        stream.wait_stream(cs_in)
+        stream.wait_stream(cs_out)
 
     steps(4)
     torch.cuda.synchronize()
@@ -668,7 +678,8 @@ def run_e2e(args, net, stream, graph, use_graph, x_host_np, world, dist, dev, B_
     return {"value": round(B_global / (te * 1e-3), 2), "unit": UNIT,
             "h2d_bytes_per_step": int(h_in.numel() * h_in.element_size()),
             "d2h_bytes_per_step": int(h_out[0].numel()), "ms_per_step": round(te, 4),
-            "copies": "double-buffered on a copy stream, overlapped with the previous step" if pipelined
+            "copies": "double-buffered; H2D and D2H on two copy streams, overlapped with each other and the compute"
+                      if pipelined
                       else "serial"}
 
 
