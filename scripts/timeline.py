@@ -47,10 +47,8 @@ epi = [w for w in range(20) if (t[4 + w] > 0).any()]
 nb = len(set(int((t[4 + w] > 0).sum()) for w in epi))
 for i in range(min(ntiles, show)):
     row = f"{i:4d} {rel(t[1][i]):9d} {rel(t[2][i]):7d} {rel(t[3][i]):9d} |"
-    for w in epi[:8]:
-        # warp w serves every NBUF-th tile: find its j-th entry for tile i
-        pass
     print(row)
+print("producer stage events: " + " ".join(str(rel(t[0][i])) for i in range(min(int((t[0] > 0).sum()), 2 * show))))
 # epilogue: per warp, its tiles' (acc, stored) pairs
 for w in epi:
     k = int((t[4 + w] > 0).sum())
