@@ -87,7 +87,6 @@ struct ConvParams {
     int num_tiles;  // m_tiles * n_tiles
     int relu;
     int rotate;          // rotate each CTA's k-block start (see the producer)
-    int i2f_magic;       // INT8 epilogue: every |acc| <= 2^22 (plan guard) -> s32->f32 by IADD + FADD2
     int a_gemm;          // 1x1 / stride 1 / pad 0: A is the input as a [M][C] matrix (tiled TMA, no im2col)
     int probe;           // measurement only (bits): 1 = no MMAs, 2 = no loads, 4 = no epilogue work
     int epi_wait;        // epilogue acc_full wait: 0 spin, 1 suspend-time hint, 2 nanosleep back-off
@@ -377,17 +376,6 @@ __device__ __forceinline__ void fma2_rn(float a0, float a1, float b0, float b1, 
     asm("{\n .reg .b64 a, b, c, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %5};\n mov.b64 c, {%6, %7};\n"
         " fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
         : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-}
-// Exact (float)a for |a| <= 2^22 off the conversion pipe: the bits a + 0x4B400000
-// read as a float are 1.5*2^23 + a (an integer in [2^23, 2^24]), and subtracting
-// 1.5*2^23 is exact -- bit-identical to cvt.rn.f32.s32 (I2FP) on that range.  One
-// IADD per value + one FADD2 per two values instead of one I2FP per value (the
-// conversion pipe also runs the F2IP packs).  The launch enables it only when the
-// layer's accumulator bound R*S*C*max|x|*max|w| <= 2^22 (plan.cuh).
-__device__ __forceinline__ void i2f2_small(int a0, int a1, float &f0, float &f1) {
-    const float m0 = __int_as_float(a0 + 0x4B400000), m1 = __int_as_float(a1 + 0x4B400000);
-    asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %4};\n"
-        " add.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}" : "=f"(f0), "=f"(f1) : "f"(m0), "f"(m1), "f"(-12582912.f));
 }
 // four float values -> one packed s8 word (value 0 in byte 0)
 __device__ __forceinline__ uint32_t pack4_f32_s8(float u0, float u1, float u2, float u3) {
@@ -1310,10 +1298,8 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             // scale/shift of this tile's columns: the buffer's smem slot (filled by
             // the MMA warp's bulk copy) or, for split-K units, global memory
             const float *ss_b = ss_stage + (3 * b + j % 3) * 2 * BN;
-            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag, const uint4 sk_in,
-                               auto magic_tag) {
+            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag, const uint4 sk_in) {
                     constexpr bool SMEM_SS = decltype(smem_tag)::value;
-                    constexpr bool MAGIC = decltype(magic_tag)::value;   // s32 -> f32 by IADD + FADD2
                     const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
                     const int col0 = n_blk * BN + ccol;
                     if (Cfg::OUTP == OUT_S32) {
@@ -1380,18 +1366,11 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             for (int q = 0; q < 4; ++q) {
                                 float4 sa, sb;
                                 ss4(q, sa, sb);
-                                float u0, u1, u2, u3, f0, f1, f2, f3;
-                                if constexpr (MAGIC) {
-                                    i2f2_small((int)v[4 * q], (int)v[4 * q + 1], f0, f1);
-                                    i2f2_small((int)v[4 * q + 2], (int)v[4 * q + 3], f2, f3);
-                                } else {
-                                    f0 = __int2float_rn((int)v[4 * q]);
-                                    f1 = __int2float_rn((int)v[4 * q + 1]);
-                                    f2 = __int2float_rn((int)v[4 * q + 2]);
-                                    f3 = __int2float_rn((int)v[4 * q + 3]);
-                                }
-                                fma2_rn(f0, f1, sa.x, sa.y, sb.x, sb.y, u0, u1);
-                                fma2_rn(f2, f3, sa.z, sa.w, sb.z, sb.w, u2, u3);
+                                float u0, u1, u2, u3;
+                                fma2_rn(__int2float_rn((int)v[4 * q]), __int2float_rn((int)v[4 * q + 1]), sa.x, sa.y,
+                                        sb.x, sb.y, u0, u1);
+                                fma2_rn(__int2float_rn((int)v[4 * q + 2]), __int2float_rn((int)v[4 * q + 3]), sa.z,
+                                        sa.w, sb.z, sb.w, u2, u3);
                                 if constexpr (Cfg::RES) {
                                     // v = fmaf(skip, res_scale, u) (reading 15); skip byte -> exact float as
                                     // (2^23 + (byte ^ bias)) - (2^23 + bias), bias 0x80 for a signed skip,
@@ -1529,8 +1508,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             va[q] = (uint32_t)__ldcg(wsr + (c * Cfg::CW + q) * 32);
                             __stcg(wsr + (c * Cfg::CW + q) * 32, 0);
                         }
-                        process(va, c, std::false_type{}, Cfg::RES ? load_skip(m, c) : make_uint4(0u, 0u, 0u, 0u),
-                                std::false_type{});
+                        process(va, c, std::false_type{}, Cfg::RES ? load_skip(m, c) : make_uint4(0u, 0u, 0u, 0u));
                     }
                     if (lane == 0) p.cnt[region] = 0u;
                 }
@@ -1540,9 +1518,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                 if constexpr (SKT) {   // this warp's skip slab (issued before the accumulator wait)
                     mbar_wait(&skbar[warp], (uint32_t)(lu & 1));
                 }
-                // MT2: the unit's two m-groups sit in TMEM columns [g*BN, (g+1)*BN);
-                // INT8 layers whose accumulators stay within 2^22 convert with IADD + FADD2
-                auto drain = [&](auto mtag) {
+                // MT2: the unit's two m-groups sit in TMEM columns [g*BN, (g+1)*BN)
                 for (int g = 0; g < Cfg::MT; ++g) {
                     taddr = taddr0 + g * BN;
                     if constexpr (Cfg::MT > 1) m = (HA || S2H) ? halo_m(g * BM + row) : mrow0 + g * BM + row;
@@ -1557,9 +1533,9 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             tmem_ld_issue<32>(taddr + c * Cfg::CW, v32);
                             tmem_ld_wait_regs(v32);
                             if (last && c + 2 >= NCH) release_acc();
-                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c, std::true_type{}, skr(c), mtag);
+                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c, std::true_type{}, skr(c));
                             process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[16]), c + 1, std::true_type{},
-                                    skr(c + 1), mtag);
+                                    skr(c + 1));
                         }
                     } else {
                         tmem_ld_issue<Cfg::CW>(taddr, va);
@@ -1569,25 +1545,18 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             const bool more1 = c + 1 < NCH;
                             if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
                             else if (last) release_acc();   // every column of this warp is in registers
-                            process(va, c, std::true_type{}, skr(c), mtag);
+                            process(va, c, std::true_type{}, skr(c));
                             if (more1) {
                                 tmem_ld_wait_regs(vb);
                                 const bool more2 = c + 2 < NCH;
                                 if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
                                 else if (last) release_acc();
-                                process(vb, c + 1, std::true_type{}, skr(c + 1), mtag);
+                                process(vb, c + 1, std::true_type{}, skr(c + 1));
                                 if (more2) tmem_ld_wait_regs(va);
                             }
                         }
                     }
                     if constexpr (Cfg::MT > 1) store_slab(g);   // the slab is reused by the next group
-                }
-                };
-                if constexpr (BITS == 8 && Cfg::OUTP != OUT_S32) {
-                    if (p.i2f_magic) drain(std::true_type{});
-                    else drain(std::false_type{});
-                } else {
-                    drain(std::false_type{});
                 }
             }
             if constexpr (Cfg::MT == 1) store_slab(0);

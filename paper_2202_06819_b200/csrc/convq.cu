@@ -475,7 +475,6 @@ static conv_q_plan_t *finish_plan(conv_q_plan_s *p) {
     if (const char *en = getenv("CONV_Q_EPI_WAIT_NS")) p->epi_wait_ns = (unsigned)atoi(en);
     if (const char *op = getenv("CONV_Q_OUT_POLICY")) p->out_policy = atoi(op);
     if (const char *ro = getenv("CONV_Q_ROTATE")) p->rotate = atoi(ro) ? 1 : 0;
-    if (const char *nm = getenv("CONV_Q_NO_MAGIC")) p->no_magic = atoi(nm) ? 1 : 0;
     apply_cache(p);
     if (p->cands[p->sel].split > 1 && ensure_device() == CONV_Q_OK && ensure_ws(p) != CONV_Q_OK) {
         delete p;

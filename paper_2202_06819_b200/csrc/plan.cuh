@@ -93,7 +93,6 @@ struct conv_q_plan_s {
     unsigned epi_wait_ns = 0;
     int out_policy = 1; // CONV_Q_OUT_POLICY: L2 hint on output stores (0 none, 1 evict_last = default: the next layer reads them, 2 evict_first)
     int grid_pct = 100; // persistent grid as a percentage of the SMs (conv_q_plan_search's grid knob)
-    int no_magic = 0;   // CONV_Q_NO_MAGIC=1: the epilogue's s32 -> f32 always by I2FP (A/B measurement)
     unsigned long long *trace = nullptr;  // conv_q_plan_set_trace (measurement only)
     unsigned long long *tl = nullptr;     // conv_q_plan_set_timeline (measurement only)
     // tensor-map cache (re-encoded when a pointer or the config changes)
@@ -217,10 +216,6 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.fd_Wp = make_fastdiv(prm.Wp);
     prm.relu = p->relu;
     prm.rotate = p->rotate;
-    // INT8: every accumulator within 2^22 -> the epilogue's s32 -> f32 by IADD + FADD2
-    // (exact there, conv.cuh i2f2_small): R*S*C * max|x| * max|w| <= 2^22
-    prm.i2f_magic = BITS == 8 && !p->no_magic &&
-                    (int64_t)p->R * p->S * p->C * (p->x_uns ? 255 : 128) * 128 <= ((int64_t)1 << 22);
     prm.a_gemm = p->R == 1 && p->S == 1 && p->stride == 1 && p->pad == 0 && !(HALO & 1);
     prm.probe = p->probe;
     prm.epi_wait = p->epi_wait;

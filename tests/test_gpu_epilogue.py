@@ -1,14 +1,15 @@
-"""The INT8 epilogue's two s32 -> f32 conversions (-m gpu): I2FP, and IADD +
-FADD2 (conv.cuh i2f2_small) for layers whose accumulators provably stay within
-2^22 (R*S*C*max|x|*max|w| <= 2^22, plan.cuh).  Both must give the oracle's bytes
-(reading 5: s32 -> f32 RN, one FMA, RNE) -- at the boundary accumulators
-+-2^22, at every candidate, signed and unsigned activations, and next to a
-layer just past the guard (I2FP)."""
+"""The INT8 epilogue's s32 -> f32 -> requant at extreme accumulators (-m gpu):
+1x1 layers whose codes sit at the range ends so the accumulators reach
++-2^22 (C = 256 signed: every |acc| <= 2^22 with equality), beyond 2^22, and
+with unsigned activations -- every candidate, ReLU on and off, against the
+oracle's bytes (reading 5: s32 -> f32 RN, one FMA, RNE).
+
+(An IADD + FADD2 conversion, exact for |acc| <= 2^22, was measured as a
+replacement for I2FP on such layers: slower -- DESIGN.md negative results.)"""
 import numpy as np
 import pytest
 
 import oracle
-import workloads as wl
 from oracle import check
 
 pytestmark = pytest.mark.gpu
@@ -28,34 +29,30 @@ def dev(a):
 
 
 def _extreme_inputs(g, N, H, W, C, K, x_uns):
-    """Codes at the extremes (plus a random share) so accumulators reach +-2^22."""
-    lo = 0 if x_uns else -128
-    hi = 255 if x_uns else 127
+    """Codes at the extremes (plus random pixels) so accumulators reach the bound."""
+    lo, hi = (0, 255) if x_uns else (-128, 127)
     x = g.choice(np.array([lo, hi, lo, lo], np.int64), size=(N, H, W, C))
-    x[0, 0, 0, :] = lo if not x_uns else hi                    # one pixel all extreme
-    x[..., : C // 8] = g.integers(lo, hi + 1, size=x[..., : C // 8].shape)
-    w = g.choice(np.array([-128, 127, -128], np.int64), size=(K, 1, 1, C))
-    w[0] = -128                                                  # channel 0 all -128: acc = C*lo*-128
+    x[:, 1:3] = g.integers(lo, hi + 1, size=x[:, 1:3].shape)       # two random rows
+    x[0, 0, 0, :] = hi if x_uns else lo                           # one pixel all extreme
+    w = g.choice(np.array([-128, 127, -128], np.int64), size=(K, C))
+    w[0] = -128                                                   # channel 0: acc = C * x * -128
     w[1] = 127
     w[2:8] = g.integers(-128, 128, size=w[2:8].shape)
-    xb = (x.astype(np.int64) & 0xFF).astype(np.uint8)
-    wb = (w.astype(np.int64) & 0xFF).astype(np.uint8)
-    acc = np.einsum("nhwc,kc->nhwk", x, w[:, 0, 0, :])
+    xb = (x & 0xFF).astype(np.uint8)
+    wb = (w & 0xFF).astype(np.uint8).reshape(K, 1, 1, C)
+    acc = np.einsum("nhwc,kc->nhwk", x, w)                        # 1x1 conv == explicit GEMM
     return xb, wb, acc
 
 
-@pytest.mark.parametrize("C,x_uns,magic", [(256, False, True), (128, True, True), (288, False, False),
-                                           (160, True, False), (64, False, True)])
-def test_conversion_boundary_every_candidate(cq, C, x_uns, magic):
+@pytest.mark.parametrize("C,x_uns", [(256, False), (128, True), (288, False), (160, True), (64, False)])
+def test_extreme_accumulators_every_candidate(cq, C, x_uns):
     N, H, W, K = 2, 9, 7, 128
     g = np.random.default_rng(2200 + C)
     x, w, acc = _extreme_inputs(g, N, H, W, C, K, x_uns)
-    bound = C * (255 if x_uns else 128) * 128
-    assert (bound <= 1 << 22) == magic
-    if magic:
-        assert np.abs(acc).max() <= 1 << 22
+    amax = int(np.abs(acc).max())
+    assert amax == C * (255 if x_uns else 128) * 128              # the layer's bound itself is reached
     if C == 256 and not x_uns:
-        assert np.abs(acc).max() == 1 << 22                      # the boundary itself is exercised
+        assert amax == 1 << 22
     # scales that keep the codes mostly unsaturated, fractional products (ties exercised)
     sc = (2.0 ** -15 * (1 + g.integers(0, 64, K) / 64.0)).astype(np.float32)
     sh = g.uniform(-2, 2, K).astype(np.float32)
