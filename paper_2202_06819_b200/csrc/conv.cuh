@@ -1298,7 +1298,12 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             // scale/shift of this tile's columns: the buffer's smem slot (filled by
             // the MMA warp's bulk copy) or, for split-K units, global memory
             const float *ss_b = ss_stage + (3 * b + j % 3) * 2 * BN;
-            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag, const uint4 sk_in) {
+            // process(): requantize + pack one chunk (CW columns) -> its 16 packed bytes
+            // (S32 mode: stores the raw accumulators itself); put(): store a packed chunk.
+            // Split so a caller can compute the next chunk -- whose scale/shift LDS would
+            // otherwise be ordered behind this chunk's staging STS (possible smem alias)
+            // -- before storing this one.
+            auto process = [&](const uint32_t (&v)[Cfg::CW], const int c, auto smem_tag, const uint4 sk_in) -> uint4 {
                     constexpr bool SMEM_SS = decltype(smem_tag)::value;
                     const int ccol = half * Cfg::EPI_COLS + c * Cfg::CW;   // column within the tile
                     const int col0 = n_blk * BN + ccol;
@@ -1439,6 +1444,12 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 pk = make_uint4(pack8_sat_s4(r), pack8_sat_s4(r + 8), pack8_sat_s4(r + 16),
                                                 pack8_sat_s4(r + 24));
                         }
+                        return pk;
+                    }
+                    return make_uint4(0u, 0u, 0u, 0u);
+            };
+            auto put = [&](const int c, const uint4 pk) {
+                    if constexpr (Cfg::OUTP != OUT_S32) {
                         const int sbyte = c * 16;                 // byte within this warp's slab row
                         if constexpr (Cfg::OUTP == OUT_TMA) {
                             if (c == 0) {   // the slab must have been read out by this warp's previous store
@@ -1508,7 +1519,7 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             va[q] = (uint32_t)__ldcg(wsr + (c * Cfg::CW + q) * 32);
                             __stcg(wsr + (c * Cfg::CW + q) * 32, 0);
                         }
-                        process(va, c, std::false_type{}, Cfg::RES ? load_skip(m, c) : make_uint4(0u, 0u, 0u, 0u));
+                        put(c, process(va, c, std::false_type{}, Cfg::RES ? load_skip(m, c) : make_uint4(0u, 0u, 0u, 0u)));
                     }
                     if (lane == 0) p.cnt[region] = 0u;
                 }
@@ -1533,9 +1544,13 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             tmem_ld_issue<32>(taddr + c * Cfg::CW, v32);
                             tmem_ld_wait_regs(v32);
                             if (last && c + 2 >= NCH) release_acc();
-                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c, std::true_type{}, skr(c));
-                            process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[16]), c + 1, std::true_type{},
-                                    skr(c + 1));
+                            // both chunks' requant (and scale/shift loads) before either staging store
+                            const uint4 pk0 = process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[0]), c,
+                                                      std::true_type{}, skr(c));
+                            const uint4 pk1 = process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[16]), c + 1,
+                                                      std::true_type{}, skr(c + 1));
+                            put(c, pk0);
+                            put(c + 1, pk1);
                         }
                     } else {
                         tmem_ld_issue<Cfg::CW>(taddr, va);
@@ -1545,13 +1560,13 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                             const bool more1 = c + 1 < NCH;
                             if (more1) tmem_ld_issue<Cfg::CW>(taddr + (c + 1) * Cfg::CW, vb);
                             else if (last) release_acc();   // every column of this warp is in registers
-                            process(va, c, std::true_type{}, skr(c));
+                            put(c, process(va, c, std::true_type{}, skr(c)));
                             if (more1) {
                                 tmem_ld_wait_regs(vb);
                                 const bool more2 = c + 2 < NCH;
                                 if (more2) tmem_ld_issue<Cfg::CW>(taddr + (c + 2) * Cfg::CW, va);
                                 else if (last) release_acc();
-                                process(vb, c + 1, std::true_type{}, skr(c + 1));
+                                put(c + 1, process(vb, c + 1, std::true_type{}, skr(c + 1)));
                                 if (more2) tmem_ld_wait_regs(va);
                             }
                         }
