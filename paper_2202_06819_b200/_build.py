@@ -65,9 +65,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(OBJ, exist_ok=True)
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    jobs = max(1, min(len(srcs), os.cpu_count() or 1))
+    # per-object staleness: an object is rebuilt when its source, any header or
+    # this script is newer (a host-only change to convq.cu recompiles convq.o only)
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "convq.h"), __file__]
+
+    def obj_of(src):
+        return os.path.join(OBJ, os.path.splitext(os.path.basename(src))[0] + ".o")
+
+    todo = [s for s in srcs if force or _stale(obj_of(s), [s] + headers)]
+    jobs = max(1, min(len(todo), os.cpu_count() or 1))
     with cf.ThreadPoolExecutor(jobs) as ex:
-        results = list(ex.map(lambda s: _compile(s, verbose), srcs))
+        built = dict(zip(todo, ex.map(lambda s: _compile(s, verbose), todo)))
+    results = [built.get(s, (obj_of(s), "")) for s in srcs]
     if verbose:
         for _, log in results:
             sys.stderr.write(log)

@@ -670,16 +670,20 @@ static int encode_maps(conv_q_plan_s *p, const void *x, const void *w, void *y) 
     // "genuine" data of PAPER.md section 3.1; OOB (padding) is zero-filled.
     const int mt = (c.halo & 8) ? 2 : 1;   // MT2: the box covers two 128-row m-groups
     if (c.halo & 4) {
-        // A (s2d window halo): tiled box {16 B, Wp stored pixels, halo rows, 1}
-        // of the stored s2d tensor [N][H2][Wp][16 B] at (0, 0, p0 - PL, n); rows
-        // outside [0, H2) are zero-filled, columns are in bounds by construction
+        // A (s2d window halo): the box is halo_rows WHOLE stored rows of the s2d
+        // tensor [N][H2][Wp][16 B] at (0, 0, p0 - PL, n) -- every column is in
+        // bounds by construction (zero borders are stored), rows outside [0, H2)
+        // are zero-filled.  A stored row is Wp*16 contiguous bytes, so the map
+        // views it as ONE inner row of 2*Wp 8-byte elements ({2 Wp, 1, H2, N}):
+        // the TMA moves halo_rows long rows instead of halo_rows*Wp 16-byte rows
+        // (same bytes, same smem image; 2 Wp <= 256 as Wp <= BM)
         const int Wp = p->xs_W;
         const int halo_rows = (int)ceil_div(mt * BM + (p->R - 1) * Wp + 3, Wp);
-        cuuint64_t dims[4] = {16, (cuuint64_t)Wp, (cuuint64_t)p->H, (cuuint64_t)p->N};
-        cuuint64_t strides[3] = {16, (cuuint64_t)16 * Wp, (cuuint64_t)16 * Wp * p->H};
-        cuuint32_t box[4] = {16, (cuuint32_t)Wp, (cuuint32_t)halo_rows, 1};
+        cuuint64_t dims[4] = {(cuuint64_t)2 * Wp, 1, (cuuint64_t)p->H, (cuuint64_t)p->N};
+        cuuint64_t strides[3] = {(cuuint64_t)16 * Wp, (cuuint64_t)16 * Wp, (cuuint64_t)16 * Wp * p->H};
+        cuuint32_t box[4] = {(cuuint32_t)(2 * Wp), 1, (cuuint32_t)halo_rows, 1};
         cuuint32_t estr[4] = {1, 1, 1, 1};
-        CUresult r = g_encode_tiled(&p->tm_a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(x), dims, strides,
+        CUresult r = g_encode_tiled(&p->tm_a, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, const_cast<void *>(x), dims, strides,
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_err(CONV_Q_ECUDA, "cuTensorMapEncodeTiled(x s2d halo) failed: %d", (int)r);
