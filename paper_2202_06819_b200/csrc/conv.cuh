@@ -155,7 +155,10 @@ constexpr int OUT_U = 16;
 #ifndef CONVQ_EPI_WG8
 #define CONVQ_EPI_WG8 4
 #endif
-constexpr int epi_warpgroups(int bits) { return bits == 8 ? CONVQ_EPI_WG8 : 2; }
+#ifndef CONVQ_EPI_WG4
+#define CONVQ_EPI_WG4 2
+#endif
+constexpr int epi_warpgroups(int bits) { return bits == 8 ? CONVQ_EPI_WG8 : CONVQ_EPI_WG4; }
 constexpr int tmem_buffers(int bits, int bn) {
     return (512 / bn) < epi_warpgroups(bits) ? ((512 / bn) < 4 ? 512 / bn : 4)
                                               : (epi_warpgroups(bits) < 4 ? epi_warpgroups(bits) : 4);
