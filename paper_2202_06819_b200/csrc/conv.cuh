@@ -380,6 +380,11 @@ __device__ __forceinline__ void fma2_rn(float a0, float a1, float b0, float b1, 
         " fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
         : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
+// two-wide RN multiply (mul.rn.f32x2)
+__device__ __forceinline__ void mul2_rn(float a0, float a1, float b, float &d0, float &d1) {
+    asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %4};\n"
+        " mul.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}" : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b));
+}
 // four float values -> one packed s8 word (value 0 in byte 0)
 __device__ __forceinline__ uint32_t pack4_f32_s8(float u0, float u1, float u2, float u3) {
     return pack2_f32_s8(u1, u0, pack2_f32_s8(u3, u2, 0u));
@@ -1408,17 +1413,23 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 float4 sa, sb;
                                 ss4(q, sa, sb);
                                 if constexpr (Cfg::RELU4) {
-                                    // ReLU epilogue: clamp(rne(u), 0, 255) in one F2I.U8 (4x the s32 F2I
-                                    // rate), then min with the top code (7 signed / 15 unsigned, reading 16)
-                                    float u0, u1, u2, u3;
-                                    fma2_rn(__int2float_rn((int)v[4 * q] >> 8), __int2float_rn((int)v[4 * q + 1] >> 8),
-                                            sa.x, sa.y, sb.x, sb.y, u0, u1);
-                                    fma2_rn(__int2float_rn((int)v[4 * q + 2] >> 8), __int2float_rn((int)v[4 * q + 3] >> 8),
-                                            sa.z, sa.w, sb.z, sb.w, u2, u3);
-                                    r[4 * q] = min(f2u8_rn(u0), p.code_hi);
-                                    r[4 * q + 1] = min(f2u8_rn(u1), p.code_hi);
-                                    r[4 * q + 2] = min(f2u8_rn(u2), p.code_hi);
-                                    r[4 * q + 3] = min(f2u8_rn(u3), p.code_hi);
+                                    // ReLU epilogue: the MMA holds 256*acc (a4), and (float)(256 acc) * 2^-8
+                                    // == (float)acc exactly (power-of-two scaling commutes with RN, no
+                                    // underflow for integers), so one I2FP + half an FMUL2 replace the
+                                    // shift; clamp(rne(u), 0, 255) in one F2I.U8 (4x the s32 F2I rate),
+                                    // and the nibble pack below saturates at the top code (7 signed /
+                                    // 15 unsigned, reading 16) -- no separate min
+                                    float f0, f1, f2, f3, u0, u1, u2, u3;
+                                    mul2_rn(__int2float_rn((int)v[4 * q]), __int2float_rn((int)v[4 * q + 1]), 0.00390625f,
+                                            f0, f1);
+                                    mul2_rn(__int2float_rn((int)v[4 * q + 2]), __int2float_rn((int)v[4 * q + 3]),
+                                            0.00390625f, f2, f3);
+                                    fma2_rn(f0, f1, sa.x, sa.y, sb.x, sb.y, u0, u1);
+                                    fma2_rn(f2, f3, sa.z, sa.w, sb.z, sb.w, u2, u3);
+                                    r[4 * q] = f2u8_rn(u0);
+                                    r[4 * q + 1] = f2u8_rn(u1);
+                                    r[4 * q + 2] = f2u8_rn(u2);
+                                    r[4 * q + 3] = f2u8_rn(u3);
                                 } else if constexpr (Cfg::RES) {
                                     // codes 4q..4q+3 = nibbles 4(q%2).. of skip word q/2; nibble -> exact
                                     // float as (2^23 + (nib ^ bias)) - (2^23 + bias), bias 8 for a signed
@@ -1440,7 +1451,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                     r[4 * q + 3] = requant_int((int)v[4 * q + 3] >> 8, sa.w, sb.w, lo);
                                 }
                             }
-                            if (Cfg::RELU4 || (Cfg::RES && p.y_uns))   // codes in [0, hi]: unsigned packing
+                            if (Cfg::RELU4 && !p.y_uns)   // ReLU codes in [0, 255] -> saturated at 7 by the s4 pack
+                                pk = make_uint4(pack8_sat_s4(r), pack8_sat_s4(r + 8), pack8_sat_s4(r + 16),
+                                                pack8_sat_s4(r + 24));
+                            else if (Cfg::RELU4 || (Cfg::RES && p.y_uns))   // codes >= 0: unsigned packing (top 15)
                                 pk = make_uint4(pack8_sat_u4(r), pack8_sat_u4(r + 8), pack8_sat_u4(r + 16),
                                                 pack8_sat_u4(r + 24));
                             else
