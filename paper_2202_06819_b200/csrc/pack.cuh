@@ -375,6 +375,65 @@ __global__ void __launch_bounds__(256) maxpool3s2_rows_kernel(const uint4 *__res
     };
     auto vmax4 = [&](uint4 a, uint4 b) { return make_uint4(vmax(a.x, b.x), vmax(a.y, b.y), vmax(a.z, b.z), vmax(a.w, b.w)); };
     const int total = N * groups * Q * vpp;     // < 2^31 (checked on the host)
+    // s8 / u8 codes: bytes widened to 16-bit lanes (sign- or zero-extended, two
+    // PRMT per word) so every max is ONE native VIMNMX.{S,U}16x2 per two codes
+    // instead of the 6-instruction byte-SIMD emulation of __vmax{s,u}4; one PRMT
+    // per output word packs the low bytes back
+    if constexpr (BITS == 8) {
+        constexpr uint32_t SEL_E = UNS ? 0x4240u : 0xA280u;   // bytes 0, 2 -> 16-bit lanes
+        constexpr uint32_t SEL_O = UNS ? 0x4341u : 0xB391u;   // bytes 1, 3 -> 16-bit lanes
+        auto mx = [](uint32_t a, uint32_t b) -> uint32_t { return UNS ? __vmaxu2(a, b) : __vmaxs2(a, b); };
+        for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
+            const int pix = fd_vpp.div(o);
+            const int v = o - pix * vpp;
+            const int t = fd_q.div(pix);
+            const int q = pix - t * Q;
+            const int n = fd_g.div(t);
+            const int p0 = (t - n * groups) * T;
+            const int w0 = 2 * q - pad;
+            const uint4 *base = x + (int64_t)n * H * W * vpp + v;
+            constexpr int NR = 2 * T + 1;
+            uint4 a[NR][3];
+#pragma unroll
+            for (int i = 0; i < NR; ++i) {
+                const int h = 2 * p0 - pad + i;
+#pragma unroll
+                for (int s = 0; s < 3; ++s) {
+                    const int w = w0 + s;
+                    a[i][s] = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(base + ((int64_t)h * W + w) * vpp)
+                                                                    : make_uint4(MINV, MINV, MINV, MINV);
+                }
+            }
+            // row maxima in widened form: hm[i][2k] = even bytes of word k, hm[i][2k+1] = odd bytes
+            uint32_t hm[NR][8];
+#pragma unroll
+            for (int i = 0; i < NR; ++i)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t w_0 = (&a[i][0].x)[k], w_1 = (&a[i][1].x)[k], w_2 = (&a[i][2].x)[k];
+                    hm[i][2 * k] = mx(mx(__byte_perm(w_0, 0u, SEL_E), __byte_perm(w_1, 0u, SEL_E)),
+                                      __byte_perm(w_2, 0u, SEL_E));
+                    hm[i][2 * k + 1] = mx(mx(__byte_perm(w_0, 0u, SEL_O), __byte_perm(w_1, 0u, SEL_O)),
+                                          __byte_perm(w_2, 0u, SEL_O));
+                }
+#pragma unroll
+            for (int kk = 0; kk < T; ++kk) {
+                const int p = p0 + kk;
+                if (p < P) {
+                    uint32_t r[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t e = mx(mx(hm[2 * kk][2 * k], hm[2 * kk + 1][2 * k]), hm[2 * kk + 2][2 * k]);
+                        const uint32_t od = mx(mx(hm[2 * kk][2 * k + 1], hm[2 * kk + 1][2 * k + 1]),
+                                               hm[2 * kk + 2][2 * k + 1]);
+                        r[k] = __byte_perm(e, od, 0x6240);   // bytes: e0, od0, e2, od2
+                    }
+                    y[(((int64_t)n * P + p) * Q + q) * vpp + v] = make_uint4(r[0], r[1], r[2], r[3]);
+                }
+            }
+        }
+        return;
+    }
     for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < total; o += gridDim.x * blockDim.x) {
         const int pix = fd_vpp.div(o);
         const int v = o - pix * vpp;
