@@ -158,6 +158,10 @@ constexpr int OUT_U = 16;
 #ifndef CONVQ_EPI_WG4
 #define CONVQ_EPI_WG4 2
 #endif
+// INT8 epilogue: double-buffered 32-column TMEM loads (A/B build option)
+#ifndef CONVQ_TMEM_PIPE
+#define CONVQ_TMEM_PIPE 0
+#endif
 constexpr int epi_warpgroups(int bits) { return bits == 8 ? CONVQ_EPI_WG8 : CONVQ_EPI_WG4; }
 constexpr int tmem_buffers(int bits, int bn) {
     return (512 / bn) < epi_warpgroups(bits) ? ((512 / bn) < 4 ? 512 / bn : 4)
@@ -1552,7 +1556,30 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     if constexpr (Cfg::MT > 1) m = (HA || S2H) ? halo_m(g * BM + row) : mrow0 + g * BM + row;
                     const bool last = g == Cfg::MT - 1;
                     auto skr = [&](int c) -> uint4 { return skp[Cfg::RES && !SKT ? g : 0][Cfg::RES && !SKT ? c : 0]; };
-                    if constexpr (BITS == 8 && NCH % 2 == 0) {
+                    if constexpr (BITS == 8 && NCH % 2 == 0 && CONVQ_TMEM_PIPE && NCH > 2) {
+                        // 32 columns per tcgen05.ld, double-buffered: the next 32 columns'
+                        // load is in flight while these are requantized (tcgen05.wait::ld
+                        // waits for every outstanding load, so the wait follows the work)
+                        uint32_t v32[2][32];
+                        tmem_ld_issue<32>(taddr, v32[0]);
+                        tmem_ld_wait_regs(v32[0]);
+#pragma unroll
+                        for (int c = 0; c < NCH; c += 2) {
+                            const int cur = (c / 2) & 1;
+                            const bool more = c + 2 < NCH;
+                            if (more) tmem_ld_issue<32>(taddr + (c + 2) * Cfg::CW, v32[cur ^ 1]);
+                            const uint4 pk0 = process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[cur][0]), c,
+                                                      std::true_type{}, skr(c));
+                            const uint4 pk1 = process(reinterpret_cast<const uint32_t(&)[Cfg::CW]>(v32[cur][16]), c + 1,
+                                                      std::true_type{}, skr(c + 1));
+                            put(c, pk0);
+                            put(c + 1, pk1);
+                            if (more) {
+                                tmem_ld_wait_regs(v32[cur ^ 1]);
+                                if (last && c + 4 >= NCH) release_acc();   // every column of this warp is in registers
+                            }
+                        }
+                    } else if constexpr (BITS == 8 && NCH % 2 == 0) {
                         // 32 columns per tcgen05.ld (two 16-byte output pieces): half
                         // the exposed TMEM-load round trips of a 16-column loop
                         uint32_t v32[32];
