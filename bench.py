@@ -351,7 +351,7 @@ def run_ours(args):
     g = wl.rng(spec.cfg_id, 1000)
     x_all = wl.fp16_activations(g, B_global, *tuple(net.x_in.shape[1:]))   # the global batch, this rank's shard
     net.x_in.copy_(torch.from_numpy(x_all[img0:img0 + B]))
-    tuned = {} if args.no_tune else net.tune(warmup=2, reps=5, search_trials=args.search)
+    tuned = {} if args.no_tune else net.tune(warmup=2, reps=10, search_trials=args.search)
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
