@@ -1414,6 +1414,23 @@ extern "C" int conv_q_s2d_quantize(const conv_q_plan_t *p, const void *x_fp16, f
     const int grid = (int)ceil_div(total, 256);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int PL = p->pad;
+    // RGB with W % 8 == 0 and a 16-byte aligned image: 4 s2d columns per thread,
+    // 16-byte loads (rows are 6*W bytes, a multiple of 48; the stored row has
+    // PL + W/2 + right-border columns, every border column written as zeros)
+    if (p->o_C == 3 && p->o_W % 8 == 0 && (reinterpret_cast<uintptr_t>(x_fp16) & 15) == 0 &&
+        p->xs_W >= PL + p->o_W / 2) {
+        const int G = p->o_W / 8, TR = G + (p->xs_W - p->o_W / 2);
+        const int64_t tv = (int64_t)p->N * p->H * TR;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)ceil_div(tv, 256));
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        auto kv = p->bits == 8 ? s2d_quantize_c3v_kernel<8> : s2d_quantize_c3v_kernel<4>;
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, kv, static_cast<const __half *>(x_fp16), static_cast<uint4 *>(xs), p->N,
+                                    p->o_H, p->o_W, p->H, p->xs_W, PL, G, TR, inv_scale, make_fastdiv(TR),
+                                    make_fastdiv(p->H)));
+        return CONV_Q_OK;
+    }
     // (even W keeps every row's 6*W-byte offset 4-byte aligned)
     const bool c3 = p->o_C == 3 && p->o_W % 2 == 0 && (reinterpret_cast<uintptr_t>(x_fp16) & 3) == 0;
     auto kern = p->bits == 8 ? (c3 ? s2d_quantize_kernel<8, true> : s2d_quantize_kernel<8, false>)

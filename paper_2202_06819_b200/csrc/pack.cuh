@@ -240,6 +240,70 @@ __global__ void __launch_bounds__(256) s2d_quantize_kernel(const __half *__restr
     }
 }
 
+// RGB fast path with 16-byte loads (C == 3, W % 8 == 0, x 16-byte aligned): one
+// thread per 4 consecutive s2d columns of a row -- 8 input pixels x 3 halves =
+// 48 contiguous bytes per input row = three 16-byte loads (instead of a thread
+// per s2d column with three 4-byte loads per row) -- and 4 stored 16-byte
+// pixels; the remaining threads of the row write its zero border columns.
+// Codes exactly as s2d_quantize_kernel (same quant1, same layout).
+template <int BITS>
+__global__ void __launch_bounds__(256) s2d_quantize_c3v_kernel(const __half *__restrict__ x, uint4 *__restrict__ y,
+                                                              int N, int H, int W, int H2, int XW, int PL, int G,
+                                                              int TR, float inv_scale, FastDiv fd_tr, FastDiv fd_h2) {
+    constexpr int CP = BITS == 8 ? 4 : 8;
+    const float lo = -(float)(1 << (BITS - 1)), hi = (float)((1 << (BITS - 1)) - 1);
+    const int total = N * H2 * TR;              // TR = G groups + border columns per row (< 2^31, host-checked)
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= total) return;
+    const int t = fd_tr.div(o);
+    const int k = o - t * TR;
+    const int n = fd_h2.div(t);
+    const int h2 = t - n * H2;
+    uint4 *row = y + ((int64_t)n * H2 + h2) * XW;
+    auto pack_pixel = [&](const int (&q)[4 * CP]) -> uint4 {
+        uint32_t out[4];
+        if constexpr (BITS == 8) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) out[i] = pack4_s8(q[4 * i], q[4 * i + 1], q[4 * i + 2], q[4 * i + 3]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                int u[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) u[e] = q[8 * i + e];
+                out[i] = pack8_s4(u);
+            }
+        }
+        return make_uint4(out[0], out[1], out[2], out[3]);
+    };
+    if (k >= G) {   // a zero border column: left [0, PL) or right [PL + W/2, XW)
+        const int b = k - G;
+        row[b < PL ? b : PL + W / 2 + (b - PL)] = make_uint4(0u, 0u, 0u, 0u);
+        return;
+    }
+    int q[4][4 * CP];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int i = 0; i < 4 * CP; ++i) q[j][i] = 0;
+#pragma unroll
+    for (int dh = 0; dh < 2; ++dh) {
+        const int h = 2 * h2 + dh;
+        if (h >= H) continue;
+        const uint4 *src = reinterpret_cast<const uint4 *>(x + (((int64_t)n * H + h) * W + 8 * k) * 3);
+        const uint4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
+        const uint32_t hw[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int e = 0; e < 24; ++e) {   // half e = pixel e / 3, channel e % 3
+            const unsigned short bits = (unsigned short)(e & 1 ? hw[e >> 1] >> 16 : hw[e >> 1] & 0xFFFFu);
+            const int px = e / 3, ch = e % 3;
+            q[px >> 1][(2 * dh + (px & 1)) * CP + ch] = quant1(__ushort_as_half(bits), inv_scale, lo, hi);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) row[PL + 4 * k + j] = pack_pixel(q[j]);
+}
+
 // Stem weights (once per model): int8 codes [K][R][S][C] -> [K][R2][S2P*16 bytes].
 // Window tap (jr, js), phase (dh, dw), channel c holds w[k, r, s, c] with
 // r = 2*(jr - PL) + dh + pad, s = 2*(js - PL) + dw + pad (0 outside the filter),
