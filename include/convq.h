@@ -102,7 +102,9 @@ typedef struct conv_q_info_s {
  * Errors (NULL + last_error):
  *   EINVAL       any dim < 1, stride not in [1,8], pad not in [0,127],
  *                R-1 or S-1 > 255, P or Q < 1, bits not in {4,8}
- *   EUNSUPPORTED C*bits or K*bits not a multiple of 128, C not a multiple of 32
+ *   EUNSUPPORTED C*bits or K*bits not a multiple of 128; s4: C not a multiple of
+ *                32; s8: C < 32 (C = 16 mod 32 is accepted: the last channel block
+ *                of each tap is zero-filled by the TMA)
  *                (pad C with conv_q_quantize), or C*bits/8 > 65535
  *   EOVERFLOW    R*S*C * 2^(2*bits-2) > 2^31-1
  */

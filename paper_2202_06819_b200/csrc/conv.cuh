@@ -81,7 +81,7 @@ struct ConvParams {
     int P, Q;
     int M;          // N*P*Q
     int row_bytes;  // packed bytes per input pixel row = C*BITS/8
-    int num_cblk;   // channel chunks per tap = C / KCH
+    int num_cblk;   // channel chunks per tap = ceil(C / KCH)
     int num_kb;     // k-blocks per tile = R*S*num_cblk
     int n_tiles;    // ceil(K / BN)
     int num_tiles;  // m_tiles * n_tiles

@@ -186,8 +186,11 @@ static void enumerate_candidates(conv_q_plan_s *p) {
         for (int cg : {1, 2})
             for (auto &q : kn) {
                 const int kch = q[0], nsub = q[1];
-                if (p->C % kch) continue;
-                if (kch < 128 && p->C % (2 * kch) == 0) continue;   // a wider k-block exists
+                // (C = 16 mod 32, s8: a ragged last k-block per tap, kch < C so the box never
+                // exceeds the channel dimension; im2col / tiled only -- no halo / WS candidates)
+                const bool ragged = p->C % 32 != 0;
+                if (ragged ? kch >= p->C : p->C % kch) continue;
+                if (!ragged && kch < 128 && p->C % (2 * kch) == 0) continue;   // a wider k-block exists
                 for (int bn : {64, 128, 256}) {
                     if (bn > 64 && bn / 2 >= p->K) continue;  // a narrower tile already covers K
                     const Cand cand{bn, kch, cg, nsub, direct};
@@ -198,7 +201,7 @@ static void enumerate_candidates(conv_q_plan_s *p) {
                     // units per SM; up to six waves, the (at most two) splits that cut the
                     // wave-quantisation loss of the last partial wave the most
                     const int64_t tiles = ceil_div(p->M, 128 * cg) * ceil_div(p->K, bn);
-                    const int64_t num_kb = (int64_t)p->R * p->S * (p->C / kch);
+                    const int64_t num_kb = (int64_t)p->R * p->S * ceil_div(p->C, kch);
                     const int sms = g_num_sms > 0 ? g_num_sms : 148;
                     const int64_t slots = sms / cg;
                     const int64_t ws = tiles * cg * 128 * bn * 4;
@@ -424,8 +427,12 @@ extern "C" conv_q_plan_t *conv_q_plan(int N, int H, int W, int C, int K, int R, 
                 (long long)C * bits, (long long)K * bits);
         return nullptr;
     }
-    if (C % 32) {
-        set_err(CONV_Q_EUNSUPPORTED, "C=%d: the implicit-GEMM kernel needs C %% 32 == 0 (one MMA K step)", C);
+    // s8 with C = 16 (mod 32): the last k-block of a tap is half a 32-byte MMA K
+    // step; its TMA box reads past the pixel's channels, which the tensor map
+    // zero-fills (activations), so whatever weight bytes sit there add zero
+    if (bits == 8 ? (C % 16 || C < 32) : C % 32) {
+        set_err(CONV_Q_EUNSUPPORTED, "C=%d: the implicit-GEMM kernel needs C %% 32 == 0 (s4) / C %% 16 == 0 and "
+                "C >= 32 (s8)", C);
         return nullptr;
     }
     if ((int64_t)C * bits / 8 > 65535) {

@@ -184,7 +184,7 @@ inline int launch_conv(conv_q_plan_s *p, const float *scale, void *y) {
     prm.N = p->N; prm.H = p->H; prm.W = p->W; prm.C = p->C; prm.K = p->K; prm.R = p->R; prm.S = p->S;
     prm.stride = p->stride; prm.pad = p->pad; prm.pad_w = p->s2d ? 0 : p->pad; prm.P = p->P; prm.Q = p->Q; prm.M = (int)p->M;
     prm.row_bytes = p->row_bytes;
-    prm.num_cblk = p->C / KCH;
+    prm.num_cblk = (int)ceil_div(p->C, KCH);   // (s8 C = 16 mod 32: the last block is partly zero-filled)
     prm.num_kb = p->R * p->S * prm.num_cblk;
     prm.n_tiles = (int)ceil_div(p->K, BN);
     prm.num_tiles = (int)(ceil_div(p->M, BM * CG * ((HALO & 5) ? 1 : ((HALO & 8) ? 2 : 1))) * prm.n_tiles);   // generic MT2: 256-row units

@@ -50,7 +50,7 @@ def test_library_exports_every_header_symbol(lib):
     ((1, 2, 2, 64, 64, 5, 5, 1, 0, 8), cq.EINVAL),        # empty output
     ((1, 56, 56, 24, 64, 3, 3, 1, 1, 8), cq.EUNSUPPORTED),  # C*bits not multiple of 128
     ((1, 56, 56, 64, 40, 3, 3, 1, 1, 4), cq.EUNSUPPORTED),  # K*bits not multiple of 128
-    ((1, 56, 56, 16, 64, 3, 3, 1, 1, 8), cq.EUNSUPPORTED),  # C % 32 (pad with quantize)
+    ((1, 56, 56, 16, 64, 3, 3, 1, 1, 8), cq.EUNSUPPORTED),  # s8 C < 32 (pad with quantize)
     ((1, 8, 8, 16384, 64, 3, 3, 1, 1, 8), cq.EOVERFLOW),  # R*S*C*2^14 > 2^31-1
 ])
 def test_plan_validation_codes(lib, args, code):
@@ -176,3 +176,17 @@ def test_fastdiv_constants_exact():
         for n in {0, 1, d - 1, d, d + 1, 2 ** 31 - 1, top, top - 1, rnd.randrange(0, 2 ** 31)}:
             if 0 <= n < 2 ** 31:
                 assert (((n * m) >> 32) + n) >> s == n // d, (d, n)
+
+
+def test_plan_ragged_channel_block_s8(lib):
+    """s8 needs only C*8 % 128 == 0 -- C = 16 (mod 32) is accepted (C >= 32):
+    im2col / tiled candidates whose k-block is narrower than C; the last block of each tap
+    reads zero-filled channels (no halo / weight-stationary candidates)."""
+    for C in (48, 80, 112):
+        p = cq.ConvPlan(2, 9, 11, C, 64, 3, 3, 1, 1, 8)
+        names = p.candidates()
+        assert names and all("_h" not in n and "_w" not in n for n in names)
+        assert all(int(n.split("_kc")[1].split("x")[0]) < C for n in names)
+    with pytest.raises(cq.ConvQError) as ei:      # s4: C*4 = 192 is not a multiple of 128
+        cq.ConvPlan(1, 8, 8, 48, 64, 3, 3, 1, 1, 4)
+    assert ei.value.code == cq.EUNSUPPORTED

@@ -122,6 +122,16 @@ def test_shape_edge_parity(cq, bits, L, N):
     check_layer(cq, L, N, bits, 1234, relu=(L.name in ("s2", "7x7")))
 
 
+@pytest.mark.parametrize("L,N", [
+    (wl.Layer("c48", 9, 11, 48, 64, 3, 3, 1, 1), 2),             # s8 C = 16 (mod 32): ragged last k-block
+    (wl.Layer("c80s2", 13, 12, 80, 96, 3, 3, 2, 1), 1),          # stride 2, K not a tile multiple
+    (wl.Layer("c112x1", 7, 9, 112, 64, 1, 1, 1, 0), 3),          # 1x1 tiled (a_gemm) path
+])
+def test_ragged_channel_block_s8(cq, L, N):
+    """SURVEY 8(b) boundary: s8 with C = 16 (mod 32), every candidate, s32 + packed."""
+    check_layer(cq, L, N, 8, 4321, relu=True)
+
+
 @pytest.mark.parametrize("bits", [8, 4])
 def test_fuzz_parity(cq, bits):
     g = np.random.default_rng(99 + bits)
