@@ -239,6 +239,7 @@ class ClockSampler:
 
     def __init__(self, gpu_index: int, period_ms: int = 50):
         self.proc = None
+        self.gpu_index = gpu_index
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -270,8 +271,20 @@ class ClockSampler:
             for n, v in zip(names, f[5:9]):
                 if v.lower() in ("active", "1", "yes"):
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        res = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if not sm:
+            # a timed region shorter than nvidia-smi's start-up + period: one sample right after it
+            try:
+                one = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                      f"-i={self.gpu_index}"], capture_output=True, text=True, timeout=10).stdout
+                f = [x.strip() for x in one.strip().splitlines()[0].split(",")]
+                res.update(sm_mhz=float(f[1]), sm_max_mhz=float(f[2]),
+                           reasons=sorted(n for n, v in zip(names, f[5:9]) if v.lower() in ("active", "1", "yes")),
+                           samples=1, note="timed region shorter than the sampling period: one sample right after it")
+            except Exception:
+                pass
+        return res
 
 
 # ---------------------------------------------------------------------------- parity leg
