@@ -103,3 +103,32 @@ def test_search_selects_correct_point(cq, bits):
     other.run(xd, wd, sd, y)
     torch.cuda.synchronize()
     assert np.array_equal(y.cpu().numpy(), ref), r["config"]
+
+
+@pytest.mark.parametrize("bits", [8, 4])
+def test_stem_space_points_parity(cq, bits):
+    """Random points of the s2d stem plan's space (window-halo / im2col TileConfigs x
+    runtime knobs) against the oracle's direct stride-2 conv on the channel-padded image."""
+    N, H, W, C, K, R, S, pad = 2, 30, 40, 3, 64, 7, 7, 3
+    g = np.random.default_rng(606 + bits)
+    x = (g.standard_normal((N, H, W, C)) * 2).astype(np.float16)
+    inv = 127 / 4 if bits == 8 else 7 / 3
+    wv = wl.weight_values(g, K, R, S, C, bits)
+    Cp = oracle.padded_channels(C, bits)
+    w_pad = np.zeros((K, R, S, Cp), dtype=np.int8)
+    w_pad[..., :C] = wv
+    ss = wl.scale_shift(g, K, R * S * C, 40.0 if bits == 8 else 3.0, wl.uniform_code_std(bits), bits)
+    ref = oracle.requant(oracle.conv_s32(oracle.quantize(x, inv, bits), oracle.pack(w_pad, bits), Cp, 2, pad, bits),
+                         ss, True, bits)
+    plan = cq.StemPlan(N, H, W, C, K, R, S, pad, bits, relu=True)
+    xs = plan.quantize(dev(x), inv)
+    wp = plan.pack_weights(dev(wv))
+    sd = dev(ss)
+    sizes, nvalid = plan.space()
+    assert nvalid > 0
+    for pt in _valid_points(cq, plan, sizes, 16, 808 + bits):
+        plan.set_point(pt)
+        y = torch.full((N, plan.P, plan.Q, K * bits // 8), 0xA5, dtype=torch.uint8, device="cuda")
+        plan.run(xs, wp, sd, y)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), ref), (bits, pt, plan.info().config)
