@@ -23,6 +23,7 @@ INSTR = os.environ.get("CONVQ_INSTRUMENT") == "1"
 _SFX = ("_instr" if INSTR else "") + (f"_wg{os.environ['CONVQ_EPI_WG8']}" if os.environ.get("CONVQ_EPI_WG8") else "") + \
     (f"_wgi4{os.environ['CONVQ_EPI_WG4']}" if os.environ.get("CONVQ_EPI_WG4") else "") + \
     ("_tp" if os.environ.get("CONVQ_TMEM_PIPE") == "1" else "") + \
+    ("_la" if os.environ.get("CONVQ_LATE_ACC") == "1" else "") + \
     ("_dual" if os.environ.get("CONVQ_DUAL_MMA") == "1" else "") + \
     ("_allw0" if os.environ.get("CONVQ_EPI_ALLW") == "0" else "")
 OBJ = os.path.join(HERE, "build_obj" + _SFX)
@@ -36,6 +37,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-
     ([f"-DCONVQ_EPI_WG8={os.environ['CONVQ_EPI_WG8']}"] if os.environ.get("CONVQ_EPI_WG8") else []) + \
     ([f"-DCONVQ_EPI_WG4={os.environ['CONVQ_EPI_WG4']}"] if os.environ.get("CONVQ_EPI_WG4") else []) + \
     (["-DCONVQ_TMEM_PIPE=1"] if os.environ.get("CONVQ_TMEM_PIPE") == "1" else []) + \
+    (["-DCONVQ_LATE_ACC=1"] if os.environ.get("CONVQ_LATE_ACC") == "1" else []) + \
     (["-DCONVQ_DUAL_MMA=1"] if os.environ.get("CONVQ_DUAL_MMA") == "1" else []) + \
     (["-DCONVQ_EPI_ALLW=0"] if os.environ.get("CONVQ_EPI_ALLW") == "0" else [])
 

@@ -162,6 +162,11 @@ constexpr int OUT_U = 16;
 #ifndef CONVQ_TMEM_PIPE
 #define CONVQ_TMEM_PIPE 0
 #endif
+// MMA warp, im2col / tiled path: commit a unit's accumulator only after the next
+// unit's first stage of MMAs is issued (A/B build option)
+#ifndef CONVQ_LATE_ACC
+#define CONVQ_LATE_ACC 0
+#endif
 constexpr int epi_warpgroups(int bits) { return bits == 8 ? CONVQ_EPI_WG8 : CONVQ_EPI_WG4; }
 constexpr int tmem_buffers(int bits, int bn) {
     return (512 / bn) < epi_warpgroups(bits) ? ((512 / bn) < 4 ? 512 / bn : 4)
@@ -888,6 +893,10 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
             auto mma_mark = [&]() {
                 if (nmma > 1 && lane == 0) stage_done[stage] = gsi;
             };
+            // CONVQ_LATE_ACC (generic path): the previous unit's accumulator buffer whose
+            // acc_full commit waits until this unit's first MMAs are issued (-1: none)
+            int pend_buf = -1;
+            constexpr bool LATE = CONVQ_LATE_ACC && !HA && !S2H;
             for (int unit = tile0 + mw * tstep, local = mw; unit < p.num_units; unit += nmma * tstep, local += nmma) {
                 int tile, kb_lo, kb_hi;
                 unit_range(p, unit, tile, kb_lo, kb_hi);
@@ -1121,14 +1130,33 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                     if (trace && lane == 0) atomicAdd(trace + blockIdx.x * TR_SLOTS + TR_MMA_ISSUE, clock64() - t0);
                     ++gsi;
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    if (LATE && pend_buf >= 0) {   // the previous unit's accumulator, behind these MMAs
+                        if (mma_elect()) {
+                            if constexpr (CG == 2) mma_commit_cg2_mc(&acc_full[pend_buf], 0x3);
+                            else mma_commit(&acc_full[pend_buf]);
+                        }
+                        mma_sync();
+                        pend_buf = -1;
+                    }
                 }
                 // accumulator ready for the epilogue (of both CTAs)
+                if (LATE) {
+                    pend_buf = buf;
+                } else {
+                    if (mma_elect()) {
+                        if constexpr (CG == 2) mma_commit_cg2_mc(&acc_full[buf], 0x3);
+                        else mma_commit(&acc_full[buf]);
+                    }
+                    mma_sync();
+                }
+                CONVQ_TL(3, local);
+            }
+            if (LATE && pend_buf >= 0) {   // the last unit's accumulator
                 if (mma_elect()) {
-                    if constexpr (CG == 2) mma_commit_cg2_mc(&acc_full[buf], 0x3);
-                    else mma_commit(&acc_full[buf]);
+                    if constexpr (CG == 2) mma_commit_cg2_mc(&acc_full[pend_buf], 0x3);
+                    else mma_commit(&acc_full[pend_buf]);
                 }
                 mma_sync();
-                CONVQ_TL(3, local);
             }
         } else if (PAIR8 && rank != 0 && mw == 0) {
             // follower CTA: relay every stage its own TMA loads filled to the
