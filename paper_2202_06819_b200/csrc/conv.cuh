@@ -389,6 +389,11 @@ __device__ __forceinline__ void fma2_rn(float a0, float a1, float b0, float b1, 
         " fma.rn.f32x2 d, a, b, c;\n mov.b64 {%0, %1}, d;\n}"
         : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
+// two-wide RN add of one scalar (add.rn.f32x2)
+__device__ __forceinline__ void add2_rn(float a0, float a1, float b, float &d0, float &d1) {
+    asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %4};\n"
+        " add.rn.f32x2 d, a, b;\n mov.b64 {%0, %1}, d;\n}" : "=f"(d0), "=f"(d1) : "f"(a0), "f"(a1), "f"(b));
+}
 // two-wide RN multiply (mul.rn.f32x2)
 __device__ __forceinline__ void mul2_rn(float a0, float a1, float b, float &d0, float &d1) {
     asm("{\n .reg .b64 a, b, d;\n mov.b64 a, {%2, %3};\n mov.b64 b, {%4, %4};\n"
@@ -1419,12 +1424,14 @@ __global__ void __launch_bounds__(ConvCfg<BITS, BN, KCH, OUT, CG, NSUB, HALO>::N
                                 if constexpr (Cfg::RES) {
                                     // v = fmaf(skip, res_scale, u) (reading 15); skip byte -> exact float as
                                     // (2^23 + (byte ^ bias)) - (2^23 + bias), bias 0x80 for a signed skip,
-                                    // 0 for an unsigned one (reading 16): one PRMT + one FADD per code
+                                    // 0 for an unsigned one (reading 16): one PRMT per code + one FADD2 per
+                                    // two codes (the subtraction is exact: integers below 2^24)
                                     const uint32_t wv = (&sk.x)[q] ^ p.skip_xor;
-                                    float k0 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7650)), p.skip_off);
-                                    float k1 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7651)), p.skip_off);
-                                    float k2 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7652)), p.skip_off);
-                                    float k3 = __fsub_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7653)), p.skip_off);
+                                    float k0, k1, k2, k3;
+                                    add2_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7650)),
+                                            __uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7651)), -p.skip_off, k0, k1);
+                                    add2_rn(__uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7652)),
+                                            __uint_as_float(__byte_perm(wv, 0x4B000000u, 0x7653)), -p.skip_off, k2, k3);
                                     fma2_rn(k0, k1, p.res_scale, p.res_scale, u0, u1, u0, u1);
                                     fma2_rn(k2, k3, p.res_scale, p.res_scale, u2, u3, u2, u3);
                                 }
